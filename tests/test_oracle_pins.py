@@ -1,0 +1,522 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+Each test names the passage it pins (P:n = PAPER.md line n, S:n = SPEC.md
+line n, Rn = DESIGN.md reading n).  The oracle is never compared with
+itself: the expected values are the paper's printed numbers (tests/golden/),
+closed forms, brute force on tiny inputs, or statistical invariants.
+"""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import EMPTY, binomial
+from workloads import make_csr
+
+E = EMPTY
+
+
+def _sk(lst):
+    return [E if v is None else v for v in lst]
+
+
+# --------------------------------------------------------------------- Eq. 10 / Table 2
+def test_table2_binomial_tails(golden):
+    """Table 2: all 20 printed rows, both columns (R8, R9)."""
+    g = golden("table2.json")
+    K, tn, td = g["K"], g["t_num"], g["t_den"]
+    for X, lo_printed, up_printed in g["rows"]:
+        lo = float(binomial.lower_tail(X - 1, K, tn, td))  # F(x < X)
+        up = float(binomial.upper_tail(X, K, tn, td))      # F(x >= X)
+        assert lo == pytest.approx(lo_printed, rel=1e-5), X
+        assert up == pytest.approx(up_printed, rel=1e-5), X
+
+
+def test_binomial_complement_and_monotone():
+    """lower(m) + upper(m+1) = 1 exactly; monotone; ends."""
+    for K, tn, td in [(16, 7, 10), (32, 4, 5), (100, 3, 5), (5, 1, 2)]:
+        lo = [binomial.lower_tail(m, K, tn, td) for m in range(-1, K + 1)]
+        up = [binomial.upper_tail(m, K, tn, td) for m in range(0, K + 2)]
+        for m in range(0, K + 1):
+            assert binomial.lower_tail(m, K, tn, td) + binomial.upper_tail(m + 1, K, tn, td) == 1
+        assert all(a <= b for a, b in zip(lo, lo[1:]))
+        assert all(a >= b for a, b in zip(up, up[1:]))
+        assert lo[0] == 0 and lo[-1] == 1 and up[0] == 1 and up[-1] == 0
+
+
+def test_binomial_brute_force_small():
+    """Brute force: enumerate all 2^K outcomes of K Bernoulli(T) trials."""
+    K, T = 8, Fraction(3, 10)
+    import itertools
+    dist = [Fraction(0)] * (K + 1)
+    for bits in itertools.product([0, 1], repeat=K):
+        p = Fraction(1)
+        for b in bits:
+            p *= T if b else 1 - T
+        dist[sum(bits)] += p
+    for m in range(K + 1):
+        assert binomial.lower_tail(m, K, 3, 10) == sum(dist[: m + 1])
+        assert binomial.upper_tail(m, K, 3, 10) == sum(dist[m:])
+
+
+# --------------------------------------------------------------------- O1 psi
+@pytest.mark.parametrize("V", [1, 2, 3, 17, 1000, 65536, 1 << 20, 1000003])
+def test_psi_is_a_bijection(V):
+    """S:33 'mapping is a bijection'; exhaustive over [0, V)."""
+    for seed in (0, 1, 0xDEADBEEF):
+        img = oracle.psi(np.arange(V, dtype=np.uint64), V, seed)
+        assert img.max(initial=0) < V
+        assert len(np.unique(img)) == V
+
+
+def test_psi_2_32_injective_on_sample():
+    """|V| = 2^32: no collision among 2^20 consecutive ids plus 2^20 random ids
+    (a random non-injective map would show ~500 birthday collisions)."""
+    rng = np.random.default_rng(7)
+    x = np.unique(np.concatenate([np.arange(1 << 20, dtype=np.uint64),
+                                  rng.integers(0, 1 << 32, size=1 << 20, dtype=np.uint64)]))
+    img = oracle.psi(x, 1 << 32, 12345)
+    assert img.max() < (1 << 32)
+    assert len(np.unique(img)) == len(x)
+
+
+def test_psi_identity_and_determinism():
+    """S:113 identity constructor; S:34 same seed + size => same mapping."""
+    x = np.arange(17, dtype=np.uint64)
+    assert (oracle.psi(x, 17, 5, identity=True) == x).all()
+    a = oracle.psi(np.arange(1000, dtype=np.uint64), 1 << 32, 42)
+    b = oracle.psi(np.arange(1000, dtype=np.uint64), 1 << 32, 42)
+    c = oracle.psi(np.arange(1000, dtype=np.uint64), 1 << 32, 43)
+    assert (a == b).all() and not (a == c).all()
+
+
+# --------------------------------------------------------------------- O2 / O3 OPH sketch
+def test_flat_layout_floor_rule_brute_force():
+    """S:38 bin i covers [floor(i|V|/k), floor((i+1)|V|/k)); S:107 |V|=17,k=4
+    gives boundaries 0,4,8,12,17.  Single-element sets under the identity
+    permutation expose (bin, offset) of every p."""
+    for V, k in [(17, 4), (100, 7), (64, 64), (1000, 3), (5, 5)]:
+        offs, ids = make_csr([[p] for p in range(V)])
+        F = oracle.oph_sketch(offs, ids, V, k, 0, identity=True)
+        starts = [b * V // k for b in range(k + 1)]
+        for p in range(V):
+            b = max(i for i in range(k) if starts[i] <= p)
+            row = F[p]
+            assert row[b] == p - starts[b]
+            assert all(row[j] == E for j in range(k) if j != b)
+    assert [b * 17 // 4 for b in range(5)] == [0, 4, 8, 12, 17]
+
+
+def test_oph_worked_example(golden):
+    """P:158-160 sketches [1,1,2,0], [1,2,2,0], [2,(x),1,0]; estimates 0.75 and
+    0.333 (EitherEmpty), 1/4 under JointEmpty (Eq. 4); exact J 0.5, 0.375."""
+    g = golden("oph_example.json")
+    names = ["D1", "D2", "D3"]
+    offs, ids = make_csr([g["sets"][n] for n in names])
+    F = oracle.oph_sketch(offs, ids, g["vocab_size"], g["k"], 0, identity=True)
+    for i, n in enumerate(names):
+        assert list(F[i]) == _sk(g["sketch"][n])
+    either = oracle.compare_full(F, F, t_num=7, t_den=10, joint=False)
+    joint = oracle.compare_full(F, F, t_num=7, t_den=10, joint=True)
+    assert either[0, 1]["n_mb"] == 3 and either[0, 1]["estimate"] == 0.75 and joint[0, 1]["estimate"] == 0.75
+    assert either[0, 2]["n_mb"] == 1
+    assert either[0, 2]["estimate"] == pytest.approx(1 / 3, abs=1e-15)
+    assert joint[0, 2]["estimate"] == 0.25
+    for p in g["pairs"]:
+        a, b = g["sets"][p["a"]], g["sets"][p["b"]]
+        j, _, _ = oracle.jaccard(a, b)
+        assert j == p["jaccard"]
+
+
+def test_oph_empty_set_sketch():
+    """S:210 empty FeatureSet -> all (x); S:251 two all-(x) sketches -> undefined."""
+    offs, ids = make_csr([[], [3]])
+    F = oracle.oph_sketch(offs, ids, 16, 4, 9)
+    assert (F[0] == E).all()
+    r = oracle.compare_full(F[:1], F[:1], t_num=1, t_den=2)
+    assert r[0, 0]["flags"] & oracle.UNDEFINED and r[0, 0]["verdict"] == 0
+
+
+# --------------------------------------------------------------------- O4 / O5 HOPH
+def test_hoph_layout_worked_example(golden):
+    """(|V|=17, 1:1, k'=2) -> [0,8), [8,12), [12,17) (R17, R18)."""
+    g = golden("hoph_example.json")
+    assert oracle.hoph_layout(g["vocab_size"], g["a"], g["b"], g["kprime"]) == [tuple(x) for x in g["layout"]]
+
+
+@pytest.mark.parametrize("V,kp,L", [(1 << 16, 16, 12), (1 << 16, 32, 11), (1 << 20, 32, 15),
+                                    (1 << 32, 32, 27), (1 << 16, 100, 10)])
+def test_hoph_layout_group_counts(V, kp, L):
+    """Recursive 1:1 split: group j has length floor(R/2) of the
+    remainder R until a half would be <= k'.  For |V| = 2^m the closed form is
+    lengths 2^(m-1), 2^(m-2), ..., then the last remainder."""
+    lay = oracle.hoph_layout(V, 1, 1, kp)
+    assert len(lay) == L
+    assert lay[0] == (0, V // 2)
+    assert sum(length for _, length in lay) == V
+    assert all(s2 == s1 + l1 for (s1, l1), (s2, _) in zip(lay, lay[1:]))
+    assert all(length >= kp for _, length in lay)
+
+
+def test_hoph_layout_properties_random():
+    """S:401 group lengths >= k' and sum to |V|; S:400 |V| = 4k' -> two groups."""
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        kp = int(rng.integers(1, 50))
+        V = int(rng.integers(2 * kp, 10 ** 6))
+        a, b = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+        lay = oracle.hoph_layout(V, a, b, kp)
+        assert sum(length for _, length in lay) == V and all(length >= kp for _, length in lay)
+        for (s, length), (s2, _) in zip(lay, lay[1:]):  # every non-final group is floor(a R/(a+b))
+            R = V - s
+            assert length == a * R // (a + b)
+    assert oracle.hoph_layout(4 * 8, 1, 1, 8) == [(0, 16), (16, 16)]
+
+
+def test_hoph_worked_example(golden):
+    """sketches [[1,1],[(x),0],[0,1]], [[1,2],[(x),0],[0,0]]; D3 from the
+    raw sample at P:478; estimates 0.625 and 0.375 with nominal weights (R21)."""
+    g = golden("hoph_example.json")
+    og = golden("oph_example.json")
+    names = ["D1", "D2", "D3"]
+    offs, ids = make_csr([og["sets"][n] for n in names])
+    H = oracle.hoph_sketch(offs, ids, g["vocab_size"], g["layout"], g["kprime"], 0, identity=True)
+    for i, n in enumerate(names):
+        assert list(H[i]) == _sk(g["sketch"][n])
+    for p in g["pairs"]:
+        a, b = names.index(p["a"]), names.index(p["b"])
+        r = oracle.hoph_estimate(H[a], H[b], L=3, kprime=2, a=1, b=1, t_num=1, t_den=2)
+        assert r["estimate"] == p["estimate_num"] / p["estimate_den"]
+
+
+def test_hoph_weights_nominal():
+    """Lemma 3 with l = L: w_j = r(1-r)^(j-1), w_L = (1-r)^(L-1).  They
+    sum to 1 and at 1:1 on |V| = 2^m equal the group shares len_j/|V|."""
+    for a, b, L in [(1, 1, 27), (1, 2, 10), (2, 1, 18), (3, 5, 7), (1, 1, 1)]:
+        c, D = oracle.hoph_weights(a, b, L)
+        r = Fraction(a, a + b)
+        want = [r * (1 - r) ** (j - 1) for j in range(1, L)] + [(1 - r) ** (L - 1)]
+        assert [Fraction(x, D) for x in c] == want
+        assert sum(c) == D
+    lay = oracle.hoph_layout(1 << 32, 1, 1, 32)
+    c, D = oracle.hoph_weights(1, 1, len(lay))
+    assert [Fraction(x, D) for x in c] == [Fraction(length, 1 << 32) for _, length in lay]
+
+
+def test_hoph_single_group_reduces_to_oph():
+    """|V| = 2k' gives one group; the HOPH estimator is then the OPH estimator
+    of that group's k' bins (Eq. 6)."""
+    rng = np.random.default_rng(11)
+    V, kp = 64, 32
+    lay = oracle.hoph_layout(V, 1, 1, kp)
+    assert lay == [(0, 64)]
+    sets = [sorted(rng.choice(V, size=int(rng.integers(0, 40)), replace=False).tolist()) for _ in range(30)]
+    offs, ids = make_csr(sets)
+    H = oracle.hoph_sketch(offs, ids, V, lay, kp, 77)
+    F = oracle.oph_sketch(offs, ids, V, kp, 77)
+    assert (H == F).all()
+    full = oracle.compare_full(F, F, t_num=1, t_den=2)
+    for i in range(30):
+        for j in range(30):
+            h = oracle.hoph_estimate(H[i], H[j], L=1, kprime=kp, a=1, b=1, t_num=1, t_den=2)
+            assert h["flags"] == full[i, j]["flags"]
+            if not h["flags"]:
+                assert h["estimate"] == pytest.approx(full[i, j]["estimate"], abs=1e-15)
+                assert h["verdict"] == full[i, j]["verdict"]
+
+
+# --------------------------------------------------------------------- O9 GOPH
+def _goph_pair(matches, kp, n):
+    """Two flat sketches whose group l has exactly matches[l] matched bins and
+    no empty bin."""
+    q = np.zeros((1, n * kp), dtype=np.uint32)
+    s = np.ones((1, n * kp), dtype=np.uint32)
+    for l, m in enumerate(matches):
+        s[0, l * kp: l * kp + m] = 0
+    return q, s
+
+
+def test_goph_example1(golden):
+    """Example 1: M_ra 59.4, 66.25, 74.28, 85 and NotSimilar after
+    group 4, F(x >= 85) = 5.0732e-8 (R10, R11, R12)."""
+    g = golden("example1.json")
+    q, s = _goph_pair(g["matches"] + [0] * 6, g["kprime"], g["n"])
+    r, tr = oracle.compare_goph(q, s, n=g["n"], kprime=g["kprime"], t_num=g["t_num"], t_den=g["t_den"],
+                                eps=g["eps"], trace=True)
+    assert r[0, 0]["groups"] == g["groups_compared"] and r[0, 0]["verdict"] == 0
+    assert r[0, 0]["flags"] == oracle.EARLY
+    for l, (printed, tol) in enumerate(g["m_ra_printed"]):
+        m_ra = tr[0, 0, l, 0] / tr[0, 0, l, 1]
+        assert abs(m_ra - printed) <= tol + 1e-12, (l, m_ra)
+    assert float(binomial.upper_tail(85, 100, 3, 5)) == pytest.approx(g["upper_85"], rel=1e-5)
+
+
+def test_goph_degenerate_traces():
+    """S:347-348 (A.2): identical sketches -> Similar at the first l where
+    lower(floor((600-100l)/(10-l))) <= 1e-4 (= group 4); zero matches ->
+    NotSimilar at the first l where M_ra > 100 or upper(ceil(600/(10-l))) <= 1e-4
+    (= group 3).  k'=100, n=10, T=0.6."""
+    def first_stop_identical():
+        for l in range(1, 10):
+            m = Fraction(600 - 100 * l, 10 - l)
+            if m <= 0 or binomial.lower_tail(int(m), 100, 3, 5) <= Fraction(1e-4):
+                return l
+
+    def first_stop_zero():
+        for l in range(1, 10):
+            m = Fraction(600, 10 - l)
+            if m > 100 or binomial.upper_tail(-(-m.numerator // m.denominator), 100, 3, 5) <= Fraction(1e-4):
+                return l
+    assert first_stop_identical() == 4 and first_stop_zero() == 3
+    q, s = _goph_pair([100] * 10, 100, 10)
+    r = oracle.compare_goph(q, s, n=10, kprime=100, t_num=3, t_den=5, eps=1e-4)
+    assert (r[0, 0]["groups"], r[0, 0]["verdict"]) == (4, 1)
+    q, s = _goph_pair([0] * 10, 100, 10)
+    r = oracle.compare_goph(q, s, n=10, kprime=100, t_num=3, t_den=5, eps=1e-4)
+    assert (r[0, 0]["groups"], r[0, 0]["verdict"]) == (3, 0)
+
+
+def test_goph_exact_rational_cross_check():
+    """Algorithm 1 re-evaluated with Fractions in the paper's own (unscaled)
+    form on random per-group match counts: same stop group and verdict as the
+    oracle's scaled-integer evaluation (guards R16, floors/ceils R12)."""
+    rng = np.random.default_rng(5)
+    for kp, n, tn, td, eps in [(16, 4, 7, 10, 1e-4), (32, 8, 7, 10, 1e-4), (32, 8, 4, 5, 1e-3), (10, 6, 1, 2, 1e-2)]:
+        T = Fraction(tn, td)
+        lo, up = binomial.small_probability_tables(kp, tn, td, eps)
+        for _ in range(300):
+            p = rng.uniform(0, 1)
+            matches = rng.binomial(kp, p, size=n).tolist()
+            q, s = _goph_pair(matches, kp, n)
+            r = oracle.compare_goph(q, s, n=n, kprime=kp, t_num=tn, t_den=td, eps=eps)[0, 0]
+            Mc, want = 0, None
+            for l in range(1, n + 1):
+                Mc += matches[l - 1]
+                if l == n:
+                    want = (n, int(Fraction(Mc, n * kp) >= T))
+                    break
+                Mra = (n * kp * T - Mc) / (n - l)
+                if Mra <= 0:
+                    want = (l, 1)
+                elif Mra > kp:
+                    want = (l, 0)
+                elif Mra < kp * T and lo[int(Mra)]:
+                    want = (l, 1)
+                elif Mra >= kp * T and up[-(-Mra.numerator // Mra.denominator)]:
+                    want = (l, 0)
+                if want:
+                    break
+            assert (r["groups"], r["verdict"]) == want
+
+
+# --------------------------------------------------------------------- O10 HOPH filter
+def test_hoph_example2(golden):
+    """Example 2: 40 matches in group 1 of a 1:1 layout -> P_r = 0.8,
+    P_r k' = 80, F(x >= 80) = 1.64119e-5 <= eps -> NotSimilar after 1 group."""
+    g = golden("example2.json")
+    lay = oracle.hoph_layout(g["vocab_size"], g["a"], g["b"], g["kprime"])
+    L, kp = len(lay), g["kprime"]
+    q = np.zeros((1, L * kp), dtype=np.uint32)
+    s = np.ones((1, L * kp), dtype=np.uint32)
+    s[0, :g["first_group_matches"]] = 0
+    r, tr = oracle.compare_hoph(q, s, L=L, kprime=kp, a=1, b=1, t_num=g["t_num"], t_den=g["t_den"],
+                                eps=g["eps"], trace=True)
+    num, den = tr[0, 0, 0]
+    assert Fraction(int(num), int(den)) == g["x"]
+    assert (r[0, 0]["groups"], r[0, 0]["verdict"]) == (g["groups_compared"], 0)
+    assert float(binomial.upper_tail(80, 100, 3, 5)) == pytest.approx(g["upper_80"], rel=1e-5)
+
+
+def test_hoph_mass_balance_cross_check():
+    """Algorithm 2 with the mass balance P_r = (T - sum_{j<=l} w_j M_j/k') /
+    sum_{j>l} w_j (R19) re-evaluated with Fractions on random match counts."""
+    rng = np.random.default_rng(9)
+    for kp, L, a, b, tn, td, eps in [(16, 12, 1, 1, 7, 10, 1e-4), (32, 10, 1, 2, 4, 5, 1e-4), (8, 6, 2, 1, 1, 2, 1e-2)]:
+        T = Fraction(tn, td)
+        r_ = Fraction(a, a + b)
+        w = [r_ * (1 - r_) ** (j - 1) for j in range(1, L)] + [(1 - r_) ** (L - 1)]
+        lo, up = binomial.small_probability_tables(kp, tn, td, eps)
+        for _ in range(300):
+            p = rng.uniform(0, 1)
+            matches = rng.binomial(kp, p, size=L).tolist()
+            q = np.zeros((1, L * kp), dtype=np.uint32)
+            s = np.ones((1, L * kp), dtype=np.uint32)
+            for l, m in enumerate(matches):
+                s[0, l * kp: l * kp + m] = 0
+            r = oracle.compare_hoph(q, s, L=L, kprime=kp, a=a, b=b, t_num=tn, t_den=td, eps=eps)[0, 0]
+            want = None
+            for l in range(1, L + 1):
+                if l == L:
+                    est = sum(w[j] * Fraction(matches[j], kp) for j in range(L))
+                    want = (L, int(est >= T))
+                    break
+                Pr = (T - sum(w[j] * Fraction(matches[j], kp) for j in range(l))) / sum(w[l:])
+                x = Pr * kp
+                if x <= 0:
+                    want = (l, 1)
+                elif x > kp:
+                    want = (l, 0)
+                elif Pr < T and lo[int(x)]:
+                    want = (l, 1)
+                elif Pr >= T and up[-(-x.numerator // x.denominator)]:
+                    want = (l, 0)
+                if want:
+                    break
+            assert (r["groups"], r["verdict"]) == want
+
+
+# --------------------------------------------------------------------- estimators: unbiasedness (Eq. 7)
+def _pair_with_union(g, J, V, rng):
+    inter = int(round(J * g))
+    a_only = (g - inter) // 2
+    b_only = g - inter - a_only
+    u = rng.choice(V, size=g, replace=False)
+    A = np.sort(u[: inter + a_only])
+    B = np.sort(np.concatenate([u[:inter], u[inter + a_only:]]))
+    return A, B, Fraction(inter, g)
+
+
+@pytest.mark.parametrize("J", [0.25, 0.5, 0.8])
+def test_oph_unbiased_joint_empty(J):
+    """Eq. 7: over 10^4 permutations, g = 4096, k = 256,
+    the mean JointEmpty OPH estimate is within 3 standard errors of J."""
+    rng = np.random.default_rng(int(J * 100))
+    V, k = 1 << 16, 256
+    A, B, Jt = _pair_with_union(4096, J, V, rng)
+    offs, ids = make_csr([A, B])
+    ests = []
+    for seed in range(10_000):
+        F = oracle.oph_sketch(offs, ids, V, k, seed)
+        r = oracle.compare_full(F[:1], F[1:], t_num=1, t_den=2, joint=True)[0, 0]
+        ests.append(r["estimate"])
+    ests = np.array(ests)
+    se = ests.std(ddof=1) / np.sqrt(len(ests))
+    assert abs(ests.mean() - float(Jt)) < 3 * se
+
+
+def test_oph_collision_probability_k1():
+    """Eq. 5: with k = 1 bin the minima collide with
+    probability J, within 3 standard errors over 4000 permutations."""
+    rng = np.random.default_rng(21)
+    V = 1 << 20
+    A, B, Jt = _pair_with_union(400, 0.6, V, rng)
+    offs, ids = make_csr([A, B])
+    hits = 0
+    n = 4000
+    for seed in range(n):
+        F = oracle.oph_sketch(offs, ids, V, 1, seed)
+        hits += int(F[0, 0] == F[1, 0])
+    p = float(Jt)
+    assert abs(hits / n - p) < 3 * np.sqrt(p * (1 - p) / n)
+
+
+def test_hoph_unbiased_joint_empty_dense():
+    """Lemma 3: the HOPH estimator is unbiased; JointEmpty, sets dense
+    relative to the bins (A.15), 3000 permutations, J = 0.5."""
+    rng = np.random.default_rng(31)
+    V, kp = 1 << 12, 16
+    lay = oracle.hoph_layout(V, 1, 1, kp)
+    L = len(lay)
+    A, B, Jt = _pair_with_union(2048, 0.5, V, rng)
+    offs, ids = make_csr([A, B])
+    ests = []
+    for seed in range(3000):
+        H = oracle.hoph_sketch(offs, ids, V, lay, kp, seed)
+        ests.append(oracle.hoph_estimate(H[0], H[1], L=L, kprime=kp, a=1, b=1, t_num=1, t_den=2,
+                                         joint=True)["estimate"])
+    ests = np.array(ests)
+    se = ests.std(ddof=1) / np.sqrt(len(ests))
+    assert abs(ests.mean() - float(Jt)) < 3 * se
+
+
+# --------------------------------------------------------------------- MinWise
+def test_minwise_properties():
+    """S:283 full vocabulary -> all fingerprints 0; S:292 disjoint sets -> 0
+    exactly; S:279 empty set flagged undefined; identical -> 1."""
+    V = 64
+    offs, ids = make_csr([range(V), range(0, 32), range(32, 64), []])
+    F, fl = oracle.minwise_sketch(offs, ids, V, 50, 3)
+    assert (F[0] == 0).all()
+    assert list(fl) == [0, 0, 0, 1]
+    r = oracle.compare_minwise(F, fl, F, fl, t_num=1, t_den=2)
+    assert r[1, 2]["estimate"] == 0.0 and r[1, 2]["n_mb"] == 0
+    assert r[1, 1]["estimate"] == 1.0 and r[1, 1]["verdict"] == 1
+    assert r[3, 1]["flags"] & oracle.UNDEFINED and r[3, 3]["verdict"] == 0
+
+
+def test_minwise_collision_rate():
+    """Each MinWise position matches with probability J (Eq. 5 per
+    permutation); k = 500 positions x 8 seeds, within 3 s.e. of J = 0.6."""
+    rng = np.random.default_rng(41)
+    V = 1 << 32
+    A, B, Jt = _pair_with_union(300, 0.6, 1 << 24, rng)
+    offs, ids = make_csr([A, B])
+    eq = 0
+    tot = 0
+    for seed in range(8):
+        F, _ = oracle.minwise_sketch(offs, ids, V, 500, seed)
+        eq += int((F[0] == F[1]).sum())
+        tot += 500
+    p = float(Jt)
+    assert abs(eq / tot - p) < 3 * np.sqrt(p * (1 - p) / tot)
+
+
+# --------------------------------------------------------------------- Jaccard, invariants
+def test_jaccard_brute_force():
+    rng = np.random.default_rng(2)
+    for _ in range(200):
+        a = set(rng.integers(0, 50, size=int(rng.integers(0, 30))).tolist())
+        b = set(rng.integers(0, 50, size=int(rng.integers(0, 30))).tolist())
+        j, i, u = oracle.jaccard(sorted(a), sorted(b))
+        assert (i, u) == (len(a & b), len(a | b))
+        assert j == (len(a & b) / len(a | b) if (a | b) else None)
+
+
+def test_pair_invariants_and_symmetry():
+    """S:192 0 <= N_mb <= k - N_excl; JointEmpty excludes <= EitherEmpty;
+    estimate in [0,1]; S:297/S:458 symmetry in the arguments."""
+    from workloads import tiny
+    w = tiny()
+    p = w.params
+    F = oracle.oph_sketch(w.offsets[:201], w.ids, w.vocab_size, p["k"], p["perm_seed"])
+    re = oracle.compare_full(F, F, t_num=7, t_den=10, joint=False)
+    rj = oracle.compare_full(F, F, t_num=7, t_den=10, joint=True)
+    assert (re["n_excl"] >= rj["n_excl"]).all()
+    for r in (re, rj):
+        assert (r["n_mb"] <= p["k"] - r["n_excl"]).all()
+        d = r["flags"] == 0
+        assert ((r["estimate"][d] >= 0) & (r["estimate"][d] <= 1)).all()
+        assert (r == r.T).all()
+
+
+def test_goph_degeneracy_dense():
+    """S:538 / S:618 on dense sets (R16, A.9): with eps = 1e-300 the filter can
+    only stop on the certain guards, so GOPH verdicts equal full-OPH verdicts."""
+    rng = np.random.default_rng(8)
+    V, k, kp = 1 << 16, 256, 32
+    sets = []
+    base = rng.choice(V, size=4096, replace=False)
+    for _ in range(40):
+        J = rng.uniform(0.3, 1.0)
+        keep = int(4096 * 2 * J / (1 + J))
+        fresh = rng.choice(np.setdiff1d(np.arange(V), base), size=4096 - keep, replace=False)
+        sets.append(np.concatenate([rng.choice(base, size=keep, replace=False), fresh]))
+    offs, ids = make_csr(sets)
+    F = oracle.oph_sketch(offs, ids, V, k, 1)
+    assert (F != E).all()
+    full = oracle.compare_full(F, F, t_num=7, t_den=10)
+    go = oracle.compare_goph(F, F, n=k // kp, kprime=kp, t_num=7, t_den=10, eps=1e-300)
+    assert (full["verdict"] == go["verdict"]).all()
+
+
+def test_result_lists():
+    """O12: threshold list sorted by (query, set_id); top-k by the
+    exact estimate, ties to the smaller set_id (R27)."""
+    recs = np.zeros((2, 5), dtype=oracle.REC_DTYPE)
+    recs["verdict"][0] = [1, 0, 1, 1, 1]
+    recs["n_mb"][0] = [3, 0, 4, 4, 2]
+    recs["verdict"][1] = [0, 1, 0, 0, 0]
+    recs["n_mb"][1] = [0, 5, 0, 0, 0]
+    assert oracle.threshold_list(recs, 10) == [(0, 10), (0, 12), (0, 13), (0, 14), (1, 11)]
+    assert oracle.topk_list(recs, 8, 2) == [(0, 2), (0, 3), (1, 1)]
