@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""bench.py -- one step of the whole OPH/GOPH/HOPH hot path (SURVEY 8(a) rows
+a1-a10) on the text-like workload (BASELINE.json configs[1]), timed on the
+device; prints ONE JSON line (rank 0).
+
+A step, per GPU (rank r owns a text-like shard of 200,000 sets, set IDs
+offset by r*200,000; the 1,000 queries are the same on every rank):
+  a1-a3  oph_build_sketches     OPH (k=256) + HOPH (1:1, k'=32, L=27) of the shard
+  a4     minwise_build_sketches MinWise (k=256) of the shard
+  a5     query sketches (rank 0) + NCCL broadcast; query prep inside compare_*
+  a6-a9  compare_full / compare_goph / compare_hoph / compare_minwise (threshold)
+  a10    hit lists gathered to rank 0 and sorted (topk_or_threshold_results)
+
+value = 3 * Q * N_total / step time: query x set comparisons per second of
+the three OPH-family methods the metric names (every pair is scored by each
+of full OPH, GOPH and HOPH in a step; MinWise and the sketch builds are
+inside the timed step but not counted).
+
+`--impl reference` times the CPU oracle (the reference arm of this tier) on
+a bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "query×set sketch comparisons/sec (HOPH, GOPH, full OPH) + sketches/sec; % HBM peak"
+UNIT = "comparisons/s"
+
+# CPU sample of the workload for the oracle legs (about 10 s of CPU work)
+CPU_SAMPLE_SETS = 20_000
+CPU_SAMPLE_QUERIES = 32
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- oracle (CPU) legs
+def cpu_sample_step(w, n_sets: int, n_q: int):
+    """The whole path on a bounded sample, with the CPU oracle: sketches of
+    n_sets sets and n_q queries, the four comparisons, threshold lists."""
+    import oracle
+    p = w.params
+    V, seed = w.vocab_size, p["perm_seed"]
+    offs = w.offsets[: n_sets + 1]
+    qoffs = w.q_offsets[: n_q + 1]
+    lay = oracle.hoph_layout(V, p["a"], p["b"], p["hoph_kprime"])
+    F = oracle.oph_sketch(offs, w.ids, V, p["k"], seed)
+    H = oracle.hoph_sketch(offs, w.ids, V, lay, p["hoph_kprime"], seed)
+    MW, fl = oracle.minwise_sketch(offs, w.ids, V, p["mw_k"], seed)
+    QF = oracle.oph_sketch(qoffs, w.q_ids, V, p["k"], seed)
+    QH = oracle.hoph_sketch(qoffs, w.q_ids, V, lay, p["hoph_kprime"], seed)
+    QMW, qfl = oracle.minwise_sketch(qoffs, w.q_ids, V, p["mw_k"], seed)
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"])
+    r1 = oracle.compare_full(QF, F, groups=p["k"] // p["kprime"], **kw)
+    r2 = oracle.compare_goph(QF, F, n=p["k"] // p["kprime"], kprime=p["kprime"], eps=p["eps"], **kw)
+    r3 = oracle.compare_hoph(QH, H, L=len(lay), kprime=p["hoph_kprime"], a=p["a"], b=p["b"], eps=p["eps"], **kw)
+    r4 = oracle.compare_minwise(QMW, qfl, MW, fl, **kw)
+    return sum(len(oracle.threshold_list(r)) for r in (r1, r2, r3, r4))
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    from workloads import text_like
+    oracle.build()
+    w = text_like()
+    n_s, n_q = CPU_SAMPLE_SETS, CPU_SAMPLE_QUERIES
+    for _ in range(args.warmup):
+        cpu_sample_step(w, n_s, n_q)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_sample_step(w, n_s, n_q)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    value = 3 * n_q * n_s / t
+    sample = (f"text-like: first {n_s} of 200,000 sets x first {n_q} of 1,000 queries; whole path "
+              f"(OPH/HOPH/MinWise sketches of the sample, full/GOPH/HOPH/MinWise scoring, threshold lists)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": "text-like", "sample_sets": n_s, "sample_queries": n_q},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU arm
+def count_launches(step_fn):
+    """Kernel launches of one step, counted with the CUDA profiler (untimed)."""
+    try:
+        import torch
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step_fn()
+            torch.cuda.synchronize()
+        n = 0
+        for e in prof.events():
+            if getattr(e, "device_type", None) is not None and "CUDA" in str(e.device_type):
+                nm = e.name
+                if "memset" in nm.lower() or "memcpy" in nm.lower():
+                    continue
+                n += 1
+        return n
+    except Exception:  # profiler unavailable: no claim
+        return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1805_11254_b200 as og
+    from paper_1805_11254_b200 import dist as odist
+    from workloads import text_like
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    og.build()
+    og.lib()
+
+    w = text_like(shard=rank)
+    p = w.params
+    V, seed = w.vocab_size, p["perm_seed"]
+    N, Q = w.n_sets, w.n_queries
+    N_total = N * world
+    base = rank * N
+    k, kp, hkp, mwk = p["k"], p["kprime"], p["hoph_kprime"], p["mw_k"]
+    flat = og.flat_layout(V, k, kp)
+    hier = og.oph_hier_layout_make(V, p["a"], p["b"], hkp)
+    L = hier.L
+    prm = og.params(p["t_num"], p["t_den"], p["eps"])
+    stream = torch.cuda.current_stream()
+
+    # resident inputs
+    sets = og.SetCollection.from_numpy(w.offsets, w.ids)
+    qsets = og.SetCollection.from_numpy(w.q_offsets, w.q_ids)
+    so, sh = og.oph_build_sketches(sets, V, seed, flat=flat, hier=hier)
+    mw = og.minwise_build_sketches(sets, V, seed, mwk)
+    qo, qh = og.oph_build_sketches(qsets, V, seed, flat=flat, hier=hier)
+    qmw = og.minwise_build_sketches(qsets, V, seed, mwk)
+    counts = torch.zeros((4,), dtype=torch.int64, device="cuda")
+    cap = 1 << 22
+    res = []
+    for i in range(4):
+        r = og.Results(cap)
+        r.count = counts[i:i + 1]
+        res.append(r)
+    surv_cap = ((Q + 31) // 32) * 32 * N
+    ws = [og.Workspace() for _ in range(5)]
+    outs = [og.Results(cap * (world if rank == 0 else 1)) for _ in range(4)]
+    merged = [og.Results(cap * world) for _ in range(4)] if world > 1 else None
+
+    names = ["build_oph_hoph", "build_minwise", "query_sketches", "compare_full", "compare_goph", "compare_hoph",
+             "compare_minwise", "select"]
+
+    def step(ev=None, inputs=None):
+        def mark(i):
+            if ev is not None:
+                ev[i].record(stream)
+        mark(0)
+        if inputs is not None:  # e2e: this step's inputs arrive from pinned host memory
+            sets.offsets.copy_(inputs[0], non_blocking=True)
+            sets.ids.copy_(inputs[1], non_blocking=True)
+            qsets.offsets.copy_(inputs[2], non_blocking=True)
+            qsets.ids.copy_(inputs[3], non_blocking=True)
+        og.oph_build_sketches(sets, V, seed, flat=flat, hier=hier, out_oph=so, out_hoph=sh)
+        mark(1)
+        og.minwise_build_sketches(sets, V, seed, mwk, out=mw)
+        mark(2)
+        if rank == 0:
+            og.oph_build_sketches(qsets, V, seed, flat=flat, hier=hier, out_oph=qo, out_hoph=qh)
+            og.minwise_build_sketches(qsets, V, seed, mwk, out=qmw)
+        if world > 1:
+            odist.broadcast_tensors([qo.values, qo.empty, qh.values, qh.empty, qmw.values, qmw.flags])
+        counts.zero_()
+        mark(3)
+        og.compare_full(qo, so, flat, prm, res[0], set_id_base=base, ws=ws[0])
+        mark(4)
+        og.compare_goph(qo, so, flat, prm, res[1], set_id_base=base, ws=ws[1], survivor_capacity=surv_cap)
+        mark(5)
+        og.compare_hoph(qh, sh, hier, prm, res[2], set_id_base=base, ws=ws[2], survivor_capacity=surv_cap)
+        mark(6)
+        og.compare_minwise(qmw, mw, prm, res[3], set_id_base=base, ws=ws[3])
+        mark(7)
+        n4 = [int(x) for x in counts.cpu()]  # one device->host read of the four hit counts
+        assert max(n4) <= cap, f"hit buffer overflow {n4}"
+        total = []
+        for i in range(4):
+            src, n = res[i], n4[i]
+            if world > 1:
+                allh, cnts = odist.gather_hits(res[i].hits, n4[i])
+                n = int(sum(cnts))
+                if rank != 0:
+                    continue
+                merged[i].hits[: allh.numel()].copy_(allh)
+                src = merged[i]
+            if rank == 0:
+                og.topk_or_threshold_results(src, n, og.OPH_SELECT_THRESHOLD, outs[i], ws=ws[4])
+                total.append(n)
+        mark(8)
+        return total
+
+    # warm-up (also JIT-free: the .so is prebuilt)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches = count_launches(step)
+
+    # ---------------- timed region: device inputs resident in HBM
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(9)] for _ in range(K)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    t_start.record(stream)
+    hits_last = None
+    for i in range(K):
+        hits_last = step(evs[i])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end) / K
+    if world > 1:
+        ms = odist.max_over_ranks(ms, device="cuda")
+    phase_ms = {names[j]: statistics.mean(evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(K))
+                for j in range(8)}
+
+    # ---------------- e2e: same step through the C-ABI with HOST (pinned) inputs and result read-back
+    e2e = None
+    if not args.no_e2e:
+        host = [torch.from_numpy(w.offsets.astype(np.int64)).pin_memory(),
+                torch.from_numpy(w.ids.view(np.int32)).pin_memory(),
+                torch.from_numpy(w.q_offsets.astype(np.int64)).pin_memory(),
+                torch.from_numpy(w.q_ids.view(np.int32)).pin_memory()]
+        h2d = sum(t.numel() * t.element_size() for t in host)
+        d2h = 0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(K):
+            tot = step(None, inputs=host)
+            d2h = 4 * 8
+            if rank == 0:
+                for j in range(4):
+                    n = tot[j]
+                    if n:
+                        _ = outs[j].hits[: n * 20].cpu()
+                        d2h += n * 20
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / K
+        if world > 1:
+            ems = odist.max_over_ranks(ems, device="cuda")
+        e2e = {"value": 3 * Q * N_total / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ems}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---------------- roofline of the dominant kernel
+    peaks, peak_src = load_peaks()
+    f_sm = peaks.get("sm_max_mhz", 1965.0) * 1e6
+    issue = 148 * 4 * f_sm                       # warp-instructions / s
+    cmp_peak = issue * 32 / 2                    # bin-compares / s at ISETP + predicated IADD
+    psi_peak = issue * 32 / 17                   # psi evaluations / s at 17 lane-instructions
+    hbm = peaks["hbm_gbs"] * 1e9
+    nnz = int(w.offsets[-1])
+    nw_k, nw_h = (k + 31) // 32, (L * hkp + 31) // 32
+    build_bytes = 4 * nnz + 8 * (N + 1) + 4 * N * (k + L * hkp) + 4 * N * (nw_k + nw_h)
+    g_l0 = og.plan_thresholds(og.OPH_METHOD_GOPH, k // kp, kp, p["t_num"], p["t_den"], p["eps"])[2]
+    kern = {
+        "build_oph_hoph": ("hbm", build_bytes / (phase_ms["build_oph_hoph"] / 1e3) / 1e9, hbm / 1e9, "GB/s",
+                           build_bytes),
+        "build_minwise": ("alu", nnz * mwk / (phase_ms["build_minwise"] / 1e3), psi_peak, "psi-evals/s", None),
+        "compare_full": ("alu", Q * N * k / (phase_ms["compare_full"] / 1e3), cmp_peak, "bin-compares/s", None),
+        "compare_goph": ("alu", Q * N * g_l0 * kp / (phase_ms["compare_goph"] / 1e3), cmp_peak, "bin-compares/s",
+                         None),
+        "compare_hoph": ("alu", Q * N * hkp / (phase_ms["compare_hoph"] / 1e3), cmp_peak, "bin-compares/s", None),
+        "compare_minwise": ("alu", Q * N * mwk / (phase_ms["compare_minwise"] / 1e3), cmp_peak, "bin-compares/s",
+                            None),
+    }
+    traffic = {}
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f)
+    dom = max(kern, key=lambda n: phase_ms[n])
+    b, a_, pk, u, _ = kern[dom]
+    roof = {"kernel": dom, "bound": b, "achieved": a_, "peak": pk, "unit": u, "frac": a_ / pk,
+            "traffic": traffic.get(dom), "peak_source": peak_src,
+            "note": "alu peaks derived from 148 SM x 4 issue/clk x sm_max_mhz (DESIGN.md)"}
+    per_kernel = {n: {"ms": phase_ms[n], "bound": v[0], "achieved": v[1], "peak": v[2], "unit": v[3],
+                      "frac": v[1] / v[2]} for n, v in kern.items()}
+    # the collection scans also against HBM: one pass over the scanned fingerprint bytes
+    scan_bytes = {"compare_full": N * (4 * k + k // 8), "compare_goph": N * (4 * g_l0 * kp + g_l0 * kp // 8),
+                  "compare_hoph": N * (4 * hkp + hkp // 8), "compare_minwise": N * 4 * mwk}
+    for n, by in scan_bytes.items():
+        per_kernel[n]["hbm_gbs_one_pass"] = by / (phase_ms[n] / 1e3) / 1e9
+
+    # ---------------- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        t0 = time.perf_counter()
+        cpu_sample_step(w, CPU_SAMPLE_SETS, CPU_SAMPLE_QUERIES)
+        t = time.perf_counter() - t0
+        cpu = {"value": 3 * CPU_SAMPLE_QUERIES * CPU_SAMPLE_SETS / t, "unit": UNIT, "cores": oracle.num_threads(),
+               "kind": "oracle",
+               "sample": f"text-like: first {CPU_SAMPLE_SETS} sets x first {CPU_SAMPLE_QUERIES} queries, whole path "
+                         f"(sketch builds incl. MinWise, 4 comparisons, threshold lists), {t:.1f} s"}
+
+    line = {
+        "metric": METRIC, "value": 3 * Q * N_total / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "text-like", "sets_per_gpu": N, "sets_total": N_total, "queries": Q, "k": k,
+                   "kprime": kp, "hoph_groups": L, "minwise_k": mwk, "T": f"{p['t_num']}/{p['t_den']}",
+                   "epsilon": p["eps"], "parallelism": f"set-sharded x{world}",
+                   "l2": "inputs larger than L2 (CSR 320 MB + sketches 1.1 GB per step)"},
+        "sketches_per_s": {"oph_hoph": (N_total) / (phase_ms["build_oph_hoph"] / 1e3),
+                           "minwise": (N_total) / (phase_ms["build_minwise"] / 1e3)},
+        "comparisons_per_s": {m: Q * N_total / (phase_ms["compare_" + m] / 1e3)
+                              for m in ("full", "goph", "hoph", "minwise")},
+        "phase_ms": phase_ms,
+        "hits": hits_last,
+        "roofline": roof,
+        "kernels": per_kernel,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches * K if launches is not None else None,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,147 @@
+// Private interface between the host planner / C-ABI (ophgpu_host.cu) and the
+// sm_100a kernels (ophgpu_kernels.cu).  Not installed, not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/ophgpu.h"
+
+namespace ophgpu {
+
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;       // collection-side empty bin ("⊗")
+constexpr uint32_t kQueryEmpty = 0xFFFFFFFEu;  // query-side empty bin: never equals a stored value
+constexpr int kMaxGroups = OPH_MAX_GROUPS;
+
+// psi, keys already derived and masked to w bits.
+struct PsiParams {
+    uint64_t V;         // |V|
+    uint32_t mask;      // 2^w - 1 (w <= 32)
+    uint32_t shift;     // ceil(w / 2)
+    uint32_t kappa[4];
+    uint32_t mu[4];     // odd
+    uint32_t identity;  // psi(x) = x
+    uint32_t pow2;      // |V| == 2^w: no cycle walking
+};
+
+// One range [start, start+len) cut into nb bins by the floor rule.
+struct RangeBins {
+    uint64_t start, len;
+    uint32_t shift;     // log2(len / nb) when len / nb is an exact power of two ...
+    uint32_t pow2;      // ... flagged here (fast path: bin = (p-start) >> shift)
+};
+
+struct BuildArgs {
+    const uint64_t *offsets;
+    const uint32_t *ids;
+    uint64_t n_sets, ld;
+    PsiParams psi;
+    // flat OPH
+    uint32_t do_flat, k;
+    RangeBins flat;
+    uint32_t *oph, *oph_empty;
+    // hierarchical
+    uint32_t do_hier, L, kp;
+    RangeBins grp[kMaxGroups];
+    uint32_t *hoph, *hoph_empty;
+};
+
+struct MinwiseArgs {
+    const uint64_t *offsets;
+    const uint32_t *ids;
+    uint64_t n_sets, ld;
+    uint64_t V, seed;
+    uint32_t k, w;
+    uint32_t *mw;
+    uint8_t *flags;
+};
+
+// Survivor list (structure of arrays), one per level parity.
+struct SurvList {
+    uint32_t *q;      // global query index
+    uint32_t *s;      // local set index
+    uint64_t *state;  // M_c (GOPH) or S_l (HOPH)
+    uint32_t *nmb;    // raw matched bins so far
+};
+
+struct OutArgs {
+    oph_hit *hits;
+    uint64_t cap;
+    unsigned long long *count;
+    uint32_t dense;
+    uint32_t set_id_base;
+    uint64_t n_sets;  // dense row length
+};
+
+enum Method : uint32_t { kFull = 0, kGoph = 1, kHoph = 2, kMinwise = 3 };
+
+struct ScanArgs {
+    const uint32_t *F;      // collection values [nb][ld]
+    const uint32_t *E;      // collection masks [nw][ld] (null for MinWise)
+    const uint8_t *sflags;  // MinWise set flags
+    uint64_t n_sets, ld;
+    const uint32_t *QT;     // prepared queries, bin-major [nb][ldq]
+    const uint32_t *QE;     // query masks [nw][ldq]
+    const uint8_t *qflags;  // MinWise query flags [ldq]
+    uint64_t ldq;
+    uint32_t q_col0;        // first query column of this chunk
+    uint32_t nq;            // queries in this chunk
+    uint32_t method;
+    uint32_t nscan;         // bins scanned (a prefix of the bins)
+    uint32_t nw_load;       // mask words held for the epilogue
+    uint32_t final_;        // the scan ends with the final verdict
+    uint32_t nbins_total;   // k for the final verdict's denominator
+    uint32_t joint, t_num, t_den;
+    uint32_t level;         // groups compared at the end of the scan
+    uint64_t w1;            // state = w1 * raw count (HOPH c_1, else 1)
+    uint64_t acc;           // Similar if state >= acc
+    int64_t rej;            // NotSimilar if state <= rej
+    uint32_t tiles_per_cta;
+    OutArgs out;
+    SurvList surv;
+    unsigned long long *surv_count;
+    uint32_t is_last_level; // unused by the scan (kept for symmetry)
+};
+
+struct LevelArgs {
+    const uint32_t *F, *E;
+    uint64_t n_sets, ld;
+    const uint32_t *QM;     // prepared queries, query-major [n_q][nb]
+    const uint32_t *QEM;    // query masks, query-major [n_q][nw]
+    uint32_t nb, nw;
+    uint32_t method;        // kGoph | kHoph
+    uint32_t level;         // 1-indexed group processed by this launch
+    uint32_t nlev;          // n (GOPH) or L (HOPH)
+    uint32_t kp, joint, t_num, t_den;
+    uint64_t acc;
+    int64_t rej;
+    uint64_t c[kMaxGroups]; // group weights (GOPH: 1)
+    unsigned __int128 lam;  // lcm(1..kp) for the HOPH final verdict
+    SurvList in, out;
+    const unsigned long long *count_in;
+    unsigned long long *count_out;
+    OutArgs res;
+};
+
+struct PrepArgs {
+    const uint32_t *values;  // caller's query sketches [nb][ld_in]
+    const uint32_t *empty;   // [nw][ld_in] or null
+    const uint8_t *flags;    // MinWise [n_q] or null
+    uint64_t ld_in;
+    uint32_t n_q, nb, nw;
+    uint32_t remap;          // OPH methods: empty -> kQueryEmpty
+    uint32_t *QT, *QE, *QM, *QEM;
+    uint8_t *qflags;
+    uint64_t ldq;
+};
+
+// ---- launchers (ophgpu_kernels.cu); all return cudaGetLastError()
+cudaError_t launch_build(const BuildArgs &a, cudaStream_t st);
+cudaError_t launch_minwise(const MinwiseArgs &a, cudaStream_t st);
+cudaError_t launch_prep(const PrepArgs &a, cudaStream_t st);
+cudaError_t launch_scan(const ScanArgs &a, uint32_t B, cudaStream_t st);
+cudaError_t launch_level(const LevelArgs &a, cudaStream_t st);
+size_t select_temp_bytes(uint64_t n);
+cudaError_t run_select(const oph_hit *in, uint64_t n, uint32_t mode, uint32_t topk, uint32_t k_bins, oph_hit *out,
+                       unsigned long long *n_out, void *ws, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace ophgpu

@@ -1,0 +1,715 @@
+// Host side of libophgpu: the C-ABI entry points of include/ophgpu.h, argument
+// validation, the HOPH layout, psi keys, and the planner that compiles the
+// paper's GOPH / HOPH early-termination rules into exact per-level integer
+// thresholds.  No device arithmetic here.
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <random>
+#include <tuple>
+#include <vector>
+
+#include "internal.h"
+
+using namespace ophgpu;
+typedef __int128 i128;
+typedef unsigned __int128 u128;
+
+namespace {
+
+// ---------------------------------------------------------------- small helpers
+uint64_t splitmix64_next(uint64_t &state) {
+    uint64_t z = (state += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+uint32_t word_bits(uint64_t V) {  // max(1, ceil(log2 V))
+    uint32_t w = 0;
+    while (w < 64 && (1ull << w) < V) w++;
+    return w == 0 ? 1 : w;
+}
+
+// psi keys: splitmix64 stream from seed, kappa_r then mu_r
+PsiParams make_psi(uint64_t V, uint64_t seed, uint32_t kind) {
+    PsiParams P{};
+    const uint32_t w = word_bits(V);
+    const uint64_t mask = (w >= 64) ? ~0ull : ((1ull << w) - 1);
+    P.V = V;
+    P.mask = (uint32_t)mask;
+    P.shift = (w + 1) / 2;
+    uint64_t st = seed;
+    for (int r = 0; r < 4; r++) {
+        P.kappa[r] = (uint32_t)(splitmix64_next(st) & mask);
+        P.mu[r] = (uint32_t)((splitmix64_next(st) & mask) | 1ull);
+    }
+    P.identity = kind == OPH_PERM_IDENTITY;
+    P.pow2 = (V == (1ull << w));
+    return P;
+}
+
+RangeBins make_range(uint64_t start, uint64_t len, uint32_t nb) {
+    RangeBins R{};
+    R.start = start;
+    R.len = len;
+    if (len % nb == 0) {
+        const uint64_t bl = len / nb;
+        if ((bl & (bl - 1)) == 0) {
+            R.pow2 = 1;
+            uint32_t sh = 0;
+            while ((1ull << sh) < bl) sh++;
+            R.shift = sh;
+        }
+    }
+    return R;
+}
+
+uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+oph_status cuda_status(cudaError_t e) { return e == cudaSuccess ? OPH_OK : OPH_ECUDA; }
+
+// ---------------------------------------------------------------- binomial tails (Eq. 9-10)
+// X ~ Bin(K, T) (R8).  lower(m) = P(X <= m), upper(m) = P(X >= m) (R9) in long
+// double from log-space terms; "tail <= eps" is certified only when the tail is
+// farther than 1e-9 relative from eps (the computed tails are accurate to
+// ~1e-15 relative), else OPH_EAMBIGUOUS.
+oph_status small_prob_tables(uint32_t K, uint32_t t_num, uint32_t t_den, double eps, std::vector<uint8_t> &lower_le,
+                             std::vector<uint8_t> &upper_le) {
+    std::vector<long double> pmf(K + 1, 0.0L);
+    if (t_num == t_den) {
+        pmf[K] = 1.0L;
+    } else {
+        const long double T = (long double)t_num / (long double)t_den;
+        const long double lT = logl(T), l1T = log1pl(-T);
+        for (uint32_t j = 0; j <= K; j++)
+            pmf[j] = expl(lgammal(K + 1.0L) - lgammal(j + 1.0L) - lgammal(K - j + 1.0L) + j * lT + (K - j) * l1T);
+    }
+    const long double e = eps;
+    auto decide = [&](long double tail, uint8_t &out) -> bool {
+        if (fabsl(tail - e) <= 1e-9L * e) return false;
+        out = tail <= e;
+        return true;
+    };
+    lower_le.assign(K + 1, 0);
+    upper_le.assign(K + 2, 0);
+    long double acc = 0.0L;
+    for (uint32_t m = 0; m <= K; m++) {
+        acc += pmf[m];
+        if (!decide(acc, lower_le[m])) return OPH_EAMBIGUOUS;
+    }
+    acc = 0.0L;
+    for (int64_t m = K + 1; m >= 0; m--) {
+        if (m <= (int64_t)K) acc += pmf[m];
+        if (!decide(acc, upper_le[m])) return OPH_EAMBIGUOUS;
+    }
+    return OPH_OK;
+}
+
+// ---------------------------------------------------------------- the filter rule
+enum Decision { kContinue = 0, kSimilar = 1, kNotSimilar = 2 };
+
+// One small-probability decision on x = num / den (den > 0), x = M_ra (GOPH,
+// Alg. 1 line 11) or x = P_r k' (HOPH, Alg. 2 line 10):
+//   x <= 0 -> Similar; x > k' -> NotSimilar (R16);
+//   x <  k'T and P(X <= floor x) <= eps -> Similar    (Alg. 1 lines 13-19, R11, R12)
+//   x >= k'T and P(X >= ceil x)  <= eps -> NotSimilar (Alg. 1 lines 20-26)
+struct Rule {
+    uint32_t kp, t_num, t_den;
+    const std::vector<uint8_t> *lower_le, *upper_le;
+    Decision operator()(i128 num, i128 den) const {
+        if (num <= 0) return kSimilar;
+        if (num > (i128)kp * den) return kNotSimilar;
+        if (num * (i128)t_den < (i128)kp * t_num * den) {
+            const i128 m = num / den;
+            return (*lower_le)[(size_t)m] ? kSimilar : kContinue;
+        }
+        const i128 m = (num + den - 1) / den;
+        return (*upper_le)[(size_t)m] ? kNotSimilar : kContinue;
+    }
+};
+
+struct LevelThr {
+    uint64_t acc;  // Similar iff state >= acc (UINT64_MAX: never)
+    int64_t rej;   // NotSimilar iff state <= rej (-1: never)
+};
+
+// Compile one level: decide(state) is, by construction, Similar on an upward
+// closed set of states and NotSimilar on a downward closed one (x is
+// decreasing in the state, the lower tail increasing and the upper tail
+// decreasing in x).  Binary search both boundaries, then verify.
+template <class F>
+bool compile_level(F decide, uint64_t smax, bool exhaustive, LevelThr &out) {
+    out.acc = UINT64_MAX;
+    out.rej = -1;
+    if (decide(smax) == kSimilar) {
+        uint64_t lo = 0, hi = smax;
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if (decide(mid) == kSimilar) hi = mid; else lo = mid + 1;
+        }
+        out.acc = lo;
+    }
+    if (decide(0) == kNotSimilar) {
+        uint64_t lo = 0, hi = smax;
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo + 1) / 2;
+            if (decide(mid) == kNotSimilar) lo = mid; else hi = mid - 1;
+        }
+        out.rej = (int64_t)lo;
+    }
+    auto check = [&](uint64_t s) {
+        const Decision want = decide(s);
+        const Decision got = s >= out.acc ? kSimilar : ((int64_t)s <= out.rej ? kNotSimilar : kContinue);
+        return want == got;
+    };
+    if (exhaustive) {
+        for (uint64_t s = 0; s <= smax; s++)
+            if (!check(s)) return false;
+        return true;
+    }
+    std::mt19937_64 rng(12345);
+    for (uint64_t s = 0; s <= std::min<uint64_t>(smax, 2048); s++)
+        if (!check(s)) return false;
+    for (int d = -3; d <= 3; d++) {
+        if (out.acc != UINT64_MAX && (int64_t)out.acc + d >= 0 && out.acc + d <= smax && !check(out.acc + d)) return false;
+        if (out.rej >= 0 && out.rej + d >= 0 && (uint64_t)(out.rej + d) <= smax && !check(out.rej + d)) return false;
+    }
+    for (int i = 0; i < 4096; i++)
+        if (!check(rng() % (smax + 1))) return false;
+    return check(smax);
+}
+
+struct Plan {
+    oph_status st = OPH_OK;
+    uint32_t nlev = 0;          // n or L
+    uint32_t l0 = 0;            // level the scan ends at
+    std::vector<LevelThr> thr;  // thr[l-1] for l = 1..nlev-1
+    std::vector<uint64_t> c;    // weights (GOPH: 1)
+    u128 lam = 1;               // lcm(1..kp)
+};
+
+std::mutex g_plan_mu;
+std::map<std::tuple<uint32_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t, double>, Plan> g_plans;
+
+u128 lcm_upto(uint32_t kp, bool &overflow) {
+    u128 l = 1;
+    overflow = false;
+    for (uint32_t d = 2; d <= kp; d++) {
+        u128 a = l, b = d;
+        while (b) { u128 t = a % b; a = b; b = t; }
+        const u128 mul = d / (uint32_t)a;
+        if (l > (((u128)1) << 120) / mul) { overflow = true; return 0; }
+        l *= mul;
+    }
+    return l;
+}
+
+// GOPH (method 1: nlev = n) or HOPH (method 2: nlev = L, ratio a:b)
+Plan make_plan(uint32_t method, uint32_t nlev, uint32_t kp, uint32_t a, uint32_t b, uint32_t t_num, uint32_t t_den,
+               double eps) {
+    const auto key = std::make_tuple(method, nlev, kp, a, b, t_num, t_den, eps);
+    {
+        std::lock_guard<std::mutex> g(g_plan_mu);
+        auto it = g_plans.find(key);
+        if (it != g_plans.end()) return it->second;
+    }
+    Plan P;
+    P.nlev = nlev;
+    std::vector<uint8_t> lo, up;
+    P.st = small_prob_tables(kp, t_num, t_den, eps, lo, up);
+    if (P.st != OPH_OK) return P;
+    const Rule rule{kp, t_num, t_den, &lo, &up};
+    P.c.assign(nlev, 1);
+    i128 D = 1;
+    if (method == OPH_METHOD_HOPH) {
+        // nominal weights w_j = r(1-r)^(j-1), w_L = (1-r)^(L-1), r = a/(a+b) (R21),
+        // as integers c_j = w_j D over D = (a+b)^(L-1)
+        const i128 ab = (i128)a + b;
+        for (uint32_t j = 1; j < nlev; j++) {
+            D *= ab;
+            if (D > ((i128)1 << 62)) { P.st = OPH_EINVAL; return P; }
+        }
+        for (uint32_t j = 1; j <= nlev; j++) {
+            i128 w = 1;
+            if (j < nlev) {
+                w = a;
+                for (uint32_t t = 1; t < j; t++) w *= b;
+                for (uint32_t t = j; t + 1 < nlev; t++) w *= ab;
+            } else {
+                for (uint32_t t = 1; t < nlev; t++) w *= b;
+            }
+            P.c[j - 1] = (uint64_t)w;
+        }
+        if ((i128)t_num * D * kp >= ((i128)1 << 62)) { P.st = OPH_EINVAL; return P; }
+        // the final verdict compares sums over the common denominator lcm(1..k');
+        // lam = 0 marks "too large for exact 128-bit arithmetic" (compare_hoph refuses)
+        bool of = false;
+        P.lam = lcm_upto(kp, of);
+        if (of || (u128)t_den * P.lam * (u128)D >= (((u128)1) << 126)) P.lam = 0;
+    }
+    P.thr.assign(nlev > 0 ? nlev - 1 : 0, LevelThr{UINT64_MAX, -1});
+    P.l0 = nlev;
+    i128 csum = 0;
+    for (uint32_t l = 1; l < nlev; l++) {
+        csum += P.c[l - 1];
+        const uint64_t smax = (uint64_t)(csum * kp);
+        LevelThr T;
+        bool ok;
+        if (method == OPH_METHOD_GOPH) {
+            // M_ra = (n k' T - M_c) / (n - l) with T = t_num / t_den   (Alg. 1 line 11, R10)
+            auto dec = [&](uint64_t Mc) {
+                return rule((i128)nlev * kp * t_num - (i128)Mc * t_den, (i128)t_den * (nlev - l));
+            };
+            ok = compile_level(dec, smax, true, T);
+        } else {
+            // x = P_r k' = (T D k' - S_l) / W_l, W_l = D - sum_{j<=l} c_j   (Alg. 2 line 10, R19)
+            const i128 W = D - csum;
+            auto dec = [&](uint64_t S) { return rule((i128)t_num * D * kp - (i128)t_den * S, (i128)t_den * W); };
+            ok = compile_level(dec, smax, smax <= (1u << 20), T);
+        }
+        if (!ok) { P.st = OPH_EINVAL; return P; }
+        P.thr[l - 1] = T;
+        if (P.l0 == nlev && (T.acc <= smax || T.rej >= 0)) P.l0 = l;
+    }
+    if (method == OPH_METHOD_HOPH && nlev > 1) P.l0 = 1;  // HOPH: the scan always covers group 1
+    std::lock_guard<std::mutex> g(g_plan_mu);
+    g_plans[key] = P;
+    return P;
+}
+
+// ---------------------------------------------------------------- validation
+oph_status check_sets(const oph_sets *s) {
+    if (!s || (s->n_sets && (!s->d_offsets || !s->d_ids)) || s->n_sets >= (1ull << 32)) return OPH_EINVAL;
+    return OPH_OK;
+}
+
+oph_status check_view(const oph_sketches *v, bool need_empty, bool need_flags) {
+    if (!v || !v->d_values || v->ld < v->n_sets || v->ld % 4 || v->n_bins == 0) return OPH_EINVAL;
+    if (v->n_sets >= 0xFFFFFFFEull) return OPH_EINVAL;
+    if (need_empty && !v->d_empty) return OPH_EINVAL;
+    if (need_flags && !v->d_flags) return OPH_EINVAL;
+    return OPH_OK;
+}
+
+oph_status check_params(const oph_params *p) {
+    if (!p || p->t_den == 0 || p->t_num == 0 || p->t_num > p->t_den || !(p->epsilon > 0.0) || !(p->epsilon < 1.0) ||
+        p->empty_mode > 1)
+        return OPH_EINVAL;
+    return OPH_OK;
+}
+
+// max bin length of a range must leave two spare uint32 values for the sentinels
+bool bins_fit(uint64_t len, uint32_t nb) { return ceil_div(len, nb) <= 0xFFFFFFFEull; }
+
+// ---------------------------------------------------------------- compare workspace
+struct Ws {
+    uint32_t *QT, *QE, *QM, *QEM;
+    uint8_t *qflags;
+    unsigned long long *counters;  // [2][kMaxGroups + 2]
+    SurvList list[2];
+    uint64_t ldq, cap;
+};
+
+size_t ws_fixed_bytes(uint64_t n_q, uint32_t nb) {
+    const uint64_t ldq = ceil_div(n_q ? n_q : 1, 32) * 32;
+    const uint64_t nw = ceil_div(nb, 32);
+    return align256(nb * ldq * 4) + align256(nw * ldq * 4) + align256(n_q * (uint64_t)nb * 4) +
+           align256(n_q * nw * 4) + align256(ldq) + align256(2 * (kMaxGroups + 2) * 8);
+}
+
+constexpr uint64_t kSurvBytes = 2 * (4 + 4 + 8 + 4);  // two lists, per entry
+
+Ws carve_ws(void *base, uint64_t n_q, uint32_t nb, uint64_t cap) {
+    Ws w{};
+    char *p = (char *)base;
+    w.ldq = ceil_div(n_q ? n_q : 1, 32) * 32;
+    const uint64_t nw = ceil_div(nb, 32);
+    w.QT = (uint32_t *)p; p += align256(nb * w.ldq * 4);
+    w.QE = (uint32_t *)p; p += align256(nw * w.ldq * 4);
+    w.QM = (uint32_t *)p; p += align256(n_q * (uint64_t)nb * 4);
+    w.QEM = (uint32_t *)p; p += align256(n_q * nw * 4);
+    w.qflags = (uint8_t *)p; p += align256(w.ldq);
+    w.counters = (unsigned long long *)p; p += align256(2 * (kMaxGroups + 2) * 8);
+    w.cap = cap;
+    for (int i = 0; i < 2; i++) {
+        w.list[i].q = (uint32_t *)p; p += align256(cap * 4);
+        w.list[i].s = (uint32_t *)p; p += align256(cap * 4);
+        w.list[i].state = (uint64_t *)p; p += align256(cap * 8);
+        w.list[i].nmb = (uint32_t *)p; p += align256(cap * 4);
+    }
+    return w;
+}
+
+size_t surv_region_bytes(uint64_t cap) { return 2 * (align256(cap * 4) * 3 + align256(cap * 8)); }
+
+// largest survivor capacity that fits in ws_bytes
+uint64_t cap_from_ws(size_t ws_bytes, size_t fixed) {
+    if (ws_bytes <= fixed) return 0;
+    uint64_t cap = (ws_bytes - fixed) / kSurvBytes;
+    while (cap > 0 && fixed + surv_region_bytes(cap) > ws_bytes) cap -= std::max<uint64_t>(1, cap / 1024);
+    return cap;
+}
+
+// ---------------------------------------------------------------- the compare driver
+oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketches *Sv, uint32_t set_id_base,
+                       uint32_t k_or_L, uint32_t kp, uint32_t a, uint32_t b, const oph_params *p, oph_results *res,
+                       void *d_ws, size_t ws_bytes, cudaStream_t stream) {
+    const bool mw = method == OPH_METHOD_MINWISE;
+    oph_status st;
+    if ((st = check_view(Qv, !mw, mw)) || (st = check_view(Sv, !mw, mw)) || (st = check_params(p))) return st;
+    if (!res || !res->d_hits || !res->d_count || res->mode > OPH_RES_DENSE) return OPH_EINVAL;
+    if (Qv->seed != Sv->seed || Qv->vocab_size != Sv->vocab_size || Qv->n_bins != Sv->n_bins) return OPH_EINCOMPAT;
+    const uint32_t nb = Qv->n_bins;
+    const uint32_t nw = (uint32_t)ceil_div(nb, 32);
+    if (nb > 16384) return OPH_EINVAL;
+    if ((uint64_t)set_id_base + Sv->n_sets > 0xFFFFFFFFull) return OPH_EINVAL;
+    const uint64_t n_q = Qv->n_sets, n_s = Sv->n_sets;
+    if (res->mode == OPH_RES_DENSE && res->capacity < n_q * n_s) return OPH_EINVAL;
+    if (n_q == 0 || n_s == 0) return OPH_OK;
+
+    Plan plan;
+    uint32_t nlev = 1;
+    if (method == OPH_METHOD_GOPH || method == OPH_METHOD_HOPH) {
+        nlev = method == OPH_METHOD_GOPH ? k_or_L / kp : k_or_L;
+        if (nlev > kMaxGroups) return OPH_EINVAL;
+        plan = make_plan(method, nlev, kp, a, b, p->t_num, p->t_den, p->epsilon);
+        if (plan.st != OPH_OK) return plan.st;
+        if (method == OPH_METHOD_HOPH && nlev > 1 && plan.lam == 0) return OPH_EINVAL;
+    }
+
+    const size_t fixed = ws_fixed_bytes(n_q, nb);
+    uint64_t chunk = ceil_div(n_q, 32) * 32;
+    uint64_t cap = 0;
+    const bool levels = (method == OPH_METHOD_GOPH || method == OPH_METHOD_HOPH) && plan.l0 < nlev;
+    if (levels) {
+        cap = cap_from_ws(ws_bytes, fixed);
+        const uint64_t fit = (cap / n_s) / 32 * 32;
+        if (fit < 32) return OPH_ENOMEM;
+        chunk = std::min(chunk, fit);
+    } else if (ws_bytes < fixed) {
+        return OPH_ENOMEM;
+    }
+    Ws w = carve_ws(d_ws, n_q, nb, cap);
+
+    PrepArgs pa{};
+    pa.values = Qv->d_values;
+    pa.empty = mw ? nullptr : Qv->d_empty;
+    pa.flags = mw ? Qv->d_flags : nullptr;
+    pa.ld_in = Qv->ld;
+    pa.n_q = (uint32_t)n_q;
+    pa.nb = nb;
+    pa.nw = nw;
+    pa.remap = !mw;
+    pa.QT = w.QT;
+    pa.QE = w.QE;
+    pa.QM = w.QM;
+    pa.QEM = w.QEM;
+    pa.qflags = w.qflags;
+    pa.ldq = w.ldq;
+    cudaError_t e = launch_prep(pa, stream);
+    if (e != cudaSuccess) return OPH_ECUDA;
+
+    OutArgs out{};
+    out.hits = res->d_hits;
+    out.cap = res->capacity;
+    out.count = res->d_count;
+    out.dense = res->mode == OPH_RES_DENSE;
+    out.set_id_base = set_id_base;
+    out.n_sets = n_s;
+
+    ScanArgs s{};
+    s.F = Sv->d_values;
+    s.E = mw ? nullptr : Sv->d_empty;
+    s.sflags = mw ? Sv->d_flags : nullptr;
+    s.n_sets = n_s;
+    s.ld = Sv->ld;
+    s.QT = w.QT;
+    s.QE = w.QE;
+    s.qflags = w.qflags;
+    s.ldq = w.ldq;
+    s.method = method;
+    s.joint = p->empty_mode == OPH_EMPTY_JOINT;
+    s.t_num = p->t_num;
+    s.t_den = p->t_den;
+    s.out = out;
+    s.w1 = 1;
+    s.acc = UINT64_MAX;
+    s.rej = -1;
+    s.nbins_total = nb;
+    if (method == OPH_METHOD_FULL || mw) {
+        s.nscan = nb;
+        s.final_ = 1;
+        s.level = mw ? 0 : nb / kp;
+        s.nw_load = mw ? 0 : nw;
+    } else if (method == OPH_METHOD_GOPH) {
+        s.nscan = plan.l0 * kp;
+        s.level = plan.l0;
+        s.final_ = plan.l0 == nlev;
+        s.nw_load = (uint32_t)(s.final_ ? nw : ceil_div(s.nscan, 32));
+        if (!s.final_) {
+            s.acc = plan.thr[plan.l0 - 1].acc;
+            s.rej = plan.thr[plan.l0 - 1].rej;
+        }
+    } else {  // HOPH: the scan compares group 1
+        s.nscan = kp;
+        s.level = 1;
+        s.final_ = nlev == 1;  // one group: the HOPH estimator is the OPH estimator of it
+        s.nw_load = (uint32_t)ceil_div(kp, 32);
+        if (!s.final_) {
+            s.w1 = plan.c[0];
+            s.acc = plan.thr[0].acc;
+            s.rej = plan.thr[0].rej;
+        }
+    }
+    if (((size_t)std::min<uint32_t>(s.nscan, 512) + s.nw_load + 1) * 32 * 4 > 227 * 1024) return OPH_EINVAL;
+
+    LevelArgs la{};
+    if (levels) {
+        la.F = Sv->d_values;
+        la.E = Sv->d_empty;
+        la.n_sets = n_s;
+        la.ld = Sv->ld;
+        la.QM = w.QM;
+        la.QEM = w.QEM;
+        la.nb = nb;
+        la.nw = nw;
+        la.method = method;
+        la.nlev = nlev;
+        la.kp = kp;
+        la.joint = s.joint;
+        la.t_num = p->t_num;
+        la.t_den = p->t_den;
+        for (uint32_t j = 0; j < nlev; j++) la.c[j] = plan.c[j];
+        la.lam = plan.lam;
+        la.res = out;
+    }
+
+    for (uint64_t q0 = 0; q0 < n_q; q0 += chunk) {
+        const uint64_t nq = std::min<uint64_t>(chunk, n_q - q0);
+        s.q_col0 = (uint32_t)q0;
+        s.nq = (uint32_t)nq;
+        if (levels) {
+            e = cudaMemsetAsync(w.counters, 0, (kMaxGroups + 2) * 8, stream);
+            if (e != cudaSuccess) return OPH_ECUDA;
+            s.surv = w.list[plan.l0 % 2];
+            s.surv_count = w.counters + plan.l0;
+        }
+        e = launch_scan(s, 32, stream);
+        if (e != cudaSuccess) return OPH_ECUDA;
+        if (!levels) continue;
+        for (uint32_t l = plan.l0 + 1; l <= nlev; l++) {
+            la.level = l;
+            if (l < nlev) {
+                la.acc = plan.thr[l - 1].acc;
+                la.rej = plan.thr[l - 1].rej;
+            }
+            la.in = w.list[(l - 1) % 2];
+            la.out = w.list[l % 2];
+            la.count_in = w.counters + (l - 1);
+            la.count_out = w.counters + l;
+            e = launch_level(la, stream);
+            if (e != cudaSuccess) return OPH_ECUDA;
+        }
+    }
+    return OPH_OK;
+}
+
+}  // namespace
+
+// ======================================================================== C-ABI
+extern "C" {
+
+const char *oph_status_string(oph_status s) {
+    switch (s) {
+        case OPH_OK: return "ok";
+        case OPH_EINVAL: return "invalid argument";
+        case OPH_EINCOMPAT: return "incompatible sketches (seed, universe or layout differ)";
+        case OPH_EOVERFLOW: return "result buffer overflow";
+        case OPH_ECUDA: return "CUDA error";
+        case OPH_EAMBIGUOUS: return "a binomial tail is within 1e-9 relative of epsilon";
+        case OPH_ENOMEM: return "workspace too small";
+    }
+    return "unknown status";
+}
+
+uint64_t oph_sketch_ld(uint64_t n_sets) { return ceil_div(n_sets ? n_sets : 1, 32) * 32; }
+
+oph_status oph_hier_layout_make(uint64_t V, uint32_t a, uint32_t b, uint32_t kp, oph_hier_layout *out) {
+    if (!out || a == 0 || b == 0 || kp == 0 || kp > 65535 || V == 0 || V > (1ull << 32) || V < 2ull * kp)
+        return OPH_EINVAL;
+    std::memset(out, 0, sizeof(*out));
+    out->vocab_size = V;
+    out->a = a;
+    out->b = b;
+    out->kprime = kp;
+    // recursive a:b split of the remaining space (R17, R18)
+    uint64_t R = V, s = 0;
+    uint32_t L = 0;
+    for (;;) {
+        if (L >= OPH_MAX_GROUPS) return OPH_EINVAL;
+        const uint64_t f = (uint64_t)(((u128)a * R) / (a + b));
+        const uint64_t r = R - f;
+        if (f <= kp || r <= kp) {
+            out->start[L] = s;
+            out->len[L] = R;
+            L++;
+            break;
+        }
+        out->start[L] = s;
+        out->len[L] = f;
+        L++;
+        s += f;
+        R = r;
+    }
+    out->L = L;
+    return OPH_OK;
+}
+
+oph_status oph_build_sketches(const oph_sets *sets, const oph_perm *perm, const oph_flat_layout *flat, uint32_t *d_oph,
+                              uint32_t *d_oph_empty, const oph_hier_layout *hier, uint32_t *d_hoph,
+                              uint32_t *d_hoph_empty, uint64_t ld, void *stream) {
+    oph_status st;
+    if ((st = check_sets(sets))) return st;
+    if (!perm || perm->vocab_size == 0 || perm->vocab_size > (1ull << 32) || perm->kind > 1) return OPH_EINVAL;
+    if (!flat && !hier) return OPH_EINVAL;
+    if (ld < sets->n_sets || ld % 4) return OPH_EINVAL;
+    const uint64_t V = perm->vocab_size;
+    BuildArgs a{};
+    a.offsets = sets->d_offsets;
+    a.ids = sets->d_ids;
+    a.n_sets = sets->n_sets;
+    a.ld = ld;
+    a.psi = make_psi(V, perm->seed, perm->kind);
+    uint64_t per_set = 0;
+    if (flat) {
+        if (flat->vocab_size != V || flat->k == 0 || flat->k > 65535 || flat->k > V || !bins_fit(V, flat->k) ||
+            !d_oph || !d_oph_empty)
+            return OPH_EINVAL;
+        a.do_flat = 1;
+        a.k = flat->k;
+        a.flat = make_range(0, V, flat->k);
+        a.oph = d_oph;
+        a.oph_empty = d_oph_empty;
+        per_set += flat->k + 1;
+    }
+    if (hier) {
+        if (hier->vocab_size != V || hier->L == 0 || hier->L > OPH_MAX_GROUPS || hier->kprime == 0 || !d_hoph ||
+            !d_hoph_empty)
+            return OPH_EINVAL;
+        uint64_t s = 0;
+        for (uint32_t g = 0; g < hier->L; g++) {  // contiguous cover of [0, V)
+            if (hier->start[g] != s || hier->len[g] < hier->kprime || !bins_fit(hier->len[g], hier->kprime))
+                return OPH_EINVAL;
+            s += hier->len[g];
+        }
+        if (s != V) return OPH_EINVAL;
+        a.do_hier = 1;
+        a.L = hier->L;
+        a.kp = hier->kprime;
+        for (uint32_t g = 0; g < hier->L; g++) a.grp[g] = make_range(hier->start[g], hier->len[g], hier->kprime);
+        a.hoph = d_hoph;
+        a.hoph_empty = d_hoph_empty;
+        per_set += (uint64_t)hier->L * hier->kprime + 1;
+    }
+    if (per_set * 4 + 16 > 200 * 1024) return OPH_EINVAL;
+    return cuda_status(launch_build(a, (cudaStream_t)stream));
+}
+
+oph_status minwise_build_sketches(const oph_sets *sets, uint64_t V, uint64_t seed, uint32_t k, uint32_t *d_mw,
+                                  uint8_t *d_set_flags, uint64_t ld, void *stream) {
+    oph_status st;
+    if ((st = check_sets(sets))) return st;
+    if (V == 0 || V > (1ull << 32) || k == 0 || k > 65535 || !d_mw || !d_set_flags || ld < sets->n_sets || ld % 4)
+        return OPH_EINVAL;
+    MinwiseArgs a{};
+    a.offsets = sets->d_offsets;
+    a.ids = sets->d_ids;
+    a.n_sets = sets->n_sets;
+    a.ld = ld;
+    a.V = V;
+    a.seed = seed;
+    a.k = k;
+    a.w = word_bits(V);
+    a.mw = d_mw;
+    a.flags = d_set_flags;
+    return cuda_status(launch_minwise(a, (cudaStream_t)stream));
+}
+
+oph_status oph_workspace_size(uint32_t method, uint64_t n_q, uint64_t n_sets, uint32_t n_bins, uint64_t cap,
+                              size_t *bytes) {
+    if (!bytes || method > OPH_METHOD_MINWISE || n_bins == 0) return OPH_EINVAL;
+    size_t b = ws_fixed_bytes(n_q, n_bins);
+    if (method == OPH_METHOD_GOPH || method == OPH_METHOD_HOPH) b += surv_region_bytes(std::max<uint64_t>(cap, 32 * n_sets));
+    *bytes = b;
+    return OPH_OK;
+}
+
+oph_status compare_full(const oph_sketches *q, const oph_sketches *s, uint32_t set_id_base,
+                        const oph_flat_layout *layout, const oph_params *p, oph_results *res, void *d_ws,
+                        size_t ws_bytes, void *stream) {
+    if (!layout || layout->kprime == 0 || layout->k % layout->kprime || !q) return OPH_EINVAL;
+    if (q->n_bins != layout->k || q->vocab_size != layout->vocab_size) return OPH_EINCOMPAT;
+    return run_compare(OPH_METHOD_FULL, q, s, set_id_base, layout->k, layout->kprime, 1, 1, p, res, d_ws, ws_bytes,
+                       (cudaStream_t)stream);
+}
+
+oph_status compare_goph(const oph_sketches *q, const oph_sketches *s, uint32_t set_id_base,
+                        const oph_flat_layout *layout, const oph_params *p, oph_results *res, void *d_ws,
+                        size_t ws_bytes, void *stream) {
+    if (!layout || layout->kprime == 0 || layout->k % layout->kprime || !q) return OPH_EINVAL;
+    if (q->n_bins != layout->k || q->vocab_size != layout->vocab_size) return OPH_EINCOMPAT;
+    return run_compare(OPH_METHOD_GOPH, q, s, set_id_base, layout->k, layout->kprime, 1, 1, p, res, d_ws, ws_bytes,
+                       (cudaStream_t)stream);
+}
+
+oph_status compare_hoph(const oph_sketches *q, const oph_sketches *s, uint32_t set_id_base,
+                        const oph_hier_layout *layout, const oph_params *p, oph_results *res, void *d_ws,
+                        size_t ws_bytes, void *stream) {
+    if (!layout || layout->L == 0 || layout->L > OPH_MAX_GROUPS || layout->kprime == 0 || !q) return OPH_EINVAL;
+    if (q->n_bins != layout->L * layout->kprime || q->vocab_size != layout->vocab_size) return OPH_EINCOMPAT;
+    return run_compare(OPH_METHOD_HOPH, q, s, set_id_base, layout->L, layout->kprime, layout->a, layout->b, p, res,
+                       d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+oph_status compare_minwise(const oph_sketches *q, const oph_sketches *s, uint32_t set_id_base, const oph_params *p,
+                           oph_results *res, void *d_ws, size_t ws_bytes, void *stream) {
+    if (!q) return OPH_EINVAL;
+    return run_compare(OPH_METHOD_MINWISE, q, s, set_id_base, q->n_bins, 1, 1, 1, p, res, d_ws, ws_bytes,
+                       (cudaStream_t)stream);
+}
+
+oph_status oph_select_workspace_size(uint64_t n_in, size_t *bytes) {
+    if (!bytes || n_in >= (1ull << 31)) return OPH_EINVAL;
+    *bytes = select_temp_bytes(n_in);
+    return OPH_OK;
+}
+
+oph_status topk_or_threshold_results(const oph_hit *d_in, uint64_t n_in, uint32_t mode, uint32_t topk,
+                                     uint32_t k_bins, oph_hit *d_out, unsigned long long *d_n_out, void *d_ws,
+                                     size_t ws_bytes, void *stream) {
+    if ((n_in && (!d_in || !d_out)) || !d_n_out || mode > OPH_SELECT_TOPK || n_in >= (1ull << 31)) return OPH_EINVAL;
+    if (mode == OPH_SELECT_TOPK && (k_bins == 0 || k_bins > 32768)) return OPH_EINVAL;
+    if (ws_bytes < select_temp_bytes(n_in)) return OPH_ENOMEM;
+    return cuda_status(run_select(d_in, n_in, mode, topk, k_bins, d_out, d_n_out, d_ws, ws_bytes, (cudaStream_t)stream));
+}
+
+// planner introspection for tests: per-level thresholds (acc, rej) and l0
+oph_status oph_plan_thresholds(uint32_t method, uint32_t nlev, uint32_t kp, uint32_t a, uint32_t b, uint32_t t_num,
+                               uint32_t t_den, double eps, uint64_t *acc, int64_t *rej, uint32_t *l0, uint64_t *weights) {
+    if (method != OPH_METHOD_GOPH && method != OPH_METHOD_HOPH) return OPH_EINVAL;
+    if (nlev == 0 || nlev > OPH_MAX_GROUPS || kp == 0 || t_den == 0 || t_num == 0 || t_num > t_den) return OPH_EINVAL;
+    Plan P = make_plan(method, nlev, kp, a, b, t_num, t_den, eps);
+    if (P.st != OPH_OK) return P.st;
+    for (uint32_t l = 1; l < nlev; l++) {
+        acc[l - 1] = P.thr[l - 1].acc;
+        rej[l - 1] = P.thr[l - 1].rej;
+    }
+    for (uint32_t j = 0; j < nlev; j++) weights[j] = P.c[j];
+    *l0 = P.l0;
+    return OPH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,846 @@
+// sm_100a kernels of the OPH / GOPH / HOPH scoring path (arxiv 1805.11254).
+//
+//   K1 build_kernel     OPH + HOPH sketches from one psi evaluation per element
+//                                             SURVEY 8(a) a1-a3
+//   K2 minwise_kernel   MinWise sketches, k keyed permutations        a4
+//   -- prep_kernel      query preparation: empty remap + both layouts        a5
+//   K3 scan_kernel      streaming compare of a register-resident query block
+//                       against set tiles; full OPH / MinWise / the first
+//                       decidable GOPH level / HOPH level 1               a6-a9
+//   K4 level_kernel     one GOPH/HOPH level over the compacted survivors;
+//                       the last level applies the final verdict            a7-a8
+//   K6 run_select       threshold / top-k result lists (CUB radix sort)     a10
+//
+// All decisions are exact integer arithmetic against thresholds the host
+// planner compiled from the paper's rules (R23); no floating
+// point decides anything.  Layouts: DESIGN.md "Data layout in HBM".
+#include <cub/cub.cuh>
+
+#include "internal.h"
+
+namespace ophgpu {
+
+// ---------------------------------------------------------------------------
+// psi: keyed 4-round bijection of [0, 2^w), cycle-walked into [0, |V|)
+// (DESIGN.md section 4).  W32: w == 32, the mask is a no-op.
+// ---------------------------------------------------------------------------
+template <bool W32>
+__device__ __forceinline__ uint32_t psi_pass(const uint32_t (&kappa)[4], const uint32_t (&mu)[4], uint32_t mask,
+                                             uint32_t shift, uint32_t x) {
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        x = (x ^ kappa[r]) * mu[r];
+        if (!W32) x &= mask;
+        x ^= x >> shift;
+    }
+    return x;
+}
+
+template <bool W32>
+__device__ __forceinline__ uint32_t psi(const PsiParams &P, uint32_t x) {
+    if (P.identity) return x;
+    x = psi_pass<W32>(P.kappa, P.mu, P.mask, P.shift, x);
+    if (!P.pow2)
+        while ((uint64_t)x >= P.V) x = psi_pass<W32>(P.kappa, P.mu, P.mask, P.shift, x);
+    return x;
+}
+
+// bin and within-bin offset of p in a range cut into nb bins by the floor
+// rule: the largest b with floor(b len / nb) <= p - start is
+// floor(((p - start + 1) nb - 1) / len).
+__device__ __forceinline__ void range_bin(const RangeBins &R, uint32_t nb, uint64_t p, uint32_t &bin, uint32_t &off) {
+    const uint64_t x = p - R.start;
+    if (R.pow2) {
+        bin = (uint32_t)(x >> R.shift);
+        off = (uint32_t)(x & ((1ull << R.shift) - 1));
+    } else {
+        const uint64_t b = ((x + 1) * nb - 1) / R.len;
+        bin = (uint32_t)b;
+        off = (uint32_t)(x - (b * R.len) / nb);
+    }
+}
+
+__device__ __forceinline__ uint64_t splitmix64_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// ---------------------------------------------------------------------------
+// K1: OPH + HOPH build.  One CTA = SB consecutive sets; their ids are one
+// contiguous CSR range, streamed by all 256 threads.  Per-set sketches live
+// in shared memory (row stride n+1 words: conflict-free column reads) and
+// are minimised with shared atomicMin (EMPTY = 0xFFFFFFFF is the identity of
+// min).  The tile is written out bin-major: SB consecutive words per bin.
+// ---------------------------------------------------------------------------
+template <bool W32>
+__global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ BuildArgs a, uint32_t SB) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t *offs = reinterpret_cast<uint64_t *>(smem_raw);             // [SB+1]
+    uint32_t *so = reinterpret_cast<uint32_t *>(offs + SB + 1);          // [SB][k+1]
+    const uint32_t kst = a.k + 1;
+    const uint32_t nbh = a.L * a.kp;
+    const uint32_t hst = nbh + 1;
+    uint32_t *sh = so + (a.do_flat ? (size_t)SB * kst : 0);              // [SB][L*kp+1]
+
+    const uint64_t s0 = (uint64_t)blockIdx.x * SB;
+    const uint32_t nloc = (uint32_t)min((uint64_t)SB, a.n_sets - s0);
+    for (uint32_t i = threadIdx.x; i <= nloc; i += blockDim.x) offs[i] = a.offsets[s0 + i];
+    if (a.do_flat)
+        for (uint32_t i = threadIdx.x; i < SB * kst; i += blockDim.x) so[i] = kEmpty;
+    if (a.do_hier)
+        for (uint32_t i = threadIdx.x; i < SB * hst; i += blockDim.x) sh[i] = kEmpty;
+    __syncthreads();
+
+    const uint64_t e0 = offs[0], e1 = offs[nloc];
+    for (uint64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const uint32_t id = __ldg(a.ids + e);
+        // owning set: largest j with offs[j] <= e
+        uint32_t lo = 0, hi = nloc - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (offs[mid] <= e) lo = mid; else hi = mid - 1;
+        }
+        const uint32_t p = psi<W32>(a.psi, id);
+        uint32_t bin, off;
+        if (a.do_flat) {
+            range_bin(a.flat, a.k, p, bin, off);
+            atomicMin(&so[lo * kst + bin], off);
+        }
+        if (a.do_hier) {
+            uint32_t g0 = 0, g1 = a.L - 1;  // largest g with start_g <= p
+            while (g0 < g1) {
+                const uint32_t mid = (g0 + g1 + 1) >> 1;
+                if (a.grp[mid].start <= p) g0 = mid; else g1 = mid - 1;
+            }
+            range_bin(a.grp[g0], a.kp, p, bin, off);
+            atomicMin(&sh[lo * hst + g0 * a.kp + bin], off);
+        }
+    }
+    __syncthreads();
+
+    // write-out: values bin-major, then empty masks (bit i of word w <=> bin 32w+i empty)
+    if (a.do_flat) {
+        for (uint32_t i = threadIdx.x; i < a.k * SB; i += blockDim.x) {
+            const uint32_t b = i / SB, j = i % SB;
+            if (j < nloc) a.oph[(uint64_t)b * a.ld + s0 + j] = so[j * kst + b];
+        }
+        const uint32_t nw = (a.k + 31) / 32;
+        for (uint32_t i = threadIdx.x; i < nw * SB; i += blockDim.x) {
+            const uint32_t w = i / SB, j = i % SB;
+            if (j >= nloc) continue;
+            uint32_t m = 0;
+            for (uint32_t t = 0; t < 32 && 32 * w + t < a.k; t++) m |= (uint32_t)(so[j * kst + 32 * w + t] == kEmpty) << t;
+            a.oph_empty[(uint64_t)w * a.ld + s0 + j] = m;
+        }
+    }
+    if (a.do_hier) {
+        for (uint32_t i = threadIdx.x; i < nbh * SB; i += blockDim.x) {
+            const uint32_t b = i / SB, j = i % SB;
+            if (j < nloc) a.hoph[(uint64_t)b * a.ld + s0 + j] = sh[j * hst + b];
+        }
+        const uint32_t nw = (nbh + 31) / 32;
+        for (uint32_t i = threadIdx.x; i < nw * SB; i += blockDim.x) {
+            const uint32_t w = i / SB, j = i % SB;
+            if (j >= nloc) continue;
+            uint32_t m = 0;
+            for (uint32_t t = 0; t < 32 && 32 * w + t < nbh; t++) m |= (uint32_t)(sh[j * hst + 32 * w + t] == kEmpty) << t;
+            a.hoph_empty[(uint64_t)w * a.ld + s0 + j] = m;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: MinWise build.  One CTA = 8 consecutive sets x all k permutations; a
+// thread owns permutation i (keys derived on the fly from the counter-based
+// splitmix64 stream, R30) and keeps 8 running minima in registers; the
+// sets' ids are staged through shared memory in chunks.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kMwSets = 8;
+constexpr uint32_t kMwChunk = 8192;
+
+template <bool W32>
+__global__ void __launch_bounds__(256) minwise_kernel(const __grid_constant__ MinwiseArgs a) {
+    __shared__ uint64_t offs[kMwSets + 1];
+    __shared__ uint32_t ids[kMwChunk];
+    const uint64_t s0 = (uint64_t)blockIdx.x * kMwSets;
+    const uint32_t nloc = (uint32_t)min((uint64_t)kMwSets, a.n_sets - s0);
+    if (threadIdx.x <= nloc) offs[threadIdx.x] = a.offsets[s0 + threadIdx.x];
+    __syncthreads();
+    const uint64_t e0 = offs[0], e1 = offs[nloc];
+    const uint32_t mask = a.w >= 32 ? 0xFFFFFFFFu : ((1u << a.w) - 1);
+    const uint32_t shift = (a.w + 1) / 2;
+    const bool pow2 = a.V == (1ull << a.w);
+    const uint64_t gamma = 0x9E3779B97F4A7C15ull;
+
+    for (uint32_t i0 = 0; i0 < a.k; i0 += blockDim.x) {  // uniform over the CTA
+        const uint32_t i = i0 + threadIdx.x;
+        uint32_t kappa[4], mu[4];
+        {
+            const uint64_t seed_i = splitmix64_mix((a.seed ^ 0x6D696E7769736521ull) + (uint64_t)(i + 1) * gamma);
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                kappa[r] = (uint32_t)splitmix64_mix(seed_i + (uint64_t)(2 * r + 1) * gamma) & mask;
+                mu[r] = ((uint32_t)splitmix64_mix(seed_i + (uint64_t)(2 * r + 2) * gamma) & mask) | 1u;
+            }
+        }
+        uint32_t mn[kMwSets];
+#pragma unroll
+        for (uint32_t j = 0; j < kMwSets; j++) mn[j] = 0xFFFFFFFFu;
+        for (uint64_t c0 = e0; c0 < e1; c0 += kMwChunk) {
+            const uint32_t cn = (uint32_t)min((uint64_t)kMwChunk, e1 - c0);
+            __syncthreads();
+            for (uint32_t t = threadIdx.x; t < cn; t += blockDim.x) ids[t] = __ldg(a.ids + c0 + t);
+            __syncthreads();
+            if (i < a.k) {
+#pragma unroll
+                for (uint32_t j = 0; j < kMwSets; j++) {
+                    if (j >= nloc) break;
+                    const uint64_t lo = max(offs[j], c0), hi = min(offs[j + 1], c0 + cn);
+                    uint32_t m = mn[j];
+                    for (uint64_t e = lo; e < hi; e++) {
+                        uint32_t x = psi_pass<W32>(kappa, mu, mask, shift, ids[e - c0]);
+                        if (!pow2)
+                            while ((uint64_t)x >= a.V) x = psi_pass<W32>(kappa, mu, mask, shift, x);
+                        m = min(m, x);
+                    }
+                    mn[j] = m;
+                }
+            }
+        }
+        if (i < a.k) {
+#pragma unroll
+            for (uint32_t j = 0; j < kMwSets; j++)
+                if (j < nloc) a.mw[(uint64_t)i * a.ld + s0 + j] = (offs[j] == offs[j + 1]) ? kEmpty : mn[j];
+        }
+    }
+    if (threadIdx.x < nloc) a.flags[s0 + threadIdx.x] = (offs[threadIdx.x] == offs[threadIdx.x + 1]) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// query preparation (row a5): remap the query-side empty bin to a value no
+// stored bin holds (so equality alone decides a match, R5), pad to whole
+// query blocks, and emit a bin-major copy (scan) and a query-major copy
+// (survivor levels).
+// ---------------------------------------------------------------------------
+__global__ void prep_kernel(const __grid_constant__ PrepArgs a) {
+    const uint64_t n_elem = (uint64_t)a.nb * a.ldq;
+    for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < n_elem;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = (uint32_t)(idx / a.ldq), q = (uint32_t)(idx % a.ldq);
+        uint32_t v;
+        if (q < a.n_q) {
+            v = a.values[(uint64_t)b * a.ld_in + q];
+            if (a.remap && v == kEmpty) v = kQueryEmpty;
+        } else {
+            v = a.remap ? kQueryEmpty : 0u;
+        }
+        a.QT[idx] = v;
+        if (q < a.n_q) a.QM[(uint64_t)q * a.nb + b] = v;
+    }
+    if (a.empty) {
+        const uint64_t n_w = (uint64_t)a.nw * a.ldq;
+        for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < n_w;
+             idx += (uint64_t)gridDim.x * blockDim.x) {
+            const uint32_t w = (uint32_t)(idx / a.ldq), q = (uint32_t)(idx % a.ldq);
+            const uint32_t m = q < a.n_q ? a.empty[(uint64_t)w * a.ld_in + q] : 0u;
+            a.QE[idx] = m;
+            if (q < a.n_q) a.QEM[(uint64_t)q * a.nw + w] = m;
+        }
+    }
+    if (a.flags)
+        for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < a.ldq;
+             q += (uint64_t)gridDim.x * blockDim.x)
+            a.qflags[q] = q < a.n_q ? a.flags[q] : 1;
+}
+
+// ---------------------------------------------------------------------------
+// emission helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long warp_append(bool pred, unsigned long long *counter) {
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, pred);
+    if (m == 0) return ~0ull;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xFFFFFFFFu, base, leader);
+    return base + __popc(m & ((1u << lane) - 1u));
+}
+
+__device__ __forceinline__ void write_hit(oph_hit *dst, uint32_t q, uint32_t set_id, uint32_t n_mb, uint32_t n_excl,
+                                          uint32_t groups, uint32_t verdict, uint32_t flags, float est) {
+    uint32_t *d = reinterpret_cast<uint32_t *>(dst);
+    d[0] = q;
+    d[1] = set_id;
+    d[2] = (n_mb & 0xFFFFu) | (n_excl << 16);
+    d[3] = (groups & 0xFFu) | ((verdict & 0xFFu) << 8) | ((flags & 0xFFu) << 16);
+    d[4] = __float_as_uint(est);
+}
+
+// emit one decided pair: dense -> fixed slot; threshold -> append if Similar.
+// Must be called by all 32 lanes (warp-aggregated append).
+__device__ __forceinline__ void emit(const OutArgs &o, bool valid, uint32_t q, uint64_t s, uint32_t n_mb,
+                                     uint32_t n_excl, uint32_t groups, uint32_t verdict, uint32_t flags, float est) {
+    if (o.dense) {
+        if (valid) write_hit(o.hits + (uint64_t)q * o.n_sets + s, q, o.set_id_base + (uint32_t)s, n_mb, n_excl, groups,
+                             verdict, flags, est);
+        return;
+    }
+    const bool h = valid && verdict;
+    const unsigned long long idx = warp_append(h, o.count);
+    if (h && idx < o.cap) write_hit(o.hits + idx, q, o.set_id_base + (uint32_t)s, n_mb, n_excl, groups, verdict, flags, est);
+}
+
+// excluded bins among bins [0, nbins) of a pair, from its two mask columns
+__device__ __forceinline__ uint32_t popc_masked(uint32_t qm, uint32_t sm, uint32_t joint, uint32_t w, uint32_t nbins) {
+    uint32_t x = joint ? (qm & sm) : (qm | sm);
+    const uint32_t lo = 32 * w;
+    if (nbins < lo + 32) x &= (nbins <= lo) ? 0u : ((1u << (nbins - lo)) - 1u);
+    return __popc(x);
+}
+
+// ---------------------------------------------------------------------------
+// K3: the collection scan.  CTA = 128 threads; a thread owns SPT consecutive
+// sets (one vectorised, coalesced load per bin: a warp reads 32*SPT
+// consecutive words of one bin row) and B query counters per set in
+// registers; the query block's values sit in shared memory (bin-major, read
+// as broadcast 128-bit loads).  grid.x = query blocks (fastest, so CTAs that
+// share a set tile run together and hit L2), grid.y = groups of
+// tiles_per_cta set tiles.
+// ---------------------------------------------------------------------------
+template <int SPT>
+struct VecT;
+template <>
+struct VecT<2> {
+    using T = uint2;
+};
+template <>
+struct VecT<4> {
+    using T = uint4;
+};
+
+template <int SPT>
+__device__ __forceinline__ void load_vals(const uint32_t *p, uint32_t (&v)[SPT]) {
+    if constexpr (SPT == 2) {
+        const uint2 x = __ldg(reinterpret_cast<const uint2 *>(p));
+        v[0] = x.x;
+        v[1] = x.y;
+    } else {
+        const uint4 x = __ldg(reinterpret_cast<const uint4 *>(p));
+        v[0] = x.x;
+        v[1] = x.y;
+        v[2] = x.z;
+        v[3] = x.w;
+    }
+}
+
+constexpr uint32_t kScanChunk = 512;  // query bins held in shared memory at once
+
+// c += (v == q) as ISETP + predicated IADD (2 instructions; the C++ form
+// compiles to 3: IADD, ISETP, predicated MOV)
+__device__ __forceinline__ void acc_eq(uint32_t &c, uint32_t v, uint32_t q) {
+    asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n}" : "+r"(c) : "r"(v), "r"(q));
+}
+
+template <int B, int SPT, int U>
+__device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool active, const uint32_t *qs,
+                                          uint32_t b0, uint32_t nb, uint32_t (&cnt)[SPT][B]) {
+    uint32_t b = 0;
+    for (; b + U <= nb; b += U) {
+        uint32_t v[U][SPT];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (active) load_vals<SPT>(Fp + (uint64_t)(b0 + b + u) * ld, v[u]);
+            else
+#pragma unroll
+                for (int j = 0; j < SPT; j++) v[u][j] = kEmpty;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint4 *q4 = reinterpret_cast<const uint4 *>(qs + (size_t)(b + u) * B);
+#pragma unroll
+            for (int q = 0; q < B / 4; q++) {
+                const uint4 x = q4[q];
+#pragma unroll
+                for (int j = 0; j < SPT; j++) {
+                    acc_eq(cnt[j][4 * q + 0], v[u][j], x.x);
+                    acc_eq(cnt[j][4 * q + 1], v[u][j], x.y);
+                    acc_eq(cnt[j][4 * q + 2], v[u][j], x.z);
+                    acc_eq(cnt[j][4 * q + 3], v[u][j], x.w);
+                }
+            }
+        }
+    }
+    for (; b < nb; b++) {
+        uint32_t v[SPT];
+        if (active) load_vals<SPT>(Fp + (uint64_t)(b0 + b) * ld, v);
+        else
+#pragma unroll
+            for (int j = 0; j < SPT; j++) v[j] = kEmpty;
+        const uint4 *q4 = reinterpret_cast<const uint4 *>(qs + (size_t)b * B);
+#pragma unroll
+        for (int q = 0; q < B / 4; q++) {
+            const uint4 x = q4[q];
+#pragma unroll
+            for (int j = 0; j < SPT; j++) {
+                acc_eq(cnt[j][4 * q + 0], v[j], x.x);
+                acc_eq(cnt[j][4 * q + 1], v[j], x.y);
+                acc_eq(cnt[j][4 * q + 2], v[j], x.z);
+                acc_eq(cnt[j][4 * q + 3], v[j], x.w);
+            }
+        }
+    }
+}
+
+template <int B, int SPT>
+__global__ void __launch_bounds__(128) scan_kernel(const __grid_constant__ ScanArgs a) {
+    constexpr int U = 4;  // bins in flight per thread
+    extern __shared__ __align__(16) uint32_t sm[];
+    const uint32_t qs_bins = min(a.nscan, kScanChunk);
+    uint32_t *qs = sm;                                  // [qs_bins][B]
+    uint32_t *qe = qs + (size_t)qs_bins * B;            // [nw_load][B]
+    uint32_t *qf = qe + (size_t)a.nw_load * B;          // [B] MinWise flags
+
+    const uint32_t qb0 = blockIdx.x * B;                // chunk-local first query
+    const uint64_t col0 = (uint64_t)a.q_col0 + qb0;     // column in the prepared arrays
+    const bool one_chunk = a.nscan <= kScanChunk;
+    if (one_chunk)
+        for (uint32_t i = threadIdx.x; i < a.nscan * B; i += blockDim.x)
+            qs[i] = a.QT[(uint64_t)(i / B) * a.ldq + col0 + (i % B)];
+    if (a.E)
+        for (uint32_t i = threadIdx.x; i < a.nw_load * B; i += blockDim.x)
+            qe[i] = a.QE[(uint64_t)(i / B) * a.ldq + col0 + (i % B)];
+    if (a.method == kMinwise)
+        for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) qf[i] = a.qflags[col0 + i];
+    __syncthreads();
+
+    const uint64_t tile_sets = 128ull * SPT;
+    const uint64_t ntiles = (a.n_sets + tile_sets - 1) / tile_sets;
+    const uint64_t t_end = min(ntiles, (uint64_t)(blockIdx.y + 1) * a.tiles_per_cta);
+    for (uint64_t t = (uint64_t)blockIdx.y * a.tiles_per_cta; t < t_end; t++) {
+        const uint64_t s0 = t * tile_sets + threadIdx.x * SPT;
+        const bool active = s0 < a.n_sets;
+        uint32_t cnt[SPT][B];
+#pragma unroll
+        for (int j = 0; j < SPT; j++)
+#pragma unroll
+            for (int q = 0; q < B; q++) cnt[j][q] = 0;
+
+        const uint32_t *Fp = a.F + s0;
+        if (one_chunk) {
+            scan_bins<B, SPT, U>(Fp, a.ld, active, qs, 0, a.nscan, cnt);
+        } else {
+            for (uint32_t c0 = 0; c0 < a.nscan; c0 += kScanChunk) {
+                const uint32_t cn = min(kScanChunk, a.nscan - c0);
+                __syncthreads();
+                for (uint32_t i = threadIdx.x; i < cn * B; i += blockDim.x)
+                    qs[i] = a.QT[(uint64_t)(c0 + i / B) * a.ldq + col0 + (i % B)];
+                __syncthreads();
+                scan_bins<B, SPT, U>(Fp, a.ld, active, qs, c0, cn, cnt);
+            }
+        }
+
+        // ---------------- epilogue: decisions and emission, one set column at a time
+#pragma unroll
+        for (int j = 0; j < SPT; j++) {
+            const uint64_t s = s0 + j;
+            const bool sv = active && s < a.n_sets;
+            uint32_t hit_mask = 0, surv_mask = 0, dec_mask = 0;
+            if (a.final_) {
+                uint32_t ex[B];
+#pragma unroll
+                for (int q = 0; q < B; q++) ex[q] = 0;
+                uint32_t sflag = 0;
+                if (a.method == kMinwise) {
+                    sflag = sv ? a.sflags[s] : 1u;
+                } else {
+                    for (uint32_t w = 0; w < a.nw_load; w++) {
+                        const uint32_t es = sv ? __ldg(a.E + (uint64_t)w * a.ld + s) : 0u;
+#pragma unroll
+                        for (int q = 0; q < B; q++) ex[q] += popc_masked(qe[w * B + q], es, a.joint, w, a.nbins_total);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < B; q++) {
+                    const bool valid = sv && (qb0 + q < a.nq);
+                    uint32_t den, undef;
+                    if (a.method == kMinwise) {
+                        den = a.nbins_total;
+                        undef = sflag | qf[q];
+                    } else {
+                        den = a.nbins_total - ex[q];
+                        undef = den == 0;
+                    }
+                    const uint32_t verdict = !undef && (uint64_t)cnt[j][q] * a.t_den >= (uint64_t)a.t_num * den;
+                    hit_mask |= (uint32_t)(valid && verdict) << q;
+                    dec_mask |= (uint32_t)valid << q;
+                }
+                const bool any = __any_sync(0xFFFFFFFFu, a.out.dense ? dec_mask != 0 : hit_mask != 0);
+                if (any) {
+#pragma unroll
+                    for (int q = 0; q < B; q++) {
+                        const bool valid = (dec_mask >> q) & 1u;
+                        uint32_t den, undef;
+                        if (a.method == kMinwise) {
+                            den = a.nbins_total;
+                            undef = sflag | qf[q];
+                        } else {
+                            den = a.nbins_total - ex[q];
+                            undef = den == 0;
+                        }
+                        const uint32_t verdict = (hit_mask >> q) & 1u;
+                        const float est = undef ? -1.0f : (float)cnt[j][q] / (float)den;
+                        emit(a.out, valid, (uint32_t)(col0 + q), s, cnt[j][q],
+                             a.method == kMinwise ? 0u : ex[q], a.level, verdict, undef ? OPH_FLAG_UNDEFINED : 0u, est);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < B; q++) {
+                    const bool valid = sv && (qb0 + q < a.nq);
+                    const uint64_t st = a.w1 * cnt[j][q];
+                    const bool acc = st >= a.acc, rej = (int64_t)st <= a.rej;
+                    hit_mask |= (uint32_t)(valid && acc) << q;
+                    dec_mask |= (uint32_t)(valid && (acc || rej)) << q;
+                    surv_mask |= (uint32_t)(valid && !acc && !rej) << q;
+                }
+                const bool any_emit = __any_sync(0xFFFFFFFFu, a.out.dense ? dec_mask != 0 : hit_mask != 0);
+                if (any_emit) {
+#pragma unroll
+                    for (int q = 0; q < B; q++) {
+                        const bool e = a.out.dense ? ((dec_mask >> q) & 1u) : ((hit_mask >> q) & 1u);
+                        uint32_t ex = 0;
+                        if (e)
+                            for (uint32_t w = 0; w < a.nw_load; w++)
+                                ex += popc_masked(qe[w * B + q], __ldg(a.E + (uint64_t)w * a.ld + s), a.joint, w, a.nscan);
+                        emit(a.out, (dec_mask >> q) & 1u, (uint32_t)(col0 + q), s, cnt[j][q], ex, a.level,
+                             (hit_mask >> q) & 1u, OPH_FLAG_EARLY, -1.0f);
+                    }
+                }
+                if (__any_sync(0xFFFFFFFFu, surv_mask != 0)) {
+#pragma unroll
+                    for (int q = 0; q < B; q++) {
+                        const bool sp = (surv_mask >> q) & 1u;
+                        const unsigned long long idx = warp_append(sp, a.surv_count);
+                        if (sp) {
+                            a.surv.q[idx] = (uint32_t)(col0 + q);
+                            a.surv.s[idx] = (uint32_t)s;
+                            a.surv.state[idx] = a.w1 * cnt[j][q];
+                            a.surv.nmb[idx] = cnt[j][q];
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4: one GOPH/HOPH level over the survivor list (one thread per surviving
+// pair; consecutive survivors mostly share a set, so the bin-row gathers
+// coalesce), appending the still-undecided pairs to the next list with
+// warp-aggregated atomics.  The last level applies the final verdict.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t group_matches(const LevelArgs &a, uint32_t q, uint32_t s, uint32_t g) {
+    const uint32_t *qp = a.QM + (uint64_t)q * a.nb + (uint64_t)g * a.kp;
+    const uint32_t *fp = a.F + (uint64_t)g * a.kp * a.ld + s;
+    uint32_t m = 0;
+#pragma unroll 8
+    for (uint32_t i = 0; i < a.kp; i++) m += (__ldg(fp + (uint64_t)i * a.ld) == __ldg(qp + i));
+    return m;
+}
+
+// excluded bins of group g (bins [g kp, (g+1) kp))
+__device__ __forceinline__ uint32_t group_excl(const LevelArgs &a, uint32_t q, uint32_t s, uint32_t g) {
+    const uint32_t lo = g * a.kp, hi = lo + a.kp;
+    uint32_t ex = 0;
+    for (uint32_t w = lo / 32; w * 32 < hi; w++) {
+        uint32_t x = a.joint ? (__ldg(a.QEM + (uint64_t)q * a.nw + w) & __ldg(a.E + (uint64_t)w * a.ld + s))
+                             : (__ldg(a.QEM + (uint64_t)q * a.nw + w) | __ldg(a.E + (uint64_t)w * a.ld + s));
+        const uint32_t b0 = max(lo, 32 * w), b1 = min(hi, 32 * w + 32);
+        const uint32_t width = b1 - b0;
+        const uint32_t mask = (width == 32 ? 0xFFFFFFFFu : ((1u << width) - 1u)) << (b0 - 32 * w);
+        ex += __popc(x & mask);
+    }
+    return ex;
+}
+
+__global__ void __launch_bounds__(256) level_kernel(const __grid_constant__ LevelArgs a) {
+    const unsigned long long n = *a.count_in;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    const bool last = a.level == a.nlev;
+    for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n;
+         base += stride) {
+        const unsigned long long i = base + (threadIdx.x & 31u);
+        const bool act = i < n;
+        uint32_t q = 0, s = 0, nmb = 0, M = 0;
+        uint64_t st = 0;
+        if (act) {
+            q = a.in.q[i];
+            s = a.in.s[i];
+            st = a.in.state[i];
+            nmb = a.in.nmb[i];
+            M = group_matches(a, q, s, a.level - 1);
+            nmb += M;
+            st += a.c[a.level - 1] * M;
+        }
+        if (last) {
+            uint32_t verdict = 0, flags = 0, ex_tot = 0;
+            float est = -1.0f;
+            if (act) {
+                if (a.method == kGoph) {
+                    for (uint32_t g = 0; g < a.nlev; g++) ex_tot += group_excl(a, q, s, g);
+                    const uint32_t den = a.nb - ex_tot;
+                    if (den == 0) {
+                        flags = OPH_FLAG_UNDEFINED;
+                    } else {
+                        verdict = (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
+                        est = (float)nmb / (float)den;
+                    }
+                } else {
+                    // HOPH estimator: sum_j c_j m_j / d_j over groups with d_j > 0, exact with the
+                    // common denominator lam = lcm(1..kp) (R21, R22)
+                    unsigned __int128 num = 0;
+                    uint64_t csum = 0;
+                    for (uint32_t g = 0; g < a.nlev; g++) {
+                        const uint32_t m = (g == a.level - 1) ? M : group_matches(a, q, s, g);
+                        const uint32_t ex = group_excl(a, q, s, g);
+                        ex_tot += ex;
+                        const uint32_t d = a.kp - ex;
+                        if (d == 0) continue;
+                        num += (unsigned __int128)a.c[g] * m * (a.lam / d);
+                        csum += a.c[g];
+                    }
+                    if (csum == 0) {
+                        flags = OPH_FLAG_UNDEFINED;
+                    } else {
+                        verdict = num * a.t_den >= (unsigned __int128)a.t_num * a.lam * csum;
+                        est = (float)((double)num / ((double)a.lam * (double)csum));
+                    }
+                }
+            }
+            emit(a.res, act, q, s, nmb, ex_tot, a.nlev, verdict, flags, est);
+        } else {
+            const bool acc = act && st >= a.acc;
+            const bool rej = act && !acc && (int64_t)st <= a.rej;
+            const bool surv = act && !acc && !rej;
+            const bool want = a.res.dense ? (acc || rej) : acc;
+            if (__any_sync(0xFFFFFFFFu, want)) {
+                uint32_t ex = 0;
+                if (want)
+                    for (uint32_t g = 0; g < a.level; g++) ex += group_excl(a, q, s, g);
+                emit(a.res, acc || rej, q, s, nmb, ex, a.level, acc ? 1u : 0u, OPH_FLAG_EARLY, -1.0f);
+            }
+            const unsigned long long idx = warp_append(surv, a.count_out);
+            if (surv) {
+                a.out.q[idx] = q;
+                a.out.s[idx] = s;
+                a.out.state[idx] = st;
+                a.out.nmb[idx] = nmb;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+cudaError_t launch_build(const BuildArgs &a, cudaStream_t st) {
+    if (a.n_sets == 0) return cudaSuccess;
+    const uint32_t per_set = (a.do_flat ? a.k + 1 : 0) + (a.do_hier ? a.L * a.kp + 1 : 0);
+    uint32_t SB = 16;
+    while (SB > 1 && (size_t)SB * per_set * 4 + (SB + 1) * 8 > 200 * 1024) SB >>= 1;
+    const size_t smem = (size_t)SB * per_set * 4 + (SB + 1) * 8;
+    const uint64_t grid = (a.n_sets + SB - 1) / SB;
+    const bool w32 = a.psi.mask == 0xFFFFFFFFu;
+    auto kern = w32 ? build_kernel<true> : build_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)grid, 256, smem, st>>>(a, SB);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_minwise(const MinwiseArgs &a, cudaStream_t st) {
+    if (a.n_sets == 0) return cudaSuccess;
+    const uint64_t grid = (a.n_sets + kMwSets - 1) / kMwSets;
+    const uint32_t threads = a.k >= 256 ? 256 : ((a.k + 31) / 32) * 32;
+    if (a.w >= 32) minwise_kernel<true><<<(unsigned)grid, threads, 0, st>>>(a);
+    else minwise_kernel<false><<<(unsigned)grid, threads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prep(const PrepArgs &a, cudaStream_t st) {
+    const uint64_t n = (uint64_t)a.nb * a.ldq;
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    prep_kernel<<<grid, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int B, int SPT>
+static cudaError_t launch_scan_t(const ScanArgs &a0, cudaStream_t st) {
+    ScanArgs a = a0;
+    const size_t smem = ((size_t)min(a.nscan, kScanChunk) * B + (size_t)a.nw_load * B + B) * 4;
+    const uint64_t tile_sets = 128ull * SPT;
+    const uint64_t ntiles = (a.n_sets + tile_sets - 1) / tile_sets;
+    const uint32_t qblocks = (a.nq + B - 1) / B;
+    // aim for >= 4 waves of CTAs over 148 SMs, otherwise longest tile runs per CTA
+    const uint64_t want_y = std::max<uint64_t>(1, (148ull * 4 * 4 + qblocks - 1) / qblocks);
+    uint64_t tpc = std::max<uint64_t>(1, (ntiles + want_y - 1) / want_y);
+    tpc = std::min<uint64_t>(tpc, 64);
+    a.tiles_per_cta = (uint32_t)tpc;
+    const uint64_t gy = (ntiles + tpc - 1) / tpc;
+    if (gy > 65535) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(scan_kernel<B, SPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    scan_kernel<B, SPT><<<dim3(qblocks, (unsigned)gy), 128, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan(const ScanArgs &a, uint32_t B, cudaStream_t st) {
+    if (a.n_sets == 0 || a.nq == 0) return cudaSuccess;
+    (void)B;
+    return launch_scan_t<32, 2>(a, st);
+}
+
+cudaError_t launch_level(const LevelArgs &a, cudaStream_t st) {
+    level_kernel<<<148 * 8, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K6: result lists.  Threshold: stable radix sort of (query << 32 | set_id).
+// Top-k: stable sort by (~estimate_key << 32 | set_id), then stable sort by
+// query; estimate_key = floor(n_mb 2^31 / den) is an exact order-preserving
+// code of the rational n_mb/den for den <= 2^15 (distinct rationals differ
+// by >= 1/(den1 den2) > 2^-31).  Then keep ranks < topk per query.
+// ---------------------------------------------------------------------------
+struct SelectWs {
+    uint64_t *k0, *k1;
+    uint32_t *v0, *v1;
+    uint32_t *q0, *q1;
+    uint64_t *head;
+    uint8_t *keep;
+    oph_hit *gathered;
+    void *cub;
+    size_t cub_bytes;
+};
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static size_t cub_bytes_needed(uint64_t n) {
+    size_t a = 0, b = 0, c = 0, d = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (uint64_t *)nullptr, (uint64_t *)nullptr, (uint32_t *)nullptr,
+                                    (uint32_t *)nullptr, (int)n);
+    cub::DeviceRadixSort::SortPairs(nullptr, b, (uint32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (uint32_t *)nullptr, (int)n);
+    cub::DeviceScan::InclusiveScan(nullptr, c, (uint64_t *)nullptr, (uint64_t *)nullptr, cuda::maximum<uint64_t>{}, (int)n);
+    cub::DeviceSelect::Flagged(nullptr, d, (oph_hit *)nullptr, (uint8_t *)nullptr, (oph_hit *)nullptr,
+                               (unsigned long long *)nullptr, (int)n);
+    return std::max(std::max(a, b), std::max(c, d));
+}
+
+size_t select_temp_bytes(uint64_t n) {
+    const uint64_t m = n ? n : 1;
+    return align_up(8 * m) * 2 + align_up(4 * m) * 4 + align_up(8 * m) + align_up(m) + align_up(sizeof(oph_hit) * m) +
+           align_up(cub_bytes_needed(m));
+}
+
+static SelectWs carve(void *ws, uint64_t n) {
+    const uint64_t m = n ? n : 1;
+    char *p = (char *)ws;
+    SelectWs w;
+    w.k0 = (uint64_t *)p; p += align_up(8 * m);
+    w.k1 = (uint64_t *)p; p += align_up(8 * m);
+    w.v0 = (uint32_t *)p; p += align_up(4 * m);
+    w.v1 = (uint32_t *)p; p += align_up(4 * m);
+    w.q0 = (uint32_t *)p; p += align_up(4 * m);
+    w.q1 = (uint32_t *)p; p += align_up(4 * m);
+    w.head = (uint64_t *)p; p += align_up(8 * m);
+    w.keep = (uint8_t *)p; p += align_up(m);
+    w.gathered = (oph_hit *)p; p += align_up(sizeof(oph_hit) * m);
+    w.cub = p;
+    w.cub_bytes = align_up(cub_bytes_needed(m));
+    return w;
+}
+
+__global__ void sel_keys_threshold(const oph_hit *in, uint64_t n, uint64_t *k, uint32_t *v) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        k[i] = ((uint64_t)in[i].query << 32) | in[i].set_id;
+        v[i] = (uint32_t)i;
+    }
+}
+
+__global__ void sel_keys_topk(const oph_hit *in, uint64_t n, uint32_t k_bins, uint64_t *k, uint32_t *v) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const oph_hit h = in[i];
+        const uint32_t den = k_bins - h.n_excl;
+        uint64_t ek = 0;
+        if (!(h.flags & OPH_FLAG_UNDEFINED) && den > 0 && h.n_mb <= den) ek = ((uint64_t)h.n_mb << 31) / den;
+        k[i] = ((uint64_t)(0xFFFFFFFFu - (uint32_t)ek) << 32) | h.set_id;
+        v[i] = (uint32_t)i;
+    }
+}
+
+__global__ void sel_query_keys(const oph_hit *in, const uint32_t *perm, uint64_t n, uint32_t *qk) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const oph_hit h = in[perm[i]];
+        qk[i] = (h.flags & OPH_FLAG_UNDEFINED) ? 0xFFFFFFFFu : h.query;
+    }
+}
+
+__global__ void sel_heads(const uint32_t *qk, uint64_t n, uint64_t *head) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        head[i] = (i == 0 || qk[i] != qk[i - 1]) ? i : 0;
+}
+
+__global__ void sel_keep(const uint32_t *qk, const uint64_t *start, uint64_t n, uint32_t topk, uint8_t *keep) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        keep[i] = (qk[i] != 0xFFFFFFFFu) && (i - start[i] < topk);
+}
+
+__global__ void sel_gather(const oph_hit *in, const uint32_t *perm, uint64_t n, oph_hit *out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = in[perm[i]];
+}
+
+__global__ void sel_set_count(unsigned long long *c, uint64_t n) { *c = n; }
+
+cudaError_t run_select(const oph_hit *in, uint64_t n, uint32_t mode, uint32_t topk, uint32_t k_bins, oph_hit *out,
+                       unsigned long long *n_out, void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (ws_bytes < select_temp_bytes(n)) return cudaErrorInvalidValue;
+    if (n == 0) {
+        sel_set_count<<<1, 1, 0, st>>>(n_out, 0);
+        return cudaGetLastError();
+    }
+    SelectWs w = carve(ws, n);
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 8);
+    size_t tb = w.cub_bytes;
+    if (mode == OPH_SELECT_THRESHOLD) {
+        sel_keys_threshold<<<grid, 256, 0, st>>>(in, n, w.k0, w.v0);
+        cudaError_t e = cub::DeviceRadixSort::SortPairs(w.cub, tb, w.k0, w.k1, w.v0, w.v1, (int)n, 0, 64, st);
+        if (e != cudaSuccess) return e;
+        sel_gather<<<grid, 256, 0, st>>>(in, w.v1, n, out);
+        sel_set_count<<<1, 1, 0, st>>>(n_out, n);
+        return cudaGetLastError();
+    }
+    sel_keys_topk<<<grid, 256, 0, st>>>(in, n, k_bins, w.k0, w.v0);
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(w.cub, tb, w.k0, w.k1, w.v0, w.v1, (int)n, 0, 64, st);
+    if (e != cudaSuccess) return e;
+    sel_query_keys<<<grid, 256, 0, st>>>(in, w.v1, n, w.q0);
+    tb = w.cub_bytes;
+    e = cub::DeviceRadixSort::SortPairs(w.cub, tb, w.q0, w.q1, w.v1, w.v0, (int)n, 0, 32, st);
+    if (e != cudaSuccess) return e;
+    sel_heads<<<grid, 256, 0, st>>>(w.q1, n, w.head);
+    tb = w.cub_bytes;
+    e = cub::DeviceScan::InclusiveScan(w.cub, tb, w.head, w.k0, cuda::maximum<uint64_t>{}, (int)n, st);
+    if (e != cudaSuccess) return e;
+    sel_keep<<<grid, 256, 0, st>>>(w.q1, w.k0, n, topk, w.keep);
+    sel_gather<<<grid, 256, 0, st>>>(in, w.v0, n, w.gathered);
+    tb = w.cub_bytes;
+    e = cub::DeviceSelect::Flagged(w.cub, tb, w.gathered, w.keep, out, n_out, (int)n, st);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+}  // namespace ophgpu

@@ -1,0 +1,323 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle.
+
+Bar (B.north_star): sketches, per-pair match / excluded-bin counts, groups
+compared, verdicts, flags and returned IDs bit-exact; estimates within 1e-6
+absolute.  Inputs: the seeded generators in workloads/ (the oracle never
+sees a value the GPU produced)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1805_11254_b200 as og
+from workloads import make_csr, text_like, tiny
+
+from gpu_helpers import (assert_records_equal, gpu_build, gpu_dense, gpu_threshold_hits, masks_from_values,
+                         oracle_records, subview)
+
+pytestmark = pytest.mark.gpu
+
+E = oracle.EMPTY
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    og.build()
+
+
+# ----------------------------------------------------------------------------- worked examples
+def test_paper_worked_examples_on_gpu(golden):
+    """P:158 OPH and P:482 HOPH goldens (identity psi) and their estimates."""
+    g, h = golden("oph_example.json"), golden("hoph_example.json")
+    names = ["D1", "D2", "D3"]
+    offs, ids = make_csr([g["sets"][n] for n in names])
+    hier = og.oph_hier_layout_make(17, 1, 1, 2)
+    _, so, sh = gpu_build(offs, ids, 17, 0, k=4, kprime=2, hier=hier, identity=True)
+    F, H = so.numpy(), sh.numpy()
+    for i, n in enumerate(names):
+        assert [None if v == E else int(v) for v in F[i]] == g["sketch"][n]
+        assert [None if v == E else int(v) for v in H[i]] == h["sketch"][n]
+    lay = og.flat_layout(17, 4, 2)
+    full = gpu_dense("full", so, so, layout=lay, t_num=1, t_den=2)
+    assert full[0, 1]["estimate"] == 0.75 and full[0, 1]["n_mb"] == 3
+    assert abs(full[0, 2]["estimate"] - 1 / 3) < 1e-7
+    joint = gpu_dense("full", so, so, layout=lay, t_num=1, t_den=2, joint=True)
+    assert joint[0, 2]["estimate"] == 0.25
+    # HOPH estimator: with eps -> 0 no small-probability stop can fire; (D1, D2) reaches the last group
+    hp = gpu_dense("hoph", sh, sh, layout=hier, t_num=1, t_den=2, eps=1e-300)
+    assert hp[0, 1]["groups"] == 3 and hp[0, 1]["estimate"] == 0.625
+
+
+# ----------------------------------------------------------------------------- tiny (configs[0])
+@pytest.fixture(scope="module")
+def tiny_run():
+    w = tiny()
+    p = w.params
+    hier = og.oph_hier_layout_make(w.vocab_size, p["a"], p["b"], p["hoph_kprime"])
+    sets, so, sh = gpu_build(w.offsets, w.ids, w.vocab_size, p["perm_seed"], k=p["k"], kprime=p["kprime"], hier=hier)
+    qsets, qo, qh = gpu_build(w.q_offsets, w.q_ids, w.vocab_size, p["perm_seed"], k=p["k"], kprime=p["kprime"],
+                              hier=hier)
+    mw = og.minwise_build_sketches(sets, w.vocab_size, p["perm_seed"], p["mw_k"])
+    qmw = og.minwise_build_sketches(qsets, w.vocab_size, p["perm_seed"], p["mw_k"])
+    lay = oracle.hoph_layout(w.vocab_size, p["a"], p["b"], p["hoph_kprime"])
+    orc = dict(
+        F=oracle.oph_sketch(w.offsets, w.ids, w.vocab_size, p["k"], p["perm_seed"]),
+        QF=oracle.oph_sketch(w.q_offsets, w.q_ids, w.vocab_size, p["k"], p["perm_seed"]),
+        H=oracle.hoph_sketch(w.offsets, w.ids, w.vocab_size, lay, p["hoph_kprime"], p["perm_seed"]),
+        QH=oracle.hoph_sketch(w.q_offsets, w.q_ids, w.vocab_size, lay, p["hoph_kprime"], p["perm_seed"]),
+        MW=oracle.minwise_sketch(w.offsets, w.ids, w.vocab_size, p["mw_k"], p["perm_seed"]),
+        QMW=oracle.minwise_sketch(w.q_offsets, w.q_ids, w.vocab_size, p["mw_k"], p["perm_seed"]),
+        L=len(lay))
+    return dict(w=w, p=p, hier=hier, so=so, sh=sh, qo=qo, qh=qh, mw=mw, qmw=qmw, orc=orc)
+
+
+def test_tiny_sketches_bit_exact(tiny_run):
+    r, o = tiny_run, tiny_run["orc"]
+    assert (r["so"].numpy() == o["F"]).all()
+    assert (r["qo"].numpy() == o["QF"]).all()
+    assert (r["sh"].numpy() == o["H"]).all()
+    assert (r["qh"].numpy() == o["QH"]).all()
+    assert (r["so"].empty_numpy() == masks_from_values(o["F"])).all()
+    assert (r["sh"].empty_numpy() == masks_from_values(o["H"])).all()
+    mw, fl = o["MW"]
+    assert (r["mw"].numpy() == mw).all()
+    assert (r["mw"].flags.cpu().numpy()[: len(fl)] == fl).all()
+
+
+@pytest.mark.parametrize("joint", [False, True])
+@pytest.mark.parametrize("method", ["full", "goph", "hoph", "minwise"])
+def test_tiny_dense_records(tiny_run, method, joint):
+    r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    if method == "minwise" and joint:
+        pytest.skip("MinWise has no empty bins")
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"], joint=joint)
+    if method in ("full", "goph"):
+        lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+        g = gpu_dense(method, r["qo"], r["so"], layout=lay, **kw)
+        want = oracle_records(method, o["QF"], o["F"], k=p["k"], kprime=p["kprime"], **kw)
+    elif method == "hoph":
+        g = gpu_dense(method, r["qh"], r["sh"], layout=r["hier"], **kw)
+        want = oracle_records(method, o["QH"], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw)
+    else:
+        g = gpu_dense(method, r["qmw"], r["mw"], **kw)
+        want = oracle_records(method, o["QMW"][0], o["MW"][0], qflags=o["QMW"][1], sflags=o["MW"][1], **kw)
+    assert_records_equal(g, want, f"tiny {method} joint={joint}")
+
+
+@pytest.mark.parametrize("method", ["full", "goph", "hoph", "minwise"])
+def test_tiny_threshold_lists(tiny_run, method):
+    """Threshold hit lists (sorted by (query, set_id)) == oracle's, with set_id_base."""
+    r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    base = 1000
+    if method in ("full", "goph"):
+        lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+        hits = gpu_threshold_hits(method, r["qo"], r["so"], layout=lay, set_id_base=base, **kw)
+        want = oracle_records(method, o["QF"], o["F"], k=p["k"], kprime=p["kprime"], **kw)
+    elif method == "hoph":
+        hits = gpu_threshold_hits(method, r["qh"], r["sh"], layout=r["hier"], set_id_base=base, **kw)
+        want = oracle_records(method, o["QH"], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw)
+    else:
+        hits = gpu_threshold_hits(method, r["qmw"], r["mw"], set_id_base=base, **kw)
+        want = oracle_records(method, o["QMW"][0], o["MW"][0], qflags=o["QMW"][1], sflags=o["MW"][1], **kw)
+    got = [(int(h["query"]), int(h["set_id"])) for h in hits]
+    assert got == oracle.threshold_list(want, base)
+    assert len(got) > 0
+    # the records themselves match the dense oracle records
+    for h in hits[:200]:
+        wr = want[h["query"], h["set_id"] - base]
+        assert (h["n_mb"], h["n_excl"], h["groups"], h["flags"]) == (wr["n_mb"], wr["n_excl"], wr["groups"], wr["flags"])
+
+
+@pytest.mark.parametrize("method", ["full", "minwise"])
+def test_tiny_topk(tiny_run, method):
+    r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    kw = dict(t_num=1, t_den=10)
+    if method == "full":
+        lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+        res = og.Results(1 << 20)
+        og.compare_full(r["qo"], r["so"], lay, og.params(1, 10, 1e-4), res)
+        want = oracle_records(method, o["QF"], o["F"], k=p["k"], kprime=p["kprime"], **kw)
+    else:
+        res = og.Results(1 << 20)
+        og.compare_minwise(r["qmw"], r["mw"], og.params(1, 10, 1e-4), res)
+        want = oracle_records(method, o["QMW"][0], o["MW"][0], qflags=o["QMW"][1], sflags=o["MW"][1], **kw)
+    n = res.n()
+    out = og.Results(n)
+    og.topk_or_threshold_results(res, n, og.OPH_SELECT_TOPK, out, topk=7, k_bins=p["k"])
+    m = out.n()
+    got = [(int(h["query"]), int(h["set_id"])) for h in out.numpy(m)]
+    assert got == oracle.topk_list(want, p["k"], 7)
+
+
+def test_tiny_query_chunking(tiny_run):
+    """A survivor capacity of 32 * n_sets forces 4 query chunks: same records."""
+    r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    n_s = r["sh"].n_sets
+    g = gpu_dense("hoph", r["qh"], r["sh"], layout=r["hier"], survivor_capacity=32 * n_s, **kw)
+    want = oracle_records("hoph", o["QH"], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw)
+    assert_records_equal(g, want, "tiny hoph chunked")
+
+
+# ----------------------------------------------------------------------------- ragged / edge cases
+@pytest.mark.parametrize("V,k,kp,hkp,seed", [(1000003, 48, 16, 8, 3), (4097, 96, 32, 32, 4), (1 << 20, 512, 32, 32, 5),
+                                             (300, 30, 10, 5, 6), (1 << 32, 256, 32, 32, 7), (2, 1, 1, 1, 8)])
+def test_ragged_and_edges(V, k, kp, hkp, seed):
+    """Non-power-of-two |V| (cycle walking, exact division path), k not a
+    multiple of 32, empty sets, n_sets and n_queries not multiples of the
+    tile / query block, sets covering the whole universe."""
+    rng = np.random.default_rng(seed)
+    nset, nq = 517, 45
+    sizes = rng.integers(0, 60, size=nset)
+    sizes[:3] = 0
+    sets = [rng.choice(V, size=min(int(s), V), replace=False) if s else [] for s in sizes]
+    if V <= 4097:
+        sets[3] = np.arange(V)
+    qsets = [sets[i] if i % 3 == 0 else rng.choice(V, size=int(rng.integers(0, 60)), replace=False) for i in range(nq)]
+    qsets[1] = []
+    offs, ids = make_csr(sets)
+    qoffs, qids = make_csr(qsets)
+    hier = og.oph_hier_layout_make(V, 1, 1, hkp) if V >= 2 * hkp else None
+    _, so, sh = gpu_build(offs, ids, V, seed, k=k, kprime=kp, hier=hier)
+    _, qo, qh = gpu_build(qoffs, qids, V, seed, k=k, kprime=kp, hier=hier)
+    F = oracle.oph_sketch(offs, ids, V, k, seed)
+    QF = oracle.oph_sketch(qoffs, qids, V, k, seed)
+    assert (so.numpy() == F).all() and (qo.numpy() == QF).all()
+    assert (so.empty_numpy() == masks_from_values(F)).all()
+    lay = og.flat_layout(V, k, kp)
+    for joint in (False, True):
+        kw = dict(t_num=7, t_den=10, eps=1e-4, joint=joint)
+        assert_records_equal(gpu_dense("full", qo, so, layout=lay, **kw),
+                             oracle_records("full", QF, F, k=k, kprime=kp, **kw), f"full {V}")
+        assert_records_equal(gpu_dense("goph", qo, so, layout=lay, **kw),
+                             oracle_records("goph", QF, F, k=k, kprime=kp, **kw), f"goph {V}")
+    if hier is not None:
+        glay = oracle.hoph_layout(V, 1, 1, hkp)
+        H = oracle.hoph_sketch(offs, ids, V, glay, hkp, seed)
+        QH = oracle.hoph_sketch(qoffs, qids, V, glay, hkp, seed)
+        assert (sh.numpy() == H).all() and (sh.empty_numpy() == masks_from_values(H)).all()
+        for joint in (False, True):
+            kw = dict(t_num=7, t_den=10, eps=1e-4, joint=joint)
+            assert_records_equal(gpu_dense("hoph", qh, sh, layout=hier, **kw),
+                                 oracle_records("hoph", QH, H, kprime=hkp, L=len(glay), **kw), f"hoph {V}")
+    sets_t = og.SetCollection.from_numpy(offs, ids)
+    q_t = og.SetCollection.from_numpy(qoffs, qids)
+    mk = min(k, 64)
+    mw = og.minwise_build_sketches(sets_t, V, seed, mk)
+    qmw = og.minwise_build_sketches(q_t, V, seed, mk)
+    MW, fl = oracle.minwise_sketch(offs, ids, V, mk, seed)
+    QMW, qfl = oracle.minwise_sketch(qoffs, qids, V, mk, seed)
+    assert (mw.numpy() == MW).all()
+    assert_records_equal(gpu_dense("minwise", qmw, mw, t_num=7, t_den=10),
+                         oracle_records("minwise", QMW, MW, qflags=qfl, sflags=fl, t_num=7, t_den=10), "minwise")
+
+
+@pytest.mark.parametrize("tn,td,eps", [(1, 1, 1e-4), (1, 20, 1e-4), (7, 10, 0.5), (7, 10, 1e-300), (4, 5, 1e-2)])
+def test_threshold_and_epsilon_extremes(tiny_run, tn, td, eps):
+    r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    kw = dict(t_num=tn, t_den=td, eps=eps)
+    lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+    q = subview(r["qo"], 40)
+    assert_records_equal(gpu_dense("goph", q, r["so"], layout=lay, **kw),
+                         oracle_records("goph", o["QF"][:40], o["F"], k=p["k"], kprime=p["kprime"], **kw), "goph")
+    qh = subview(r["qh"], 40)
+    assert_records_equal(gpu_dense("hoph", qh, r["sh"], layout=r["hier"], **kw),
+                         oracle_records("hoph", o["QH"][:40], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw), "hoph")
+
+
+def test_empty_inputs():
+    """Zero queries or zero sets: nothing is written, no error."""
+    offs, ids = make_csr([[1, 2, 3]])
+    e_offs, e_ids = make_csr([])
+    _, so, _ = gpu_build(offs, ids, 1 << 16, 1, k=64, kprime=16)
+    res = og.Results(10)
+    lay = og.flat_layout(1 << 16, 64, 16)
+    q0 = subview(so, 0)
+    og.compare_full(q0, so, lay, og.params(7, 10, 1e-4), res)
+    og.compare_goph(so, q0, lay, og.params(7, 10, 1e-4), res)
+    assert res.n() == 0
+
+
+# ----------------------------------------------------------------------------- text-like (configs[1]) at full size
+@pytest.fixture(scope="module")
+def text_run():
+    w = text_like()
+    p = w.params
+    hier = og.oph_hier_layout_make(w.vocab_size, 1, 1, p["hoph_kprime"])
+    sets, so, sh = gpu_build(w.offsets, w.ids, w.vocab_size, p["perm_seed"], k=p["k"], kprime=p["kprime"], hier=hier)
+    qsets, qo, qh = gpu_build(w.q_offsets, w.q_ids, w.vocab_size, p["perm_seed"], k=p["k"], kprime=p["kprime"],
+                              hier=hier)
+    lay = oracle.hoph_layout(w.vocab_size, 1, 1, p["hoph_kprime"])
+    return dict(w=w, p=p, hier=hier, sets=sets, so=so, sh=sh, qsets=qsets, qo=qo, qh=qh, glay=lay)
+
+
+def test_text_sketches_full_collection(text_run):
+    r = text_run
+    w, p = r["w"], r["p"]
+    F = oracle.oph_sketch(w.offsets, w.ids, w.vocab_size, p["k"], p["perm_seed"])
+    assert (r["so"].numpy() == F).all()
+    assert (r["so"].empty_numpy() == masks_from_values(F)).all()
+    H = oracle.hoph_sketch(w.offsets, w.ids, w.vocab_size, r["glay"], p["hoph_kprime"], p["perm_seed"])
+    assert (r["sh"].numpy() == H).all()
+    r["F"], r["H"] = F, H
+
+
+@pytest.mark.parametrize("method", ["full", "goph", "hoph"])
+def test_text_full_size_sampled_queries(text_run, method):
+    """All 1,000 queries x 200,000 sets in the bench launch configuration
+    (threshold mode); the hit lists of 8 sampled queries == the oracle's, and
+    dense records of those 8 queries x all sets are bit-exact."""
+    r = text_run
+    w, p = r["w"], r["p"]
+    if "F" not in r:
+        r["F"] = oracle.oph_sketch(w.offsets, w.ids, w.vocab_size, p["k"], p["perm_seed"])
+        r["H"] = oracle.hoph_sketch(w.offsets, w.ids, w.vocab_size, r["glay"], p["hoph_kprime"], p["perm_seed"])
+    sample = [0, 1, 7, 100, 333, 500, 998, 999]
+    qo_np = oracle.oph_sketch(w.q_offsets, w.q_ids, w.vocab_size, p["k"], p["perm_seed"])
+    qh_np = oracle.hoph_sketch(w.q_offsets, w.q_ids, w.vocab_size, r["glay"], p["hoph_kprime"], p["perm_seed"])
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    lay = og.flat_layout(w.vocab_size, p["k"], p["kprime"])
+    if method == "hoph":
+        hits = gpu_threshold_hits(method, r["qh"], r["sh"], layout=r["hier"], **kw)
+        want = oracle_records(method, qh_np[sample], r["H"], kprime=p["hoph_kprime"], L=len(r["glay"]), **kw)
+    else:
+        hits = gpu_threshold_hits(method, r["qo"], r["so"], layout=lay, **kw)
+        want = oracle_records(method, qo_np[sample], r["F"], k=p["k"], kprime=p["kprime"], **kw)
+    got = [(int(h["query"]), int(h["set_id"])) for h in hits if int(h["query"]) in sample]
+    exp = [(sample[q], s) for q, s in oracle.threshold_list(want)]
+    assert got == exp
+    # every planted duplicate of a sampled query with high J is found by full OPH
+    if method == "full":
+        planted = {(int(q), int(s)) for q, s, i, u in w.planted if q in sample and i / u >= 0.9}
+        assert planted <= set(got)
+    # dense records of the first sampled queries (a contiguous query subview)
+    q8 = subview(r["qh"] if method == "hoph" else r["qo"], 8)
+    if method == "hoph":
+        g = gpu_dense(method, q8, r["sh"], layout=r["hier"], **kw)
+        o8 = oracle_records(method, qh_np[:8], r["H"], kprime=p["hoph_kprime"], L=len(r["glay"]), **kw)
+    else:
+        g = gpu_dense(method, q8, r["so"], layout=lay, **kw)
+        o8 = oracle_records(method, qo_np[:8], r["F"], k=p["k"], kprime=p["kprime"], **kw)
+    assert_records_equal(g, o8, f"text {method}")
+
+
+def test_text_minwise_subset(text_run):
+    """MinWise sketches (sampled 20,000 sets) and scoring of 32 queries."""
+    r = text_run
+    w, p = r["w"], r["p"]
+    n = 20_000
+    offs = w.offsets[: n + 1]
+    sets = og.SetCollection.from_numpy(offs, w.ids[: int(offs[-1])])
+    mw = og.minwise_build_sketches(sets, w.vocab_size, p["perm_seed"], p["mw_k"])
+    MW, fl = oracle.minwise_sketch(offs, w.ids, w.vocab_size, p["mw_k"], p["perm_seed"])
+    assert (mw.numpy() == MW).all()
+    qoffs = w.q_offsets[:33]
+    qs = og.SetCollection.from_numpy(qoffs, w.q_ids[: int(qoffs[-1])])
+    qmw = og.minwise_build_sketches(qs, w.vocab_size, p["perm_seed"], p["mw_k"])
+    QMW, qfl = oracle.minwise_sketch(qoffs, w.q_ids, w.vocab_size, p["mw_k"], p["perm_seed"])
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"])
+    assert_records_equal(gpu_dense("minwise", qmw, mw, **kw),
+                         oracle_records("minwise", QMW, MW, qflags=qfl, sflags=fl, **kw), "text minwise")

@@ -221,18 +221,23 @@ def _lognormal_sizes(rng, n, mean=400.0, sigma=0.8):
 
 
 def text_like(seed: int = 2, n_sets: int = 200_000, n_queries: int = 1000,
-              planted_frac: float = 0.01) -> Workload:
+              planted_frac: float = 0.01, shard: int = 0) -> Workload:
     """configs[1]: 200,000 shingle sets over 2^32, sizes lognormal(mean 400,
     sigma 0.8), 1,000 queries, 1% of the sets planted duplicates at
-    J ~ U[0.6, 0.98]; k=256."""
-    rng = np.random.default_rng(seed)
+    J ~ U[0.6, 0.98]; k=256.
+
+    The query batch depends on `seed` only; the collection on (seed, shard),
+    so shard r of a multi-GPU run is an independent text-like collection of
+    n_sets sets with its own planted duplicates of the SAME queries."""
     V = 2 ** 32
     draw = _uniform_sampler(V)
-    q_off, q_ids = sample_sets(rng, _lognormal_sizes(rng, n_queries), V, draw)
+    rq = np.random.default_rng(seed)
+    q_off, q_ids = sample_sets(rq, _lognormal_sizes(rq, n_queries), V, draw)
+    rng = np.random.default_rng([seed, shard])
     n_pl = int(round(planted_frac * n_sets))
     planted_sets, meta = [], []
     for j in range(n_pl):
-        q = j % n_queries
+        q = (j + shard * n_pl) % n_queries
         qv = q_ids[int(q_off[q]):int(q_off[q + 1])]
         p, inter, union = plant_duplicate(rng, qv, float(rng.uniform(0.6, 0.98)), V, draw)
         planted_sets.append(p)
