@@ -285,7 +285,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    launches = count_launches(step)
+    launches = None if args.no_launch_count else count_launches(step)
 
     # ---------------- timed region: device inputs resident in HBM
     K = args.steps
@@ -436,6 +436,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-launch-count", action="store_true", help="skip the CUPTI launch count (use under ncu)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -348,9 +348,12 @@ size_t surv_region_bytes(uint64_t cap) { return 2 * (align256(cap * 4) * 3 + ali
 // largest survivor capacity that fits in ws_bytes
 uint64_t cap_from_ws(size_t ws_bytes, size_t fixed) {
     if (ws_bytes <= fixed) return 0;
-    uint64_t cap = (ws_bytes - fixed) / kSurvBytes;
-    while (cap > 0 && fixed + surv_region_bytes(cap) > ws_bytes) cap -= std::max<uint64_t>(1, cap / 1024);
-    return cap;
+    uint64_t lo = 0, hi = (ws_bytes - fixed) / kSurvBytes + 1;
+    while (lo + 1 < hi) {  // invariant: lo fits, hi does not
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (fixed + surv_region_bytes(mid) <= ws_bytes) lo = mid; else hi = mid;
+    }
+    return lo;
 }
 
 // ---------------------------------------------------------------- the compare driver

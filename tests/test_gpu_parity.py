@@ -176,7 +176,8 @@ def test_ragged_and_edges(V, k, kp, hkp, seed):
     sets = [rng.choice(V, size=min(int(s), V), replace=False) if s else [] for s in sizes]
     if V <= 4097:
         sets[3] = np.arange(V)
-    qsets = [sets[i] if i % 3 == 0 else rng.choice(V, size=int(rng.integers(0, 60)), replace=False) for i in range(nq)]
+    qsets = [sets[i] if i % 3 == 0 else rng.choice(V, size=min(V, int(rng.integers(0, 60))), replace=False)
+             for i in range(nq)]
     qsets[1] = []
     offs, ids = make_csr(sets)
     qoffs, qids = make_csr(qsets)
