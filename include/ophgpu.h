@@ -120,8 +120,21 @@ typedef struct {
     uint32_t t_num, t_den;
     double epsilon;
     uint32_t empty_mode; /* OPH_EMPTY_EITHER | OPH_EMPTY_JOINT */
-    uint32_t pad;
+    uint32_t strategy;   /* OPH_STRATEGY_*: how the collection scan finds matched bins (results identical) */
 } oph_params;
+
+/* Collection-scan strategies; every strategy returns
+ * identical results.
+ *   AUTO : PROBE when it applies (threshold results, and pairs with no matched
+ *          bin are decided NotSimilar at the scanned level), else BRUTE.
+ *   BRUTE: every (query, set, bin) equality is tested (register-blocked
+ *          query tiles; cost ~ Q N bins; best when most pairs share bins).
+ *   PROBE: per bin, the query values are hashed into a table; each set bin
+ *          probes it, so only matching (query, set, bin) triples cost work
+ *          (cost ~ N bins + matches; best for low background similarity).
+ *          Sets matching more than 16 distinct queries are re-scanned by
+ *          BRUTE. */
+enum { OPH_STRATEGY_AUTO = 0, OPH_STRATEGY_BRUTE = 1, OPH_STRATEGY_PROBE = 2 };
 
 /* One scored pair (20 bytes).
  *   full OPH : n_mb = N_mb, n_excl = excluded bins, over all k bins (Eq. 1-4)

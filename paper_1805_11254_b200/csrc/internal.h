@@ -99,7 +99,43 @@ struct ScanArgs {
     OutArgs out;
     SurvList surv;
     unsigned long long *surv_count;
-    uint32_t is_last_level; // unused by the scan (kept for symmetry)
+    // list mode: the sets to scan are set_list[0 .. *list_count) (PROBE overflow sets)
+    const uint32_t *set_list;
+    const unsigned long long *list_count;
+};
+
+// PROBE strategy: per scanned bin b, the chunk's query values are hashed into
+// an open-addressing table T_b of 2^log2S slots, slot = value << 32 | (q+1)
+// (0 = free, linear probing; duplicates occupy separate slots).
+struct TableArgs {
+    const uint32_t *QT;     // prepared queries, bin-major [nb][ldq]
+    const uint8_t *qflags;  // MinWise query flags (flagged queries never match)
+    uint64_t ldq;
+    uint32_t q_col0, nq, nscan, log2S;
+    uint32_t minwise;
+    unsigned long long *table;  // [nscan][2^log2S]
+};
+
+constexpr int kProbeList = 16;  // distinct matched queries tracked per set before falling back to BRUTE
+
+struct ProbeArgs {
+    const uint32_t *F, *E;
+    const uint8_t *sflags;
+    uint64_t n_sets, ld;
+    const unsigned long long *table;
+    uint32_t log2S, nscan;
+    const uint32_t *QEM;    // query masks, query-major [n_q][nw]
+    const uint8_t *qflags;  // MinWise query flags, indexed by global query
+    uint32_t nw, nbins_total;
+    uint32_t q_col0;        // global index of the chunk's first query
+    uint32_t method, final_, level, joint, t_num, t_den;
+    uint64_t w1, acc;
+    int64_t rej;
+    OutArgs out;
+    SurvList surv;
+    unsigned long long *surv_count;
+    uint32_t *ovf_list;     // sets that matched more than kProbeList queries
+    unsigned long long *ovf_count;
 };
 
 struct LevelArgs {
@@ -139,6 +175,8 @@ cudaError_t launch_build(const BuildArgs &a, cudaStream_t st);
 cudaError_t launch_minwise(const MinwiseArgs &a, cudaStream_t st);
 cudaError_t launch_prep(const PrepArgs &a, cudaStream_t st);
 cudaError_t launch_scan(const ScanArgs &a, uint32_t B, cudaStream_t st);
+cudaError_t launch_table(const TableArgs &a, cudaStream_t st);
+cudaError_t launch_probe(const ProbeArgs &a, cudaStream_t st);
 cudaError_t launch_level(const LevelArgs &a, cudaStream_t st);
 size_t select_temp_bytes(uint64_t n);
 cudaError_t run_select(const oph_hit *in, uint64_t n, uint32_t mode, uint32_t topk, uint32_t k_bins, oph_hit *out,

@@ -308,21 +308,33 @@ bool bins_fit(uint64_t len, uint32_t nb) { return ceil_div(len, nb) <= 0xFFFFFFF
 struct Ws {
     uint32_t *QT, *QE, *QM, *QEM;
     uint8_t *qflags;
-    unsigned long long *counters;  // [2][kMaxGroups + 2]
+    unsigned long long *counters;  // [kMaxGroups + 2] level counters, then the PROBE overflow counter
+    unsigned long long *table;     // PROBE tables [nb][S]
+    uint32_t *ovf_list;            // PROBE overflow sets [n_sets]
     SurvList list[2];
     uint64_t ldq, cap;
 };
 
-size_t ws_fixed_bytes(uint64_t n_q, uint32_t nb) {
+constexpr uint32_t kCounters = kMaxGroups + 4;
+
+// PROBE table slots per bin for a chunk of nq queries: load factor <= 1/4
+uint32_t probe_log2S(uint64_t nq) {
+    uint32_t l = 4;
+    while ((1ull << l) < 4 * nq) l++;
+    return l;
+}
+
+size_t ws_fixed_bytes(uint64_t n_q, uint64_t n_sets, uint32_t nb) {
     const uint64_t ldq = ceil_div(n_q ? n_q : 1, 32) * 32;
     const uint64_t nw = ceil_div(nb, 32);
     return align256(nb * ldq * 4) + align256(nw * ldq * 4) + align256(n_q * (uint64_t)nb * 4) +
-           align256(n_q * nw * 4) + align256(ldq) + align256(2 * (kMaxGroups + 2) * 8);
+           align256(n_q * nw * 4) + align256(ldq) + align256(kCounters * 8) +
+           align256((uint64_t)nb * (1ull << probe_log2S(ldq)) * 8) + align256(n_sets * 4);
 }
 
 constexpr uint64_t kSurvBytes = 2 * (4 + 4 + 8 + 4);  // two lists, per entry
 
-Ws carve_ws(void *base, uint64_t n_q, uint32_t nb, uint64_t cap) {
+Ws carve_ws(void *base, uint64_t n_q, uint64_t n_sets, uint32_t nb, uint64_t cap) {
     Ws w{};
     char *p = (char *)base;
     w.ldq = ceil_div(n_q ? n_q : 1, 32) * 32;
@@ -332,7 +344,9 @@ Ws carve_ws(void *base, uint64_t n_q, uint32_t nb, uint64_t cap) {
     w.QM = (uint32_t *)p; p += align256(n_q * (uint64_t)nb * 4);
     w.QEM = (uint32_t *)p; p += align256(n_q * nw * 4);
     w.qflags = (uint8_t *)p; p += align256(w.ldq);
-    w.counters = (unsigned long long *)p; p += align256(2 * (kMaxGroups + 2) * 8);
+    w.counters = (unsigned long long *)p; p += align256(kCounters * 8);
+    w.table = (unsigned long long *)p; p += align256((uint64_t)nb * (1ull << probe_log2S(w.ldq)) * 8);
+    w.ovf_list = (uint32_t *)p; p += align256(n_sets * 4);
     w.cap = cap;
     for (int i = 0; i < 2; i++) {
         w.list[i].q = (uint32_t *)p; p += align256(cap * 4);
@@ -364,6 +378,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     oph_status st;
     if ((st = check_view(Qv, !mw, mw)) || (st = check_view(Sv, !mw, mw)) || (st = check_params(p))) return st;
     if (!res || !res->d_hits || !res->d_count || res->mode > OPH_RES_DENSE) return OPH_EINVAL;
+    if (p->strategy > OPH_STRATEGY_PROBE) return OPH_EINVAL;
     if (Qv->seed != Sv->seed || Qv->vocab_size != Sv->vocab_size || Qv->n_bins != Sv->n_bins) return OPH_EINCOMPAT;
     const uint32_t nb = Qv->n_bins;
     const uint32_t nw = (uint32_t)ceil_div(nb, 32);
@@ -383,7 +398,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         if (method == OPH_METHOD_HOPH && nlev > 1 && plan.lam == 0) return OPH_EINVAL;
     }
 
-    const size_t fixed = ws_fixed_bytes(n_q, nb);
+    const size_t fixed = ws_fixed_bytes(n_q, n_s, nb);
     uint64_t chunk = ceil_div(n_q, 32) * 32;
     uint64_t cap = 0;
     const bool levels = (method == OPH_METHOD_GOPH || method == OPH_METHOD_HOPH) && plan.l0 < nlev;
@@ -395,7 +410,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     } else if (ws_bytes < fixed) {
         return OPH_ENOMEM;
     }
-    Ws w = carve_ws(d_ws, n_q, nb, cap);
+    Ws w = carve_ws(d_ws, n_q, n_s, nb, cap);
 
     PrepArgs pa{};
     pa.values = Qv->d_values;
@@ -469,6 +484,11 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     }
     if (((size_t)std::min<uint32_t>(s.nscan, 512) + s.nw_load + 1) * 32 * 4 > 227 * 1024) return OPH_EINVAL;
 
+    // PROBE applies to threshold results when a pair with no matched bin is
+    // decided NotSimilar at the scanned level (final verdicts: N_mb = 0 is
+    // never >= T > 0; otherwise the level must reject state 0)
+    const bool probe = p->strategy != OPH_STRATEGY_BRUTE && !out.dense && (s.final_ || s.rej >= 0);
+
     LevelArgs la{};
     if (levels) {
         la.F = Sv->d_values;
@@ -490,18 +510,72 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         la.res = out;
     }
 
+    unsigned long long *ovf_count = w.counters + kMaxGroups + 2;
     for (uint64_t q0 = 0; q0 < n_q; q0 += chunk) {
         const uint64_t nq = std::min<uint64_t>(chunk, n_q - q0);
         s.q_col0 = (uint32_t)q0;
         s.nq = (uint32_t)nq;
         if (levels) {
-            e = cudaMemsetAsync(w.counters, 0, (kMaxGroups + 2) * 8, stream);
-            if (e != cudaSuccess) return OPH_ECUDA;
             s.surv = w.list[plan.l0 % 2];
             s.surv_count = w.counters + plan.l0;
         }
-        e = launch_scan(s, 32, stream);
-        if (e != cudaSuccess) return OPH_ECUDA;
+        if (levels || probe) {
+            e = cudaMemsetAsync(w.counters, 0, kCounters * 8, stream);
+            if (e != cudaSuccess) return OPH_ECUDA;
+        }
+        if (probe) {
+            const uint32_t log2S = probe_log2S(nq);
+            e = cudaMemsetAsync(w.table, 0, (size_t)s.nscan * (1ull << log2S) * 8, stream);
+            if (e != cudaSuccess) return OPH_ECUDA;
+            TableArgs ta{};
+            ta.QT = w.QT;
+            ta.qflags = w.qflags;
+            ta.ldq = w.ldq;
+            ta.q_col0 = (uint32_t)q0;
+            ta.nq = (uint32_t)nq;
+            ta.nscan = s.nscan;
+            ta.log2S = log2S;
+            ta.minwise = mw;
+            ta.table = w.table;
+            if ((e = launch_table(ta, stream)) != cudaSuccess) return OPH_ECUDA;
+            ProbeArgs pr{};
+            pr.F = s.F;
+            pr.E = s.E;
+            pr.sflags = s.sflags;
+            pr.n_sets = n_s;
+            pr.ld = s.ld;
+            pr.table = w.table;
+            pr.log2S = log2S;
+            pr.nscan = s.nscan;
+            pr.QEM = w.QEM;
+            pr.qflags = w.qflags;
+            pr.nw = nw;
+            pr.nbins_total = nb;
+            pr.q_col0 = (uint32_t)q0;
+            pr.method = method;
+            pr.final_ = s.final_;
+            pr.level = s.level;
+            pr.joint = s.joint;
+            pr.t_num = s.t_num;
+            pr.t_den = s.t_den;
+            pr.w1 = s.w1;
+            pr.acc = s.acc;
+            pr.rej = s.rej;
+            pr.out = out;
+            pr.surv = s.surv;
+            pr.surv_count = s.surv_count;
+            pr.ovf_list = w.ovf_list;
+            pr.ovf_count = ovf_count;
+            if ((e = launch_probe(pr, stream)) != cudaSuccess) return OPH_ECUDA;
+            // sets with too many distinct matched queries: BRUTE over that list (device-side count)
+            ScanArgs sl = s;
+            sl.set_list = w.ovf_list;
+            sl.list_count = ovf_count;
+            if ((e = launch_scan(sl, 32, stream)) != cudaSuccess) return OPH_ECUDA;
+        } else {
+            e = launch_scan(s, 32, stream);
+            if (e != cudaSuccess) return OPH_ECUDA;
+        }
         if (!levels) continue;
         for (uint32_t l = plan.l0 + 1; l <= nlev; l++) {
             la.level = l;
@@ -644,7 +718,7 @@ oph_status minwise_build_sketches(const oph_sets *sets, uint64_t V, uint64_t see
 oph_status oph_workspace_size(uint32_t method, uint64_t n_q, uint64_t n_sets, uint32_t n_bins, uint64_t cap,
                               size_t *bytes) {
     if (!bytes || method > OPH_METHOD_MINWISE || n_bins == 0) return OPH_EINVAL;
-    size_t b = ws_fixed_bytes(n_q, n_bins);
+    size_t b = ws_fixed_bytes(n_q, n_sets, n_bins);
     if (method == OPH_METHOD_GOPH || method == OPH_METHOD_HOPH) b += surv_region_bytes(std::max<uint64_t>(cap, 32 * n_sets));
     *bytes = b;
     return OPH_OK;

@@ -31,7 +31,10 @@ __device__ __forceinline__ uint32_t psi_pass(const uint32_t (&kappa)[4], const u
     for (int r = 0; r < 4; r++) {
         x = (x ^ kappa[r]) * mu[r];
         if (!W32) x &= mask;
-        x ^= x >> shift;
+        // w = 32: x >> 16 as a high multiply, which issues on the FMA pipe and
+        // relieves the ALU pipe that the xors already saturate (rounds 0 and 2)
+        if (W32 && (r & 1) == 0) x ^= __umulhi(x, 1u << 16);
+        else x ^= x >> shift;
     }
     return x;
 }
@@ -393,8 +396,9 @@ __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool 
     }
 }
 
-template <int B, int SPT>
+template <int B, int SPT, bool LIST>
 __global__ void __launch_bounds__(128) scan_kernel(const __grid_constant__ ScanArgs a) {
+    static_assert(!LIST || SPT == 1, "list mode scans one gathered set per thread");
     constexpr int U = 4;  // bins in flight per thread
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t qs_bins = min(a.nscan, kScanChunk);
@@ -416,11 +420,15 @@ __global__ void __launch_bounds__(128) scan_kernel(const __grid_constant__ ScanA
     __syncthreads();
 
     const uint64_t tile_sets = 128ull * SPT;
-    const uint64_t ntiles = (a.n_sets + tile_sets - 1) / tile_sets;
-    const uint64_t t_end = min(ntiles, (uint64_t)(blockIdx.y + 1) * a.tiles_per_cta);
-    for (uint64_t t = (uint64_t)blockIdx.y * a.tiles_per_cta; t < t_end; t++) {
-        const uint64_t s0 = t * tile_sets + threadIdx.x * SPT;
-        const bool active = s0 < a.n_sets;
+    const uint64_t n_items = LIST ? *a.list_count : a.n_sets;
+    const uint64_t ntiles = (n_items + tile_sets - 1) / tile_sets;
+    const uint64_t t_first = LIST ? blockIdx.y : (uint64_t)blockIdx.y * a.tiles_per_cta;
+    const uint64_t t_end = LIST ? ntiles : min(ntiles, (uint64_t)(blockIdx.y + 1) * a.tiles_per_cta);
+    const uint64_t t_step = LIST ? gridDim.y : 1;
+    for (uint64_t t = t_first; t < t_end; t += t_step) {
+        const uint64_t i0 = t * tile_sets + threadIdx.x * SPT;
+        const bool active = i0 < n_items;
+        const uint64_t s0 = LIST ? (active ? a.set_list[i0] : 0ull) : i0;
         uint32_t cnt[SPT][B];
 #pragma unroll
         for (int j = 0; j < SPT; j++)
@@ -445,7 +453,7 @@ __global__ void __launch_bounds__(128) scan_kernel(const __grid_constant__ ScanA
 #pragma unroll
         for (int j = 0; j < SPT; j++) {
             const uint64_t s = s0 + j;
-            const bool sv = active && s < a.n_sets;
+            const bool sv = active && (LIST || s < a.n_sets);
             uint32_t hit_mask = 0, surv_mask = 0, dec_mask = 0;
             if (a.final_) {
                 uint32_t ex[B];
@@ -491,7 +499,9 @@ __global__ void __launch_bounds__(128) scan_kernel(const __grid_constant__ ScanA
                         }
                         const uint32_t verdict = (hit_mask >> q) & 1u;
                         const float est = undef ? -1.0f : (float)cnt[j][q] / (float)den;
-                        emit(a.out, valid, (uint32_t)(col0 + q), s, cnt[j][q],
+                        // an empty MinWise set has no sketch: nothing is compared
+                        const uint32_t nmb = (a.method == kMinwise && undef) ? 0u : cnt[j][q];
+                        emit(a.out, valid, (uint32_t)(col0 + q), s, nmb,
                              a.method == kMinwise ? 0u : ex[q], a.level, verdict, undef ? OPH_FLAG_UNDEFINED : 0u, est);
                     }
                 }
@@ -531,6 +541,151 @@ __global__ void __launch_bounds__(128) scan_kernel(const __grid_constant__ ScanA
                         }
                     }
                 }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3' PROBE: the same scan as a hash join.  A query bin matches a set bin
+// only when the values are equal, so instead of testing every (query, set,
+// bin) triple, the chunk's query values of each scanned bin are hashed into
+// a table (table_kernel) and every set bin probes it once (probe_kernel):
+// work ~ N * bins + matches instead of Q * N * bins.  Per set, the matched
+// queries and their counts are collected in shared memory; pairs with no
+// matched bin have N_mb = 0 (full OPH / MinWise: never Similar for T > 0;
+// GOPH / HOPH: the host only picks PROBE when state 0 is rejected at the
+// scanned level), so only listed pairs are decided and emitted.  A set that
+// matches more than kProbeList distinct queries is handed to the BRUTE scan
+// (list mode) instead.  Threshold results only.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t probe_hash(uint32_t v, uint32_t log2S) {
+    return (v * 0x9E3779B1u) >> (32 - log2S);  // Fibonacci hashing
+}
+
+__global__ void table_kernel(const __grid_constant__ TableArgs a) {
+    const uint64_t S = 1ull << a.log2S;
+    const uint64_t n = (uint64_t)a.nscan * a.nq;
+    for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < n;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = (uint32_t)(idx / a.nq), q = (uint32_t)(idx % a.nq);
+        const uint64_t col = (uint64_t)a.q_col0 + q;
+        if (a.minwise && a.qflags[col]) continue;       // an empty query matches nothing
+        const uint32_t v = a.QT[(uint64_t)b * a.ldq + col];
+        if (!a.minwise && v == kQueryEmpty) continue;   // an empty query bin matches nothing
+        const unsigned long long entry = ((unsigned long long)v << 32) | (q + 1u);
+        unsigned long long *T = a.table + (uint64_t)b * S;
+        uint32_t h = probe_hash(v, a.log2S);
+        while (atomicCAS(&T[h], 0ull, entry) != 0ull) h = (h + 1) & (uint32_t)(S - 1);
+    }
+}
+
+constexpr int kProbeThreads = 256;
+constexpr int kProbeUnroll = 8;
+
+__global__ void __launch_bounds__(kProbeThreads) probe_kernel(const __grid_constant__ ProbeArgs a) {
+    __shared__ uint32_t lq[kProbeList][kProbeThreads];  // matched query (chunk-local), per thread column
+    __shared__ uint32_t lc[kProbeList][kProbeThreads];  // its matched-bin count
+    const uint32_t tid = threadIdx.x;
+    const uint32_t smask = (1u << a.log2S) - 1u;
+    const bool mw = a.method == kMinwise;
+    for (uint64_t base = (uint64_t)blockIdx.x * kProbeThreads; base < a.n_sets;
+         base += (uint64_t)gridDim.x * kProbeThreads) {
+        const uint64_t s = base + tid;
+        const bool act = s < a.n_sets && !(mw && a.sflags[s]);
+        int nl = 0;
+        bool ovf = false;
+        if (act) {
+            for (uint32_t b0 = 0; b0 < a.nscan && !ovf; b0 += kProbeUnroll) {
+                uint32_t v[kProbeUnroll];
+                unsigned long long slot[kProbeUnroll];
+#pragma unroll
+                for (int u = 0; u < kProbeUnroll; u++)
+                    v[u] = (b0 + u < a.nscan) ? __ldg(a.F + (uint64_t)(b0 + u) * a.ld + s) : kEmpty;
+#pragma unroll
+                for (int u = 0; u < kProbeUnroll; u++) {
+                    const bool skip = (b0 + u >= a.nscan) || (!mw && v[u] == kEmpty);
+                    slot[u] = skip ? 0ull
+                                   : __ldg(a.table + ((uint64_t)(b0 + u) << a.log2S) + probe_hash(v[u], a.log2S));
+                }
+#pragma unroll
+                for (int u = 0; u < kProbeUnroll; u++) {
+                    if (slot[u] == 0ull || ovf) continue;
+                    const unsigned long long *T = a.table + ((uint64_t)(b0 + u) << a.log2S);
+                    uint32_t h = probe_hash(v[u], a.log2S);
+                    unsigned long long sl = slot[u];
+                    while (sl != 0ull) {
+                        if ((uint32_t)(sl >> 32) == v[u]) {
+                            const uint32_t q = (uint32_t)sl - 1u;
+                            int e = 0;
+                            while (e < nl && lq[e][tid] != q) e++;
+                            if (e < nl) {
+                                lc[e][tid]++;
+                            } else if (nl < kProbeList) {
+                                lq[nl][tid] = q;
+                                lc[nl][tid] = 1;
+                                nl++;
+                            } else {
+                                ovf = true;
+                                break;
+                            }
+                        }
+                        h = (h + 1) & smask;
+                        sl = __ldg(T + h);
+                    }
+                }
+            }
+        }
+        {   // overflowing sets go to the BRUTE list scan
+            const unsigned long long idx = warp_append(act && ovf, a.ovf_count);
+            if (act && ovf) a.ovf_list[idx] = (uint32_t)s;
+        }
+        const int ne = (act && !ovf) ? nl : 0;
+        for (int e = 0; e < kProbeList; e++) {
+            const bool has = e < ne;
+            if (!__any_sync(0xFFFFFFFFu, has)) break;
+            uint32_t q = 0, m = 0, ex = 0, flags = 0, verdict = 0;
+            bool surv = false;
+            float est = -1.0f;
+            uint64_t st = 0;
+            if (has) {
+                q = lq[e][tid];
+                m = lc[e][tid];
+                const uint32_t qg = a.q_col0 + q;
+                if (a.final_) {
+                    uint32_t den;
+                    bool undef;
+                    if (mw) {
+                        den = a.nbins_total;
+                        undef = a.qflags[qg] != 0;
+                    } else {
+                        for (uint32_t w = 0; w < a.nw; w++)
+                            ex += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + w), __ldg(a.E + (uint64_t)w * a.ld + s),
+                                              a.joint, w, a.nbins_total);
+                        den = a.nbins_total - ex;
+                        undef = den == 0;
+                    }
+                    verdict = !undef && (uint64_t)m * a.t_den >= (uint64_t)a.t_num * den;
+                    if (undef) flags = OPH_FLAG_UNDEFINED;
+                    else est = (float)m / (float)den;
+                } else {
+                    st = a.w1 * m;
+                    verdict = st >= a.acc;
+                    surv = !verdict && (int64_t)st > a.rej;
+                    flags = OPH_FLAG_EARLY;
+                    if (verdict)
+                        for (uint32_t w = 0; w * 32 < a.nscan; w++)
+                            ex += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + w), __ldg(a.E + (uint64_t)w * a.ld + s),
+                                              a.joint, w, a.nscan);
+                }
+            }
+            emit(a.out, has, a.q_col0 + q, s, m, ex, a.level, verdict, flags, est);
+            const unsigned long long idx = warp_append(surv, a.surv_count);
+            if (surv) {
+                a.surv.q[idx] = a.q_col0 + q;
+                a.surv.s[idx] = (uint32_t)s;
+                a.surv.state[idx] = st;
+                a.surv.nmb[idx] = m;
             }
         }
     }
@@ -677,30 +832,53 @@ cudaError_t launch_prep(const PrepArgs &a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int B, int SPT>
+template <int B, int SPT, bool LIST>
 static cudaError_t launch_scan_t(const ScanArgs &a0, cudaStream_t st) {
     ScanArgs a = a0;
     const size_t smem = ((size_t)min(a.nscan, kScanChunk) * B + (size_t)a.nw_load * B + B) * 4;
     const uint64_t tile_sets = 128ull * SPT;
-    const uint64_t ntiles = (a.n_sets + tile_sets - 1) / tile_sets;
     const uint32_t qblocks = (a.nq + B - 1) / B;
-    // aim for >= 4 waves of CTAs over 148 SMs, otherwise longest tile runs per CTA
-    const uint64_t want_y = std::max<uint64_t>(1, (148ull * 4 * 4 + qblocks - 1) / qblocks);
-    uint64_t tpc = std::max<uint64_t>(1, (ntiles + want_y - 1) / want_y);
-    tpc = std::min<uint64_t>(tpc, 64);
-    a.tiles_per_cta = (uint32_t)tpc;
-    const uint64_t gy = (ntiles + tpc - 1) / tpc;
+    uint64_t gy;
+    if (LIST) {  // grid-stride over a device-side list: the count is not known on the host
+        gy = std::max<uint64_t>(1, (148ull * 4 + qblocks - 1) / qblocks);
+        a.tiles_per_cta = 1;
+    } else {
+        const uint64_t ntiles = (a.n_sets + tile_sets - 1) / tile_sets;
+        // aim for >= 4 waves of CTAs over 148 SMs, otherwise longest tile runs per CTA
+        const uint64_t want_y = std::max<uint64_t>(1, (148ull * 4 * 4 + qblocks - 1) / qblocks);
+        uint64_t tpc = std::max<uint64_t>(1, (ntiles + want_y - 1) / want_y);
+        tpc = std::min<uint64_t>(tpc, 64);
+        a.tiles_per_cta = (uint32_t)tpc;
+        gy = (ntiles + tpc - 1) / tpc;
+    }
     if (gy > 65535) return cudaErrorInvalidConfiguration;
-    cudaError_t e = cudaFuncSetAttribute(scan_kernel<B, SPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(scan_kernel<B, SPT, LIST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    scan_kernel<B, SPT><<<dim3(qblocks, (unsigned)gy), 128, smem, st>>>(a);
+    scan_kernel<B, SPT, LIST><<<dim3(qblocks, (unsigned)gy), 128, smem, st>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_scan(const ScanArgs &a, uint32_t B, cudaStream_t st) {
     if (a.n_sets == 0 || a.nq == 0) return cudaSuccess;
     (void)B;
-    return launch_scan_t<32, 2>(a, st);
+    if (a.set_list) return launch_scan_t<32, 1, true>(a, st);
+    return launch_scan_t<32, 2, false>(a, st);
+}
+
+cudaError_t launch_table(const TableArgs &a, cudaStream_t st) {
+    const uint64_t n = (uint64_t)a.nscan * a.nq;
+    if (n == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    table_kernel<<<grid, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_probe(const ProbeArgs &a, cudaStream_t st) {
+    if (a.n_sets == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<uint64_t>((a.n_sets + kProbeThreads - 1) / kProbeThreads, 148ull * 8);
+    probe_kernel<<<grid, kProbeThreads, 0, st>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_level(const LevelArgs &a, cudaStream_t st) {

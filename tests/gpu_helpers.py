@@ -52,10 +52,10 @@ def assert_records_equal(gpu, orc, what=""):
 
 
 def gpu_threshold_hits(method, q, s, *, layout=None, t_num, t_den, eps=1e-4, joint=False, capacity=1 << 20,
-                       set_id_base=0, survivor_capacity=0):
+                       set_id_base=0, survivor_capacity=0, strategy=og.OPH_STRATEGY_AUTO):
     """Sorted threshold hit list from the GPU (compare + topk_or_threshold_results)."""
     res = og.Results(capacity)
-    prm = og.params(t_num, t_den, eps, joint)
+    prm = og.params(t_num, t_den, eps, joint, strategy)
     if method == "full":
         og.compare_full(q, s, layout, prm, res, set_id_base=set_id_base)
     elif method == "goph":

@@ -106,21 +106,22 @@ def test_tiny_dense_records(tiny_run, method, joint):
     assert_records_equal(g, want, f"tiny {method} joint={joint}")
 
 
+@pytest.mark.parametrize("strategy", [og.OPH_STRATEGY_BRUTE, og.OPH_STRATEGY_PROBE])
 @pytest.mark.parametrize("method", ["full", "goph", "hoph", "minwise"])
-def test_tiny_threshold_lists(tiny_run, method):
-    """Threshold hit lists (sorted by (query, set_id)) == oracle's, with set_id_base."""
+def test_tiny_threshold_lists(tiny_run, method, strategy):
+    """Threshold hit lists (sorted by (query, set_id)) == oracle's, with set_id_base, for both scan strategies."""
     r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
     kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
     base = 1000
     if method in ("full", "goph"):
         lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
-        hits = gpu_threshold_hits(method, r["qo"], r["so"], layout=lay, set_id_base=base, **kw)
+        hits = gpu_threshold_hits(method, r["qo"], r["so"], layout=lay, set_id_base=base, strategy=strategy, **kw)
         want = oracle_records(method, o["QF"], o["F"], k=p["k"], kprime=p["kprime"], **kw)
     elif method == "hoph":
-        hits = gpu_threshold_hits(method, r["qh"], r["sh"], layout=r["hier"], set_id_base=base, **kw)
+        hits = gpu_threshold_hits(method, r["qh"], r["sh"], layout=r["hier"], set_id_base=base, strategy=strategy, **kw)
         want = oracle_records(method, o["QH"], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw)
     else:
-        hits = gpu_threshold_hits(method, r["qmw"], r["mw"], set_id_base=base, **kw)
+        hits = gpu_threshold_hits(method, r["qmw"], r["mw"], set_id_base=base, strategy=strategy, **kw)
         want = oracle_records(method, o["QMW"][0], o["MW"][0], qflags=o["QMW"][1], sflags=o["MW"][1], **kw)
     got = [(int(h["query"]), int(h["set_id"])) for h in hits]
     assert got == oracle.threshold_list(want, base)
@@ -229,6 +230,56 @@ def test_threshold_and_epsilon_extremes(tiny_run, tn, td, eps):
                          oracle_records("hoph", o["QH"][:40], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw), "hoph")
 
 
+@pytest.mark.parametrize("method", ["full", "goph", "hoph", "minwise"])
+def test_probe_overflow_falls_back_to_brute(method):
+    """40 identical queries (plus 20 others): every set near them matches more
+    than 16 distinct queries, so PROBE hands those sets to the BRUTE list
+    scan; the hit lists still equal the oracle's."""
+    rng = np.random.default_rng(12)
+    V = 1 << 20
+    A = rng.choice(V, size=300, replace=False)
+    sets = []
+    for i in range(700):
+        if i % 7 == 0:  # near-duplicates of A
+            keep = rng.choice(A, size=int(rng.integers(200, 300)), replace=False)
+            sets.append(np.concatenate([keep, rng.choice(V, size=300 - len(keep), replace=False)]))
+        else:
+            sets.append(rng.choice(V, size=int(rng.integers(100, 400)), replace=False))
+    qsets = [A] * 40 + [rng.choice(V, size=250, replace=False) for _ in range(20)]
+    offs, ids = make_csr(sets)
+    qoffs, qids = make_csr(qsets)
+    hier = og.oph_hier_layout_make(V, 1, 1, 32)
+    k, kp = 256, 32
+    _, so, sh = gpu_build(offs, ids, V, 9, k=k, kprime=kp, hier=hier)
+    _, qo, qh = gpu_build(qoffs, qids, V, 9, k=k, kprime=kp, hier=hier)
+    kw = dict(t_num=3, t_den=5, eps=1e-4)
+    lay = og.flat_layout(V, k, kp)
+    if method == "hoph":
+        glay = oracle.hoph_layout(V, 1, 1, 32)
+        H = oracle.hoph_sketch(offs, ids, V, glay, 32, 9)
+        QH = oracle.hoph_sketch(qoffs, qids, V, glay, 32, 9)
+        want = oracle_records(method, QH, H, kprime=32, L=len(glay), **kw)
+        hits = gpu_threshold_hits(method, qh, sh, layout=hier, strategy=og.OPH_STRATEGY_PROBE, **kw)
+    elif method == "minwise":
+        st, qt = og.SetCollection.from_numpy(offs, ids), og.SetCollection.from_numpy(qoffs, qids)
+        mw, qmw = og.minwise_build_sketches(st, V, 9, 128), og.minwise_build_sketches(qt, V, 9, 128)
+        MW, fl = oracle.minwise_sketch(offs, ids, V, 128, 9)
+        QMW, qfl = oracle.minwise_sketch(qoffs, qids, V, 128, 9)
+        want = oracle_records(method, QMW, MW, qflags=qfl, sflags=fl, **kw)
+        hits = gpu_threshold_hits(method, qmw, mw, strategy=og.OPH_STRATEGY_PROBE, **kw)
+    else:
+        F = oracle.oph_sketch(offs, ids, V, k, 9)
+        QF = oracle.oph_sketch(qoffs, qids, V, k, 9)
+        want = oracle_records(method, QF, F, k=k, kprime=kp, **kw)
+        hits = gpu_threshold_hits(method, qo, so, layout=lay, strategy=og.OPH_STRATEGY_PROBE, **kw)
+    got = [(int(h["query"]), int(h["set_id"])) for h in hits]
+    assert got == oracle.threshold_list(want)
+    assert len(got) >= 40 * 50
+    for h in hits[:500]:
+        wr = want[h["query"], h["set_id"]]
+        assert (h["n_mb"], h["n_excl"], h["groups"], h["flags"]) == (wr["n_mb"], wr["n_excl"], wr["groups"], wr["flags"])
+
+
 def test_empty_inputs():
     """Zero queries or zero sets: nothing is written, no error."""
     offs, ids = make_csr([[1, 2, 3]])
@@ -266,8 +317,9 @@ def test_text_sketches_full_collection(text_run):
     r["F"], r["H"] = F, H
 
 
+@pytest.mark.parametrize("strategy", [og.OPH_STRATEGY_AUTO, og.OPH_STRATEGY_BRUTE])
 @pytest.mark.parametrize("method", ["full", "goph", "hoph"])
-def test_text_full_size_sampled_queries(text_run, method):
+def test_text_full_size_sampled_queries(text_run, method, strategy):
     """All 1,000 queries x 200,000 sets in the bench launch configuration
     (threshold mode); the hit lists of 8 sampled queries == the oracle's, and
     dense records of those 8 queries x all sets are bit-exact."""
@@ -282,10 +334,10 @@ def test_text_full_size_sampled_queries(text_run, method):
     kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
     lay = og.flat_layout(w.vocab_size, p["k"], p["kprime"])
     if method == "hoph":
-        hits = gpu_threshold_hits(method, r["qh"], r["sh"], layout=r["hier"], **kw)
+        hits = gpu_threshold_hits(method, r["qh"], r["sh"], layout=r["hier"], strategy=strategy, **kw)
         want = oracle_records(method, qh_np[sample], r["H"], kprime=p["hoph_kprime"], L=len(r["glay"]), **kw)
     else:
-        hits = gpu_threshold_hits(method, r["qo"], r["so"], layout=lay, **kw)
+        hits = gpu_threshold_hits(method, r["qo"], r["so"], layout=lay, strategy=strategy, **kw)
         want = oracle_records(method, qo_np[sample], r["F"], k=p["k"], kprime=p["kprime"], **kw)
     got = [(int(h["query"]), int(h["set_id"])) for h in hits if int(h["query"]) in sample]
     exp = [(sample[q], s) for q, s in oracle.threshold_list(want)]
