@@ -31,10 +31,7 @@ __device__ __forceinline__ uint32_t psi_pass(const uint32_t (&kappa)[4], const u
     for (int r = 0; r < 4; r++) {
         x = (x ^ kappa[r]) * mu[r];
         if (!W32) x &= mask;
-        // w = 32: x >> 16 as a high multiply, which issues on the FMA pipe and
-        // relieves the ALU pipe that the xors already saturate (rounds 0 and 2)
-        if (W32 && (r & 1) == 0) x ^= __umulhi(x, 1u << 16);
-        else x ^= x >> shift;
+        x ^= x >> shift;
     }
     return x;
 }
