@@ -145,11 +145,12 @@ struct LevelArgs {
     const uint32_t *QEM;    // query masks, query-major [n_q][nw]
     uint32_t nb, nw;
     uint32_t method;        // kGoph | kHoph
-    uint32_t level;         // 1-indexed group processed by this launch
+    uint32_t level;         // first 1-indexed group processed by this launch
+    uint32_t level_last;    // last group processed by this launch (<= nlev)
     uint32_t nlev;          // n (GOPH) or L (HOPH)
     uint32_t kp, joint, t_num, t_den;
-    uint64_t acc;
-    int64_t rej;
+    uint64_t acc[kMaxGroups];  // per-level thresholds, index l-1
+    int64_t rej[kMaxGroups];
     uint64_t c[kMaxGroups]; // group weights (GOPH: 1)
     unsigned __int128 lam;  // lcm(1..kp) for the HOPH final verdict
     SurvList in, out;

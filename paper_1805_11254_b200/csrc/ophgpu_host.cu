@@ -316,6 +316,7 @@ struct Ws {
 };
 
 constexpr uint32_t kCounters = kMaxGroups + 4;
+constexpr uint32_t kLevelsPerLaunch = 4;  // GOPH/HOPH levels per survivor-kernel launch
 
 // PROBE table slots per bin for a chunk of nq queries: load factor <= 1/4
 uint32_t probe_log2S(uint64_t nq) {
@@ -506,6 +507,10 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         la.t_num = p->t_num;
         la.t_den = p->t_den;
         for (uint32_t j = 0; j < nlev; j++) la.c[j] = plan.c[j];
+        for (uint32_t l = 1; l < nlev; l++) {
+            la.acc[l - 1] = plan.thr[l - 1].acc;
+            la.rej[l - 1] = plan.thr[l - 1].rej;
+        }
         la.lam = plan.lam;
         la.res = out;
     }
@@ -577,16 +582,15 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
             if (e != cudaSuccess) return OPH_ECUDA;
         }
         if (!levels) continue;
-        for (uint32_t l = plan.l0 + 1; l <= nlev; l++) {
+        // later levels, kLevelsPerLaunch per launch, survivors compacted between launches
+        for (uint32_t l = plan.l0 + 1; l <= nlev; l += kLevelsPerLaunch) {
+            const uint32_t l_last = std::min(nlev, l + kLevelsPerLaunch - 1);
             la.level = l;
-            if (l < nlev) {
-                la.acc = plan.thr[l - 1].acc;
-                la.rej = plan.thr[l - 1].rej;
-            }
+            la.level_last = l_last;
             la.in = w.list[(l - 1) % 2];
-            la.out = w.list[l % 2];
+            la.out = w.list[l_last % 2];
             la.count_in = w.counters + (l - 1);
-            la.count_out = w.counters + l;
+            la.count_out = w.counters + l_last;
             e = launch_level(la, stream);
             if (e != cudaSuccess) return OPH_ECUDA;
         }

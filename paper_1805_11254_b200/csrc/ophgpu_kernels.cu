@@ -76,6 +76,9 @@ __device__ __forceinline__ uint64_t splitmix64_mix(uint64_t z) {
 template <bool W32>
 __global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ BuildArgs a, uint32_t SB) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // group table in shared memory: lanes index it divergently, which would
+    // serialise on the constant cache if read from the kernel parameters
+    __shared__ RangeBins grp[kMaxGroups];
     uint64_t *offs = reinterpret_cast<uint64_t *>(smem_raw);             // [SB+1]
     uint32_t *so = reinterpret_cast<uint32_t *>(offs + SB + 1);          // [SB][k+1]
     const uint32_t kst = a.k + 1;
@@ -86,6 +89,8 @@ __global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ Buil
     const uint64_t s0 = (uint64_t)blockIdx.x * SB;
     const uint32_t nloc = (uint32_t)min((uint64_t)SB, a.n_sets - s0);
     for (uint32_t i = threadIdx.x; i <= nloc; i += blockDim.x) offs[i] = a.offsets[s0 + i];
+    if (a.do_hier)
+        for (uint32_t i = threadIdx.x; i < a.L; i += blockDim.x) grp[i] = a.grp[i];
     if (a.do_flat)
         for (uint32_t i = threadIdx.x; i < SB * kst; i += blockDim.x) so[i] = kEmpty;
     if (a.do_hier)
@@ -111,9 +116,9 @@ __global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ Buil
             uint32_t g0 = 0, g1 = a.L - 1;  // largest g with start_g <= p
             while (g0 < g1) {
                 const uint32_t mid = (g0 + g1 + 1) >> 1;
-                if (a.grp[mid].start <= p) g0 = mid; else g1 = mid - 1;
+                if (grp[mid].start <= p) g0 = mid; else g1 = mid - 1;
             }
-            range_bin(a.grp[g0], a.kp, p, bin, off);
+            range_bin(grp[g0], a.kp, p, bin, off);
             atomicMin(&sh[lo * hst + g0 * a.kp + bin], off);
         }
     }
@@ -718,79 +723,88 @@ __device__ __forceinline__ uint32_t group_excl(const LevelArgs &a, uint32_t q, u
     return ex;
 }
 
+// levels [level, level_last] per launch: a warp walks its 32 survivors level
+// by level (lanes that stopped idle), emitting decided pairs at every level;
+// pairs still undecided after level_last are compacted into the next list.
 __global__ void __launch_bounds__(256) level_kernel(const __grid_constant__ LevelArgs a) {
     const unsigned long long n = *a.count_in;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    const bool last = a.level == a.nlev;
     for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n;
          base += stride) {
         const unsigned long long i = base + (threadIdx.x & 31u);
-        const bool act = i < n;
-        uint32_t q = 0, s = 0, nmb = 0, M = 0;
+        bool alive = i < n;
+        uint32_t q = 0, s = 0, nmb = 0;
         uint64_t st = 0;
-        if (act) {
+        if (alive) {
             q = a.in.q[i];
             s = a.in.s[i];
             st = a.in.state[i];
             nmb = a.in.nmb[i];
-            M = group_matches(a, q, s, a.level - 1);
-            nmb += M;
-            st += a.c[a.level - 1] * M;
         }
-        if (last) {
-            uint32_t verdict = 0, flags = 0, ex_tot = 0;
-            float est = -1.0f;
-            if (act) {
-                if (a.method == kGoph) {
-                    for (uint32_t g = 0; g < a.nlev; g++) ex_tot += group_excl(a, q, s, g);
-                    const uint32_t den = a.nb - ex_tot;
-                    if (den == 0) {
-                        flags = OPH_FLAG_UNDEFINED;
+        for (uint32_t l = a.level; l <= a.level_last; l++) {
+            if (!__any_sync(0xFFFFFFFFu, alive)) break;
+            uint32_t M = 0;
+            if (alive) {
+                M = group_matches(a, q, s, l - 1);
+                nmb += M;
+                st += a.c[l - 1] * M;
+            }
+            if (l == a.nlev) {  // the last group: final verdict
+                uint32_t verdict = 0, flags = 0, ex_tot = 0;
+                float est = -1.0f;
+                if (alive) {
+                    if (a.method == kGoph) {
+                        for (uint32_t g = 0; g < a.nlev; g++) ex_tot += group_excl(a, q, s, g);
+                        const uint32_t den = a.nb - ex_tot;
+                        if (den == 0) {
+                            flags = OPH_FLAG_UNDEFINED;
+                        } else {
+                            verdict = (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
+                            est = (float)nmb / (float)den;
+                        }
                     } else {
-                        verdict = (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
-                        est = (float)nmb / (float)den;
-                    }
-                } else {
-                    // HOPH estimator: sum_j c_j m_j / d_j over groups with d_j > 0, exact with the
-                    // common denominator lam = lcm(1..kp) (R21, R22)
-                    unsigned __int128 num = 0;
-                    uint64_t csum = 0;
-                    for (uint32_t g = 0; g < a.nlev; g++) {
-                        const uint32_t m = (g == a.level - 1) ? M : group_matches(a, q, s, g);
-                        const uint32_t ex = group_excl(a, q, s, g);
-                        ex_tot += ex;
-                        const uint32_t d = a.kp - ex;
-                        if (d == 0) continue;
-                        num += (unsigned __int128)a.c[g] * m * (a.lam / d);
-                        csum += a.c[g];
-                    }
-                    if (csum == 0) {
-                        flags = OPH_FLAG_UNDEFINED;
-                    } else {
-                        verdict = num * a.t_den >= (unsigned __int128)a.t_num * a.lam * csum;
-                        est = (float)((double)num / ((double)a.lam * (double)csum));
+                        // HOPH estimator: sum_j c_j m_j / d_j over groups with d_j > 0, exact with
+                        // the common denominator lam = lcm(1..kp) (R21, R22)
+                        unsigned __int128 num = 0;
+                        uint64_t csum = 0;
+                        for (uint32_t g = 0; g < a.nlev; g++) {
+                            const uint32_t m = (g == l - 1) ? M : group_matches(a, q, s, g);
+                            const uint32_t ex = group_excl(a, q, s, g);
+                            ex_tot += ex;
+                            const uint32_t d = a.kp - ex;
+                            if (d == 0) continue;
+                            num += (unsigned __int128)a.c[g] * m * (a.lam / d);
+                            csum += a.c[g];
+                        }
+                        if (csum == 0) {
+                            flags = OPH_FLAG_UNDEFINED;
+                        } else {
+                            verdict = num * a.t_den >= (unsigned __int128)a.t_num * a.lam * csum;
+                            est = (float)((double)num / ((double)a.lam * (double)csum));
+                        }
                     }
                 }
+                emit(a.res, alive, q, s, nmb, ex_tot, a.nlev, verdict, flags, est);
+                alive = false;
+                break;
             }
-            emit(a.res, act, q, s, nmb, ex_tot, a.nlev, verdict, flags, est);
-        } else {
-            const bool acc = act && st >= a.acc;
-            const bool rej = act && !acc && (int64_t)st <= a.rej;
-            const bool surv = act && !acc && !rej;
+            const bool acc = alive && st >= a.acc[l - 1];
+            const bool rej = alive && !acc && (int64_t)st <= a.rej[l - 1];
             const bool want = a.res.dense ? (acc || rej) : acc;
             if (__any_sync(0xFFFFFFFFu, want)) {
                 uint32_t ex = 0;
                 if (want)
-                    for (uint32_t g = 0; g < a.level; g++) ex += group_excl(a, q, s, g);
-                emit(a.res, acc || rej, q, s, nmb, ex, a.level, acc ? 1u : 0u, OPH_FLAG_EARLY, -1.0f);
+                    for (uint32_t g = 0; g < l; g++) ex += group_excl(a, q, s, g);
+                emit(a.res, acc || rej, q, s, nmb, ex, l, acc ? 1u : 0u, OPH_FLAG_EARLY, -1.0f);
             }
-            const unsigned long long idx = warp_append(surv, a.count_out);
-            if (surv) {
-                a.out.q[idx] = q;
-                a.out.s[idx] = s;
-                a.out.state[idx] = st;
-                a.out.nmb[idx] = nmb;
-            }
+            alive = alive && !acc && !rej;
+        }
+        const unsigned long long idx = warp_append(alive, a.count_out);
+        if (alive) {
+            a.out.q[idx] = q;
+            a.out.s[idx] = s;
+            a.out.state[idx] = st;
+            a.out.nmb[idx] = nmb;
         }
     }
 }
