@@ -231,38 +231,52 @@ def run_ours(args):
     outs = [og.Results(cap * (world if rank == 0 else 1)) for _ in range(4)]
     merged = [og.Results(cap * world) for _ in range(4)] if world > 1 else None
 
-    names = ["build_oph_hoph", "build_minwise", "query_sketches", "compare_full", "compare_goph", "compare_hoph",
-             "compare_minwise", "select"]
+    side = torch.cuda.Stream()  # MinWise (the baseline) runs beside the OPH family
 
-    def step(ev=None, inputs=None):
-        def mark(i):
+    def step(ev=None, inputs=None, sets=sets, qsets=qsets):
+        """One pass of rows a1-a10.  Stream `stream`: OPH/HOPH build, query
+        sketches, full OPH / GOPH / HOPH; stream `side`: the MinWise build and
+        scoring (ALU-bound) overlapping the OPH family (memory/latency-bound).
+        ev[j] marks phase boundaries on the stream that runs the phase."""
+        def mark(i, st=stream):
             if ev is not None:
-                ev[i].record(stream)
+                ev[i].record(st)
         mark(0)
-        if inputs is not None:  # e2e: this step's inputs arrive from pinned host memory
-            sets.offsets.copy_(inputs[0], non_blocking=True)
-            sets.ids.copy_(inputs[1], non_blocking=True)
-            qsets.offsets.copy_(inputs[2], non_blocking=True)
-            qsets.ids.copy_(inputs[3], non_blocking=True)
+        counts.zero_()
+        fork = torch.cuda.Event()
+        fork.record(stream)
+        side.wait_event(fork)
+        # ---- side stream: a4 MinWise build (collection + queries), a9 MinWise scoring
+        with torch.cuda.stream(side):
+            mark(9, side)
+            og.minwise_build_sketches(sets, V, seed, mwk, out=mw)
+            mark(10, side)
+            if rank == 0:
+                og.minwise_build_sketches(qsets, V, seed, mwk, out=qmw)
+            if world > 1:
+                odist.broadcast_tensors([qmw.values, qmw.flags])
+            mark(11, side)
+            og.compare_minwise(qmw, mw, prm, res[3], set_id_base=base, ws=ws[3])
+            mark(12, side)
+        # ---- main stream: a1-a3 OPH+HOPH build, a5 queries, a6-a8 scoring
         og.oph_build_sketches(sets, V, seed, flat=flat, hier=hier, out_oph=so, out_hoph=sh)
         mark(1)
-        og.minwise_build_sketches(sets, V, seed, mwk, out=mw)
-        mark(2)
         if rank == 0:
             og.oph_build_sketches(qsets, V, seed, flat=flat, hier=hier, out_oph=qo, out_hoph=qh)
-            og.minwise_build_sketches(qsets, V, seed, mwk, out=qmw)
         if world > 1:
-            odist.broadcast_tensors([qo.values, qo.empty, qh.values, qh.empty, qmw.values, qmw.flags])
-        counts.zero_()
-        mark(3)
+            odist.broadcast_tensors([qo.values, qo.empty, qh.values, qh.empty])
+        mark(2)
         og.compare_full(qo, so, flat, prm, res[0], set_id_base=base, ws=ws[0])
-        mark(4)
+        mark(3)
         og.compare_goph(qo, so, flat, prm, res[1], set_id_base=base, ws=ws[1], survivor_capacity=surv_cap)
-        mark(5)
+        mark(4)
         og.compare_hoph(qh, sh, hier, prm, res[2], set_id_base=base, ws=ws[2], survivor_capacity=surv_cap)
+        mark(5)
+        join = torch.cuda.Event()
+        join.record(side)
+        stream.wait_event(join)
         mark(6)
-        og.compare_minwise(qmw, mw, prm, res[3], set_id_base=base, ws=ws[3])
-        mark(7)
+        # ---- a10: gather (N > 1) and sort the four hit lists
         n4 = [int(x) for x in counts.cpu()]  # one device->host read of the four hit counts
         assert max(n4) <= cap, f"hit buffer overflow {n4}"
         total = []
@@ -278,8 +292,13 @@ def run_ours(args):
             if rank == 0:
                 og.topk_or_threshold_results(src, n, og.OPH_SELECT_THRESHOLD, outs[i], ws=ws[4])
                 total.append(n)
-        mark(8)
+        mark(7)
         return total
+
+    # phases: (name, start event, end event); 0..7 on the main stream, 9..12 on the side stream
+    phase_ev = [("build_oph_hoph", 0, 1), ("query_sketches_oph_hoph", 1, 2), ("compare_full", 2, 3),
+                ("compare_goph", 3, 4), ("compare_hoph", 4, 5), ("join_minwise", 5, 6), ("select", 6, 7),
+                ("build_minwise", 9, 10), ("query_sketches_minwise", 10, 11), ("compare_minwise", 11, 12)]
 
     # warm-up (also JIT-free: the .so is prebuilt)
     for _ in range(args.warmup):
@@ -289,7 +308,7 @@ def run_ours(args):
 
     # ---------------- timed region: device inputs resident in HBM
     K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(9)] for _ in range(K)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(13)] for _ in range(K)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
     if world > 1:
@@ -309,10 +328,12 @@ def run_ours(args):
     ms = t_start.elapsed_time(t_end) / K
     if world > 1:
         ms = odist.max_over_ranks(ms, device="cuda")
-    phase_ms = {names[j]: statistics.mean(evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(K))
-                for j in range(8)}
+    phase_ms = {n: statistics.mean(evs[i][a].elapsed_time(evs[i][b]) for i in range(K)) for n, a, b in phase_ev}
 
-    # ---------------- e2e: same step through the C-ABI with HOST (pinned) inputs and result read-back
+    # ---------------- e2e: same step through the C-ABI with HOST (pinned) inputs and result read-back.
+    # Every step copies its inputs (collection CSR + query CSR) host->device and reads its sorted hit
+    # lists back; the copies run on a copy stream into a second input buffer while the previous step
+    # computes (double buffering), so they are inside the timed region but overlap compute.
     e2e = None
     if not args.no_e2e:
         host = [torch.from_numpy(w.offsets.astype(np.int64)).pin_memory(),
@@ -320,14 +341,37 @@ def run_ours(args):
                 torch.from_numpy(w.q_offsets.astype(np.int64)).pin_memory(),
                 torch.from_numpy(w.q_ids.view(np.int32)).pin_memory()]
         h2d = sum(t.numel() * t.element_size() for t in host)
+        bufs = [(og.SetCollection(torch.empty_like(sets.offsets), torch.empty_like(sets.ids)),
+                 og.SetCollection(torch.empty_like(qsets.offsets), torch.empty_like(qsets.ids))) for _ in range(2)]
+        cstream = torch.cuda.Stream()
+        copied = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
+
+        def enqueue_copy(j):
+            b = bufs[j % 2]
+            with torch.cuda.stream(cstream):
+                if j >= 2:
+                    cstream.wait_event(consumed[j % 2])
+                b[0].offsets.copy_(host[0], non_blocking=True)
+                b[0].ids.copy_(host[1], non_blocking=True)
+                b[1].offsets.copy_(host[2], non_blocking=True)
+                b[1].ids.copy_(host[3], non_blocking=True)
+                copied[j % 2].record(cstream)
+
         d2h = 0
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0.record(stream)
+        cstream.wait_event(e0)
+        enqueue_copy(0)
         for i in range(K):
-            tot = step(None, inputs=host)
+            stream.wait_event(copied[i % 2])
+            if i + 1 < K:
+                enqueue_copy(i + 1)
+            tot = step(None, sets=bufs[i % 2][0], qsets=bufs[i % 2][1])
+            consumed[i % 2].record(stream)
             d2h = 4 * 8
             if rank == 0:
                 for j in range(4):
@@ -341,7 +385,8 @@ def run_ours(args):
         if world > 1:
             ems = odist.max_over_ranks(ems, device="cuda")
         e2e = {"value": 3 * Q * N_total / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": ems}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ems,
+               "note": "H2D of step i+1 inputs overlaps step i compute (copy stream, double buffer)"}
 
     if rank != 0:
         if world > 1:
@@ -351,25 +396,24 @@ def run_ours(args):
     # ---------------- roofline of the dominant kernel
     peaks, peak_src = load_peaks()
     f_sm = peaks.get("sm_max_mhz", 1965.0) * 1e6
-    issue = 148 * 4 * f_sm                       # warp-instructions / s
-    cmp_peak = issue * 32 / 2                    # bin-compares / s at ISETP + predicated IADD
-    psi_peak = issue * 32 / 17                   # psi evaluations / s at 17 lane-instructions
+    # ALU pipe (IADD3/LOP3/SHF/min): 16 lanes/clk/SMSP (B300_MICROARCH "rt_SMSP=2"), 148 SM x 4 SMSP;
+    # one psi evaluation + running min needs >= 9.5 ALU-pipe lane-ops at w = 32
+    alu_lanes = 148 * 4 * 16 * f_sm
+    psi_peak = alu_lanes / 9.5
     hbm = peaks["hbm_gbs"] * 1e9
     nnz = int(w.offsets[-1])
     nw_k, nw_h = (k + 31) // 32, (L * hkp + 31) // 32
-    build_bytes = 4 * nnz + 8 * (N + 1) + 4 * N * (k + L * hkp) + 4 * N * (nw_k + nw_h)
     g_l0 = og.plan_thresholds(og.OPH_METHOD_GOPH, k // kp, kp, p["t_num"], p["t_den"], p["eps"])[2]
-    kern = {
-        "build_oph_hoph": ("hbm", build_bytes / (phase_ms["build_oph_hoph"] / 1e3) / 1e9, hbm / 1e9, "GB/s",
-                           build_bytes),
-        "build_minwise": ("alu", nnz * mwk / (phase_ms["build_minwise"] / 1e3), psi_peak, "psi-evals/s", None),
-        "compare_full": ("alu", Q * N * k / (phase_ms["compare_full"] / 1e3), cmp_peak, "bin-compares/s", None),
-        "compare_goph": ("alu", Q * N * g_l0 * kp / (phase_ms["compare_goph"] / 1e3), cmp_peak, "bin-compares/s",
-                         None),
-        "compare_hoph": ("alu", Q * N * hkp / (phase_ms["compare_hoph"] / 1e3), cmp_peak, "bin-compares/s", None),
-        "compare_minwise": ("alu", Q * N * mwk / (phase_ms["compare_minwise"] / 1e3), cmp_peak, "bin-compares/s",
-                            None),
+    # algorithmic bytes per launch: inputs read once + outputs written once
+    by = {
+        "build_oph_hoph": 4 * nnz + 8 * (N + 1) + 4 * N * (k + L * hkp) + 4 * N * (nw_k + nw_h),
+        "compare_full": N * (4 * k + 4 * nw_k),
+        "compare_goph": N * (4 * g_l0 * kp + 4 * ((g_l0 * kp + 31) // 32)),
+        "compare_hoph": N * (4 * hkp + 4),
+        "compare_minwise": N * (4 * mwk + 1),
     }
+    kern = {n: ("hbm", b / (phase_ms[n] / 1e3) / 1e9, hbm / 1e9, "GB/s", b) for n, b in by.items()}
+    kern["build_minwise"] = ("alu", nnz * mwk / (phase_ms["build_minwise"] / 1e3), psi_peak, "psi-evals/s", None)
     traffic = {}
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -378,15 +422,10 @@ def run_ours(args):
     dom = max(kern, key=lambda n: phase_ms[n])
     b, a_, pk, u, _ = kern[dom]
     roof = {"kernel": dom, "bound": b, "achieved": a_, "peak": pk, "unit": u, "frac": a_ / pk,
-            "traffic": traffic.get(dom), "peak_source": peak_src,
-            "note": "alu peaks derived from 148 SM x 4 issue/clk x sm_max_mhz (DESIGN.md)"}
+            "traffic": traffic.get(dom), "peak_source": peak_src if b == "hbm" else
+            "derived: 148 SM x 4 SMSP x 16 ALU lanes x sm_max_mhz / 9.5 ALU ops per psi (DESIGN.md)"}
     per_kernel = {n: {"ms": phase_ms[n], "bound": v[0], "achieved": v[1], "peak": v[2], "unit": v[3],
-                      "frac": v[1] / v[2]} for n, v in kern.items()}
-    # the collection scans also against HBM: one pass over the scanned fingerprint bytes
-    scan_bytes = {"compare_full": N * (4 * k + k // 8), "compare_goph": N * (4 * g_l0 * kp + g_l0 * kp // 8),
-                  "compare_hoph": N * (4 * hkp + hkp // 8), "compare_minwise": N * 4 * mwk}
-    for n, by in scan_bytes.items():
-        per_kernel[n]["hbm_gbs_one_pass"] = by / (phase_ms[n] / 1e3) / 1e9
+                      "frac": v[1] / v[2], "bytes": v[4]} for n, v in kern.items()}
 
     # ---------------- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
@@ -409,6 +448,7 @@ def run_ours(args):
                    "kprime": kp, "hoph_groups": L, "minwise_k": mwk, "T": f"{p['t_num']}/{p['t_den']}",
                    "epsilon": p["eps"], "parallelism": f"set-sharded x{world}",
                    "l2": "inputs larger than L2 (CSR 320 MB + sketches 1.1 GB per step)"},
+        "value_definition": "3 * queries * sets_total / step time (each pair scored by full OPH, GOPH, HOPH)",
         "sketches_per_s": {"oph_hoph": (N_total) / (phase_ms["build_oph_hoph"] / 1e3),
                            "minwise": (N_total) / (phase_ms["build_minwise"] / 1e3)},
         "comparisons_per_s": {m: Q * N_total / (phase_ms["compare_" + m] / 1e3)

@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(128) scan_kernel(const __grid_constant__ ScanA
     uint32_t *qe = qs + (size_t)qs_bins * B;            // [nw_load][B]
     uint32_t *qf = qe + (size_t)a.nw_load * B;          // [B] MinWise flags
 
+    if (LIST && (uint64_t)blockIdx.y * 128 * SPT >= *a.list_count) return;  // nothing listed for this CTA
     const uint32_t qb0 = blockIdx.x * B;                // chunk-local first query
     const uint64_t col0 = (uint64_t)a.q_col0 + qb0;     // column in the prepared arrays
     const bool one_chunk = a.nscan <= kScanChunk;
@@ -893,7 +894,9 @@ cudaError_t launch_probe(const ProbeArgs &a, cudaStream_t st) {
 }
 
 cudaError_t launch_level(const LevelArgs &a, cudaStream_t st) {
-    level_kernel<<<148 * 8, 256, 0, st>>>(a);
+    // grid-stride over a device-side count: one CTA per SM covers sparse
+    // survivor lists cheaply and still fills the chip for dense ones
+    level_kernel<<<148 * 2, 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 
