@@ -267,6 +267,7 @@ def run_ours(args):
             og.compare_minwise(qmw, mw, prm, res[3], set_id_base=base, ws=ws[3])
             mark(12, side)
         # ---- main stream: a1-a3 OPH+HOPH build, a5 queries, a6-a8 scoring
+        mark(8)
         og.oph_build_sketches(sets, V, seed, flat=flat, hier=hier, out_oph=so, out_hoph=sh)
         mark(1)
         if rank == 0:
@@ -304,7 +305,7 @@ def run_ours(args):
         return total
 
     # phases: (name, start event, end event); 0..7 on the main stream, 9..12 on the side stream
-    phase_ev = [("build_oph_hoph", 0, 1), ("query_sketches_oph_hoph", 1, 2), ("compare_full", 2, 3),
+    phase_ev = [("build_oph_hoph", 8, 1),("query_sketches_oph_hoph", 1, 2), ("compare_full", 2, 3),
                 ("compare_goph", 3, 4), ("compare_hoph", 4, 5), ("join_minwise", 5, 6), ("select", 6, 7),
                 ("build_minwise", 9, 10), ("query_sketches_minwise", 10, 11), ("compare_minwise", 11, 12)]
 

@@ -41,6 +41,8 @@ struct BuildArgs {
     uint32_t *oph, *oph_empty;
     // hierarchical
     uint32_t do_hier, L, kp;
+    uint32_t hier_pow2_halves;  // 1:1 split of |V| = 2^log2V, kp = 2^log2kp: group = leading ones of p
+    uint32_t log2V, log2kp;
     RangeBins grp[kMaxGroups];
     uint32_t *hoph, *hoph_empty;
 };

@@ -691,6 +691,17 @@ oph_status oph_build_sketches(const oph_sets *sets, const oph_perm *perm, const 
         a.L = hier->L;
         a.kp = hier->kprime;
         for (uint32_t g = 0; g < hier->L; g++) a.grp[g] = make_range(hier->start[g], hier->len[g], hier->kprime);
+        // fast path: the 1:1 split of a power-of-two universe (group g = [V - V/2^g, V - V/2^(g+1)),
+        // the last group the remaining V/2^(L-1)) with a power-of-two kprime
+        const uint32_t m = word_bits(V), lk = word_bits(hier->kprime);
+        bool halves = V == (1ull << m) && hier->kprime == (1u << lk) && hier->kprime > 1 && hier->L >= 1;
+        for (uint32_t g = 0; halves && g < hier->L; g++) {
+            const uint64_t len = (g + 1 < hier->L) ? (V >> (g + 1)) : (V >> (hier->L - 1));
+            halves = hier->start[g] == V - (V >> g) && hier->len[g] == len && len >= hier->kprime;
+        }
+        a.hier_pow2_halves = halves;
+        a.log2V = m;
+        a.log2kp = lk;
         a.hoph = d_hoph;
         a.hoph_empty = d_hoph_empty;
         per_set += (uint64_t)hier->L * hier->kprime + 1;

@@ -68,90 +68,124 @@ __device__ __forceinline__ uint64_t splitmix64_mix(uint64_t z) {
 
 // ---------------------------------------------------------------------------
 // K1: OPH + HOPH build.  One CTA = SB consecutive sets; their ids are one
-// contiguous CSR range, streamed by all 256 threads.  Per-set sketches live
-// in shared memory (row stride n+1 words: conflict-free column reads) and
-// are minimised with shared atomicMin (EMPTY = 0xFFFFFFFF is the identity of
-// min).  The tile is written out bin-major: SB consecutive words per bin.
+// contiguous CSR range, streamed by all 256 threads (a thread tracks the set
+// of its element incrementally: elements advance by 256 per iteration).
+// Per-set sketches live in shared memory (row stride n+1 words) and are
+// minimised with shared atomicMin (EMPTY = 0xFFFFFFFF is the identity of
+// min).  HOPH group lookup: for the 1:1 split of a power-of-two universe the
+// group of p is its count of leading one bits (capped at L-1) and its bins
+// are shifts; other layouts binary-search a group table in shared memory.
+// Write-out: 128-bit stores of 4 consecutive sets of one bin row; empty masks
+// by warp ballot over 32 bins.
 // ---------------------------------------------------------------------------
 template <bool W32>
-__global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ BuildArgs a, uint32_t SB) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    // group table in shared memory: lanes index it divergently, which would
-    // serialise on the constant cache if read from the kernel parameters
-    __shared__ RangeBins grp[kMaxGroups];
-    uint64_t *offs = reinterpret_cast<uint64_t *>(smem_raw);             // [SB+1]
-    uint32_t *so = reinterpret_cast<uint32_t *>(offs + SB + 1);          // [SB][k+1]
-    const uint32_t kst = a.k + 1;
-    const uint32_t nbh = a.L * a.kp;
-    const uint32_t hst = nbh + 1;
-    uint32_t *sh = so + (a.do_flat ? (size_t)SB * kst : 0);              // [SB][L*kp+1]
-
-    const uint64_t s0 = (uint64_t)blockIdx.x * SB;
-    const uint32_t nloc = (uint32_t)min((uint64_t)SB, a.n_sets - s0);
-    for (uint32_t i = threadIdx.x; i <= nloc; i += blockDim.x) offs[i] = a.offsets[s0 + i];
-    if (a.do_hier)
-        for (uint32_t i = threadIdx.x; i < a.L; i += blockDim.x) grp[i] = a.grp[i];
-    if (a.do_flat)
-        for (uint32_t i = threadIdx.x; i < SB * kst; i += blockDim.x) so[i] = kEmpty;
-    if (a.do_hier)
-        for (uint32_t i = threadIdx.x; i < SB * hst; i += blockDim.x) sh[i] = kEmpty;
-    __syncthreads();
-
-    const uint64_t e0 = offs[0], e1 = offs[nloc];
-    for (uint64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-        const uint32_t id = __ldg(a.ids + e);
-        // owning set: largest j with offs[j] <= e
-        uint32_t lo = 0, hi = nloc - 1;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) >> 1;
-            if (offs[mid] <= e) lo = mid; else hi = mid - 1;
-        }
-        const uint32_t p = psi<W32>(a.psi, id);
-        uint32_t bin, off;
-        if (a.do_flat) {
-            range_bin(a.flat, a.k, p, bin, off);
-            atomicMin(&so[lo * kst + bin], off);
-        }
-        if (a.do_hier) {
+__device__ __forceinline__ void build_one(const BuildArgs &a, const RangeBins *grp, uint32_t *so, uint32_t *sh,
+                                          uint32_t kst, uint32_t hst, uint32_t j, uint32_t id) {
+    const uint32_t p = psi<W32>(a.psi, id);
+    uint32_t bin, off;
+    if (a.do_flat) {
+        range_bin(a.flat, a.k, p, bin, off);
+        atomicMin(&so[j * kst + bin], off);
+    }
+    if (a.do_hier) {
+        uint32_t g;
+        if (a.hier_pow2_halves) {
+            // group g = [V - V/2^g, V - V/2^(g+1)): g = leading ones of p in m bits
+            g = min((uint32_t)__clz(~(p << (32 - a.log2V))), a.L - 1);
+            const uint32_t e = (g + 1 < a.L) ? a.log2V - 1 - g : a.log2V - (a.L - 1);  // log2 of the group length
+            const uint32_t sh_bits = e - a.log2kp;
+            const uint32_t x = p & ((e >= 32) ? 0xFFFFFFFFu : ((1u << e) - 1u));
+            bin = x >> sh_bits;
+            off = x & ((1u << sh_bits) - 1u);
+        } else {
             uint32_t g0 = 0, g1 = a.L - 1;  // largest g with start_g <= p
             while (g0 < g1) {
                 const uint32_t mid = (g0 + g1 + 1) >> 1;
                 if (grp[mid].start <= p) g0 = mid; else g1 = mid - 1;
             }
-            range_bin(grp[g0], a.kp, p, bin, off);
-            atomicMin(&sh[lo * hst + g0 * a.kp + bin], off);
+            g = g0;
+            range_bin(grp[g], a.kp, p, bin, off);
         }
+        atomicMin(&sh[j * hst + g * a.kp + bin], off);
+    }
+}
+
+__device__ __forceinline__ void write_tile(const uint32_t *src, uint32_t stride, uint32_t nbins, uint32_t SB,
+                                           uint32_t nloc, uint32_t *dst, uint64_t ld, uint64_t s0) {
+    // values: bin-major rows of SB sets; thread = (bin, quad of 4 sets) -> one 16-B store
+    const uint32_t quads = SB / 4;
+    if (SB % 4 == 0 && nloc == SB) {
+        for (uint32_t i = threadIdx.x; i < nbins * quads; i += blockDim.x) {
+            const uint32_t b = i / quads, j = 4 * (i % quads);
+            uint4 v;
+            v.x = src[(j + 0) * stride + b];
+            v.y = src[(j + 1) * stride + b];
+            v.z = src[(j + 2) * stride + b];
+            v.w = src[(j + 3) * stride + b];
+            *reinterpret_cast<uint4 *>(dst + (uint64_t)b * ld + s0 + j) = v;
+        }
+    } else {
+        for (uint32_t i = threadIdx.x; i < nbins * SB; i += blockDim.x) {
+            const uint32_t b = i / SB, j = i % SB;
+            if (j < nloc) dst[(uint64_t)b * ld + s0 + j] = src[j * stride + b];
+        }
+    }
+}
+
+__device__ __forceinline__ void write_masks(const uint32_t *src, uint32_t stride, uint32_t nbins, uint32_t nloc,
+                                            uint32_t *dst, uint64_t ld, uint64_t s0) {
+    // warp per (set, word): bit t of word w <=> bin 32w + t empty
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const uint32_t nw = (nbins + 31) / 32;
+    for (uint32_t i = warp; i < nw * nloc; i += nwarps) {
+        const uint32_t j = i / nw, w = i % nw;
+        const uint32_t b = 32 * w + lane;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, b < nbins && src[j * stride + b] == kEmpty);
+        if (lane == 0) dst[(uint64_t)w * ld + s0 + j] = m;
+    }
+}
+
+template <bool W32>
+__global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ BuildArgs a, uint32_t SB) {
+    extern __shared__ __align__(16) uint32_t smem_u32[];
+    // group table in shared memory: lanes index it divergently, which would
+    // serialise on the constant cache if read from the kernel parameters
+    __shared__ RangeBins grp[kMaxGroups];
+    __shared__ uint64_t offs[33];
+    const uint32_t kst = a.k + 1;
+    const uint32_t nbh = a.L * a.kp;
+    const uint32_t hst = nbh + 1;
+    uint32_t *so = smem_u32;                                               // [SB][k+1]
+    uint32_t *sh = so + (a.do_flat ? (size_t)SB * kst : 0);               // [SB][L*kp+1]
+    const uint32_t words = (a.do_flat ? SB * kst : 0) + (a.do_hier ? SB * hst : 0);
+
+    const uint64_t s0 = (uint64_t)blockIdx.x * SB;
+    const uint32_t nloc = (uint32_t)min((uint64_t)SB, a.n_sets - s0);
+    for (uint32_t i = threadIdx.x; i <= nloc; i += blockDim.x) offs[i] = a.offsets[s0 + i];
+    if (a.do_hier && !a.hier_pow2_halves)
+        for (uint32_t i = threadIdx.x; i < a.L; i += blockDim.x) grp[i] = a.grp[i];
+    {
+        uint4 *s4 = reinterpret_cast<uint4 *>(smem_u32);
+        const uint4 e4 = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+        for (uint32_t i = threadIdx.x; i < (words + 3) / 4; i += blockDim.x) s4[i] = e4;
     }
     __syncthreads();
 
-    // write-out: values bin-major, then empty masks (bit i of word w <=> bin 32w+i empty)
+    const uint64_t e0 = offs[0], e1 = offs[nloc];
+    uint32_t j = 0;
+    for (uint64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        while (offs[j + 1] <= e) j++;  // the set owning element e (empty sets are skipped)
+        build_one<W32>(a, grp, so, sh, kst, hst, j, __ldg(a.ids + e));
+    }
+    __syncthreads();
+
     if (a.do_flat) {
-        for (uint32_t i = threadIdx.x; i < a.k * SB; i += blockDim.x) {
-            const uint32_t b = i / SB, j = i % SB;
-            if (j < nloc) a.oph[(uint64_t)b * a.ld + s0 + j] = so[j * kst + b];
-        }
-        const uint32_t nw = (a.k + 31) / 32;
-        for (uint32_t i = threadIdx.x; i < nw * SB; i += blockDim.x) {
-            const uint32_t w = i / SB, j = i % SB;
-            if (j >= nloc) continue;
-            uint32_t m = 0;
-            for (uint32_t t = 0; t < 32 && 32 * w + t < a.k; t++) m |= (uint32_t)(so[j * kst + 32 * w + t] == kEmpty) << t;
-            a.oph_empty[(uint64_t)w * a.ld + s0 + j] = m;
-        }
+        write_tile(so, kst, a.k, SB, nloc, a.oph, a.ld, s0);
+        write_masks(so, kst, a.k, nloc, a.oph_empty, a.ld, s0);
     }
     if (a.do_hier) {
-        for (uint32_t i = threadIdx.x; i < nbh * SB; i += blockDim.x) {
-            const uint32_t b = i / SB, j = i % SB;
-            if (j < nloc) a.hoph[(uint64_t)b * a.ld + s0 + j] = sh[j * hst + b];
-        }
-        const uint32_t nw = (nbh + 31) / 32;
-        for (uint32_t i = threadIdx.x; i < nw * SB; i += blockDim.x) {
-            const uint32_t w = i / SB, j = i % SB;
-            if (j >= nloc) continue;
-            uint32_t m = 0;
-            for (uint32_t t = 0; t < 32 && 32 * w + t < nbh; t++) m |= (uint32_t)(sh[j * hst + 32 * w + t] == kEmpty) << t;
-            a.hoph_empty[(uint64_t)w * a.ld + s0 + j] = m;
-        }
+        write_tile(sh, hst, nbh, SB, nloc, a.hoph, a.ld, s0);
+        write_masks(sh, hst, nbh, nloc, a.hoph_empty, a.ld, s0);
     }
 }
 
@@ -817,8 +851,8 @@ cudaError_t launch_build(const BuildArgs &a, cudaStream_t st) {
     if (a.n_sets == 0) return cudaSuccess;
     const uint32_t per_set = (a.do_flat ? a.k + 1 : 0) + (a.do_hier ? a.L * a.kp + 1 : 0);
     uint32_t SB = 16;
-    while (SB > 1 && (size_t)SB * per_set * 4 + (SB + 1) * 8 > 200 * 1024) SB >>= 1;
-    const size_t smem = (size_t)SB * per_set * 4 + (SB + 1) * 8;
+    while (SB > 1 && (size_t)SB * per_set * 4 + 16 > 200 * 1024) SB >>= 1;
+    const size_t smem = ((size_t)SB * per_set * 4 + 15) / 16 * 16;
     const uint64_t grid = (a.n_sets + SB - 1) / SB;
     const bool w32 = a.psi.mask == 0xFFFFFFFFu;
     auto kern = w32 ? build_kernel<true> : build_kernel<false>;

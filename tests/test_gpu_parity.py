@@ -280,6 +280,29 @@ def test_probe_overflow_falls_back_to_brute(method):
         assert (h["n_mb"], h["n_excl"], h["groups"], h["flags"]) == (wr["n_mb"], wr["n_excl"], wr["groups"], wr["flags"])
 
 
+@pytest.mark.parametrize("a,b,V,kp", [(1, 2, 1 << 20, 32), (2, 1, 1 << 20, 32), (3, 1, 1 << 16, 16), (1, 1, 100003, 16)])
+def test_hoph_split_ratios(a, b, V, kp):
+    """(a:b)HOPH variants of P:801-803 (general nominal weights, binary-search
+    group lookup): sketches and dense records bit-exact, both empty modes."""
+    rng = np.random.default_rng(a * 10 + b)
+    sets = [rng.choice(V, size=int(rng.integers(0, 700)), replace=False) for _ in range(300)]
+    qsets = [sets[i] if i % 2 == 0 else rng.choice(V, size=400, replace=False) for i in range(40)]
+    offs, ids = make_csr(sets)
+    qoffs, qids = make_csr(qsets)
+    hier = og.oph_hier_layout_make(V, a, b, kp)
+    glay = oracle.hoph_layout(V, a, b, kp)
+    assert hier.groups() == glay
+    _, _, sh = gpu_build(offs, ids, V, 21, hier=hier)
+    _, _, qh = gpu_build(qoffs, qids, V, 21, hier=hier)
+    H = oracle.hoph_sketch(offs, ids, V, glay, kp, 21)
+    QH = oracle.hoph_sketch(qoffs, qids, V, glay, kp, 21)
+    assert (sh.numpy() == H).all() and (qh.numpy() == QH).all()
+    for joint in (False, True):
+        kw = dict(t_num=3, t_den=5, eps=1e-4, joint=joint)
+        assert_records_equal(gpu_dense("hoph", qh, sh, layout=hier, **kw),
+                             oracle_records("hoph", QH, H, kprime=kp, L=len(glay), a=a, b=b, **kw), f"hoph {a}:{b}")
+
+
 def test_empty_inputs():
     """Zero queries or zero sets: nothing is written, no error."""
     offs, ids = make_csr([[1, 2, 3]])
