@@ -172,10 +172,22 @@ __global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ Buil
     __syncthreads();
 
     const uint64_t e0 = offs[0], e1 = offs[nloc];
+    constexpr int kU = 4;  // ids in flight per thread
     uint32_t j = 0;
-    for (uint64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-        while (offs[j + 1] <= e) j++;  // the set owning element e (empty sets are skipped)
-        build_one<W32>(a, grp, so, sh, kst, hst, j, __ldg(a.ids + e));
+    for (uint64_t e = e0 + threadIdx.x; e < e1; e += kU * blockDim.x) {
+        uint32_t id[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            const uint64_t eu = e + (uint64_t)u * blockDim.x;
+            id[u] = eu < e1 ? __ldg(a.ids + eu) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            const uint64_t eu = e + (uint64_t)u * blockDim.x;
+            if (eu >= e1) break;
+            while (offs[j + 1] <= eu) j++;  // the set owning element eu (empty sets are skipped)
+            build_one<W32>(a, grp, so, sh, kst, hst, j, id[u]);
+        }
     }
     __syncthreads();
 
@@ -850,7 +862,9 @@ __global__ void __launch_bounds__(256) level_kernel(const __grid_constant__ Leve
 cudaError_t launch_build(const BuildArgs &a, cudaStream_t st) {
     if (a.n_sets == 0) return cudaSuccess;
     const uint32_t per_set = (a.do_flat ? a.k + 1 : 0) + (a.do_hier ? a.L * a.kp + 1 : 0);
-    uint32_t SB = 16;
+    // 8 sets per CTA: 36 KB of shared memory at text-like sizes -> 6 CTAs (48 warps) per SM,
+    // and a bin row of the tile is one full 32-B sector
+    uint32_t SB = 8;
     while (SB > 1 && (size_t)SB * per_set * 4 + 16 > 200 * 1024) SB >>= 1;
     const size_t smem = ((size_t)SB * per_set * 4 + 15) / 16 * 16;
     const uint64_t grid = (a.n_sets + SB - 1) / SB;
