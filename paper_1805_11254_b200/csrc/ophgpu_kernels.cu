@@ -85,7 +85,10 @@ __device__ __forceinline__ void build_one(const BuildArgs &a, const RangeBins *g
     uint32_t bin, off;
     if (a.do_flat) {
         range_bin(a.flat, a.k, p, bin, off);
-        atomicMin(&so[j * kst + bin], off);
+        // a shared load first: most elements do not lower their bin minimum (for m elements in
+        // a bin only ~ln m do), and a load is much cheaper than a shared atomic
+        uint32_t *slot = &so[j * kst + bin];
+        if (off < *slot) atomicMin(slot, off);
     }
     if (a.do_hier) {
         uint32_t g;
@@ -106,7 +109,8 @@ __device__ __forceinline__ void build_one(const BuildArgs &a, const RangeBins *g
             g = g0;
             range_bin(grp[g], a.kp, p, bin, off);
         }
-        atomicMin(&sh[j * hst + g * a.kp + bin], off);
+        uint32_t *hslot = &sh[j * hst + g * a.kp + bin];
+        if (off < *hslot) atomicMin(hslot, off);
     }
 }
 
