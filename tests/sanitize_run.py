@@ -1,0 +1,58 @@
+"""Small end-to-end run of every kernel for compute-sanitizer (not a pytest file):
+
+    compute-sanitizer --tool memcheck python tests/sanitize_run.py
+
+Tiny config: builds (OPH, HOPH, MinWise), every compare in dense and in
+threshold mode with both scan strategies (PROBE incl. its BRUTE list fallback
+and the survivor levels), threshold and top-k selection."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1805_11254_b200 as og  # noqa: E402
+from workloads import tiny  # noqa: E402
+
+
+def main():
+    w = tiny()
+    p = w.params
+    V, seed = w.vocab_size, p["perm_seed"]
+    hier = og.oph_hier_layout_make(V, 1, 1, p["hoph_kprime"])
+    flat = og.flat_layout(V, p["k"], p["kprime"])
+    sets = og.SetCollection.from_numpy(w.offsets, w.ids)
+    # 40 copies of query 0 force PROBE overflow -> BRUTE list scan
+    qo_np = [w.query_ids(q) for q in range(w.n_queries)] + [w.query_ids(0)] * 40
+    qoff = np.zeros(len(qo_np) + 1, dtype=np.uint64)
+    np.cumsum([len(x) for x in qo_np], out=qoff[1:])
+    qs = og.SetCollection.from_numpy(qoff, np.concatenate(qo_np))
+    so, sh = og.oph_build_sketches(sets, V, seed, flat=flat, hier=hier)
+    qo, qh = og.oph_build_sketches(qs, V, seed, flat=flat, hier=hier)
+    mw = og.minwise_build_sketches(sets, V, seed, p["mw_k"])
+    qmw = og.minwise_build_sketches(qs, V, seed, p["mw_k"])
+    total = 0
+    for strategy in (og.OPH_STRATEGY_BRUTE, og.OPH_STRATEGY_PROBE):
+        prm = og.params(p["t_num"], p["t_den"], p["eps"], strategy=strategy)
+        for dense in (False, True):
+            for name, fn, args in [("full", og.compare_full, (qo, so, flat)), ("goph", og.compare_goph, (qo, so, flat)),
+                                   ("hoph", og.compare_hoph, (qh, sh, hier))]:
+                r = og.Results(qo.n_sets * so.n_sets if dense else 1 << 16, dense=dense)
+                fn(*args, prm, r)
+                total += r.n()
+            r = og.Results(qo.n_sets * so.n_sets if dense else 1 << 16, dense=dense)
+            og.compare_minwise(qmw, mw, prm, r)
+            n = r.n()
+            total += n
+            if not dense:
+                out = og.Results(max(n, 1))
+                og.topk_or_threshold_results(r, n, og.OPH_SELECT_THRESHOLD, out)
+                og.topk_or_threshold_results(r, n, og.OPH_SELECT_TOPK, out, topk=3, k_bins=p["mw_k"])
+    torch.cuda.synchronize()
+    print("sanitize_run ok", total)
+
+
+if __name__ == "__main__":
+    main()
