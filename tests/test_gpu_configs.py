@@ -35,7 +35,9 @@ def _check_sketches_chunked(gpu_sk, orc, chunk=100_000):
         assert (ge == masks_from_values(orc[c0:c1])).all(), f"mask mismatch in sets [{c0},{c1})"
 
 
-def check_config(w, sample, strategy, methods=("full", "goph", "hoph"), dense_q=4):
+def check_config(w, sample, strategy, methods=("full", "goph", "hoph"), dense_q=4, hit_queries=None):
+    """hit_queries: score only the first hit_queries queries in threshold mode
+    (the sweep's all-similar collections give ~10^8-10^9 hits for all queries)."""
     p = w.params
     V, seed = w.vocab_size, p["perm_seed"]
     hier = og.oph_hier_layout_make(V, p["a"], p["b"], p["hoph_kprime"])
@@ -53,14 +55,19 @@ def check_config(w, sample, strategy, methods=("full", "goph", "hoph"), dense_q=
     QH = oracle.hoph_sketch(w.q_offsets, w.q_ids, V, glay, p["hoph_kprime"], seed)
     assert (qo.numpy() == QF).all() and (qh.numpy() == QH).all()
     kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    if hit_queries is not None:
+        qo_t, qh_t = subview(qo, hit_queries), subview(qh, hit_queries)
+        assert max(sample) < hit_queries
+    else:
+        qo_t, qh_t = qo, qh
     for m in methods:
         if m == "hoph":
-            hits = gpu_threshold_hits(m, qh, sh, layout=hier, strategy=strategy, capacity=1 << 24, **kw)
+            hits = gpu_threshold_hits(m, qh_t, sh, layout=hier, strategy=strategy, capacity=1 << 26, **kw)
             want = oracle_records(m, QH[sample], H, kprime=p["hoph_kprime"], L=len(glay), **kw)
             dense = gpu_dense(m, subview(qh, dense_q), sh, layout=hier, **kw)
             dwant = oracle_records(m, QH[:dense_q], H, kprime=p["hoph_kprime"], L=len(glay), **kw)
         else:
-            hits = gpu_threshold_hits(m, qo, so, layout=flat, strategy=strategy, capacity=1 << 24, **kw)
+            hits = gpu_threshold_hits(m, qo_t, so, layout=flat, strategy=strategy, capacity=1 << 26, **kw)
             want = oracle_records(m, QF[sample], F, k=p["k"], kprime=p["kprime"], **kw)
             dense = gpu_dense(m, subview(qo, dense_q), so, layout=flat, **kw)
             dwant = oracle_records(m, QF[:dense_q], F, k=p["k"], kprime=p["kprime"], **kw)
@@ -105,4 +112,4 @@ def test_scale_shard_full_size():
 def test_sweep(jmax, n_sets):
     from workloads.gen_gpu import sweep
     w = sweep(jmax, n_sets=n_sets)
-    check_config(w, sample=[0, 3, 511, 1023], strategy=og.OPH_STRATEGY_AUTO, dense_q=2)
+    check_config(w, sample=[0, 3, 17, 31], strategy=og.OPH_STRATEGY_AUTO, dense_q=2, hit_queries=32)
