@@ -126,7 +126,11 @@ typedef struct {
 /* Collection-scan strategies; every strategy returns
  * identical results.
  *   AUTO : PROBE when it applies (threshold results, and pairs with no matched
- *          bin are decided NotSimilar at the scanned level), else BRUTE.
+ *          bin are decided NotSimilar at the scanned level), else BRUTE.  It
+ *          probes a leading sample (1/16 of the sets, >= 16384) first and
+ *          scans the rest with BRUTE if more than a quarter of the sample
+ *          matched more than 16 distinct queries (one host synchronisation
+ *          per call).
  *   BRUTE: every (query, set, bin) equality is tested (register-blocked
  *          query tiles; cost ~ Q N bins; best when most pairs share bins).
  *   PROBE: per bin, the query values are hashed into a table; each set bin

@@ -104,6 +104,7 @@ struct ScanArgs {
     // list mode: the sets to scan are set_list[0 .. *list_count) (PROBE overflow sets)
     const uint32_t *set_list;
     const unsigned long long *list_count;
+    uint64_t s_begin;       // range mode: scan sets [s_begin, n_sets) (s_begin even)
 };
 
 // PROBE strategy: per scanned bin b, the chunk's query values are hashed into
@@ -138,6 +139,7 @@ struct ProbeArgs {
     unsigned long long *surv_count;
     uint32_t *ovf_list;     // sets that matched more than kProbeList queries
     unsigned long long *ovf_count;
+    uint64_t s_begin, s_end;  // the sets [s_begin, s_end) are probed
 };
 
 struct LevelArgs {

@@ -571,7 +571,30 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
             pr.surv_count = s.surv_count;
             pr.ovf_list = w.ovf_list;
             pr.ovf_count = ovf_count;
+            // AUTO probes a leading sample of the sets first; when more than a quarter of it
+            // matches too many distinct queries (a high-similarity collection), the rest goes
+            // to BRUTE as one contiguous scan instead of the list fallback
+            const uint64_t n1 = p->strategy == OPH_STRATEGY_AUTO
+                                    ? std::min<uint64_t>(n_s, std::max<uint64_t>(16384, ceil_div(n_s / 16, 256) * 256))
+                                    : n_s;
+            pr.s_begin = 0;
+            pr.s_end = n1;
             if ((e = launch_probe(pr, stream)) != cudaSuccess) return OPH_ECUDA;
+            if (n1 < n_s) {
+                unsigned long long ovf = 0;
+                if (cudaMemcpyAsync(&ovf, ovf_count, sizeof(ovf), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+                    cudaStreamSynchronize(stream) != cudaSuccess)
+                    return OPH_ECUDA;
+                if (ovf * 4 > n1) {
+                    ScanArgs sr = s;
+                    sr.s_begin = n1;
+                    if ((e = launch_scan(sr, 32, stream)) != cudaSuccess) return OPH_ECUDA;
+                } else {
+                    pr.s_begin = n1;
+                    pr.s_end = n_s;
+                    if ((e = launch_probe(pr, stream)) != cudaSuccess) return OPH_ECUDA;
+                }
+            }
             // sets with too many distinct matched queries: BRUTE over that list (device-side count)
             ScanArgs sl = s;
             sl.set_list = w.ovf_list;

@@ -473,7 +473,8 @@ __global__ void __launch_bounds__(128) scan_kernel(const __grid_constant__ ScanA
     __syncthreads();
 
     const uint64_t tile_sets = 128ull * SPT;
-    const uint64_t n_items = LIST ? *a.list_count : a.n_sets;
+    // list mode: items = listed sets; else items = sets [s_begin, n_sets)
+    const uint64_t n_items = LIST ? *a.list_count : a.n_sets - a.s_begin;
     const uint64_t ntiles = (n_items + tile_sets - 1) / tile_sets;
     const uint64_t t_first = LIST ? blockIdx.y : (uint64_t)blockIdx.y * a.tiles_per_cta;
     const uint64_t t_end = LIST ? ntiles : min(ntiles, (uint64_t)(blockIdx.y + 1) * a.tiles_per_cta);
@@ -481,7 +482,7 @@ __global__ void __launch_bounds__(128) scan_kernel(const __grid_constant__ ScanA
     for (uint64_t t = t_first; t < t_end; t += t_step) {
         const uint64_t i0 = t * tile_sets + threadIdx.x * SPT;
         const bool active = i0 < n_items;
-        const uint64_t s0 = LIST ? (active ? a.set_list[i0] : 0ull) : i0;
+        const uint64_t s0 = LIST ? (active ? a.set_list[i0] : 0ull) : a.s_begin + i0;
         uint32_t cnt[SPT][B];
 #pragma unroll
         for (int j = 0; j < SPT; j++)
@@ -642,10 +643,10 @@ __global__ void __launch_bounds__(kProbeThreads) probe_kernel(const __grid_const
     const uint32_t tid = threadIdx.x;
     const uint32_t smask = (1u << a.log2S) - 1u;
     const bool mw = a.method == kMinwise;
-    for (uint64_t base = (uint64_t)blockIdx.x * kProbeThreads; base < a.n_sets;
+    for (uint64_t base = a.s_begin + (uint64_t)blockIdx.x * kProbeThreads; base < a.s_end;
          base += (uint64_t)gridDim.x * kProbeThreads) {
         const uint64_t s = base + tid;
-        const bool act = s < a.n_sets && !(mw && a.sflags[s]);
+        const bool act = s < a.s_end && !(mw && a.sflags[s]);
         int nl = 0;
         bool ovf = false;
         if (act) {
@@ -907,7 +908,7 @@ static cudaError_t launch_scan_t(const ScanArgs &a0, cudaStream_t st) {
         gy = std::max<uint64_t>(1, (148ull * 4 + qblocks - 1) / qblocks);
         a.tiles_per_cta = 1;
     } else {
-        const uint64_t ntiles = (a.n_sets + tile_sets - 1) / tile_sets;
+        const uint64_t ntiles = (a.n_sets - a.s_begin + tile_sets - 1) / tile_sets;
         // aim for >= 4 waves of CTAs over 148 SMs, otherwise longest tile runs per CTA
         const uint64_t want_y = std::max<uint64_t>(1, (148ull * 4 * 4 + qblocks - 1) / qblocks);
         uint64_t tpc = std::max<uint64_t>(1, (ntiles + want_y - 1) / want_y);
@@ -924,7 +925,7 @@ static cudaError_t launch_scan_t(const ScanArgs &a0, cudaStream_t st) {
 }
 
 cudaError_t launch_scan(const ScanArgs &a, uint32_t B, cudaStream_t st) {
-    if (a.n_sets == 0 || a.nq == 0) return cudaSuccess;
+    if (a.n_sets <= a.s_begin || a.nq == 0) return cudaSuccess;
     (void)B;
     if (a.set_list) return launch_scan_t<32, 1, true>(a, st);
     return launch_scan_t<32, 2, false>(a, st);
@@ -939,8 +940,9 @@ cudaError_t launch_table(const TableArgs &a, cudaStream_t st) {
 }
 
 cudaError_t launch_probe(const ProbeArgs &a, cudaStream_t st) {
-    if (a.n_sets == 0) return cudaSuccess;
-    const unsigned grid = (unsigned)std::min<uint64_t>((a.n_sets + kProbeThreads - 1) / kProbeThreads, 148ull * 8);
+    if (a.s_end <= a.s_begin) return cudaSuccess;
+    const uint64_t n = a.s_end - a.s_begin;
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + kProbeThreads - 1) / kProbeThreads, 148ull * 8);
     probe_kernel<<<grid, kProbeThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
