@@ -162,6 +162,32 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------- GPU arm
+CONFIG_NAMES = ["text-like", "image-like", "scale", "sweep-0.2", "sweep-0.5", "sweep-0.9", "tiny"]
+
+
+def make_workload(config: str, rank: int):
+    """(workload of this rank's shard, scan strategy, hit capacity per method,
+    survivor-capacity limit).  Every rank scores the same queries against its
+    own independent shard (weak scaling).  Strategy: PROBE where background
+    similarity is low (text-like law), BRUTE where every set shares bins with
+    the queries (Zipf image words, the sweep's hub)."""
+    import paper_1805_11254_b200 as og
+    from workloads import gen_gpu, text_like, tiny
+    if config == "text-like":
+        return text_like(shard=rank), og.OPH_STRATEGY_PROBE, 1 << 22, 1 << 28
+    if config == "scale":  # configs[3]: 8 shards x 1.25M sets, 16,384 queries, T = 0.8
+        return gen_gpu.scale_shard(shard=rank), og.OPH_STRATEGY_PROBE, 1 << 23, 1 << 28
+    if config == "image-like":
+        return gen_gpu.image_like(shard=rank), og.OPH_STRATEGY_BRUTE, 1 << 23, 1 << 28
+    if config.startswith("sweep-"):
+        # 256 of the 1,024 hub perturbations per step: at Jmax = 0.9 a quarter of all pairs are hits
+        return (gen_gpu.sweep(float(config.split("-")[1]), shard=rank, n_queries=256), og.OPH_STRATEGY_BRUTE,
+                1 << 28, 1 << 28)
+    if config == "tiny":
+        return tiny(), og.OPH_STRATEGY_AUTO, 1 << 20, 1 << 24
+    raise ValueError(config)
+
+
 def count_launches(step_fn):
     """Kernel launches of one step, counted with the CUDA profiler (untimed)."""
     try:
@@ -199,7 +225,7 @@ def run_ours(args):
     og.build()
     og.lib()
 
-    w = text_like(shard=rank)
+    w, strategy, cap, surv_limit = make_workload(args.config, rank)
     p = w.params
     V, seed = w.vocab_size, p["perm_seed"]
     N, Q = w.n_sets, w.n_queries
@@ -209,7 +235,7 @@ def run_ours(args):
     flat = og.flat_layout(V, k, kp)
     hier = og.oph_hier_layout_make(V, p["a"], p["b"], hkp)
     L = hier.L
-    prm = og.params(p["t_num"], p["t_den"], p["eps"])
+    prm = og.params(p["t_num"], p["t_den"], p["eps"], strategy=strategy)
     # the OPH family runs on a high-priority stream; the MinWise baseline (one long ALU-bound
     # kernel of short CTAs) on a normal-priority side stream fills the SMs around it
     lo_prio, hi_prio = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
@@ -225,13 +251,12 @@ def run_ours(args):
     qo, qh = og.oph_build_sketches(qsets, V, seed, flat=flat, hier=hier)
     qmw = og.minwise_build_sketches(qsets, V, seed, mwk)
     counts = torch.zeros((4,), dtype=torch.int64, device="cuda")
-    cap = 1 << 22
     res = []
     for i in range(4):
         r = og.Results(cap)
         r.count = counts[i:i + 1]
         res.append(r)
-    surv_cap = ((Q + 31) // 32) * 32 * N
+    surv_cap = min(((Q + 31) // 32) * 32 * N, surv_limit)
     ws = [og.Workspace() for _ in range(5)]
     outs = [og.Results(cap * (world if rank == 0 else 1)) for _ in range(4)]
     merged = [og.Results(cap * world) for _ in range(4)] if world > 1 else None
@@ -460,17 +485,19 @@ def run_ours(args):
         t = time.perf_counter() - t0
         cpu = {"value": 3 * CPU_SAMPLE_QUERIES * CPU_SAMPLE_SETS / t, "unit": UNIT, "cores": oracle.num_threads(),
                "kind": "oracle",
-               "sample": f"text-like: first {CPU_SAMPLE_SETS} sets x first {CPU_SAMPLE_QUERIES} queries, whole path "
+               "sample": f"{args.config}: first {CPU_SAMPLE_SETS} sets x first {CPU_SAMPLE_QUERIES} queries, whole path "
                          f"(sketch builds incl. MinWise, 4 comparisons, threshold lists), {t:.1f} s"}
 
     line = {
         "metric": METRIC, "value": 3 * Q * N_total / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32", "data": "synthetic",
-        "config": {"workload": "text-like", "sets_per_gpu": N, "sets_total": N_total, "queries": Q, "k": k,
+        "config": {"workload": args.config, "sets_per_gpu": N, "sets_total": N_total, "queries": Q, "k": k,
                    "kprime": kp, "hoph_groups": L, "minwise_k": mwk, "T": f"{p['t_num']}/{p['t_den']}",
                    "epsilon": p["eps"], "parallelism": f"set-sharded x{world}",
-                   "l2": "inputs larger than L2 (CSR 320 MB + sketches 1.1 GB per step)"},
+                   "scan_strategy": ["auto", "brute", "probe"][strategy],
+                   "l2": f"inputs larger than L2 (CSR {4 * nnz / 1e6:.0f} MB + sketches "
+                         f"{4 * N * (k + L * hkp + mwk) / 1e9:.2f} GB per step)"},
         "value_definition": "3 * queries * sets_total / step time (each pair scored by full OPH, GOPH, HOPH)",
         "sketches_per_s": {"oph_hoph": (N_total) / (phase_ms["build_oph_hoph"] / 1e3),
                            "minwise": (N_total) / (phase_ms["build_minwise"] / 1e3)},
@@ -502,6 +529,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="text-like", choices=CONFIG_NAMES,
+                    help="workload (BASELINE.json configs); text-like is the headline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-launch-count", action="store_true", help="skip the CUPTI launch count (use under ncu)")

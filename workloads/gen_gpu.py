@@ -114,14 +114,20 @@ def _zipf_draw(V, s):
     return draw
 
 
-def image_like(seed: int = 3, n_sets: int = 1_000_000, n_queries: int = 4096, planted_per_query: int = 4) -> Workload:
+def image_like(seed: int = 3, n_sets: int = 1_000_000, n_queries: int = 4096, planted_per_query: int = 4,
+               shard: int = 0) -> Workload:
+    """The queries depend on `seed` only; the collection (with its planted
+    duplicates of those queries) on (seed, shard)."""
     torch = _torch()
     V = 2 ** 20
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(seed)
-    rng = np.random.default_rng(seed)
+    qgen = torch.Generator(device="cuda")
+    qgen.manual_seed(seed)
+    rq = np.random.default_rng(seed)
     zd = _zipf_draw(V, 1.1)
-    q_off, q_ids = sample_sets_gpu(gen, np.maximum(1, rng.poisson(800, size=n_queries)), V, zd)
+    q_off, q_ids = sample_sets_gpu(qgen, np.maximum(1, rq.poisson(800, size=n_queries)), V, zd)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed * 1000 + 7 + shard)
+    rng = np.random.default_rng([seed, shard])
     cpu_draw = _zipf_sampler(V, 1.1)
     planted_sets, meta = [], []
     for q in range(n_queries):
@@ -136,8 +142,10 @@ def image_like(seed: int = 3, n_sets: int = 1_000_000, n_queries: int = 4096, pl
     return _assemble(rng, "image-like", V, bg_off, bg_ids, n_sets, planted_sets, q_off, q_ids, meta, params)
 
 
-def sweep(jmax: float, seed: int = 5, n_sets: int = 2_000_000, n_queries: int = 1024, chunk: int = 65536) -> Workload:
-    """configs[4] at one Jmax: every set is a gen_pair duplicate of the hub H at J ~ U(0, Jmax)."""
+def sweep(jmax: float, seed: int = 5, n_sets: int = 2_000_000, n_queries: int = 1024, chunk: int = 65536,
+          shard: int = 0) -> Workload:
+    """configs[4] at one Jmax: every set is a gen_pair duplicate of the hub H at J ~ U(0, Jmax).
+    The hub and the queries depend on (seed, Jmax); the collection also on shard."""
     torch = _torch()
     V = 2 ** 20
     gen = torch.Generator(device="cuda")
@@ -145,6 +153,8 @@ def sweep(jmax: float, seed: int = 5, n_sets: int = 2_000_000, n_queries: int = 
     rng = np.random.default_rng([seed, int(round(jmax * 100))])
     draw = _uniform_draw(V)
     h_off, H = sample_sets_gpu(gen, np.array([max(2, rng.poisson(800))]), V, draw)
+    if shard:
+        gen.manual_seed(seed * 1000 + int(round(jmax * 100)) + 100003 * shard)
     s = len(H)
     cpu_draw = _uniform_sampler(V)
     qsets, meta_q = [], []
