@@ -101,6 +101,7 @@ struct ScanArgs {
     OutArgs out;
     SurvList surv;
     unsigned long long *surv_count;
+    uint64_t surv_cap;      // survivor list capacity
     // list mode: the sets to scan are set_list[0 .. *list_count) (PROBE overflow sets)
     const uint32_t *set_list;
     const unsigned long long *list_count;
@@ -137,6 +138,7 @@ struct ProbeArgs {
     OutArgs out;
     SurvList surv;
     unsigned long long *surv_count;
+    uint64_t surv_cap;
     uint32_t *ovf_list;     // sets that matched more than kProbeList queries
     unsigned long long *ovf_count;
     uint64_t s_begin, s_end;  // the sets [s_begin, s_end) are probed

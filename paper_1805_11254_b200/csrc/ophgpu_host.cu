@@ -516,96 +516,95 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     }
 
     unsigned long long *ovf_count = w.counters + kMaxGroups + 2;
-    for (uint64_t q0 = 0; q0 < n_q; q0 += chunk) {
-        const uint64_t nq = std::min<uint64_t>(chunk, n_q - q0);
+    unsigned long long *saved_hits = w.counters + kMaxGroups + 3;  // not cleared per chunk
+
+    // the collection scan of queries [q0, q0+nq): BRUTE, or PROBE + its BRUTE list fallback
+    auto scan_chunk = [&](uint64_t q0, uint64_t nq) -> cudaError_t {
+        cudaError_t e;
         s.q_col0 = (uint32_t)q0;
         s.nq = (uint32_t)nq;
+        s.surv_cap = cap;
         if (levels) {
             s.surv = w.list[plan.l0 % 2];
             s.surv_count = w.counters + plan.l0;
         }
-        if (levels || probe) {
-            e = cudaMemsetAsync(w.counters, 0, kCounters * 8, stream);
-            if (e != cudaSuccess) return OPH_ECUDA;
-        }
-        if (probe) {
-            const uint32_t log2S = probe_log2S(nq);
-            e = cudaMemsetAsync(w.table, 0, (size_t)s.nscan * (1ull << log2S) * 8, stream);
-            if (e != cudaSuccess) return OPH_ECUDA;
-            TableArgs ta{};
-            ta.QT = w.QT;
-            ta.qflags = w.qflags;
-            ta.ldq = w.ldq;
-            ta.q_col0 = (uint32_t)q0;
-            ta.nq = (uint32_t)nq;
-            ta.nscan = s.nscan;
-            ta.log2S = log2S;
-            ta.minwise = mw;
-            ta.table = w.table;
-            if ((e = launch_table(ta, stream)) != cudaSuccess) return OPH_ECUDA;
-            ProbeArgs pr{};
-            pr.F = s.F;
-            pr.E = s.E;
-            pr.sflags = s.sflags;
-            pr.n_sets = n_s;
-            pr.ld = s.ld;
-            pr.table = w.table;
-            pr.log2S = log2S;
-            pr.nscan = s.nscan;
-            pr.QEM = w.QEM;
-            pr.qflags = w.qflags;
-            pr.nw = nw;
-            pr.nbins_total = nb;
-            pr.q_col0 = (uint32_t)q0;
-            pr.method = method;
-            pr.final_ = s.final_;
-            pr.level = s.level;
-            pr.joint = s.joint;
-            pr.t_num = s.t_num;
-            pr.t_den = s.t_den;
-            pr.w1 = s.w1;
-            pr.acc = s.acc;
-            pr.rej = s.rej;
-            pr.out = out;
-            pr.surv = s.surv;
-            pr.surv_count = s.surv_count;
-            pr.ovf_list = w.ovf_list;
-            pr.ovf_count = ovf_count;
-            // AUTO probes a leading sample of the sets first; when more than a quarter of it
-            // matches too many distinct queries (a high-similarity collection), the rest goes
-            // to BRUTE as one contiguous scan instead of the list fallback
-            const uint64_t n1 = p->strategy == OPH_STRATEGY_AUTO
-                                    ? std::min<uint64_t>(n_s, std::max<uint64_t>(16384, ceil_div(n_s / 16, 256) * 256))
-                                    : n_s;
-            pr.s_begin = 0;
-            pr.s_end = n1;
-            if ((e = launch_probe(pr, stream)) != cudaSuccess) return OPH_ECUDA;
-            if (n1 < n_s) {
-                unsigned long long ovf = 0;
-                if (cudaMemcpyAsync(&ovf, ovf_count, sizeof(ovf), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
-                    cudaStreamSynchronize(stream) != cudaSuccess)
-                    return OPH_ECUDA;
-                if (ovf * 4 > n1) {
-                    ScanArgs sr = s;
-                    sr.s_begin = n1;
-                    if ((e = launch_scan(sr, 32, stream)) != cudaSuccess) return OPH_ECUDA;
-                } else {
-                    pr.s_begin = n1;
-                    pr.s_end = n_s;
-                    if ((e = launch_probe(pr, stream)) != cudaSuccess) return OPH_ECUDA;
-                }
+        if (levels || probe)
+            if ((e = cudaMemsetAsync(w.counters, 0, (kMaxGroups + 3) * 8, stream)) != cudaSuccess) return e;
+        if (!probe) return launch_scan(s, 32, stream);
+        const uint32_t log2S = probe_log2S(nq);
+        if ((e = cudaMemsetAsync(w.table, 0, (size_t)s.nscan * (1ull << log2S) * 8, stream)) != cudaSuccess) return e;
+        TableArgs ta{};
+        ta.QT = w.QT;
+        ta.qflags = w.qflags;
+        ta.ldq = w.ldq;
+        ta.q_col0 = (uint32_t)q0;
+        ta.nq = (uint32_t)nq;
+        ta.nscan = s.nscan;
+        ta.log2S = log2S;
+        ta.minwise = mw;
+        ta.table = w.table;
+        if ((e = launch_table(ta, stream)) != cudaSuccess) return e;
+        ProbeArgs pr{};
+        pr.F = s.F;
+        pr.E = s.E;
+        pr.sflags = s.sflags;
+        pr.n_sets = n_s;
+        pr.ld = s.ld;
+        pr.table = w.table;
+        pr.log2S = log2S;
+        pr.nscan = s.nscan;
+        pr.QEM = w.QEM;
+        pr.qflags = w.qflags;
+        pr.nw = nw;
+        pr.nbins_total = nb;
+        pr.q_col0 = (uint32_t)q0;
+        pr.method = method;
+        pr.final_ = s.final_;
+        pr.level = s.level;
+        pr.joint = s.joint;
+        pr.t_num = s.t_num;
+        pr.t_den = s.t_den;
+        pr.w1 = s.w1;
+        pr.acc = s.acc;
+        pr.rej = s.rej;
+        pr.out = out;
+        pr.surv = s.surv;
+        pr.surv_count = s.surv_count;
+        pr.surv_cap = cap;
+        pr.ovf_list = w.ovf_list;
+        pr.ovf_count = ovf_count;
+        // AUTO probes a leading sample of the sets first; when more than a quarter of it
+        // matches too many distinct queries (a high-similarity collection), the rest goes
+        // to BRUTE as one contiguous scan instead of the list fallback
+        const uint64_t n1 = p->strategy == OPH_STRATEGY_AUTO
+                                ? std::min<uint64_t>(n_s, std::max<uint64_t>(16384, ceil_div(n_s / 16, 256) * 256))
+                                : n_s;
+        pr.s_begin = 0;
+        pr.s_end = n1;
+        if ((e = launch_probe(pr, stream)) != cudaSuccess) return e;
+        if (n1 < n_s) {
+            unsigned long long ovf = 0;
+            if ((e = cudaMemcpyAsync(&ovf, ovf_count, sizeof(ovf), cudaMemcpyDeviceToHost, stream)) != cudaSuccess)
+                return e;
+            if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return e;
+            if (ovf * 4 > n1) {
+                ScanArgs sr = s;
+                sr.s_begin = n1;
+                if ((e = launch_scan(sr, 32, stream)) != cudaSuccess) return e;
+            } else {
+                pr.s_begin = n1;
+                pr.s_end = n_s;
+                if ((e = launch_probe(pr, stream)) != cudaSuccess) return e;
             }
-            // sets with too many distinct matched queries: BRUTE over that list (device-side count)
-            ScanArgs sl = s;
-            sl.set_list = w.ovf_list;
-            sl.list_count = ovf_count;
-            if ((e = launch_scan(sl, 32, stream)) != cudaSuccess) return OPH_ECUDA;
-        } else {
-            e = launch_scan(s, 32, stream);
-            if (e != cudaSuccess) return OPH_ECUDA;
         }
-        if (!levels) continue;
-        // later levels, kLevelsPerLaunch per launch, survivors compacted between launches
+        // sets with too many distinct matched queries: BRUTE over that list (device-side count)
+        ScanArgs sl = s;
+        sl.set_list = w.ovf_list;
+        sl.list_count = ovf_count;
+        return launch_scan(sl, 32, stream);
+    };
+    // later levels, kLevelsPerLaunch per launch, survivors compacted between launches
+    auto level_chunk = [&]() -> cudaError_t {
         for (uint32_t l = plan.l0 + 1; l <= nlev; l += kLevelsPerLaunch) {
             const uint32_t l_last = std::min(nlev, l + kLevelsPerLaunch - 1);
             la.level = l;
@@ -614,11 +613,39 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
             la.out = w.list[l_last % 2];
             la.count_in = w.counters + (l - 1);
             la.count_out = w.counters + l_last;
-            e = launch_level(la, stream);
-            if (e != cudaSuccess) return OPH_ECUDA;
+            cudaError_t e = launch_level(la, stream);
+            if (e != cudaSuccess) return e;
         }
+        return cudaSuccess;
+    };
+    auto safe_range = [&](uint64_t q0, uint64_t q1) -> cudaError_t {
+        for (uint64_t a0 = q0; a0 < q1; a0 += chunk) {
+            cudaError_t e = scan_chunk(a0, std::min<uint64_t>(chunk, q1 - a0));
+            if (e != cudaSuccess) return e;
+            if (levels && (e = level_chunk()) != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    };
+
+    if (levels && probe && chunk < n_q) {
+        // PROBE leaves few survivors: try every query at once; if the survivor list overflowed,
+        // roll the hit counter back and redo the queries in chunks sized for the worst case
+        e = cudaMemcpyAsync(saved_hits, res->d_count, 8, cudaMemcpyDeviceToDevice, stream);
+        if (e == cudaSuccess) e = scan_chunk(0, n_q);
+        unsigned long long n_surv = 0;
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(&n_surv, w.counters + plan.l0, sizeof(n_surv), cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) return OPH_ECUDA;
+        if (n_surv <= cap) {
+            e = level_chunk();
+        } else {
+            e = cudaMemcpyAsync(res->d_count, saved_hits, 8, cudaMemcpyDeviceToDevice, stream);
+            if (e == cudaSuccess) e = safe_range(0, n_q);
+        }
+        return e == cudaSuccess ? OPH_OK : OPH_ECUDA;
     }
-    return OPH_OK;
+    return safe_range(0, n_q) == cudaSuccess ? OPH_OK : OPH_ECUDA;
 }
 
 }  // namespace

@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(128) scan_kernel(const __grid_constant__ ScanA
                     for (int q = 0; q < B; q++) {
                         const bool sp = (surv_mask >> q) & 1u;
                         const unsigned long long idx = warp_append(sp, a.surv_count);
-                        if (sp) {
+                        if (sp && idx < a.surv_cap) {  // past capacity: counted, the host redoes the chunk
                             a.surv.q[idx] = (uint32_t)(col0 + q);
                             a.surv.s[idx] = (uint32_t)s;
                             a.surv.state[idx] = a.w1 * cnt[j][q];
@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(kProbeThreads) probe_kernel(const __grid_const
             }
             emit(a.out, has, a.q_col0 + q, s, m, ex, a.level, verdict, flags, est);
             const unsigned long long idx = warp_append(surv, a.surv_count);
-            if (surv) {
+            if (surv && idx < a.surv_cap) {  // past capacity: counted, the host redoes the chunk
                 a.surv.q[idx] = a.q_col0 + q;
                 a.surv.s[idx] = (uint32_t)s;
                 a.surv.state[idx] = st;

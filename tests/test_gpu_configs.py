@@ -108,6 +108,38 @@ def test_scale_shard_full_size():
     check_config(w, sample=[0, 5, 777, 8191, 16383], strategy=og.OPH_STRATEGY_AUTO)
 
 
+@pytest.mark.parametrize("method", ["goph", "hoph"])
+def test_probe_survivor_overflow_redo(method):
+    """PROBE first scores every query at once; on a high-similarity collection
+    the survivor list overflows a minimal workspace, the hit counter is rolled
+    back and the queries are redone in worst-case-sized chunks: the hit list
+    still equals the oracle's exactly."""
+    from workloads.gen_gpu import sweep
+    w = sweep(0.9, n_sets=20_000, n_queries=128)
+    p = w.params
+    V, seed = w.vocab_size, p["perm_seed"]
+    hier = og.oph_hier_layout_make(V, 1, 1, p["hoph_kprime"])
+    flat = og.flat_layout(V, p["k"], p["kprime"])
+    so, sh = og.oph_build_sketches(og.SetCollection.from_numpy(w.offsets, w.ids), V, seed, flat=flat, hier=hier)
+    qo, qh = og.oph_build_sketches(og.SetCollection.from_numpy(w.q_offsets, w.q_ids), V, seed, flat=flat, hier=hier)
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    cap = 32 * w.n_sets
+    if method == "hoph":
+        glay = oracle.hoph_layout(V, 1, 1, p["hoph_kprime"])
+        H = oracle.hoph_sketch(w.offsets, w.ids, V, glay, p["hoph_kprime"], seed)
+        QH = oracle.hoph_sketch(w.q_offsets, w.q_ids, V, glay, p["hoph_kprime"], seed)
+        want = oracle_records(method, QH, H, kprime=p["hoph_kprime"], L=len(glay), **kw)
+        hits = gpu_threshold_hits(method, qh, sh, layout=hier, strategy=og.OPH_STRATEGY_PROBE, capacity=1 << 23,
+                                  survivor_capacity=cap, **kw)
+    else:
+        F = oracle.oph_sketch(w.offsets, w.ids, V, p["k"], seed)
+        QF = oracle.oph_sketch(w.q_offsets, w.q_ids, V, p["k"], seed)
+        want = oracle_records(method, QF, F, k=p["k"], kprime=p["kprime"], **kw)
+        hits = gpu_threshold_hits(method, qo, so, layout=flat, strategy=og.OPH_STRATEGY_PROBE, capacity=1 << 23,
+                                  survivor_capacity=cap, **kw)
+    assert [(int(h["query"]), int(h["set_id"])) for h in hits] == oracle.threshold_list(want)
+
+
 @pytest.mark.parametrize("jmax,n_sets", [(0.9, 2_000_000), (0.5, 200_000), (0.2, 200_000)])
 def test_sweep(jmax, n_sets):
     from workloads.gen_gpu import sweep
