@@ -106,6 +106,7 @@ struct ScanArgs {
     const uint32_t *set_list;
     const unsigned long long *list_count;
     uint64_t s_begin;       // range mode: scan sets [s_begin, n_sets) (s_begin even)
+    uint32_t one;           // = 1, opaque to the compiler (see acc_eq)
 };
 
 // PROBE strategy: per scanned bin b, the chunk's query values are hashed into

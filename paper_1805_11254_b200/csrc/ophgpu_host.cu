@@ -455,6 +455,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     s.t_den = p->t_den;
     s.out = out;
     s.w1 = 1;
+    s.one = 1;
     s.acc = UINT64_MAX;
     s.rej = -1;
     s.nbins_total = nb;

@@ -392,15 +392,19 @@ __device__ __forceinline__ void load_vals(const uint32_t *p, uint32_t (&v)[SPT])
 
 constexpr uint32_t kScanChunk = 512;  // query bins held in shared memory at once
 
-// c += (v == q) as ISETP + predicated IADD (2 instructions; the C++ form
-// compiles to 3: IADD, ISETP, predicated MOV)
-__device__ __forceinline__ void acc_eq(uint32_t &c, uint32_t v, uint32_t q) {
-    asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n}" : "+r"(c) : "r"(v), "r"(q));
+// c += (v == q) as ISETP (ALU pipe) + predicated IMAD c = c*one + one (FMA
+// pipe), `one` a runtime 1 the compiler cannot fold: 2 instructions split
+// over both integer pipes.  (The C++ form compiles to 3 instructions, a
+// predicated IADD puts both on the ALU pipe, which then bounds the scan.)
+__device__ __forceinline__ void acc_eq(uint32_t &c, uint32_t v, uint32_t q, uint32_t one) {
+    asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\t@p mad.lo.u32 %0, %0, %3, %3;\n}"
+        : "+r"(c)
+        : "r"(v), "r"(q), "r"(one));
 }
 
 template <int B, int SPT, int U>
 __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool active, const uint32_t *qs,
-                                          uint32_t b0, uint32_t nb, uint32_t (&cnt)[SPT][B]) {
+                                          uint32_t b0, uint32_t nb, uint32_t (&cnt)[SPT][B], uint32_t one) {
     uint32_t b = 0;
     for (; b + U <= nb; b += U) {
         uint32_t v[U][SPT];
@@ -419,10 +423,10 @@ __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool 
                 const uint4 x = q4[q];
 #pragma unroll
                 for (int j = 0; j < SPT; j++) {
-                    acc_eq(cnt[j][4 * q + 0], v[u][j], x.x);
-                    acc_eq(cnt[j][4 * q + 1], v[u][j], x.y);
-                    acc_eq(cnt[j][4 * q + 2], v[u][j], x.z);
-                    acc_eq(cnt[j][4 * q + 3], v[u][j], x.w);
+                    acc_eq(cnt[j][4 * q + 0], v[u][j], x.x, one);
+                    acc_eq(cnt[j][4 * q + 1], v[u][j], x.y, one);
+                    acc_eq(cnt[j][4 * q + 2], v[u][j], x.z, one);
+                    acc_eq(cnt[j][4 * q + 3], v[u][j], x.w, one);
                 }
             }
         }
@@ -439,10 +443,10 @@ __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool 
             const uint4 x = q4[q];
 #pragma unroll
             for (int j = 0; j < SPT; j++) {
-                acc_eq(cnt[j][4 * q + 0], v[j], x.x);
-                acc_eq(cnt[j][4 * q + 1], v[j], x.y);
-                acc_eq(cnt[j][4 * q + 2], v[j], x.z);
-                acc_eq(cnt[j][4 * q + 3], v[j], x.w);
+                acc_eq(cnt[j][4 * q + 0], v[j], x.x, one);
+                acc_eq(cnt[j][4 * q + 1], v[j], x.y, one);
+                acc_eq(cnt[j][4 * q + 2], v[j], x.z, one);
+                acc_eq(cnt[j][4 * q + 3], v[j], x.w, one);
             }
         }
     }
@@ -491,7 +495,7 @@ __global__ void __launch_bounds__(128) scan_kernel(const __grid_constant__ ScanA
 
         const uint32_t *Fp = a.F + s0;
         if (one_chunk) {
-            scan_bins<B, SPT, U>(Fp, a.ld, active, qs, 0, a.nscan, cnt);
+            scan_bins<B, SPT, U>(Fp, a.ld, active, qs, 0, a.nscan, cnt, a.one);
         } else {
             for (uint32_t c0 = 0; c0 < a.nscan; c0 += kScanChunk) {
                 const uint32_t cn = min(kScanChunk, a.nscan - c0);
@@ -499,7 +503,7 @@ __global__ void __launch_bounds__(128) scan_kernel(const __grid_constant__ ScanA
                 for (uint32_t i = threadIdx.x; i < cn * B; i += blockDim.x)
                     qs[i] = a.QT[(uint64_t)(c0 + i / B) * a.ldq + col0 + (i % B)];
                 __syncthreads();
-                scan_bins<B, SPT, U>(Fp, a.ld, active, qs, c0, cn, cnt);
+                scan_bins<B, SPT, U>(Fp, a.ld, active, qs, c0, cn, cnt, a.one);
             }
         }
 
