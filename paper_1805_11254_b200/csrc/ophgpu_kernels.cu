@@ -405,16 +405,23 @@ __device__ __forceinline__ void acc_eq(uint32_t &c, uint32_t v, uint32_t q, uint
 template <int B, int SPT, int U>
 __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool active, const uint32_t *qs,
                                           uint32_t b0, uint32_t nb, uint32_t (&cnt)[SPT][B], uint32_t one) {
+    // software pipeline: the U bin rows of the next group are loaded while the
+    // current group is compared, so HBM latency hides behind ~2*SPT*B*U instructions
     uint32_t b = 0;
-    for (; b + U <= nb; b += U) {
-        uint32_t v[U][SPT];
+    uint32_t v[U][SPT];
+    auto load_group = [&](uint32_t bb, uint32_t (&dst)[U][SPT]) {
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            if (active) load_vals<SPT>(Fp + (uint64_t)(b0 + b + u) * ld, v[u]);
+            if (active && bb + u < nb) load_vals<SPT>(Fp + (uint64_t)(b0 + bb + u) * ld, dst[u]);
             else
 #pragma unroll
-                for (int j = 0; j < SPT; j++) v[u][j] = kEmpty;
+                for (int j = 0; j < SPT; j++) dst[u][j] = kEmpty;
         }
+    };
+    if (U <= nb) load_group(0, v);
+    for (; b + U <= nb; b += U) {
+        uint32_t vn[U][SPT];
+        load_group(b + U, vn);  // past the end: fills kEmpty, never read
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint4 *q4 = reinterpret_cast<const uint4 *>(qs + (size_t)(b + u) * B);
@@ -430,6 +437,10 @@ __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool 
                 }
             }
         }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+#pragma unroll
+            for (int j = 0; j < SPT; j++) v[u][j] = vn[u][j];
     }
     for (; b < nb; b++) {
         uint32_t v[SPT];
