@@ -464,7 +464,7 @@ __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool 
 }
 
 template <int B, int SPT, bool LIST>
-__global__ void __launch_bounds__(128) scan_kernel(const __grid_constant__ ScanArgs a) {
+__global__ void __launch_bounds__(128, 3) scan_kernel(const __grid_constant__ ScanArgs a) {
     static_assert(!LIST || SPT == 1, "list mode scans one gathered set per thread");
     constexpr int U = 4;  // bins in flight per thread
     extern __shared__ __align__(16) uint32_t sm[];
