@@ -464,6 +464,8 @@ __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool 
 }
 
 template <int B, int SPT, bool LIST>
+// 3 CTAs/SM (<= 168 registers): 4 spills into the compare loop and 2 CTAs/SM leaves
+// HBM latency exposed (measured on image-like: 294 / 190 / 227 ms for 4 / 3 / 2)
 __global__ void __launch_bounds__(128, 3) scan_kernel(const __grid_constant__ ScanArgs a) {
     static_assert(!LIST || SPT == 1, "list mode scans one gathered set per thread");
     constexpr int U = 4;  // bins in flight per thread
