@@ -111,7 +111,10 @@ struct ScanArgs {
 
 // PROBE strategy: per scanned bin b, the chunk's query values are hashed into
 // an open-addressing table T_b of 2^log2S slots, slot = value << 32 | (q+1)
-// (0 = free, linear probing; duplicates occupy separate slots).
+// (0 = free, linear probing; duplicates occupy separate slots), and into a
+// blocked Bloom filter of 2^log2W 32-bit words per bin, bin-major
+// [bin][word] (a slab of 32 bins is the contiguous image the join kernel
+// copies into shared memory in one piece).
 struct TableArgs {
     const uint32_t *QT;     // prepared queries, bin-major [nb][ldq]
     const uint8_t *qflags;  // MinWise query flags (flagged queries never match)
@@ -119,16 +122,23 @@ struct TableArgs {
     uint32_t q_col0, nq, nscan, log2S;
     uint32_t minwise;
     unsigned long long *table;  // [nscan][2^log2S]
+    uint32_t *bloom;            // [32 * ceil(nscan/32)][2^log2W]
+    uint32_t log2W;
 };
 
-constexpr int kProbeList = 16;  // distinct matched queries tracked per set before falling back to BRUTE
+constexpr int kJoinList = 4;        // distinct matched queries tracked per set before falling back to BRUTE
+constexpr uint32_t kJoinMaxQ = 1024;  // queries per join pass (Bloom words per bin <= 512 -> 64 KB per slab)
+constexpr uint32_t kJoinMaxLog2W = 9;
 
 struct ProbeArgs {
     const uint32_t *F, *E;
     const uint8_t *sflags;
     uint64_t n_sets, ld;
     const unsigned long long *table;
-    uint32_t log2S, nscan;
+    const uint32_t *bloom;
+    uint32_t log2S, nscan, log2W;
+    uint32_t R;             // sets per CTA (multiple of 32; set by launch_probe)
+    uint32_t nst;           // unused
     const uint32_t *QEM;    // query masks, query-major [n_q][nw]
     const uint8_t *qflags;  // MinWise query flags, indexed by global query
     uint32_t nw, nbins_total;
@@ -140,7 +150,7 @@ struct ProbeArgs {
     SurvList surv;
     unsigned long long *surv_count;
     uint64_t surv_cap;
-    uint32_t *ovf_list;     // sets that matched more than kProbeList queries
+    uint32_t *ovf_list;     // sets that matched more than kJoinList queries
     unsigned long long *ovf_count;
     uint64_t s_begin, s_end;  // the sets [s_begin, s_end) are probed
 };

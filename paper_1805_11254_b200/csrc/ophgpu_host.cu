@@ -309,7 +309,8 @@ struct Ws {
     uint32_t *QT, *QE, *QM, *QEM;
     uint8_t *qflags;
     unsigned long long *counters;  // [kMaxGroups + 2] level counters, then the PROBE overflow counter
-    unsigned long long *table;     // PROBE tables [nb][S]
+    unsigned long long *table;     // PROBE exact tables [nb][S]
+    uint32_t *bloom;               // PROBE filters [ceil(nb/32)][W][32]
     uint32_t *ovf_list;            // PROBE overflow sets [n_sets]
     SurvList list[2];
     uint64_t ldq, cap;
@@ -318,19 +319,30 @@ struct Ws {
 constexpr uint32_t kCounters = kMaxGroups + 4;
 constexpr uint32_t kLevelsPerLaunch = 4;  // GOPH/HOPH levels per survivor-kernel launch
 
-// PROBE table slots per bin for a chunk of nq queries: load factor <= 1/4
+// PROBE exact-table slots per bin for a pass of nq queries: load factor <= 1/4
 uint32_t probe_log2S(uint64_t nq) {
     uint32_t l = 4;
     while ((1ull << l) < 4 * nq) l++;
     return l;
 }
 
+// Bloom words per bin for a pass of nq queries: >= 16 bits per query, >= 8 words
+uint32_t probe_log2W(uint64_t nq) {
+    uint32_t l = 3;
+    while ((1ull << l) * 32 < 16 * nq) l++;
+    return l;
+}
+
+uint64_t probe_pass(uint64_t ldq) { return std::min<uint64_t>(ldq, kJoinMaxQ); }
+
 size_t ws_fixed_bytes(uint64_t n_q, uint64_t n_sets, uint32_t nb) {
     const uint64_t ldq = ceil_div(n_q ? n_q : 1, 32) * 32;
     const uint64_t nw = ceil_div(nb, 32);
+    const uint64_t pq = probe_pass(ldq);
     return align256(nb * ldq * 4) + align256(nw * ldq * 4) + align256(n_q * (uint64_t)nb * 4) +
            align256(n_q * nw * 4) + align256(ldq) + align256(kCounters * 8) +
-           align256((uint64_t)nb * (1ull << probe_log2S(ldq)) * 8) + align256(n_sets * 4);
+           align256((uint64_t)nb * (1ull << probe_log2S(pq)) * 8) +
+           align256(ceil_div(nb, 32) * (1ull << probe_log2W(pq)) * 32 * 4) + align256(n_sets * 4);
 }
 
 constexpr uint64_t kSurvBytes = 2 * (4 + 4 + 8 + 4);  // two lists, per entry
@@ -346,7 +358,9 @@ Ws carve_ws(void *base, uint64_t n_q, uint64_t n_sets, uint32_t nb, uint64_t cap
     w.QEM = (uint32_t *)p; p += align256(n_q * nw * 4);
     w.qflags = (uint8_t *)p; p += align256(w.ldq);
     w.counters = (unsigned long long *)p; p += align256(kCounters * 8);
-    w.table = (unsigned long long *)p; p += align256((uint64_t)nb * (1ull << probe_log2S(w.ldq)) * 8);
+    const uint64_t pq = probe_pass(w.ldq);
+    w.table = (unsigned long long *)p; p += align256((uint64_t)nb * (1ull << probe_log2S(pq)) * 8);
+    w.bloom = (uint32_t *)p; p += align256(ceil_div(nb, 32) * (1ull << probe_log2W(pq)) * 32 * 4);
     w.ovf_list = (uint32_t *)p; p += align256(n_sets * 4);
     w.cap = cap;
     for (int i = 0; i < 2; i++) {
@@ -520,20 +534,17 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     unsigned long long *saved_hits = w.counters + kMaxGroups + 3;  // not cleared per chunk
 
     // the collection scan of queries [q0, q0+nq): BRUTE, or PROBE + its BRUTE list fallback
-    auto scan_chunk = [&](uint64_t q0, uint64_t nq) -> cudaError_t {
+    // (PROBE in passes of <= kJoinMaxQ queries, each one stream over the collection)
+    auto probe_pass_run = [&](uint64_t q0, uint64_t nq) -> cudaError_t {
         cudaError_t e;
         s.q_col0 = (uint32_t)q0;
         s.nq = (uint32_t)nq;
-        s.surv_cap = cap;
-        if (levels) {
-            s.surv = w.list[plan.l0 % 2];
-            s.surv_count = w.counters + plan.l0;
-        }
-        if (levels || probe)
-            if ((e = cudaMemsetAsync(w.counters, 0, (kMaxGroups + 3) * 8, stream)) != cudaSuccess) return e;
-        if (!probe) return launch_scan(s, 32, stream);
-        const uint32_t log2S = probe_log2S(nq);
+        if ((e = cudaMemsetAsync(ovf_count, 0, 8, stream)) != cudaSuccess) return e;
+        const uint32_t log2S = probe_log2S(nq), log2W = probe_log2W(nq);
         if ((e = cudaMemsetAsync(w.table, 0, (size_t)s.nscan * (1ull << log2S) * 8, stream)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(w.bloom, 0, (size_t)ceil_div(s.nscan, 32) * (1ull << log2W) * 32 * 4, stream)) !=
+            cudaSuccess)
+            return e;
         TableArgs ta{};
         ta.QT = w.QT;
         ta.qflags = w.qflags;
@@ -544,6 +555,8 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         ta.log2S = log2S;
         ta.minwise = mw;
         ta.table = w.table;
+        ta.bloom = w.bloom;
+        ta.log2W = log2W;
         if ((e = launch_table(ta, stream)) != cudaSuccess) return e;
         ProbeArgs pr{};
         pr.F = s.F;
@@ -552,7 +565,9 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         pr.n_sets = n_s;
         pr.ld = s.ld;
         pr.table = w.table;
+        pr.bloom = w.bloom;
         pr.log2S = log2S;
+        pr.log2W = log2W;
         pr.nscan = s.nscan;
         pr.QEM = w.QEM;
         pr.qflags = w.qflags;
@@ -603,6 +618,22 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         sl.set_list = w.ovf_list;
         sl.list_count = ovf_count;
         return launch_scan(sl, 32, stream);
+    };
+    auto scan_chunk = [&](uint64_t q0, uint64_t nq) -> cudaError_t {
+        cudaError_t e;
+        s.q_col0 = (uint32_t)q0;
+        s.nq = (uint32_t)nq;
+        s.surv_cap = cap;
+        if (levels) {
+            s.surv = w.list[plan.l0 % 2];
+            s.surv_count = w.counters + plan.l0;
+        }
+        if (levels || probe)
+            if ((e = cudaMemsetAsync(w.counters, 0, (kMaxGroups + 3) * 8, stream)) != cudaSuccess) return e;
+        if (!probe) return launch_scan(s, 32, stream);
+        for (uint64_t a0 = q0; a0 < q0 + nq; a0 += kJoinMaxQ)
+            if ((e = probe_pass_run(a0, std::min<uint64_t>(kJoinMaxQ, q0 + nq - a0))) != cudaSuccess) return e;
+        return cudaSuccess;
     };
     // later levels, kLevelsPerLaunch per launch, survivors compacted between launches
     auto level_chunk = [&]() -> cudaError_t {

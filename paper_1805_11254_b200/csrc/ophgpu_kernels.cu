@@ -618,20 +618,40 @@ __global__ void __launch_bounds__(128, 3) scan_kernel(const __grid_constant__ Sc
 }
 
 // ---------------------------------------------------------------------------
-// K3' PROBE: the same scan as a hash join.  A query bin matches a set bin
-// only when the values are equal, so instead of testing every (query, set,
-// bin) triple, the chunk's query values of each scanned bin are hashed into
-// a table (table_kernel) and every set bin probes it once (probe_kernel):
-// work ~ N * bins + matches instead of Q * N * bins.  Per set, the matched
-// queries and their counts are collected in shared memory; pairs with no
-// matched bin have N_mb = 0 (full OPH / MinWise: never Similar for T > 0;
-// GOPH / HOPH: the host only picks PROBE when state 0 is rejected at the
-// scanned level), so only listed pairs are decided and emitted.  A set that
-// matches more than kProbeList distinct queries is handed to the BRUTE scan
-// (list mode) instead.  Threshold results only.
+// K3' PROBE: the same scan as a hash join, streaming the collection once per
+// pass of up to kJoinMaxQ queries.  A query bin matches a set bin only when
+// the values are equal, so instead of testing every (query, set, bin) triple
+// the pass's query values of each scanned bin go into an exact hash table
+// (L2) and a blocked Bloom filter (table_kernel); the join kernel tests every
+// set bin against the filter held in shared memory and verifies the rare
+// positives in the exact table: work ~ N * bins + matches instead of
+// Q * N * bins.  Per set, the matched queries and their counts are collected
+// in shared memory; pairs with no matched bin have N_mb = 0 (full OPH /
+// MinWise: never Similar for T > 0; GOPH / HOPH: the host only picks PROBE
+// when state 0 is rejected at the scanned level), so only listed pairs are
+// decided and emitted.  A set that matches more than kJoinList distinct
+// queries is handed to the BRUTE scan (list mode).  Threshold results only.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t probe_hash(uint32_t v, uint32_t log2S) {
     return (v * 0x9E3779B1u) >> (32 - log2S);  // Fibonacci hashing
+}
+
+// Bloom filter of one bin: 2^log2W words; value v sets two bits of word
+// (v * golden) >> (32 - log2W).  The bit positions come from the high halves
+// of two more products (they depend on every bit of v, and IMAD.HI issues on
+// the FMA pipe, not the ALU pipe the probe loop is bound by).
+__device__ __forceinline__ uint32_t bloom_bits(uint32_t v) {
+    return __funnelshift_l(0u, 1u, __umulhi(v, 0x85EBCA6Bu)) | __funnelshift_l(0u, 1u, __umulhi(v, 0xC2B2AE35u));
+}
+
+// (b1 | b2) & ~word in one LOP3: zero iff both filter bits of v are set in word
+__device__ __forceinline__ uint32_t bloom_miss(uint32_t v, uint32_t word) {
+    uint32_t z;
+    asm("lop3.b32 %0, %1, %2, %3, 0x54;"
+        : "=r"(z)
+        : "r"(__funnelshift_l(0u, 1u, __umulhi(v, 0x85EBCA6Bu))), "r"(__funnelshift_l(0u, 1u, __umulhi(v, 0xC2B2AE35u))),
+          "r"(word));
+    return z;
 }
 
 __global__ void table_kernel(const __grid_constant__ TableArgs a) {
@@ -648,85 +668,289 @@ __global__ void table_kernel(const __grid_constant__ TableArgs a) {
         unsigned long long *T = a.table + (uint64_t)b * S;
         uint32_t h = probe_hash(v, a.log2S);
         while (atomicCAS(&T[h], 0ull, entry) != 0ull) h = (h + 1) & (uint32_t)(S - 1);
+        atomicOr(a.bloom + ((uint64_t)b << a.log2W) + ((v * 0x9E3779B1u) >> (32 - a.log2W)), bloom_bits(v));
     }
 }
 
-constexpr int kProbeThreads = 256;
-constexpr int kProbeUnroll = 8;
+// ---- mbarrier / bulk-copy (TMA engine) primitives
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// waits for the phase of the given parity; a protocol bug traps after ~4 s
+// (a failed launch) instead of hanging the device
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    if (mbar_try_wait(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_wait(bar, parity))
+        if (clock64() - t0 > 8000000000ll) __trap();
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
 
-__global__ void __launch_bounds__(kProbeThreads) probe_kernel(const __grid_constant__ ProbeArgs a) {
-    __shared__ uint32_t lq[kProbeList][kProbeThreads];  // matched query (chunk-local), per thread column
-    __shared__ uint32_t lc[kProbeList][kProbeThreads];  // its matched-bin count
-    const uint32_t tid = threadIdx.x;
+constexpr int kJoinWarps = 16;
+constexpr int kJoinThreads = 32 * kJoinWarps;
+constexpr uint32_t kJoinQCap = 256;  // candidate queue per warp (4-B entries)
+constexpr uint32_t kJoinTile = 64;  // sets per warp tile (2 per lane, one 8-B load per bin row)
+
+// shared-memory carve-up of the join kernel (bytes, 128-B aligned regions)
+struct JoinLayout {
+    uint32_t bars, tab, lists, ovf, queue, qcount, total;
+};
+__host__ __device__ inline uint32_t join_align(uint32_t x) { return (x + 127u) & ~127u; }
+__host__ __device__ inline JoinLayout join_layout(uint32_t W, uint32_t R) {
+    JoinLayout L;
+    L.bars = 0;
+    L.tab = 128;
+    L.lists = L.tab + 2 * 32 * W * 4;
+    L.ovf = join_align(L.lists + kJoinList * R * 4);
+    L.queue = join_align(L.ovf + R / 8);
+    L.qcount = L.queue + kJoinWarps * kJoinQCap * 4;
+    L.total = join_align(L.qcount + kJoinWarps * 4);
+    return L;
+}
+
+// count one more matched bin of query q for the set at local index sl:
+// list entry = (q + 1) << 16 | count, 0 = free; a full list flags the set
+__device__ __forceinline__ void list_add(uint32_t *lists, uint32_t R, uint32_t *ovf, uint32_t sl, uint32_t q) {
+    const uint32_t key = (q + 1u) << 16;
+#pragma unroll
+    for (int e = 0; e < kJoinList; e++) {
+        uint32_t *p = lists + e * R + sl;
+        uint32_t x = *(volatile uint32_t *)p;
+        for (;;) {
+            if (x == 0u) {
+                const uint32_t old = atomicCAS(p, 0u, key | 1u);
+                if (old == 0u) return;
+                x = old;
+                continue;
+            }
+            if ((x & 0xFFFF0000u) == key) {
+                atomicAdd(p, 1u);
+                return;
+            }
+            break;
+        }
+    }
+    atomicOr(ovf + (sl >> 5), 1u << (sl & 31));
+}
+
+// verify n queued filter positives (warp-collective; entry = local set | bin << 16):
+// every query whose value of that bin equals the set's value counts one matched
+// bin.  The values are re-read from the collection (the tile was just streamed,
+// so L2 hits), and each lane issues all its loads before walking any chain.
+__device__ __noinline__ void join_flush(const ProbeArgs &a, uint64_t s_lo, uint32_t *lists, uint32_t *ovf,
+                                        const uint32_t *queue, uint32_t n) {
+    constexpr int kPer = kJoinQCap / 32;
+    const uint32_t lane = threadIdx.x & 31u;
     const uint32_t smask = (1u << a.log2S) - 1u;
-    const bool mw = a.method == kMinwise;
-    for (uint64_t base = a.s_begin + (uint64_t)blockIdx.x * kProbeThreads; base < a.s_end;
-         base += (uint64_t)gridDim.x * kProbeThreads) {
-        const uint64_t s = base + tid;
-        const bool act = s < a.s_end && !(mw && a.sflags[s]);
-        int nl = 0;
-        bool ovf = false;
-        if (act) {
-            for (uint32_t b0 = 0; b0 < a.nscan && !ovf; b0 += kProbeUnroll) {
-                uint32_t v[kProbeUnroll];
-                unsigned long long slot[kProbeUnroll];
+    __syncwarp();  // the queue entries of every lane are visible
+    uint32_t c[kPer], v[kPer];
 #pragma unroll
-                for (int u = 0; u < kProbeUnroll; u++)
-                    v[u] = (b0 + u < a.nscan) ? __ldg(a.F + (uint64_t)(b0 + u) * a.ld + s) : kEmpty;
+    for (int r = 0; r < kPer; r++) {
+        const uint32_t e = lane + 32u * r;
+        c[r] = e < n ? queue[e] : 0xFFFFFFFFu;
+        if (c[r] != 0xFFFFFFFFu) v[r] = __ldg(a.F + (uint64_t)(c[r] >> 16) * a.ld + s_lo + (c[r] & 0xFFFFu));
+    }
+    unsigned long long slot[kPer];
 #pragma unroll
-                for (int u = 0; u < kProbeUnroll; u++) {
-                    const bool skip = (b0 + u >= a.nscan) || (!mw && v[u] == kEmpty);
-                    slot[u] = skip ? 0ull
-                                   : __ldg(a.table + ((uint64_t)(b0 + u) << a.log2S) + probe_hash(v[u], a.log2S));
-                }
+    for (int r = 0; r < kPer; r++)
+        if (c[r] != 0xFFFFFFFFu)
+            slot[r] = __ldg(a.table + ((uint64_t)(c[r] >> 16) << a.log2S) + probe_hash(v[r], a.log2S));
 #pragma unroll
-                for (int u = 0; u < kProbeUnroll; u++) {
-                    if (slot[u] == 0ull || ovf) continue;
-                    const unsigned long long *T = a.table + ((uint64_t)(b0 + u) << a.log2S);
-                    uint32_t h = probe_hash(v[u], a.log2S);
-                    unsigned long long sl = slot[u];
-                    while (sl != 0ull) {
-                        if ((uint32_t)(sl >> 32) == v[u]) {
-                            const uint32_t q = (uint32_t)sl - 1u;
-                            int e = 0;
-                            while (e < nl && lq[e][tid] != q) e++;
-                            if (e < nl) {
-                                lc[e][tid]++;
-                            } else if (nl < kProbeList) {
-                                lq[nl][tid] = q;
-                                lc[nl][tid] = 1;
-                                nl++;
-                            } else {
-                                ovf = true;
-                                break;
-                            }
-                        }
-                        h = (h + 1) & smask;
-                        sl = __ldg(T + h);
+    for (int r = 0; r < kPer; r++) {
+        if (c[r] == 0xFFFFFFFFu) break;
+        const unsigned long long *T = a.table + ((uint64_t)(c[r] >> 16) << a.log2S);
+        unsigned long long sl8 = slot[r];
+        uint32_t h = probe_hash(v[r], a.log2S);
+        while (sl8 != 0ull) {
+            if ((uint32_t)(sl8 >> 32) == v[r]) list_add(lists, a.R, ovf, c[r] & 0xFFFFu, (uint32_t)sl8 - 1u);
+            h = (h + 1) & smask;
+            sl8 = __ldg(T + h);
+        }
+    }
+    __syncwarp();
+}
+
+// append the positives of this lane's two masks (bit r = row r of slab j) to the
+// warp's queue: a warp prefix sum places every lane's entries, no atomics; the
+// fill level qn is warp-uniform (a register).  A tile with more positives than
+// the queue holds is verified through it in queue-sized rounds.
+__device__ __forceinline__ void join_push(const ProbeArgs &a, uint64_t s_lo, uint32_t cm0, uint32_t cm1, uint32_t sl,
+                                          uint32_t j, uint32_t *lists, uint32_t *ovf, uint32_t *queue,
+                                          uint32_t &qn) {
+    const uint32_t lane = threadIdx.x & 31u;
+    for (;;) {
+        const uint32_t c = __popc(cm0) + __popc(cm1);
+        uint32_t incl = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+            if (lane >= (uint32_t)d) incl += t;
+        }
+        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        if (tot == 0) return;
+        if (qn + tot > kJoinQCap && qn) {  // make room
+            join_flush(a, s_lo, lists, ovf, queue, qn);
+            qn = 0;
+        }
+        // this round: the entries whose warp-wide position fits in the queue
+        uint32_t pos = qn + incl - c;
+        const uint32_t base = j * 32u;
+        while (cm0 && pos < kJoinQCap) {
+            const uint32_t r = __ffs(cm0) - 1;
+            cm0 &= cm0 - 1;
+            queue[pos++] = sl | ((base + r) << 16);
+        }
+        while (cm1 && pos < kJoinQCap) {
+            const uint32_t r = __ffs(cm1) - 1;
+            cm1 &= cm1 - 1;
+            queue[pos++] = (sl + 1u) | ((base + r) << 16);
+        }
+        qn = min(qn + tot, kJoinQCap);
+        if (qn + 0u < kJoinQCap || !__any_sync(0xFFFFFFFFu, (cm0 | cm1) != 0u)) return;
+        join_flush(a, s_lo, lists, ovf, queue, qn);  // overfull tile: verify and continue
+        qn = 0;
+    }
+}
+
+// One CTA (16 warps, one per SM) owns R consecutive sets, warp w the w-th
+// sixteenth.  Per slab of 32 scanned bins the slab's filters (32 x 2^log2W
+// words, bin-major) sit in shared memory (double-buffered, filled by bulk
+// copies one slab ahead); a warp tile is 64 sets x 32 bins: lane = 2 adjacent
+// sets, one coalesced 8-B load per bin row, all 32 rows in flight at once.
+template <bool MW>
+__global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_constant__ ProbeArgs a) {
+    extern __shared__ __align__(128) unsigned char jsm[];
+    const uint32_t W = 1u << a.log2W, R = a.R;
+    const JoinLayout Ly = join_layout(W, R);
+    uint64_t *tfull = reinterpret_cast<uint64_t *>(jsm + Ly.bars);
+    uint32_t *tab = reinterpret_cast<uint32_t *>(jsm + Ly.tab);      // [2][32][W]
+    uint32_t *lists = reinterpret_cast<uint32_t *>(jsm + Ly.lists);  // [kJoinList][R]
+    uint32_t *ovf = reinterpret_cast<uint32_t *>(jsm + Ly.ovf);      // [R / 32]
+    uint32_t *queue = reinterpret_cast<uint32_t *>(jsm + Ly.queue);  // [kJoinWarps][kJoinQCap]
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint64_t s_lo = a.s_begin + (uint64_t)blockIdx.x * R;
+    const uint32_t nset = (uint32_t)(min(s_lo + R, a.s_end) - s_lo);
+    const uint32_t nslab = (a.nscan + 31u) / 32u;
+    const uint32_t slab_bytes = 32u * W * 4u;
+
+    for (uint32_t x = threadIdx.x; x < kJoinList * R; x += blockDim.x) lists[x] = 0u;
+    for (uint32_t x = threadIdx.x; x < R / 32; x += blockDim.x) ovf[x] = 0u;
+    if (threadIdx.x == 0) {
+        mbar_init(&tfull[0], 1);
+        mbar_init(&tfull[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (uint32_t j = 0; j < 2 && j < nslab; j++) {
+            mbar_expect_tx(&tfull[j], slab_bytes);
+            bulk_g2s(tab + (size_t)j * 32 * W, a.bloom + (size_t)j * 32 * W, slab_bytes, &tfull[j]);
+        }
+    }
+    __syncthreads();
+
+    uint32_t *myq = queue + warp * kJoinQCap;
+    uint32_t qn = 0;  // queued positives of this warp (warp-uniform)
+    const uint32_t shW = 32u - a.log2W;
+    const uint32_t per_warp = R / kJoinWarps;  // multiple of kJoinTile
+    const uint32_t w0 = warp * per_warp;
+    const uint32_t w1 = min(w0 + per_warp, nset);
+    for (uint32_t j = 0; j < nslab; j++) {
+        mbar_wait(&tfull[j & 1u], (j >> 1) & 1u);
+        const uint32_t *tabj = tab + (size_t)(j & 1u) * 32 * W;
+        const uint32_t rows = min(32u, a.nscan - 32u * j);
+        const uint32_t *Fj = a.F + (uint64_t)(32u * j) * a.ld;
+        for (uint32_t t0 = w0; t0 < w1; t0 += kJoinTile) {
+            const uint32_t sl = t0 + 2u * lane;  // this lane's first set (local index)
+            const bool ok0 = sl < w1, ok1 = sl + 1u < w1;
+            const uint64_t s = s_lo + sl;
+            uint32_t v0[32], v1[32];
+#pragma unroll
+            for (int r = 0; r < 32; r++) {
+                v0[r] = v1[r] = kEmpty;
+                if (ok0 && (uint32_t)r < rows) {
+                    const uint32_t *p = Fj + (uint64_t)r * a.ld + s;
+                    if (ok1) {  // s is even: 8-B aligned (ld % 4 == 0)
+                        const uint2 x = __ldg(reinterpret_cast<const uint2 *>(p));
+                        v0[r] = x.x;
+                        v1[r] = x.y;
+                    } else {
+                        v0[r] = __ldg(p);
                     }
                 }
             }
+            uint32_t cm0 = 0, cm1 = 0;
+#pragma unroll
+            for (int r = 0; r < 32; r++) {
+                const uint32_t *tb = tabj + r * W;
+                if (bloom_miss(v0[r], tb[(v0[r] * 0x9E3779B1u) >> shW]) == 0u) cm0 |= 1u << r;
+                if (bloom_miss(v1[r], tb[(v1[r] * 0x9E3779B1u) >> shW]) == 0u) cm1 |= 1u << r;
+            }
+            // rows past the scanned bins and sets past this warp's range: the verification
+            // re-reads the value from the collection, so they must not be queued
+            {
+                const uint32_t rm = rows >= 32u ? 0xFFFFFFFFu : ((1u << rows) - 1u);
+                cm0 = ok0 ? (cm0 & rm) : 0u;
+                cm1 = ok1 ? (cm1 & rm) : 0u;
+            }
+            // (an empty collection bin that passes the filter -- ~10 % of the positives --
+            // is rejected by the verification: no query inserts the value kEmpty)
+            join_push(a, s_lo, cm0, cm1, sl, j, lists, ovf, myq, qn);
         }
+        __syncthreads();  // every warp is done with filter buffer j & 1
+        if (threadIdx.x == 0 && j + 2 < nslab) {
+            mbar_expect_tx(&tfull[j & 1u], slab_bytes);
+            bulk_g2s(tab + (size_t)(j & 1u) * 32 * W, a.bloom + (size_t)(j + 2) * 32 * W, slab_bytes, &tfull[j & 1u]);
+        }
+    }
+    if (qn) join_flush(a, s_lo, lists, ovf, myq, qn);
+    __syncthreads();  // all counts are in
+
+    // ---------------- epilogue: decide every listed pair (one set per lane)
+    for (uint32_t base = warp * 32u; base < R; base += kJoinWarps * 32u) {
+        const uint32_t sl = base + lane;
+        const uint64_t s = s_lo + sl;
+        const bool act = sl < nset && !(MW && a.sflags[s]);
+        const bool of = act && ((ovf[sl >> 5] >> (sl & 31)) & 1u);
         {   // overflowing sets go to the BRUTE list scan
-            const unsigned long long idx = warp_append(act && ovf, a.ovf_count);
-            if (act && ovf) a.ovf_list[idx] = (uint32_t)s;
+            const unsigned long long idx = warp_append(of, a.ovf_count);
+            if (of) a.ovf_list[idx] = (uint32_t)s;
         }
-        const int ne = (act && !ovf) ? nl : 0;
-        for (int e = 0; e < kProbeList; e++) {
-            const bool has = e < ne;
+#pragma unroll 1
+        for (int e = 0; e < kJoinList; e++) {
+            const uint32_t x = (act && !of) ? lists[e * R + sl] : 0u;
+            const bool has = x != 0u;
             if (!__any_sync(0xFFFFFFFFu, has)) break;
             uint32_t q = 0, m = 0, ex = 0, flags = 0, verdict = 0;
             bool surv = false;
             float est = -1.0f;
             uint64_t st = 0;
             if (has) {
-                q = lq[e][tid];
-                m = lc[e][tid];
+                q = (x >> 16) - 1u;
+                m = x & 0xFFFFu;
                 const uint32_t qg = a.q_col0 + q;
                 if (a.final_) {
                     uint32_t den;
                     bool undef;
-                    if (mw) {
+                    if (MW) {
                         den = a.nbins_total;
                         undef = a.qflags[qg] != 0;
                     } else {
@@ -956,11 +1180,27 @@ cudaError_t launch_table(const TableArgs &a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_probe(const ProbeArgs &a, cudaStream_t st) {
-    if (a.s_end <= a.s_begin) return cudaSuccess;
+cudaError_t launch_probe(const ProbeArgs &a0, cudaStream_t st) {
+    if (a0.s_end <= a0.s_begin) return cudaSuccess;
+    ProbeArgs a = a0;
     const uint64_t n = a.s_end - a.s_begin;
-    const unsigned grid = (unsigned)std::min<uint64_t>((n + kProbeThreads - 1) / kProbeThreads, 148ull * 8);
-    probe_kernel<<<grid, kProbeThreads, 0, st>>>(a);
+    const uint32_t W = 1u << a.log2W;
+    constexpr uint32_t kSmemMax = 227 * 1024;
+    // one CTA per SM; sets per CTA: the fewest waves whose per-CTA lists fit next to
+    // the filter double buffer, split evenly (multiple of 32)
+    uint32_t Rmax = 32;
+    while (join_layout(W, Rmax + 32).total <= kSmemMax && Rmax + 32 <= 65504) Rmax += 32;
+    const uint64_t waves = (n + 148ull * Rmax - 1) / (148ull * Rmax);
+    const uint32_t R = (uint32_t)((((n + 148 * waves - 1) / (148 * waves)) + 31) / 32 * 32);
+    a.R = R;
+    a.nst = 0;
+    const size_t smem = join_layout(W, R).total;
+    if (smem > kSmemMax) return cudaErrorInvalidConfiguration;
+    auto kern = a.method == kMinwise ? join_kernel<true> : join_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const uint64_t grid = (n + R - 1) / R;
+    kern<<<(unsigned)grid, kJoinThreads, smem, st>>>(a);
     return cudaGetLastError();
 }
 
