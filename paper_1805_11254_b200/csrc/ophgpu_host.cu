@@ -326,12 +326,9 @@ uint32_t probe_log2S(uint64_t nq) {
     return l;
 }
 
-// Bloom words per bin for a pass of nq queries: >= 16 bits per query, >= 8 words
-uint32_t probe_log2W(uint64_t nq) {
-    uint32_t l = 3;
-    while ((1ull << l) * 32 < 16 * nq) l++;
-    return l;
-}
+// Bloom words per bin: fixed (the join kernel's filter rows are immediate offsets);
+// >= 16 bits per query for passes of <= kJoinMaxQ queries
+uint32_t probe_log2W(uint64_t) { return kJoinMaxLog2W; }
 
 uint64_t probe_pass(uint64_t ldq) { return std::min<uint64_t>(ldq, kJoinMaxQ); }
 

@@ -636,21 +636,20 @@ __device__ __forceinline__ uint32_t probe_hash(uint32_t v, uint32_t log2S) {
     return (v * 0x9E3779B1u) >> (32 - log2S);  // Fibonacci hashing
 }
 
-// Bloom filter of one bin: 2^log2W words; value v sets two bits of word
-// (v * golden) >> (32 - log2W).  The bit positions come from the high halves
-// of two more products (they depend on every bit of v, and IMAD.HI issues on
-// the FMA pipe, not the ALU pipe the probe loop is bound by).
-__device__ __forceinline__ uint32_t bloom_bits(uint32_t v) {
-    return __funnelshift_l(0u, 1u, __umulhi(v, 0x85EBCA6Bu)) | __funnelshift_l(0u, 1u, __umulhi(v, 0xC2B2AE35u));
+// Bloom filter of one bin: 2^log2W words; value v, h = v * golden, sets two
+// bits of word h >> (32 - log2W): bit umulhi(v, C) mod 32 (the high half of a
+// second product depends on every bit of v; IMAD.HI issues on the FMA pipe)
+// and bit h mod 32 (a bijection of v mod 32).
+__device__ __forceinline__ uint32_t bloom_bits(uint32_t v, uint32_t h) {
+    return __funnelshift_l(0u, 1u, __umulhi(v, 0x85EBCA6Bu)) | __funnelshift_l(0u, 1u, h);
 }
 
 // (b1 | b2) & ~word in one LOP3: zero iff both filter bits of v are set in word
-__device__ __forceinline__ uint32_t bloom_miss(uint32_t v, uint32_t word) {
+__device__ __forceinline__ uint32_t bloom_miss(uint32_t v, uint32_t h, uint32_t word) {
     uint32_t z;
     asm("lop3.b32 %0, %1, %2, %3, 0x54;"
         : "=r"(z)
-        : "r"(__funnelshift_l(0u, 1u, __umulhi(v, 0x85EBCA6Bu))), "r"(__funnelshift_l(0u, 1u, __umulhi(v, 0xC2B2AE35u))),
-          "r"(word));
+        : "r"(__funnelshift_l(0u, 1u, __umulhi(v, 0x85EBCA6Bu))), "r"(__funnelshift_l(0u, 1u, h)), "r"(word));
     return z;
 }
 
@@ -668,7 +667,8 @@ __global__ void table_kernel(const __grid_constant__ TableArgs a) {
         unsigned long long *T = a.table + (uint64_t)b * S;
         uint32_t h = probe_hash(v, a.log2S);
         while (atomicCAS(&T[h], 0ull, entry) != 0ull) h = (h + 1) & (uint32_t)(S - 1);
-        atomicOr(a.bloom + ((uint64_t)b << a.log2W) + ((v * 0x9E3779B1u) >> (32 - a.log2W)), bloom_bits(v));
+        const uint32_t hv = v * 0x9E3779B1u;
+        atomicOr(a.bloom + ((uint64_t)b << a.log2W) + (hv >> (32 - a.log2W)), bloom_bits(v, hv));
     }
 }
 
@@ -706,10 +706,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  : "memory");
 }
 
-constexpr int kJoinWarps = 16;
+constexpr int kJoinWarps = 24;
 constexpr int kJoinThreads = 32 * kJoinWarps;
 constexpr uint32_t kJoinQCap = 256;  // candidate queue per warp (4-B entries)
-constexpr uint32_t kJoinTile = 64;  // sets per warp tile (2 per lane, one 8-B load per bin row)
+constexpr uint32_t kJoinTile = 32;  // sets per warp tile (one per lane, one coalesced 4-B load per bin row)
+constexpr uint32_t kJoinW = 1u << kJoinMaxLog2W;  // filter words per bin (fixed: row offsets are immediates)
+constexpr uint32_t kJoinMaxSlabs = 512;  // nscan <= 16384
 
 // shared-memory carve-up of the join kernel (bytes, 128-B aligned regions)
 struct JoinLayout {
@@ -723,8 +725,8 @@ __host__ __device__ inline JoinLayout join_layout(uint32_t W, uint32_t R) {
     L.lists = L.tab + 2 * 32 * W * 4;
     L.ovf = join_align(L.lists + kJoinList * R * 4);
     L.queue = join_align(L.ovf + R / 8);
-    L.qcount = L.queue + kJoinWarps * kJoinQCap * 4;
-    L.total = join_align(L.qcount + kJoinWarps * 4);
+    L.qcount = L.queue + kJoinWarps * kJoinQCap * 4;  // per slab: tile counter, done counter
+    L.total = join_align(L.qcount + 2 * kJoinMaxSlabs * 4);
     return L;
 }
 
@@ -832,21 +834,24 @@ __device__ __forceinline__ void join_push(const ProbeArgs &a, uint64_t s_lo, uin
     }
 }
 
-// One CTA (16 warps, one per SM) owns R consecutive sets, warp w the w-th
-// sixteenth.  Per slab of 32 scanned bins the slab's filters (32 x 2^log2W
-// words, bin-major) sit in shared memory (double-buffered, filled by bulk
-// copies one slab ahead); a warp tile is 64 sets x 32 bins: lane = 2 adjacent
-// sets, one coalesced 8-B load per bin row, all 32 rows in flight at once.
+// One CTA (24 warps, one per SM) owns R consecutive sets.  Per slab of 32
+// scanned bins the slab's filters (32 x kJoinW words, bin-major) sit in
+// shared memory (double-buffered: the last warp to finish slab j bulk-copies
+// slab j + 2, so no CTA-wide barrier between slabs); warps take 32-set tiles
+// from a shared counter: lane = one set, one coalesced 4-B load per bin row,
+// all 32 rows in flight at once.
 template <bool MW>
 __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_constant__ ProbeArgs a) {
     extern __shared__ __align__(128) unsigned char jsm[];
-    const uint32_t W = 1u << a.log2W, R = a.R;
+    constexpr uint32_t W = kJoinW;
+    const uint32_t R = a.R;
     const JoinLayout Ly = join_layout(W, R);
     uint64_t *tfull = reinterpret_cast<uint64_t *>(jsm + Ly.bars);
     uint32_t *tab = reinterpret_cast<uint32_t *>(jsm + Ly.tab);      // [2][32][W]
     uint32_t *lists = reinterpret_cast<uint32_t *>(jsm + Ly.lists);  // [kJoinList][R]
     uint32_t *ovf = reinterpret_cast<uint32_t *>(jsm + Ly.ovf);      // [R / 32]
     uint32_t *queue = reinterpret_cast<uint32_t *>(jsm + Ly.queue);  // [kJoinWarps][kJoinQCap]
+    uint32_t *tctl = reinterpret_cast<uint32_t *>(jsm + Ly.qcount);  // per slab: next tile, warps done
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint64_t s_lo = a.s_begin + (uint64_t)blockIdx.x * R;
@@ -856,6 +861,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
 
     for (uint32_t x = threadIdx.x; x < kJoinList * R; x += blockDim.x) lists[x] = 0u;
     for (uint32_t x = threadIdx.x; x < R / 32; x += blockDim.x) ovf[x] = 0u;
+    for (uint32_t x = threadIdx.x; x < 2 * nslab; x += blockDim.x) tctl[x] = 0u;
     if (threadIdx.x == 0) {
         mbar_init(&tfull[0], 1);
         mbar_init(&tfull[1], 1);
@@ -869,57 +875,60 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
 
     uint32_t *myq = queue + warp * kJoinQCap;
     uint32_t qn = 0;  // queued positives of this warp (warp-uniform)
-    const uint32_t shW = 32u - a.log2W;
-    const uint32_t per_warp = R / kJoinWarps;  // multiple of kJoinTile
-    const uint32_t w0 = warp * per_warp;
-    const uint32_t w1 = min(w0 + per_warp, nset);
+    const uint32_t ntile = (nset + kJoinTile - 1) / kJoinTile;
     for (uint32_t j = 0; j < nslab; j++) {
-        mbar_wait(&tfull[j & 1u], (j >> 1) & 1u);
-        const uint32_t *tabj = tab + (size_t)(j & 1u) * 32 * W;
+        const uint32_t tb = j & 1u;
+        const uint32_t *tabj = tab + (size_t)tb * 32 * W;
         const uint32_t rows = min(32u, a.nscan - 32u * j);
         const uint32_t *Fj = a.F + (uint64_t)(32u * j) * a.ld;
-        for (uint32_t t0 = w0; t0 < w1; t0 += kJoinTile) {
-            const uint32_t sl = t0 + 2u * lane;  // this lane's first set (local index)
-            const bool ok0 = sl < w1, ok1 = sl + 1u < w1;
-            const uint64_t s = s_lo + sl;
-            uint32_t v0[32], v1[32];
+        mbar_wait(&tfull[tb], (j >> 1) & 1u);  // the slab's filters
+        for (;;) {  // tiles of this slab, handed out dynamically
+            uint32_t t = 0;
+            if (lane == 0) t = atomicAdd(&tctl[2 * j], 1u);
+            t = __shfl_sync(0xFFFFFFFFu, t, 0);
+            if (t >= ntile) break;
+            const uint32_t sl = t * kJoinTile + lane;  // this lane's set (local index)
+            const bool ok = sl < nset;
+            const uint32_t *Fs = Fj + s_lo + sl;
+            uint32_t v[32];
+            if ((t + 1) * kJoinTile <= nset && rows == 32u) {  // full tile (warp-uniform): no checks
+#pragma unroll
+                for (int r = 0; r < 32; r++) v[r] = __ldg(Fs + (uint64_t)r * a.ld);
+            } else {
+#pragma unroll
+                for (int r = 0; r < 32; r++) v[r] = (ok && (uint32_t)r < rows) ? __ldg(Fs + (uint64_t)r * a.ld) : kEmpty;
+            }
+            // filter test per row: h = v * golden; word (h >> 23) of row r; both bits set -> bit r of cm
+            uint32_t cm = 0;
 #pragma unroll
             for (int r = 0; r < 32; r++) {
-                v0[r] = v1[r] = kEmpty;
-                if (ok0 && (uint32_t)r < rows) {
-                    const uint32_t *p = Fj + (uint64_t)r * a.ld + s;
-                    if (ok1) {  // s is even: 8-B aligned (ld % 4 == 0)
-                        const uint2 x = __ldg(reinterpret_cast<const uint2 *>(p));
-                        v0[r] = x.x;
-                        v1[r] = x.y;
-                    } else {
-                        v0[r] = __ldg(p);
-                    }
+                const uint32_t h = v[r] * 0x9E3779B1u;
+                const uint32_t word = tabj[r * kJoinW + (h >> (32 - kJoinMaxLog2W))];
+                const uint32_t z = bloom_miss(v[r], h, word);
+                asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, 0;\n\t@p or.b32 %0, %0, %2;\n}"
+                    : "+r"(cm)
+                    : "r"(z), "r"(1u << r));
+            }
+            // rows past the scanned bins and sets past the end: the verification
+            // re-reads the value from the collection, so they must not be queued
+            // (an empty collection bin that passes the filter -- ~10 % of the
+            // positives -- is rejected there: no query inserts the value kEmpty)
+            cm = ok ? (cm & (rows >= 32u ? 0xFFFFFFFFu : ((1u << rows) - 1u))) : 0u;
+            join_push(a, s_lo, cm, 0u, sl, j, lists, ovf, myq, qn);
+        }
+        // the last warp done with slab j recycles its filter buffer for slab j + 2
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(&tctl[2 * j + 1], 1u) == kJoinWarps - 1) {
+                if (j + 2 < nslab) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(&tfull[tb], slab_bytes);
+                    bulk_g2s(tab + (size_t)tb * 32 * W, a.bloom + (size_t)(j + 2) * 32 * W, slab_bytes, &tfull[tb]);
                 }
             }
-            uint32_t cm0 = 0, cm1 = 0;
-#pragma unroll
-            for (int r = 0; r < 32; r++) {
-                const uint32_t *tb = tabj + r * W;
-                if (bloom_miss(v0[r], tb[(v0[r] * 0x9E3779B1u) >> shW]) == 0u) cm0 |= 1u << r;
-                if (bloom_miss(v1[r], tb[(v1[r] * 0x9E3779B1u) >> shW]) == 0u) cm1 |= 1u << r;
-            }
-            // rows past the scanned bins and sets past this warp's range: the verification
-            // re-reads the value from the collection, so they must not be queued
-            {
-                const uint32_t rm = rows >= 32u ? 0xFFFFFFFFu : ((1u << rows) - 1u);
-                cm0 = ok0 ? (cm0 & rm) : 0u;
-                cm1 = ok1 ? (cm1 & rm) : 0u;
-            }
-            // (an empty collection bin that passes the filter -- ~10 % of the positives --
-            // is rejected by the verification: no query inserts the value kEmpty)
-            join_push(a, s_lo, cm0, cm1, sl, j, lists, ovf, myq, qn);
         }
-        __syncthreads();  // every warp is done with filter buffer j & 1
-        if (threadIdx.x == 0 && j + 2 < nslab) {
-            mbar_expect_tx(&tfull[j & 1u], slab_bytes);
-            bulk_g2s(tab + (size_t)(j & 1u) * 32 * W, a.bloom + (size_t)(j + 2) * 32 * W, slab_bytes, &tfull[j & 1u]);
-        }
+        __syncwarp();
     }
     if (qn) join_flush(a, s_lo, lists, ovf, myq, qn);
     __syncthreads();  // all counts are in
@@ -1184,7 +1193,8 @@ cudaError_t launch_probe(const ProbeArgs &a0, cudaStream_t st) {
     if (a0.s_end <= a0.s_begin) return cudaSuccess;
     ProbeArgs a = a0;
     const uint64_t n = a.s_end - a.s_begin;
-    const uint32_t W = 1u << a.log2W;
+    const uint32_t W = kJoinW;
+    if (a.log2W != kJoinMaxLog2W) return cudaErrorInvalidValue;
     constexpr uint32_t kSmemMax = 227 * 1024;
     // one CTA per SM; sets per CTA: the fewest waves whose per-CTA lists fit next to
     // the filter double buffer, split evenly (multiple of 32)
