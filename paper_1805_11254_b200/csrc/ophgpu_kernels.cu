@@ -709,7 +709,9 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 constexpr int kJoinWarps = 24;
 constexpr int kJoinThreads = 32 * kJoinWarps;
 constexpr uint32_t kJoinQCap = 256;  // candidate queue per warp (4-B entries)
-constexpr uint32_t kJoinTile = 32;  // sets per warp tile (one per lane, one coalesced 4-B load per bin row)
+constexpr uint32_t kJoinSPL = 4;                  // sets per lane (one 16-B load per bin row)
+constexpr uint32_t kJoinRPT = 32 / kJoinSPL;      // bin rows per tile
+constexpr uint32_t kJoinTile = 32 * kJoinSPL;     // sets per tile
 constexpr uint32_t kJoinW = 1u << kJoinMaxLog2W;  // filter words per bin (fixed: row offsets are immediates)
 constexpr uint32_t kJoinMaxSlabs = 512;  // nscan <= 16384
 
@@ -792,16 +794,23 @@ __device__ __noinline__ void join_flush(const ProbeArgs &a, uint64_t s_lo, uint3
     __syncwarp();
 }
 
-// append the positives of this lane's two masks (bit r = row r of slab j) to the
-// warp's queue: a warp prefix sum places every lane's entries, no atomics; the
-// fill level qn is warp-uniform (a register).  A tile with more positives than
-// the queue holds is verified through it in queue-sized rounds.
-__device__ __forceinline__ void join_push(const ProbeArgs &a, uint64_t s_lo, uint32_t cm0, uint32_t cm1, uint32_t sl,
-                                          uint32_t j, uint32_t *lists, uint32_t *ovf, uint32_t *queue,
-                                          uint32_t &qn) {
+// append the positives of this lane's mask (bit i = set i / RPT, row i % RPT) to the
+// warp's queue: a warp prefix sum places every lane's entries (no atomics; the
+// fill level qn is warp-uniform, a register).  Lanes with <= 2 positives write
+// their own; the rare lane with more (a near-duplicate set: ~25 matched rows)
+// is expanded by the whole warp, one bit per lane.  A tile with more positives
+// than the queue holds is verified through it in queue-sized rounds.
+// queue entry of mask bit i: set sl + i / RPT, bin bin0 + i % RPT
+__device__ __forceinline__ uint32_t join_entry(uint32_t sl, uint32_t bin0, uint32_t i) {
+    return (sl + i / kJoinRPT) | ((bin0 + i % kJoinRPT) << 16);
+}
+
+__device__ __forceinline__ void join_push(const ProbeArgs &a, uint64_t s_lo, uint32_t cm, uint32_t sl, uint32_t bin0,
+                                          uint32_t *lists, uint32_t *ovf, uint32_t *queue, uint32_t &qn) {
     const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t lt = (1u << lane) - 1u;
     for (;;) {
-        const uint32_t c = __popc(cm0) + __popc(cm1);
+        const uint32_t c = __popc(cm);
         uint32_t incl = c;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -814,22 +823,34 @@ __device__ __forceinline__ void join_push(const ProbeArgs &a, uint64_t s_lo, uin
             join_flush(a, s_lo, lists, ovf, queue, qn);
             qn = 0;
         }
-        // this round: the entries whose warp-wide position fits in the queue
-        uint32_t pos = qn + incl - c;
-        const uint32_t base = j * 32u;
-        while (cm0 && pos < kJoinQCap) {
-            const uint32_t r = __ffs(cm0) - 1;
-            cm0 &= cm0 - 1;
-            queue[pos++] = sl | ((base + r) << 16);
+        if (qn + tot <= kJoinQCap) {  // the common case: everything fits
+            const uint32_t pos = qn + incl - c;
+            if (c <= 2u) {
+                uint32_t m = cm, p = pos;
+                while (m) {
+                    queue[p++] = join_entry(sl, bin0, __ffs(m) - 1);
+                    m &= m - 1;
+                }
+            }
+            uint32_t heavy = __ballot_sync(0xFFFFFFFFu, c > 2u);
+            while (heavy) {
+                const uint32_t L = __ffs(heavy) - 1;
+                heavy &= heavy - 1;
+                const uint32_t m = __shfl_sync(0xFFFFFFFFu, cm, L);
+                const uint32_t p = __shfl_sync(0xFFFFFFFFu, pos, L);
+                const uint32_t sL = __shfl_sync(0xFFFFFFFFu, sl, L);
+                if ((m >> lane) & 1u) queue[p + __popc(m & lt)] = join_entry(sL, bin0, lane);
+            }
+            qn += tot;
+            return;
         }
-        while (cm1 && pos < kJoinQCap) {
-            const uint32_t r = __ffs(cm1) - 1;
-            cm1 &= cm1 - 1;
-            queue[pos++] = (sl + 1u) | ((base + r) << 16);
+        // overfull tile (qn == 0, tot > capacity): queue what fits, verify, repeat
+        uint32_t pos = incl - c;
+        while (cm && pos < kJoinQCap) {
+            queue[pos++] = join_entry(sl, bin0, __ffs(cm) - 1);
+            cm &= cm - 1;
         }
-        qn = min(qn + tot, kJoinQCap);
-        if (qn + 0u < kJoinQCap || !__any_sync(0xFFFFFFFFu, (cm0 | cm1) != 0u)) return;
-        join_flush(a, s_lo, lists, ovf, queue, qn);  // overfull tile: verify and continue
+        join_flush(a, s_lo, lists, ovf, queue, kJoinQCap);
         qn = 0;
     }
 }
@@ -875,46 +896,81 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
 
     uint32_t *myq = queue + warp * kJoinQCap;
     uint32_t qn = 0;  // queued positives of this warp (warp-uniform)
-    const uint32_t ntile = (nset + kJoinTile - 1) / kJoinTile;
+    const uint32_t ntile = (nset + kJoinTile - 1) / kJoinTile * kJoinSPL;
+    const uint32_t ldb = (uint32_t)(a.ld * 4u);  // row stride in bytes
     for (uint32_t j = 0; j < nslab; j++) {
         const uint32_t tb = j & 1u;
         const uint32_t *tabj = tab + (size_t)tb * 32 * W;
         const uint32_t rows = min(32u, a.nscan - 32u * j);
         const uint32_t *Fj = a.F + (uint64_t)(32u * j) * a.ld;
-        mbar_wait(&tfull[tb], (j >> 1) & 1u);  // the slab's filters
-        for (;;) {  // tiles of this slab, handed out dynamically
+        // tiles are handed out dynamically (a 24-warp SM hides the row-load latency of one
+        // warp behind the others' probing; a per-warp double buffer measured slower)
+        auto next_tile = [&]() {
             uint32_t t = 0;
             if (lane == 0) t = atomicAdd(&tctl[2 * j], 1u);
-            t = __shfl_sync(0xFFFFFFFFu, t, 0);
-            if (t >= ntile) break;
-            const uint32_t sl = t * kJoinTile + lane;  // this lane's set (local index)
-            const bool ok = sl < nset;
-            const uint32_t *Fs = Fj + s_lo + sl;
-            uint32_t v[32];
-            if ((t + 1) * kJoinTile <= nset && rows == 32u) {  // full tile (warp-uniform): no checks
+            return __shfl_sync(0xFFFFFFFFu, t, 0);
+        };
+        // tile t: sets [sb * 32 * SPL, +32 * SPL) x rows [rb * RPT, +RPT) of the slab,
+        // sb = t / SPL, rb = t % SPL; lane = SPL adjacent sets (one vector load per row),
+        // v[k * RPT + r] = set k, row r
+        auto load_tile = [&](uint32_t t, uint32_t (&v)[32]) {
+            const uint32_t sb = t / kJoinSPL, rb = t % kJoinSPL;
+            const uint32_t sl = sb * kJoinTile + lane * kJoinSPL;
+            const char *Fs = reinterpret_cast<const char *>(Fj + (uint64_t)(rb * kJoinRPT) * a.ld + s_lo + sl);
+            // row r at Fs + r * ldb: one IMAD.WIDE.U32 per row (ldb < 2^32, checked by the launcher)
+            if ((sb + 1) * kJoinTile <= nset && rows == 32u) {  // full tile (warp-uniform): no checks
 #pragma unroll
-                for (int r = 0; r < 32; r++) v[r] = __ldg(Fs + (uint64_t)r * a.ld);
+                for (int r = 0; r < (int)kJoinRPT; r++) {
+                    const uint4 x = __ldg(reinterpret_cast<const uint4 *>(Fs + (uint64_t)((uint32_t)r) * ldb));
+                    v[0 * kJoinRPT + r] = x.x;
+                    v[1 * kJoinRPT + r] = x.y;
+                    v[2 * kJoinRPT + r] = x.z;
+                    v[3 * kJoinRPT + r] = x.w;
+                }
             } else {
 #pragma unroll
-                for (int r = 0; r < 32; r++) v[r] = (ok && (uint32_t)r < rows) ? __ldg(Fs + (uint64_t)r * a.ld) : kEmpty;
-            }
-            // filter test per row: h = v * golden; word (h >> 23) of row r; both bits set -> bit r of cm
-            uint32_t cm = 0;
+                for (int r = 0; r < (int)kJoinRPT; r++)
 #pragma unroll
-            for (int r = 0; r < 32; r++) {
-                const uint32_t h = v[r] * 0x9E3779B1u;
-                const uint32_t word = tabj[r * kJoinW + (h >> (32 - kJoinMaxLog2W))];
-                const uint32_t z = bloom_miss(v[r], h, word);
+                    for (int k = 0; k < (int)kJoinSPL; k++)
+                        v[k * kJoinRPT + r] =
+                            (sl + k < nset && rb * kJoinRPT + r < rows)
+                                ? __ldg(reinterpret_cast<const uint32_t *>(Fs + (uint64_t)((uint32_t)r) * ldb) + k)
+                                : kEmpty;
+            }
+        };
+        auto probe_tile = [&](uint32_t t, const uint32_t (&v)[32]) {
+            const uint32_t sb = t / kJoinSPL, rb = t % kJoinSPL;
+            // filter test: h = v * golden; word (h >> 23) of the row's filter; both bits set -> bit of cm
+            uint32_t cm = 0;
+            const uint32_t *tabr = tabj + rb * kJoinRPT * kJoinW;
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+                const uint32_t r = (uint32_t)i % kJoinRPT;
+                const uint32_t h = v[i] * 0x9E3779B1u;
+                const uint32_t word = tabr[r * kJoinW + (h >> (32 - kJoinMaxLog2W))];
+                const uint32_t z = bloom_miss(v[i], h, word);
                 asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, 0;\n\t@p or.b32 %0, %0, %2;\n}"
                     : "+r"(cm)
-                    : "r"(z), "r"(1u << r));
+                    : "r"(z), "r"(1u << i));
             }
             // rows past the scanned bins and sets past the end: the verification
             // re-reads the value from the collection, so they must not be queued
             // (an empty collection bin that passes the filter -- ~10 % of the
             // positives -- is rejected there: no query inserts the value kEmpty)
-            cm = ok ? (cm & (rows >= 32u ? 0xFFFFFFFFu : ((1u << rows) - 1u))) : 0u;
-            join_push(a, s_lo, cm, 0u, sl, j, lists, ovf, myq, qn);
+            const uint32_t sl = sb * kJoinTile + lane * kJoinSPL;
+            if (!((sb + 1) * kJoinTile <= nset && rows == 32u)) {
+#pragma unroll
+                for (int i = 0; i < 32; i++)
+                    if (sl + (uint32_t)i / kJoinRPT >= nset || rb * kJoinRPT + (uint32_t)i % kJoinRPT >= rows)
+                        cm &= ~(1u << i);
+            }
+            join_push(a, s_lo, cm, sl, j * 32u + rb * kJoinRPT, lists, ovf, myq, qn);
+        };
+        mbar_wait(&tfull[tb], (j >> 1) & 1u);  // the slab's filters
+        for (uint32_t t = next_tile(); t < ntile; t = next_tile()) {
+            uint32_t v[32];
+            load_tile(t, v);
+            probe_tile(t, v);
         }
         // the last warp done with slab j recycles its filter buffer for slab j + 2
         __syncwarp();
@@ -1194,14 +1250,15 @@ cudaError_t launch_probe(const ProbeArgs &a0, cudaStream_t st) {
     ProbeArgs a = a0;
     const uint64_t n = a.s_end - a.s_begin;
     const uint32_t W = kJoinW;
-    if (a.log2W != kJoinMaxLog2W) return cudaErrorInvalidValue;
+    if (a.log2W != kJoinMaxLog2W || a.ld * 4 >= (1ull << 32)) return cudaErrorInvalidValue;
     constexpr uint32_t kSmemMax = 227 * 1024;
     // one CTA per SM; sets per CTA: the fewest waves whose per-CTA lists fit next to
     // the filter double buffer, split evenly (multiple of 32)
-    uint32_t Rmax = 32;
-    while (join_layout(W, Rmax + 32).total <= kSmemMax && Rmax + 32 <= 65504) Rmax += 32;
+    // (multiple of the tile's kJoinTile sets)
+    uint32_t Rmax = kJoinTile;
+    while (join_layout(W, Rmax + kJoinTile).total <= kSmemMax && Rmax + kJoinTile <= 65504) Rmax += kJoinTile;
     const uint64_t waves = (n + 148ull * Rmax - 1) / (148ull * Rmax);
-    const uint32_t R = (uint32_t)((((n + 148 * waves - 1) / (148 * waves)) + 31) / 32 * 32);
+    const uint32_t R = (uint32_t)((((n + 148 * waves - 1) / (148 * waves)) + kJoinTile - 1) / kJoinTile * kJoinTile);
     a.R = R;
     a.nst = 0;
     const size_t smem = join_layout(W, R).total;
