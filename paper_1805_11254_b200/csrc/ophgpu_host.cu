@@ -753,7 +753,7 @@ oph_status oph_build_sketches(const oph_sets *sets, const oph_perm *perm, const 
         a.flat = make_range(0, V, flat->k);
         a.oph = d_oph;
         a.oph_empty = d_oph_empty;
-        per_set += flat->k + 1;
+        per_set += (flat->k + 31) / 32 * 32 + 1;  // row stride of the build kernel's smem tile
     }
     if (hier) {
         if (hier->vocab_size != V || hier->L == 0 || hier->L > OPH_MAX_GROUPS || hier->kprime == 0 || !d_hoph ||
@@ -783,7 +783,7 @@ oph_status oph_build_sketches(const oph_sets *sets, const oph_perm *perm, const 
         a.log2kp = lk;
         a.hoph = d_hoph;
         a.hoph_empty = d_hoph_empty;
-        per_set += (uint64_t)hier->L * hier->kprime + 1;
+        per_set += ((uint64_t)hier->L * hier->kprime + 31) / 32 * 32 + 1;
     }
     if (per_set * 4 + 16 > 200 * 1024) return OPH_EINVAL;
     return cuda_status(launch_build(a, (cudaStream_t)stream));

@@ -114,51 +114,55 @@ __device__ __forceinline__ void build_one(const BuildArgs &a, const RangeBins *g
     }
 }
 
-__device__ __forceinline__ void write_tile(const uint32_t *src, uint32_t stride, uint32_t nbins, uint32_t SB,
-                                           uint32_t nloc, uint32_t *dst, uint64_t ld, uint64_t s0) {
-    // values: bin-major rows of SB sets; thread = (bin, quad of 4 sets) -> one 16-B store
-    const uint32_t quads = SB / 4;
-    if (SB % 4 == 0 && nloc == SB) {
-        for (uint32_t i = threadIdx.x; i < nbins * quads; i += blockDim.x) {
-            const uint32_t b = i / quads, j = 4 * (i % quads);
-            uint4 v;
-            v.x = src[(j + 0) * stride + b];
-            v.y = src[(j + 1) * stride + b];
-            v.z = src[(j + 2) * stride + b];
-            v.w = src[(j + 3) * stride + b];
-            *reinterpret_cast<uint4 *>(dst + (uint64_t)b * ld + s0 + j) = v;
+// write-out of SB sets' sketches (smem rows of `stride` words, stride = 1 mod 32
+// so that a lane per bin reads the SB sets conflict-free): a warp takes 32
+// consecutive bins; each lane stores its bin's SB values as 128-bit stores of 4
+// consecutive sets, and SB ballots give the SB sets' empty-mask words of these
+// 32 bins (bit t of word w <=> bin 32 w + t empty), stored by lanes 0..SB-1.
+template <int SB>
+__device__ __forceinline__ void write_sketch(const uint32_t *src, uint32_t stride, uint32_t nbins, uint32_t nloc,
+                                             uint32_t *dst, uint32_t *dst_mask, uint64_t ld, uint64_t s0) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const bool full = nloc == SB && SB % 4 == 0;
+    for (uint32_t b0 = warp * 32u; b0 < nbins; b0 += nwarps * 32u) {  // warp-uniform
+        const uint32_t b = b0 + lane;
+        const bool in = b < nbins;
+        uint32_t v[SB];
+#pragma unroll
+        for (int j = 0; j < SB; j++) v[j] = in ? src[j * stride + b] : 0u;
+        if (in) {
+            uint32_t *d = dst + (uint64_t)b * ld + s0;
+            if (full) {
+#pragma unroll
+                for (int q = 0; q < SB / 4; q++)
+                    *reinterpret_cast<uint4 *>(d + 4 * q) = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < SB; j++)
+                    if ((uint32_t)j < nloc) d[j] = v[j];
+            }
         }
-    } else {
-        for (uint32_t i = threadIdx.x; i < nbins * SB; i += blockDim.x) {
-            const uint32_t b = i / SB, j = i % SB;
-            if (j < nloc) dst[(uint64_t)b * ld + s0 + j] = src[j * stride + b];
+        uint32_t mine = 0;
+#pragma unroll
+        for (int j = 0; j < SB; j++) {
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, v[j] == kEmpty);
+            if (lane == (uint32_t)j) mine = m;
         }
+        if (lane < nloc) dst_mask[(uint64_t)(b0 >> 5) * ld + s0 + lane] = mine;
     }
 }
 
-__device__ __forceinline__ void write_masks(const uint32_t *src, uint32_t stride, uint32_t nbins, uint32_t nloc,
-                                            uint32_t *dst, uint64_t ld, uint64_t s0) {
-    // warp per (set, word): bit t of word w <=> bin 32w + t empty
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const uint32_t nw = (nbins + 31) / 32;
-    for (uint32_t i = warp; i < nw * nloc; i += nwarps) {
-        const uint32_t j = i / nw, w = i % nw;
-        const uint32_t b = 32 * w + lane;
-        const uint32_t m = __ballot_sync(0xFFFFFFFFu, b < nbins && src[j * stride + b] == kEmpty);
-        if (lane == 0) dst[(uint64_t)w * ld + s0 + j] = m;
-    }
-}
-
-template <bool W32>
-__global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ BuildArgs a, uint32_t SB) {
+template <bool W32, int SB>
+__global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ BuildArgs a) {
     extern __shared__ __align__(16) uint32_t smem_u32[];
     // group table in shared memory: lanes index it divergently, which would
     // serialise on the constant cache if read from the kernel parameters
     __shared__ RangeBins grp[kMaxGroups];
     __shared__ uint64_t offs[33];
-    const uint32_t kst = a.k + 1;
+    // row strides = 1 mod 32: the write-out reads the SB sets of one bin conflict-free
+    const uint32_t kst = (a.k + 31u) / 32u * 32u + 1u;
     const uint32_t nbh = a.L * a.kp;
-    const uint32_t hst = nbh + 1;
+    const uint32_t hst = (nbh + 31u) / 32u * 32u + 1u;
     uint32_t *so = smem_u32;                                               // [SB][k+1]
     uint32_t *sh = so + (a.do_flat ? (size_t)SB * kst : 0);               // [SB][L*kp+1]
     const uint32_t words = (a.do_flat ? SB * kst : 0) + (a.do_hier ? SB * hst : 0);
@@ -195,14 +199,8 @@ __global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ Buil
     }
     __syncthreads();
 
-    if (a.do_flat) {
-        write_tile(so, kst, a.k, SB, nloc, a.oph, a.ld, s0);
-        write_masks(so, kst, a.k, nloc, a.oph_empty, a.ld, s0);
-    }
-    if (a.do_hier) {
-        write_tile(sh, hst, nbh, SB, nloc, a.hoph, a.ld, s0);
-        write_masks(sh, hst, nbh, nloc, a.hoph_empty, a.ld, s0);
-    }
+    if (a.do_flat) write_sketch<SB>(so, kst, a.k, nloc, a.oph, a.oph_empty, a.ld, s0);
+    if (a.do_hier) write_sketch<SB>(sh, hst, nbh, nloc, a.hoph, a.hoph_empty, a.ld, s0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1170,21 +1168,31 @@ __global__ void __launch_bounds__(256) level_kernel(const __grid_constant__ Leve
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+template <int SB>
+static cudaError_t launch_build_sb(const BuildArgs &a, size_t smem, cudaStream_t st) {
+    const uint64_t grid = (a.n_sets + SB - 1) / SB;
+    auto kern = a.psi.mask == 0xFFFFFFFFu ? build_kernel<true, SB> : build_kernel<false, SB>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)grid, 256, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_build(const BuildArgs &a, cudaStream_t st) {
     if (a.n_sets == 0) return cudaSuccess;
-    const uint32_t per_set = (a.do_flat ? a.k + 1 : 0) + (a.do_hier ? a.L * a.kp + 1 : 0);
+    const uint32_t per_set = (a.do_flat ? (a.k + 31) / 32 * 32 + 1 : 0) +
+                             (a.do_hier ? (a.L * a.kp + 31) / 32 * 32 + 1 : 0);
     // 8 sets per CTA: 36 KB of shared memory at text-like sizes -> 6 CTAs (48 warps) per SM,
-    // and a bin row of the tile is one full 32-B sector
+    // and a bin row of the tile is one full 32-B sector; fewer for very large sketches
     uint32_t SB = 8;
     while (SB > 1 && (size_t)SB * per_set * 4 + 16 > 200 * 1024) SB >>= 1;
     const size_t smem = ((size_t)SB * per_set * 4 + 15) / 16 * 16;
-    const uint64_t grid = (a.n_sets + SB - 1) / SB;
-    const bool w32 = a.psi.mask == 0xFFFFFFFFu;
-    auto kern = w32 ? build_kernel<true> : build_kernel<false>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kern<<<(unsigned)grid, 256, smem, st>>>(a, SB);
-    return cudaGetLastError();
+    switch (SB) {
+        case 8: return launch_build_sb<8>(a, smem, st);
+        case 4: return launch_build_sb<4>(a, smem, st);
+        case 2: return launch_build_sb<2>(a, smem, st);
+        default: return launch_build_sb<1>(a, smem, st);
+    }
 }
 
 cudaError_t launch_minwise(const MinwiseArgs &a, cudaStream_t st) {
