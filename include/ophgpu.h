@@ -129,15 +129,18 @@ typedef struct {
  *          bin are decided NotSimilar at the scanned level), else BRUTE.  It
  *          probes a leading sample (1/16 of the sets, >= 16384) first and
  *          scans the rest with BRUTE if more than a quarter of the sample
- *          matched more than 16 distinct queries (one host synchronisation
+ *          matched more than 4 distinct queries (one host synchronisation
  *          per call).
  *   BRUTE: every (query, set, bin) equality is tested (register-blocked
  *          query tiles; cost ~ Q N bins; best when most pairs share bins).
- *   PROBE: per bin, the query values are hashed into a table; each set bin
- *          probes it, so only matching (query, set, bin) triples cost work
- *          (cost ~ N bins + matches; best for low background similarity).
- *          Sets matching more than 16 distinct queries are re-scanned by
- *          BRUTE. */
+ *   PROBE: a hash join in passes of <= 1024 queries, each one stream over
+ *          the scanned collection bins: per bin, the pass's query values go
+ *          into an exact hash table and a Bloom filter; every set bin tests
+ *          the filter (held in shared memory) and the rare positives are
+ *          verified in the table, so only matching (query, set, bin) triples
+ *          cost more than a filter test (cost ~ N bins + matches; best for
+ *          low background similarity).  Sets matching more than 4 distinct
+ *          queries are re-scanned by BRUTE. */
 enum { OPH_STRATEGY_AUTO = 0, OPH_STRATEGY_BRUTE = 1, OPH_STRATEGY_PROBE = 2 };
 
 /* One scored pair (20 bytes).

@@ -127,8 +127,11 @@ struct TableArgs {
 };
 
 constexpr int kJoinList = 4;        // distinct matched queries tracked per set before falling back to BRUTE
-constexpr uint32_t kJoinMaxQ = 1024;  // queries per join pass (Bloom words per bin <= 512 -> 64 KB per slab)
-constexpr uint32_t kJoinMaxLog2W = 9;
+// queries per join pass: the Bloom filter keeps >= 16 bits per query per bin in
+// 64-KB slabs of 32 bins x 512 words (<= 1024 queries), 16 x 1024 (<= 2048) or
+// 8 x 2048 (<= 4096)
+constexpr uint32_t kJoinMaxQ = 4096;
+constexpr uint32_t kJoinMaxLog2W = 11;
 
 struct ProbeArgs {
     const uint32_t *F, *E;

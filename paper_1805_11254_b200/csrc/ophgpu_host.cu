@@ -326,11 +326,19 @@ uint32_t probe_log2S(uint64_t nq) {
     return l;
 }
 
-// Bloom words per bin: fixed (the join kernel's filter rows are immediate offsets);
-// >= 16 bits per query for passes of <= kJoinMaxQ queries
-uint32_t probe_log2W(uint64_t) { return kJoinMaxLog2W; }
+// Bloom words per bin for a pass of nq queries: >= 16 bits per query, 512 .. 2048
+// words (the join kernel is compiled for these three widths)
+uint32_t probe_log2W(uint64_t nq) {
+    uint32_t l = 9;
+    while (l < kJoinMaxLog2W && (1ull << l) * 32 < 16 * nq) l++;
+    return l;
+}
 
-uint64_t probe_pass(uint64_t ldq) { return std::min<uint64_t>(ldq, kJoinMaxQ); }
+// queries per PROBE pass: all of them up to kJoinMaxQ, else balanced passes
+uint64_t probe_pass(uint64_t ldq) {
+    const uint64_t passes = ceil_div(ldq, kJoinMaxQ);
+    return ceil_div(ceil_div(ldq, passes), 32) * 32;
+}
 
 size_t ws_fixed_bytes(uint64_t n_q, uint64_t n_sets, uint32_t nb) {
     const uint64_t ldq = ceil_div(n_q ? n_q : 1, 32) * 32;
@@ -628,8 +636,9 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         if (levels || probe)
             if ((e = cudaMemsetAsync(w.counters, 0, (kMaxGroups + 3) * 8, stream)) != cudaSuccess) return e;
         if (!probe) return launch_scan(s, 32, stream);
-        for (uint64_t a0 = q0; a0 < q0 + nq; a0 += kJoinMaxQ)
-            if ((e = probe_pass_run(a0, std::min<uint64_t>(kJoinMaxQ, q0 + nq - a0))) != cudaSuccess) return e;
+        const uint64_t pq = probe_pass(nq);
+        for (uint64_t a0 = q0; a0 < q0 + nq; a0 += pq)
+            if ((e = probe_pass_run(a0, std::min<uint64_t>(pq, q0 + nq - a0))) != cudaSuccess) return e;
         return cudaSuccess;
     };
     // later levels, kLevelsPerLaunch per launch, survivors compacted between launches

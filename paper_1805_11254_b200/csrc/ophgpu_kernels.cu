@@ -710,7 +710,7 @@ constexpr uint32_t kJoinQCap = 256;  // candidate queue per warp (4-B entries)
 constexpr uint32_t kJoinSPL = 4;                  // sets per lane (one 16-B load per bin row)
 constexpr uint32_t kJoinRPT = 32 / kJoinSPL;      // bin rows per tile
 constexpr uint32_t kJoinTile = 32 * kJoinSPL;     // sets per tile
-constexpr uint32_t kJoinW = 1u << kJoinMaxLog2W;  // filter words per bin (fixed: row offsets are immediates)
+constexpr uint32_t kJoinSlabWords = 16384;  // one filter buffer: 64 KB = SBN bins x W words (W = 512 / 1024 / 2048)
 constexpr uint32_t kJoinMaxSlabs = 512;  // nscan <= 16384
 
 // shared-memory carve-up of the join kernel (bytes, 128-B aligned regions)
@@ -722,7 +722,7 @@ __host__ __device__ inline JoinLayout join_layout(uint32_t W, uint32_t R) {
     JoinLayout L;
     L.bars = 0;
     L.tab = 128;
-    L.lists = L.tab + 2 * 32 * W * 4;
+    L.lists = L.tab + 2 * kJoinSlabWords * 4;
     L.ovf = join_align(L.lists + kJoinList * R * 4);
     L.queue = join_align(L.ovf + R / 8);
     L.qcount = L.queue + kJoinWarps * kJoinQCap * 4;  // per slab: tile counter, done counter
@@ -859,10 +859,12 @@ __device__ __forceinline__ void join_push(const ProbeArgs &a, uint64_t s_lo, uin
 // slab j + 2, so no CTA-wide barrier between slabs); warps take 32-set tiles
 // from a shared counter: lane = one set, one coalesced 4-B load per bin row,
 // all 32 rows in flight at once.
-template <bool MW>
+template <bool MW, int LOG2W>
 __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_constant__ ProbeArgs a) {
     extern __shared__ __align__(128) unsigned char jsm[];
-    constexpr uint32_t W = kJoinW;
+    constexpr uint32_t W = 1u << LOG2W;             // filter words per bin (row offsets are immediates)
+    constexpr uint32_t SBN = kJoinSlabWords / W;   // bins per slab: 32 / 16 / 8
+    static_assert(SBN % kJoinRPT == 0, "a slab holds whole tile row blocks");
     const uint32_t R = a.R;
     const JoinLayout Ly = join_layout(W, R);
     uint64_t *tfull = reinterpret_cast<uint64_t *>(jsm + Ly.bars);
@@ -875,8 +877,8 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint64_t s_lo = a.s_begin + (uint64_t)blockIdx.x * R;
     const uint32_t nset = (uint32_t)(min(s_lo + R, a.s_end) - s_lo);
-    const uint32_t nslab = (a.nscan + 31u) / 32u;
-    const uint32_t slab_bytes = 32u * W * 4u;
+    const uint32_t nslab = (a.nscan + SBN - 1) / SBN;
+    const uint32_t slab_bytes = kJoinSlabWords * 4u;
 
     for (uint32_t x = threadIdx.x; x < kJoinList * R; x += blockDim.x) lists[x] = 0u;
     for (uint32_t x = threadIdx.x; x < R / 32; x += blockDim.x) ovf[x] = 0u;
@@ -887,20 +889,21 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (uint32_t j = 0; j < 2 && j < nslab; j++) {
             mbar_expect_tx(&tfull[j], slab_bytes);
-            bulk_g2s(tab + (size_t)j * 32 * W, a.bloom + (size_t)j * 32 * W, slab_bytes, &tfull[j]);
+            bulk_g2s(tab + (size_t)j * kJoinSlabWords, a.bloom + (size_t)j * kJoinSlabWords, slab_bytes, &tfull[j]);
         }
     }
     __syncthreads();
 
     uint32_t *myq = queue + warp * kJoinQCap;
     uint32_t qn = 0;  // queued positives of this warp (warp-uniform)
-    const uint32_t ntile = (nset + kJoinTile - 1) / kJoinTile * kJoinSPL;
+    constexpr uint32_t RB = SBN / kJoinRPT;  // tile row blocks per slab
+    const uint32_t ntile = (nset + kJoinTile - 1) / kJoinTile * RB;
     const uint32_t ldb = (uint32_t)(a.ld * 4u);  // row stride in bytes
     for (uint32_t j = 0; j < nslab; j++) {
         const uint32_t tb = j & 1u;
-        const uint32_t *tabj = tab + (size_t)tb * 32 * W;
-        const uint32_t rows = min(32u, a.nscan - 32u * j);
-        const uint32_t *Fj = a.F + (uint64_t)(32u * j) * a.ld;
+        const uint32_t *tabj = tab + (size_t)tb * kJoinSlabWords;
+        const uint32_t rows = min(SBN, a.nscan - SBN * j);
+        const uint32_t *Fj = a.F + (uint64_t)(SBN * j) * a.ld;
         // tiles are handed out dynamically (a 24-warp SM hides the row-load latency of one
         // warp behind the others' probing; a per-warp double buffer measured slower)
         auto next_tile = [&]() {
@@ -909,14 +912,14 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
             return __shfl_sync(0xFFFFFFFFu, t, 0);
         };
         // tile t: sets [sb * 32 * SPL, +32 * SPL) x rows [rb * RPT, +RPT) of the slab,
-        // sb = t / SPL, rb = t % SPL; lane = SPL adjacent sets (one vector load per row),
+        // sb = t / RB, rb = t % RB; lane = SPL adjacent sets (one vector load per row),
         // v[k * RPT + r] = set k, row r
         auto load_tile = [&](uint32_t t, uint32_t (&v)[32]) {
-            const uint32_t sb = t / kJoinSPL, rb = t % kJoinSPL;
+            const uint32_t sb = t / RB, rb = t % RB;
             const uint32_t sl = sb * kJoinTile + lane * kJoinSPL;
             const char *Fs = reinterpret_cast<const char *>(Fj + (uint64_t)(rb * kJoinRPT) * a.ld + s_lo + sl);
             // row r at Fs + r * ldb: one IMAD.WIDE.U32 per row (ldb < 2^32, checked by the launcher)
-            if ((sb + 1) * kJoinTile <= nset && rows == 32u) {  // full tile (warp-uniform): no checks
+            if ((sb + 1) * kJoinTile <= nset && (rb + 1) * kJoinRPT <= rows) {  // full tile (warp-uniform): no checks
 #pragma unroll
                 for (int r = 0; r < (int)kJoinRPT; r++) {
                     const uint4 x = __ldg(reinterpret_cast<const uint4 *>(Fs + (uint64_t)((uint32_t)r) * ldb));
@@ -937,15 +940,15 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
             }
         };
         auto probe_tile = [&](uint32_t t, const uint32_t (&v)[32]) {
-            const uint32_t sb = t / kJoinSPL, rb = t % kJoinSPL;
+            const uint32_t sb = t / RB, rb = t % RB;
             // filter test: h = v * golden; word (h >> 23) of the row's filter; both bits set -> bit of cm
             uint32_t cm = 0;
-            const uint32_t *tabr = tabj + rb * kJoinRPT * kJoinW;
+            const uint32_t *tabr = tabj + rb * kJoinRPT * W;
 #pragma unroll
             for (int i = 0; i < 32; i++) {
                 const uint32_t r = (uint32_t)i % kJoinRPT;
                 const uint32_t h = v[i] * 0x9E3779B1u;
-                const uint32_t word = tabr[r * kJoinW + (h >> (32 - kJoinMaxLog2W))];
+                const uint32_t word = tabr[r * W + (h >> (32 - LOG2W))];
                 const uint32_t z = bloom_miss(v[i], h, word);
                 asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, 0;\n\t@p or.b32 %0, %0, %2;\n}"
                     : "+r"(cm)
@@ -956,13 +959,13 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
             // (an empty collection bin that passes the filter -- ~10 % of the
             // positives -- is rejected there: no query inserts the value kEmpty)
             const uint32_t sl = sb * kJoinTile + lane * kJoinSPL;
-            if (!((sb + 1) * kJoinTile <= nset && rows == 32u)) {
+            if (!((sb + 1) * kJoinTile <= nset && (rb + 1) * kJoinRPT <= rows)) {
 #pragma unroll
                 for (int i = 0; i < 32; i++)
                     if (sl + (uint32_t)i / kJoinRPT >= nset || rb * kJoinRPT + (uint32_t)i % kJoinRPT >= rows)
                         cm &= ~(1u << i);
             }
-            join_push(a, s_lo, cm, sl, j * 32u + rb * kJoinRPT, lists, ovf, myq, qn);
+            join_push(a, s_lo, cm, sl, j * SBN + rb * kJoinRPT, lists, ovf, myq, qn);
         };
         mbar_wait(&tfull[tb], (j >> 1) & 1u);  // the slab's filters
         for (uint32_t t = next_tile(); t < ntile; t = next_tile()) {
@@ -978,7 +981,8 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
                 if (j + 2 < nslab) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     mbar_expect_tx(&tfull[tb], slab_bytes);
-                    bulk_g2s(tab + (size_t)tb * 32 * W, a.bloom + (size_t)(j + 2) * 32 * W, slab_bytes, &tfull[tb]);
+                    bulk_g2s(tab + (size_t)tb * kJoinSlabWords, a.bloom + (size_t)(j + 2) * kJoinSlabWords, slab_bytes,
+                             &tfull[tb]);
                 }
             }
         }
@@ -1257,12 +1261,11 @@ cudaError_t launch_probe(const ProbeArgs &a0, cudaStream_t st) {
     if (a0.s_end <= a0.s_begin) return cudaSuccess;
     ProbeArgs a = a0;
     const uint64_t n = a.s_end - a.s_begin;
-    const uint32_t W = kJoinW;
-    if (a.log2W != kJoinMaxLog2W || a.ld * 4 >= (1ull << 32)) return cudaErrorInvalidValue;
+    if (a.log2W < 9 || a.log2W > kJoinMaxLog2W || a.ld * 4 >= (1ull << 32)) return cudaErrorInvalidValue;
+    const uint32_t W = 0;  // the layout does not depend on the filter width (64-KB buffers)
     constexpr uint32_t kSmemMax = 227 * 1024;
     // one CTA per SM; sets per CTA: the fewest waves whose per-CTA lists fit next to
-    // the filter double buffer, split evenly (multiple of 32)
-    // (multiple of the tile's kJoinTile sets)
+    // the filter double buffer, split evenly (multiple of the tile's kJoinTile sets)
     uint32_t Rmax = kJoinTile;
     while (join_layout(W, Rmax + kJoinTile).total <= kSmemMax && Rmax + kJoinTile <= 65504) Rmax += kJoinTile;
     const uint64_t waves = (n + 148ull * Rmax - 1) / (148ull * Rmax);
@@ -1271,7 +1274,10 @@ cudaError_t launch_probe(const ProbeArgs &a0, cudaStream_t st) {
     a.nst = 0;
     const size_t smem = join_layout(W, R).total;
     if (smem > kSmemMax) return cudaErrorInvalidConfiguration;
-    auto kern = a.method == kMinwise ? join_kernel<true> : join_kernel<false>;
+    const bool mw = a.method == kMinwise;
+    auto kern = mw ? join_kernel<true, 9> : join_kernel<false, 9>;
+    if (a.log2W == 10) kern = mw ? join_kernel<true, 10> : join_kernel<false, 10>;
+    if (a.log2W == 11) kern = mw ? join_kernel<true, 11> : join_kernel<false, 11>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const uint64_t grid = (n + R - 1) / R;

@@ -233,7 +233,7 @@ def test_threshold_and_epsilon_extremes(tiny_run, tn, td, eps):
 @pytest.mark.parametrize("method", ["full", "goph", "hoph", "minwise"])
 def test_probe_overflow_falls_back_to_brute(method):
     """40 identical queries (plus 20 others): every set near them matches more
-    than 16 distinct queries, so PROBE hands those sets to the BRUTE list
+    than 4 distinct queries, so PROBE hands those sets to the BRUTE list
     scan; the hit lists still equal the oracle's."""
     rng = np.random.default_rng(12)
     V = 1 << 20
