@@ -704,11 +704,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  : "memory");
 }
 
-constexpr int kJoinWarps = 24;
+constexpr int kJoinWarps = 28;
 constexpr int kJoinThreads = 32 * kJoinWarps;
 constexpr uint32_t kJoinQCap = 256;  // candidate queue per warp (4-B entries)
 constexpr uint32_t kJoinSPL = 4;                  // sets per lane (one 16-B load per bin row)
-constexpr uint32_t kJoinRPT = 32 / kJoinSPL;      // bin rows per tile
+constexpr uint32_t kJoinRPT = 8;                  // bin rows per tile
+constexpr uint32_t kJoinVals = kJoinSPL * kJoinRPT;  // values per lane per tile (mask bits)
 constexpr uint32_t kJoinTile = 32 * kJoinSPL;     // sets per tile
 constexpr uint32_t kJoinSlabWords = 16384;  // one filter buffer: 64 KB = SBN bins x W words (W = 512 / 1024 / 2048)
 constexpr uint32_t kJoinMaxSlabs = 512;  // nscan <= 16384
@@ -853,7 +854,7 @@ __device__ __forceinline__ void join_push(const ProbeArgs &a, uint64_t s_lo, uin
     }
 }
 
-// One CTA (24 warps, one per SM) owns R consecutive sets.  Per slab of 32
+// One CTA (28 warps, one per SM) owns R consecutive sets.  Per slab of 32
 // scanned bins the slab's filters (32 x kJoinW words, bin-major) sit in
 // shared memory (double-buffered: the last warp to finish slab j bulk-copies
 // slab j + 2, so no CTA-wide barrier between slabs); warps take 32-set tiles
@@ -904,7 +905,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
         const uint32_t *tabj = tab + (size_t)tb * kJoinSlabWords;
         const uint32_t rows = min(SBN, a.nscan - SBN * j);
         const uint32_t *Fj = a.F + (uint64_t)(SBN * j) * a.ld;
-        // tiles are handed out dynamically (a 24-warp SM hides the row-load latency of one
+        // tiles are handed out dynamically (a 28-warp SM hides the row-load latency of one
         // warp behind the others' probing; a per-warp double buffer measured slower)
         auto next_tile = [&]() {
             uint32_t t = 0;
@@ -914,7 +915,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
         // tile t: sets [sb * 32 * SPL, +32 * SPL) x rows [rb * RPT, +RPT) of the slab,
         // sb = t / RB, rb = t % RB; lane = SPL adjacent sets (one vector load per row),
         // v[k * RPT + r] = set k, row r
-        auto load_tile = [&](uint32_t t, uint32_t (&v)[32]) {
+        auto load_tile = [&](uint32_t t, uint32_t (&v)[kJoinVals]) {
             const uint32_t sb = t / RB, rb = t % RB;
             const uint32_t sl = sb * kJoinTile + lane * kJoinSPL;
             const char *Fs = reinterpret_cast<const char *>(Fj + (uint64_t)(rb * kJoinRPT) * a.ld + s_lo + sl);
@@ -939,13 +940,13 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
                                 : kEmpty;
             }
         };
-        auto probe_tile = [&](uint32_t t, const uint32_t (&v)[32]) {
+        auto probe_tile = [&](uint32_t t, const uint32_t (&v)[kJoinVals]) {
             const uint32_t sb = t / RB, rb = t % RB;
             // filter test: h = v * golden; word (h >> 23) of the row's filter; both bits set -> bit of cm
             uint32_t cm = 0;
             const uint32_t *tabr = tabj + rb * kJoinRPT * W;
 #pragma unroll
-            for (int i = 0; i < 32; i++) {
+            for (int i = 0; i < (int)kJoinVals; i++) {
                 const uint32_t r = (uint32_t)i % kJoinRPT;
                 const uint32_t h = v[i] * 0x9E3779B1u;
                 const uint32_t word = tabr[r * W + (h >> (32 - LOG2W))];
@@ -961,7 +962,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
             const uint32_t sl = sb * kJoinTile + lane * kJoinSPL;
             if (!((sb + 1) * kJoinTile <= nset && (rb + 1) * kJoinRPT <= rows)) {
 #pragma unroll
-                for (int i = 0; i < 32; i++)
+                for (int i = 0; i < (int)kJoinVals; i++)
                     if (sl + (uint32_t)i / kJoinRPT >= nset || rb * kJoinRPT + (uint32_t)i % kJoinRPT >= rows)
                         cm &= ~(1u << i);
             }
@@ -969,7 +970,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
         };
         mbar_wait(&tfull[tb], (j >> 1) & 1u);  // the slab's filters
         for (uint32_t t = next_tile(); t < ntile; t = next_tile()) {
-            uint32_t v[32];
+            uint32_t v[kJoinVals];
             load_tile(t, v);
             probe_tile(t, v);
         }
