@@ -397,3 +397,48 @@ def test_text_minwise_subset(text_run):
     kw = dict(t_num=p["t_num"], t_den=p["t_den"])
     assert_records_equal(gpu_dense("minwise", qmw, mw, **kw),
                          oracle_records("minwise", QMW, MW, qflags=qfl, sflags=fl, **kw), "text minwise")
+
+
+# ----------------------------------------------------------------------------- PROBE filter widths / passes
+@pytest.fixture(scope="module")
+def wide_run():
+    """6,000 text-like sets (30 % planted) and 5,000 queries: 1,500 queries make one
+    PROBE pass with 1,024-word filters, 5,000 make two balanced passes of 2,528
+    queries with 2,048-word filters (8-bin slabs)."""
+    w = text_like(seed=11, n_sets=6000, n_queries=5000, planted_frac=0.3)
+    p = w.params
+    V, seed = w.vocab_size, p["perm_seed"]
+    hier = og.oph_hier_layout_make(V, p["a"], p["b"], p["hoph_kprime"])
+    _, so, sh = gpu_build(w.offsets, w.ids, V, seed, k=p["k"], kprime=p["kprime"], hier=hier)
+    _, qo, qh = gpu_build(w.q_offsets, w.q_ids, V, seed, k=p["k"], kprime=p["kprime"], hier=hier)
+    lay = oracle.hoph_layout(V, p["a"], p["b"], p["hoph_kprime"])
+    return dict(w=w, p=p, hier=hier, so=so, sh=sh, qo=qo, qh=qh, L=len(lay),
+                F=oracle.oph_sketch(w.offsets, w.ids, V, p["k"], seed),
+                QF=oracle.oph_sketch(w.q_offsets, w.q_ids, V, p["k"], seed),
+                H=oracle.hoph_sketch(w.offsets, w.ids, V, lay, p["hoph_kprime"], seed),
+                QH=oracle.hoph_sketch(w.q_offsets, w.q_ids, V, lay, p["hoph_kprime"], seed))
+
+
+@pytest.mark.parametrize("method,nq", [("full", 1500), ("goph", 1500), ("full", 5000), ("hoph", 5000)])
+def test_probe_filter_widths(wide_run, method, nq):
+    """PROBE threshold lists == oracle's for 1,024- and 2,048-word filters and multi-pass query batches."""
+    r, p = wide_run, wide_run["p"]
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    if method == "hoph":
+        q = subview(r["qh"], nq)
+        hits = gpu_threshold_hits(method, q, r["sh"], layout=r["hier"], strategy=og.OPH_STRATEGY_PROBE,
+                                  capacity=1 << 22, **kw)
+        want = oracle_records(method, r["QH"][:nq], r["H"], kprime=p["hoph_kprime"], L=r["L"], **kw)
+    else:
+        lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+        q = subview(r["qo"], nq)
+        hits = gpu_threshold_hits(method, q, r["so"], layout=lay, strategy=og.OPH_STRATEGY_PROBE,
+                                  capacity=1 << 22, **kw)
+        want = oracle_records(method, r["QF"][:nq], r["F"], k=p["k"], kprime=p["kprime"], **kw)
+    got = [(int(h["query"]), int(h["set_id"])) for h in hits]
+    assert got == oracle.threshold_list(want, 0)
+    assert len(got) > 100
+    for h in hits[:: max(1, len(hits) // 300)]:  # sampled records: counts and flags bit-exact
+        o = want[int(h["query"]), int(h["set_id"])]
+        assert (int(h["n_mb"]), int(h["n_excl"]), int(h["groups"]), int(h["verdict"]), int(h["flags"])) == \
+            (int(o["n_mb"]), int(o["n_excl"]), int(o["groups"]), int(o["verdict"]), int(o["flags"]))
