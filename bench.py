@@ -189,7 +189,8 @@ def make_workload(config: str, rank: int):
 
 
 def count_launches(step_fn):
-    """Kernel launches of one step, counted with the CUDA profiler (untimed)."""
+    """Kernel launches of one step and their device times, from the CUDA profiler
+    (CUPTI) over one extra, untimed step: (launch count, {kernel: [count, total us]})."""
     try:
         import torch
         from torch.profiler import ProfilerActivity, profile
@@ -197,15 +198,20 @@ def count_launches(step_fn):
             step_fn()
             torch.cuda.synchronize()
         n = 0
+        per = {}
         for e in prof.events():
             if getattr(e, "device_type", None) is not None and "CUDA" in str(e.device_type):
                 nm = e.name
                 if "memset" in nm.lower() or "memcpy" in nm.lower():
                     continue
                 n += 1
-        return n
+                key = nm.split("(")[0].replace("void ", "").replace("ophgpu::", "")
+                c = per.setdefault(key, [0, 0.0])
+                c[0] += 1
+                c[1] += float(e.device_time_total)
+        return n, per
     except Exception:  # profiler unavailable: no claim
-        return None
+        return None, {}
 
 
 def run_ours(args):
@@ -338,7 +344,9 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    launches = None if args.no_launch_count else count_launches(step)
+    # (the profiled step runs every call on one stream, so per-kernel device times are not
+    # inflated by the MinWise side stream sharing the SMs)
+    launches, kernel_us = (None, {}) if args.no_launch_count else count_launches(lambda: step(serial=True))
 
     # ---------------- timed region: device inputs resident in HBM
     K = args.steps
@@ -474,6 +482,19 @@ def run_ours(args):
             "derived: 148 SM x 4 SMSP x 16 ALU lanes x sm_max_mhz / 9.5 ALU ops per psi (DESIGN.md)"}
     per_kernel = {n: {"ms": phase_ms[n], "bound": v[0], "achieved": v[1], "peak": v[2], "unit": v[3],
                       "frac": v[1] / v[2], "bytes": v[4]} for n, v in kern.items()}
+    # the PROBE collection scans on their own (CUPTI device time of the join kernels over the
+    # untimed profiled step): algorithmic bytes = one stream of the scanned bins per pass of
+    # <= 4096 queries (full + GOPH prefix + HOPH group 1; MinWise separately)
+    scan = {}
+    passes = -(-Q // 4096)
+    for name, mw_flag, byt in (("oph_family", "false", by["compare_full"] + by["compare_goph"] + by["compare_hoph"]),
+                               ("minwise", "true", by["compare_minwise"])):
+        hit = [v for kname, v in kernel_us.items() if kname.startswith(f"join_kernel<{mw_flag}")]
+        if hit:
+            us = sum(v[1] for v in hit)
+            scan[name] = {"kernel": f"join_kernel<{mw_flag}, ...>", "launches": sum(v[0] for v in hit), "us": us,
+                          "bytes": byt * passes, "achieved": byt * passes / (us / 1e6) / 1e9, "peak": hbm / 1e9,
+                          "unit": "GB/s", "frac": byt * passes / (us / 1e6) / hbm}
 
     # ---------------- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
@@ -512,6 +533,9 @@ def run_ours(args):
         "hits": hits_last,
         "roofline": roof,
         "kernels": per_kernel,
+        "probe_scan": scan,
+        "device_us_per_step": {n: {"launches": v[0], "us": round(v[1], 1)} for n, v in sorted(
+            kernel_us.items(), key=lambda kv: -kv[1][1])},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches * K if launches is not None else None,
