@@ -165,13 +165,22 @@ typedef struct {
  *     caller-side status for that case).  *d_count is NOT reset by the call:
  *     several calls may append to one sink.
  *   OPH_RES_DENSE: one record per pair at d_hits[query * n_sets + set]
- *     (capacity >= n_queries * n_sets), for parity tests on small inputs. */
+ *     (capacity >= n_queries * n_sets), for parity tests on small inputs.
+ *   d_stop_hist (optional, may be NULL): OPH_STOP_HIST_LEN counters; the call
+ *     ADDS, for every (query, set) pair it scores, one to entry g where g is
+ *     the pair's `groups` field (groups compared when the pair was decided:
+ *     GOPH/HOPH early termination, Alg. 1 l / Alg. 2 l; n for
+ *     full OPH; 0 for MinWise), so after a call the entries sum to
+ *     n_queries * n_sets more than before -- the termination-level histogram
+ *     of SURVEY 8(d) (work saved = bins not compared). */
+#define OPH_STOP_HIST_LEN (OPH_MAX_GROUPS + 1)
 typedef struct {
     oph_hit *d_hits;
     uint64_t capacity;
     unsigned long long *d_count;
     uint32_t mode;
     uint32_t pad;
+    unsigned long long *d_stop_hist;
 } oph_results;
 
 /* ---------------------------------------------------------------- host helpers */

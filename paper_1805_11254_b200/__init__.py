@@ -70,7 +70,11 @@ class oph_params(ctypes.Structure):
 
 
 class oph_results(ctypes.Structure):
-    _fields_ = [("d_hits", c_vp), ("capacity", c_u64), ("d_count", c_vp), ("mode", c_u32), ("pad", c_u32)]
+    _fields_ = [("d_hits", c_vp), ("capacity", c_u64), ("d_count", c_vp), ("mode", c_u32), ("pad", c_u32),
+                ("d_stop_hist", c_vp)]
+
+
+OPH_STOP_HIST_LEN = 65  # include/ophgpu.h: OPH_MAX_GROUPS + 1
 
 
 class OphError(RuntimeError):
@@ -264,18 +268,27 @@ def minwise_build_sketches(sets: SetCollection, vocab_size: int, seed: int, k: i
 class Results:
     """A result sink: `capacity` oph_hit records + a device counter."""
 
-    def __init__(self, capacity: int, dense: bool = False):
+    def __init__(self, capacity: int, dense: bool = False, stop_hist: bool = False):
         torch = _torch()
         self.capacity = int(capacity)
         self.mode = OPH_RES_DENSE if dense else OPH_RES_THRESHOLD
         self.hits = torch.zeros((max(1, self.capacity) * HIT_DTYPE.itemsize,), dtype=torch.uint8, device="cuda")
         self.count = torch.zeros((1,), dtype=torch.int64, device="cuda")
+        # termination-level histogram (include/ophgpu.h d_stop_hist), accumulated over calls
+        self.stop_hist = torch.zeros((OPH_STOP_HIST_LEN,), dtype=torch.int64, device="cuda") if stop_hist else None
 
     def reset(self):
         self.count.zero_()
+        if self.stop_hist is not None:
+            self.stop_hist.zero_()
 
     def c(self) -> oph_results:
-        return oph_results(_ptr(self.hits), self.capacity, _ptr(self.count), self.mode, 0)
+        return oph_results(_ptr(self.hits), self.capacity, _ptr(self.count), self.mode, 0,
+                           _ptr(self.stop_hist) if self.stop_hist is not None else None)
+
+    def hist(self) -> np.ndarray:
+        """The termination-level histogram (synchronises)."""
+        return self.stop_hist.cpu().numpy().astype(np.uint64)
 
     def n(self) -> int:
         """Records reported (synchronises); may exceed capacity (truncation)."""

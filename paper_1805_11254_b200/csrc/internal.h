@@ -72,6 +72,7 @@ struct OutArgs {
     uint32_t dense;
     uint32_t set_id_base;
     uint64_t n_sets;  // dense row length
+    unsigned long long *hist;  // optional termination-level histogram [OPH_STOP_HIST_LEN]
 };
 
 enum Method : uint32_t { kFull = 0, kGoph = 1, kHoph = 2, kMinwise = 3 };
@@ -146,6 +147,7 @@ struct ProbeArgs {
     const uint8_t *qflags;  // MinWise query flags, indexed by global query
     uint32_t nw, nbins_total;
     uint32_t q_col0;        // global index of the chunk's first query
+    uint32_t nq;            // queries in this pass
     uint32_t method, final_, level, joint, t_num, t_den;
     uint64_t w1, acc;
     int64_t rej;

@@ -316,7 +316,7 @@ struct Ws {
     uint64_t ldq, cap;
 };
 
-constexpr uint32_t kCounters = kMaxGroups + 4;
+constexpr uint32_t kCounters = kMaxGroups + 4 + OPH_STOP_HIST_LEN;  // level counters, PROBE counters, saved histogram
 constexpr uint32_t kLevelsPerLaunch = 4;  // GOPH/HOPH levels per survivor-kernel launch
 
 // PROBE exact-table slots per bin for a pass of nq queries: load factor <= 1/4
@@ -457,6 +457,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     out.dense = res->mode == OPH_RES_DENSE;
     out.set_id_base = set_id_base;
     out.n_sets = n_s;
+    out.hist = res->d_stop_hist;
 
     ScanArgs s{};
     s.F = Sv->d_values;
@@ -537,6 +538,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
 
     unsigned long long *ovf_count = w.counters + kMaxGroups + 2;
     unsigned long long *saved_hits = w.counters + kMaxGroups + 3;  // not cleared per chunk
+    unsigned long long *saved_hist = w.counters + kMaxGroups + 4;  // [OPH_STOP_HIST_LEN], likewise
 
     // the collection scan of queries [q0, q0+nq): BRUTE, or PROBE + its BRUTE list fallback
     // (PROBE in passes of <= kJoinMaxQ queries, each one stream over the collection)
@@ -579,6 +581,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         pr.nw = nw;
         pr.nbins_total = nb;
         pr.q_col0 = (uint32_t)q0;
+        pr.nq = (uint32_t)nq;
         pr.method = method;
         pr.final_ = s.final_;
         pr.level = s.level;
@@ -669,6 +672,8 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         // PROBE leaves few survivors: try every query at once; if the survivor list overflowed,
         // roll the hit counter back and redo the queries in chunks sized for the worst case
         e = cudaMemcpyAsync(saved_hits, res->d_count, 8, cudaMemcpyDeviceToDevice, stream);
+        if (e == cudaSuccess && res->d_stop_hist)
+            e = cudaMemcpyAsync(saved_hist, res->d_stop_hist, 8 * OPH_STOP_HIST_LEN, cudaMemcpyDeviceToDevice, stream);
         if (e == cudaSuccess) e = scan_chunk(0, n_q);
         unsigned long long n_surv = 0;
         if (e == cudaSuccess)
@@ -679,6 +684,9 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
             e = level_chunk();
         } else {
             e = cudaMemcpyAsync(res->d_count, saved_hits, 8, cudaMemcpyDeviceToDevice, stream);
+            if (e == cudaSuccess && res->d_stop_hist)
+                e = cudaMemcpyAsync(res->d_stop_hist, saved_hist, 8 * OPH_STOP_HIST_LEN, cudaMemcpyDeviceToDevice,
+                                    stream);
             if (e == cudaSuccess) e = safe_range(0, n_q);
         }
         return e == cudaSuccess ? OPH_OK : OPH_ECUDA;

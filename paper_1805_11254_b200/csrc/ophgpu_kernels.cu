@@ -321,6 +321,14 @@ __device__ __forceinline__ unsigned long long warp_append(bool pred, unsigned lo
     return base + __popc(m & ((1u << lane) - 1u));
 }
 
+// termination-level histogram: add the warp's per-lane counts of pairs decided at
+// `level` (warp-uniform; all 32 lanes call)
+__device__ __forceinline__ void hist_add(unsigned long long *hist, uint32_t level, uint32_t n) {
+    if (!hist) return;
+    const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, n);
+    if ((threadIdx.x & 31u) == 0 && tot) atomicAdd(hist + level, (unsigned long long)tot);
+}
+
 __device__ __forceinline__ void write_hit(oph_hit *dst, uint32_t q, uint32_t set_id, uint32_t n_mb, uint32_t n_excl,
                                           uint32_t groups, uint32_t verdict, uint32_t flags, float est) {
     uint32_t *d = reinterpret_cast<uint32_t *>(dst);
@@ -553,6 +561,7 @@ __global__ void __launch_bounds__(128, 3) scan_kernel(const __grid_constant__ Sc
                     hit_mask |= (uint32_t)(valid && verdict) << q;
                     dec_mask |= (uint32_t)valid << q;
                 }
+                hist_add(a.out.hist, a.level, __popc(dec_mask));
                 const bool any = __any_sync(0xFFFFFFFFu, a.out.dense ? dec_mask != 0 : hit_mask != 0);
                 if (any) {
 #pragma unroll
@@ -584,6 +593,7 @@ __global__ void __launch_bounds__(128, 3) scan_kernel(const __grid_constant__ Sc
                     dec_mask |= (uint32_t)(valid && (acc || rej)) << q;
                     surv_mask |= (uint32_t)(valid && !acc && !rej) << q;
                 }
+                hist_add(a.out.hist, a.level, __popc(dec_mask));
                 const bool any_emit = __any_sync(0xFFFFFFFFu, a.out.dense ? dec_mask != 0 : hit_mask != 0);
                 if (any_emit) {
 #pragma unroll
@@ -1002,6 +1012,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
             const unsigned long long idx = warp_append(of, a.ovf_count);
             if (of) a.ovf_list[idx] = (uint32_t)s;
         }
+        uint32_t n_surv = 0;  // this set's pairs that go on to the next level
 #pragma unroll 1
         for (int e = 0; e < kJoinList; e++) {
             const uint32_t x = (act && !of) ? lists[e * R + sl] : 0u;
@@ -1050,7 +1061,12 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
                 a.surv.state[idx] = st;
                 a.surv.nmb[idx] = m;
             }
+            n_surv += surv;
         }
+        // every pair of this set except the survivors is decided at this level: the listed
+        // ones above, the unlisted ones (no matched bin) NotSimilar; an overflowing set's
+        // pairs are counted by the BRUTE list scan
+        hist_add(a.out.hist, a.level, (sl < nset && !of) ? a.nq - n_surv : 0u);
     }
 }
 
@@ -1146,11 +1162,13 @@ __global__ void __launch_bounds__(256) level_kernel(const __grid_constant__ Leve
                     }
                 }
                 emit(a.res, alive, q, s, nmb, ex_tot, a.nlev, verdict, flags, est);
+                hist_add(a.res.hist, a.nlev, alive ? 1u : 0u);
                 alive = false;
                 break;
             }
             const bool acc = alive && st >= a.acc[l - 1];
             const bool rej = alive && !acc && (int64_t)st <= a.rej[l - 1];
+            hist_add(a.res.hist, l, (acc || rej) ? 1u : 0u);
             const bool want = a.res.dense ? (acc || rej) : acc;
             if (__any_sync(0xFFFFFFFFu, want)) {
                 uint32_t ex = 0;

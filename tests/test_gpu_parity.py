@@ -442,3 +442,34 @@ def test_probe_filter_widths(wide_run, method, nq):
         o = want[int(h["query"]), int(h["set_id"])]
         assert (int(h["n_mb"]), int(h["n_excl"]), int(h["groups"]), int(h["verdict"]), int(h["flags"])) == \
             (int(o["n_mb"]), int(o["n_excl"]), int(o["groups"]), int(o["verdict"]), int(o["flags"]))
+
+
+# ----------------------------------------------------------------------------- termination-level histograms
+@pytest.mark.parametrize("strategy", [og.OPH_STRATEGY_BRUTE, og.OPH_STRATEGY_PROBE])
+@pytest.mark.parametrize("method", ["full", "goph", "hoph", "minwise"])
+def test_tiny_stop_histogram(tiny_run, method, strategy):
+    """d_stop_hist == the histogram of the oracle's per-pair `groups` (groups compared when
+    decided: Alg. 1 / Alg. 2 early termination), summing to Q x N, for both scan strategies."""
+    r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    res = og.Results(1 << 20, stop_hist=True)
+    prm = og.params(p["t_num"], p["t_den"], p["eps"], False, strategy)
+    if method in ("full", "goph"):
+        lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+        (og.compare_full if method == "full" else og.compare_goph)(r["qo"], r["so"], lay, prm, res)
+        want = oracle_records(method, o["QF"], o["F"], k=p["k"], kprime=p["kprime"], **kw)
+        q, s = r["qo"], r["so"]
+    elif method == "hoph":
+        og.compare_hoph(r["qh"], r["sh"], r["hier"], prm, res)
+        want = oracle_records(method, o["QH"], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw)
+        q, s = r["qh"], r["sh"]
+    else:
+        og.compare_minwise(r["qmw"], r["mw"], prm, res)
+        want = oracle_records(method, o["QMW"][0], o["MW"][0], qflags=o["QMW"][1], sflags=o["MW"][1], **kw)
+        q, s = r["qmw"], r["mw"]
+    got = res.hist()
+    exp = np.bincount(want["groups"].astype(np.int64).ravel(), minlength=og.OPH_STOP_HIST_LEN)
+    assert int(got.sum()) == q.n_sets * s.n_sets
+    assert (got.astype(np.int64) == exp).all(), (got[:20], exp[:20])
+    if method in ("goph", "hoph"):  # early termination does save work on tiny
+        assert exp[: (p["k"] // p["kprime"] if method == "goph" else o["L"])].sum() > 0
