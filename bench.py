@@ -257,10 +257,13 @@ def run_ours(args):
     qo, qh = og.oph_build_sketches(qsets, V, seed, flat=flat, hier=hier)
     qmw = og.minwise_build_sketches(qsets, V, seed, mwk)
     counts = torch.zeros((4,), dtype=torch.int64, device="cuda")
+    # termination-level histograms of the four scorings (include/ophgpu.h d_stop_hist), per step
+    hists = torch.zeros((4, og.OPH_STOP_HIST_LEN), dtype=torch.int64, device="cuda")
     res = []
     for i in range(4):
         r = og.Results(cap)
         r.count = counts[i:i + 1]
+        r.stop_hist = hists[i]
         res.append(r)
     surv_cap = min(((Q + 31) // 32) * 32 * N, surv_limit)
     ws = [og.Workspace() for _ in range(5)]
@@ -282,6 +285,7 @@ def run_ours(args):
                 ev[i].record(st)
         mark(0)
         counts.zero_()
+        hists.zero_()
         fork = torch.cuda.Event()
         fork.record(stream)
         side.wait_event(fork)
@@ -496,6 +500,64 @@ def run_ours(args):
                           "bytes": byt * passes, "achieved": byt * passes / (us / 1e6) / 1e9, "peak": hbm / 1e9,
                           "unit": "GB/s", "frac": byt * passes / (us / 1e6) / hbm}
 
+    # ---------------- work saved by early termination: per method, the pairs
+    # decided after each number of groups compared (the last step's histograms, this rank)
+    hh = hists.cpu().numpy()
+    term = {}
+    for i, (m, gsize, gtot) in enumerate((("full", kp, k // kp), ("goph", kp, k // kp), ("hoph", hkp, L),
+                                          ("minwise", mwk, 1))):
+        h = hh[i]
+        npairs = int(h.sum())
+        groups = float((h * np.arange(len(h))).sum() / max(1, npairs))
+        bins = mwk if m == "minwise" else groups * gsize
+        term[m] = {"pairs": npairs, "hist": {str(g): int(c) for g, c in enumerate(h) if c},
+                   "mean_groups_compared": groups if m != "minwise" else None,
+                   "mean_bins_compared": bins, "bins_total": (mwk if m == "minwise" else gtot * gsize)}
+
+    # ---------------- quality vs exact Jaccard, untimed: every reported pair of the
+    # last step is verified with exact_jaccard_pairs (precision); recall counts the planted pairs
+    # whose realised J >= T (background pairs are random sets: a 100,000-pair random sample is
+    # verified too), for both empty-bin modes (EitherEmpty = the timed run; JointEmpty re-scored)
+    quality = None
+    if not args.no_quality and getattr(w, "planted", None) is not None and len(w.planted):
+        tn, td = p["t_num"], p["t_den"]
+        pl = np.asarray(w.planted)
+        truth = {(int(q), int(s_)) for q, s_, i_, u_ in pl if u_ and i_ * td >= tn * u_}
+
+        def verify(qi, si):
+            qa = torch.as_tensor(np.asarray(qi, dtype=np.int32), device="cuda")
+            sa = torch.as_tensor(np.asarray(si, dtype=np.int32), device="cuda")
+            it, un = og.exact_jaccard_pairs(qsets, sets, qa, sa)
+            it, un = it.cpu().numpy().astype(np.int64), un.cpu().numpy().astype(np.int64)
+            return (un > 0) & (it * td >= tn * un)
+
+        def score(r, n):
+            h = r.numpy(min(n, r.capacity))
+            qi, si = h["query"].astype(np.int64), h["set_id"].astype(np.int64) - base
+            good = verify(qi, si) if len(h) else np.zeros(0, bool)
+            rep = set(zip(qi.tolist(), si.tolist()))
+            return {"hits": int(len(h)), "precision": float(good.mean()) if len(h) else None,
+                    "recall": len(rep & truth) / max(1, len(truth))}
+
+        rng = np.random.default_rng(12345)
+        bq, bs = rng.integers(0, Q, 100_000), rng.integers(0, N, 100_000)
+        planted_pairs = {(int(q), int(s_)) for q, s_, _, _ in pl}
+        keep = np.array([(int(a_), int(b_)) not in planted_pairs for a_, b_ in zip(bq, bs)], dtype=bool)
+        bq, bs = bq[keep], bs[keep]
+        bg_above = int(verify(bq, bs).sum())
+        n4q = counts.cpu().numpy()
+        quality = {"T": f"{tn}/{td}", "true_pairs": len(truth),
+                   "truth": "planted pairs with realised J >= T; background check: "
+                            f"{bg_above} of {len(bq)} random non-planted (query, set) pairs have exact J >= T",
+                   "either_empty": {m: score(res[i], int(n4q[i])) for i, m in enumerate(("full", "goph", "hoph",
+                                                                                          "minwise"))}}
+        prm_j = og.params(p["t_num"], p["t_den"], p["eps"], joint=True, strategy=strategy)
+        jr = [og.Results(cap) for _ in range(3)]
+        og.compare_full(qo, so, flat, prm_j, jr[0], set_id_base=base, ws=ws[0])
+        og.compare_goph(qo, so, flat, prm_j, jr[1], set_id_base=base, ws=ws[1], survivor_capacity=surv_cap)
+        og.compare_hoph(qh, sh, hier, prm_j, jr[2], set_id_base=base, ws=ws[2], survivor_capacity=surv_cap)
+        quality["joint_empty"] = {m: score(jr[i], jr[i].n()) for i, m in enumerate(("full", "goph", "hoph"))}
+
     # ---------------- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -534,6 +596,8 @@ def run_ours(args):
         "roofline": roof,
         "kernels": per_kernel,
         "probe_scan": scan,
+        "termination": term,
+        "quality": quality,
         "device_us_per_step": {n: {"launches": v[0], "us": round(v[1], 1)} for n, v in sorted(
             kernel_us.items(), key=lambda kv: -kv[1][1])},
         "cpu_baseline": cpu,
@@ -557,6 +621,7 @@ def main():
                     help="workload (BASELINE.json configs); text-like is the headline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-quality", action="store_true", help="skip the precision/recall pass (untimed)")
     ap.add_argument("--no-launch-count", action="store_true", help="skip the CUPTI launch count (use under ncu)")
     args = ap.parse_args()
     if args.impl == "reference":

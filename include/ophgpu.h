@@ -270,6 +270,21 @@ oph_status compare_minwise(const oph_sketches *queries, const oph_sketches *sets
 /* ---------------------------------------------------------------- select (row a10) */
 
 /* Workspace bytes for topk_or_threshold_results on up to n_in records. */
+/* Exact Jaccard of (query, set) pairs -- the quality check of the estimators
+ * (Eq. 5: J = |A n B| / |A u B|; SURVEY 8(d) "precision/recall vs exact
+ * Jaccard", 8(f) rank 2 "GPU sorted-merge verifier for hits").
+ *   For pair i: d_inter[i] = |Q_a n S_b|, d_union[i] = |Q_a u S_b| with
+ *   a = d_query[i] (index into `queries`) and b = d_set[i] (local index into
+ *   `sets`); J is undefined when d_union[i] == 0 (both sets empty).
+ *   Ids of each set strictly increasing (the CSR contract); indices in range
+ *   (not checked on the device).  One warp per pair: each lane merges a
+ *   contiguous slice of the smaller set against the larger from a binary-
+ *   searched start.  Asynchronous on `stream`; caller-owned device buffers.
+ *   Errors: OPH_EINVAL for NULL arguments (n_pairs == 0 is a no-op). */
+oph_status exact_jaccard_pairs(const oph_sets *queries, const oph_sets *sets, const uint32_t *d_query,
+                               const uint32_t *d_set, uint64_t n_pairs, uint32_t *d_inter, uint32_t *d_union,
+                               void *stream);
+
 oph_status oph_select_workspace_size(uint64_t n_in, size_t *bytes);
 
 /* Result lists.  d_in: n_in records (n_in is a

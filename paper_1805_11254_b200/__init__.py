@@ -88,7 +88,8 @@ _lib = None
 # every symbol include/ophgpu.h declares
 EXPORTS = ["oph_status_string", "oph_sketch_ld", "oph_hier_layout_make", "oph_build_sketches",
            "minwise_build_sketches", "oph_workspace_size", "compare_full", "compare_goph", "compare_hoph",
-           "compare_minwise", "oph_select_workspace_size", "topk_or_threshold_results", "oph_plan_thresholds"]
+           "compare_minwise", "oph_select_workspace_size", "topk_or_threshold_results", "oph_plan_thresholds",
+           "exact_jaccard_pairs"]
 
 
 def lib():
@@ -365,6 +366,19 @@ def oph_select_workspace_size(n_in: int) -> int:
     out = ctypes.c_size_t()
     _check(lib().oph_select_workspace_size(c_u64(n_in), ctypes.byref(out)), "oph_select_workspace_size")
     return int(out.value)
+
+
+def exact_jaccard_pairs(queries: SetCollection, sets: SetCollection, query_idx, set_idx, stream=None):
+    """|Q_a n S_b| and |Q_a u S_b| for pairs (query_idx[i], set_idx[i]) (int32/uint32
+    device tensors; set_idx local to `sets`) -> (inter, union) uint32-as-int32 tensors."""
+    torch = _torch()
+    n = int(query_idx.numel())
+    inter = torch.zeros((max(1, n),), dtype=torch.int32, device="cuda")
+    union = torch.zeros((max(1, n),), dtype=torch.int32, device="cuda")
+    _check(lib().exact_jaccard_pairs(ctypes.byref(queries.c()), ctypes.byref(sets.c()), _ptr(query_idx),
+                                     _ptr(set_idx), c_u64(n), _ptr(inter), _ptr(union), _stream(stream)),
+           "exact_jaccard_pairs")
+    return inter[:n], union[:n]
 
 
 def topk_or_threshold_results(res_in: Results, n_in: int, mode: int, out: Results, topk: int = 0, k_bins: int = 0,

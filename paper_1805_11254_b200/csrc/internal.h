@@ -193,6 +193,14 @@ struct PrepArgs {
     uint64_t ldq;
 };
 
+struct JaccardArgs {
+    const uint64_t *q_offsets, *s_offsets;
+    const uint32_t *q_ids, *s_ids;
+    const uint32_t *query, *set;
+    uint64_t n;
+    uint32_t *inter, *uni;
+};
+
 // ---- launchers (ophgpu_kernels.cu); all return cudaGetLastError()
 cudaError_t launch_build(const BuildArgs &a, cudaStream_t st);
 cudaError_t launch_minwise(const MinwiseArgs &a, cudaStream_t st);
@@ -201,6 +209,7 @@ cudaError_t launch_scan(const ScanArgs &a, uint32_t B, cudaStream_t st);
 cudaError_t launch_table(const TableArgs &a, cudaStream_t st);
 cudaError_t launch_probe(const ProbeArgs &a, cudaStream_t st);
 cudaError_t launch_level(const LevelArgs &a, cudaStream_t st);
+cudaError_t launch_jaccard(const JaccardArgs &a, cudaStream_t st);
 size_t select_temp_bytes(uint64_t n);
 cudaError_t run_select(const oph_hit *in, uint64_t n, uint32_t mode, uint32_t topk, uint32_t k_bins, oph_hit *out,
                        unsigned long long *n_out, void *ws, size_t ws_bytes, cudaStream_t st);

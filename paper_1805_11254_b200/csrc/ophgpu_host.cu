@@ -869,6 +869,26 @@ oph_status compare_minwise(const oph_sketches *q, const oph_sketches *s, uint32_
                        (cudaStream_t)stream);
 }
 
+oph_status exact_jaccard_pairs(const oph_sets *queries, const oph_sets *sets, const uint32_t *d_query,
+                               const uint32_t *d_set, uint64_t n_pairs, uint32_t *d_inter, uint32_t *d_union,
+                               void *stream) {
+    oph_status st;
+    if ((st = check_sets(queries)) || (st = check_sets(sets))) return st;
+    if (n_pairs == 0) return OPH_OK;
+    if (!d_query || !d_set || !d_inter || !d_union || !queries->d_offsets || !sets->d_offsets) return OPH_EINVAL;
+    JaccardArgs a{};
+    a.q_offsets = queries->d_offsets;
+    a.s_offsets = sets->d_offsets;
+    a.q_ids = queries->d_ids;
+    a.s_ids = sets->d_ids;
+    a.query = d_query;
+    a.set = d_set;
+    a.n = n_pairs;
+    a.inter = d_inter;
+    a.uni = d_union;
+    return cuda_status(launch_jaccard(a, (cudaStream_t)stream));
+}
+
 oph_status oph_select_workspace_size(uint64_t n_in, size_t *bytes) {
     if (!bytes || n_in >= (1ull << 31)) return OPH_EINVAL;
     *bytes = select_temp_bytes(n_in);

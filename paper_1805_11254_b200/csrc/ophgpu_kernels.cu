@@ -1189,6 +1189,61 @@ __global__ void __launch_bounds__(256) level_kernel(const __grid_constant__ Leve
 }
 
 // ---------------------------------------------------------------------------
+// Exact Jaccard of (query, set) pairs (Eq. 5): warp per pair.  The smaller set
+// A is cut into 32 contiguous slices; lane l binary-searches the first element
+// of its slice in the larger set B, then merges the slice with B linearly,
+// counting equal ids (ids strictly increasing).  |A u B| = |A| + |B| - |A n B|.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) jaccard_kernel(const __grid_constant__ JaccardArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t i = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < a.n; i += nwarps) {
+        const uint32_t qi = a.query[i], si = a.set[i];
+        const uint64_t q0 = a.q_offsets[qi], q1 = a.q_offsets[qi + 1];
+        const uint64_t s0 = a.s_offsets[si], s1 = a.s_offsets[si + 1];
+        const uint32_t *A = a.q_ids + q0, *B = a.s_ids + s0;
+        uint64_t na = q1 - q0, nb = s1 - s0;
+        if (na > nb) {
+            const uint32_t *t = A;
+            A = B;
+            B = t;
+            const uint64_t u = na;
+            na = nb;
+            nb = u;
+        }
+        const uint64_t lo = na * lane / 32, hi = na * (lane + 1) / 32;  // this lane's slice of A
+        uint32_t c = 0;
+        if (lo < hi) {
+            uint64_t l = 0, h = nb;  // first position in B with B[pos] >= A[lo]
+            const uint32_t x0 = __ldg(A + lo);
+            while (l < h) {
+                const uint64_t m = (l + h) >> 1;
+                if (__ldg(B + m) < x0) l = m + 1; else h = m;
+            }
+            uint64_t ia = lo, ib = l;
+            while (ia < hi && ib < nb) {
+                const uint32_t xa = __ldg(A + ia), xb = __ldg(B + ib);
+                c += xa == xb;
+                ia += xa <= xb;
+                ib += xb <= xa;
+            }
+        }
+        const uint32_t inter = __reduce_add_sync(0xFFFFFFFFu, c);
+        if (lane == 0) {
+            a.inter[i] = inter;
+            a.uni[i] = (uint32_t)(na + nb - inter);
+        }
+    }
+}
+
+cudaError_t launch_jaccard(const JaccardArgs &a, cudaStream_t st) {
+    if (a.n == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<uint64_t>((a.n + 7) / 8, 148ull * 16);
+    jaccard_kernel<<<grid, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 template <int SB>

@@ -473,3 +473,34 @@ def test_tiny_stop_histogram(tiny_run, method, strategy):
     assert (got.astype(np.int64) == exp).all(), (got[:20], exp[:20])
     if method in ("goph", "hoph"):  # early termination does save work on tiny
         assert exp[: (p["k"] // p["kprime"] if method == "goph" else o["L"])].sum() > 0
+
+
+# ----------------------------------------------------------------------------- exact Jaccard verifier
+def test_exact_jaccard_pairs_vs_oracle():
+    """exact_jaccard_pairs: |A n B|, |A u B| bit-exact vs the oracle's sorted merge (O11, Eq. 5)
+    for planted near-duplicates, random pairs, and empty / singleton / identical sets."""
+    w = tiny()
+    sets_l = [w.ids[int(w.offsets[i]):int(w.offsets[i + 1])] for i in range(w.n_sets)]
+    qs_l = [w.q_ids[int(w.q_offsets[i]):int(w.q_offsets[i + 1])] for i in range(len(w.q_offsets) - 1)]
+    sets_l += [np.zeros(0, np.uint32), np.array([5], np.uint32), qs_l[0]]   # empty, singleton, identical
+    qs_l += [np.zeros(0, np.uint32)]                                        # empty query
+    so, si = make_csr(sets_l)
+    qo, qi = make_csr(qs_l)
+    S = og.SetCollection.from_numpy(so, si)
+    Qc = og.SetCollection.from_numpy(qo, qi)
+    rng = np.random.default_rng(7)
+    nq, ns = len(qs_l), len(sets_l)
+    pairs = [(int(q), int(s)) for q, s, _, _ in w.planted]
+    pairs += [(int(rng.integers(nq)), int(rng.integers(ns))) for _ in range(3000)]
+    pairs += [(q, s) for q in (0, nq - 1) for s in (ns - 3, ns - 2, ns - 1)]
+    import torch
+    qa = torch.tensor([p[0] for p in pairs], dtype=torch.int32, device="cuda")
+    sa = torch.tensor([p[1] for p in pairs], dtype=torch.int32, device="cuda")
+    inter, union = og.exact_jaccard_pairs(Qc, S, qa, sa)
+    inter, union = inter.cpu().numpy(), union.cpu().numpy()
+    for i, (q, s) in enumerate(pairs):
+        _, oi, ou = oracle.jaccard(qs_l[q], sets_l[s])
+        assert (int(inter[i]), int(union[i])) == (oi, ou), (q, s)
+    # the planted pairs carry their realised intersection / union (workloads: i = round(2sJ/(1+J)))
+    for i, (q, s, pi, pu) in enumerate(w.planted):
+        assert (int(inter[i]), int(union[i])) == (int(pi), int(pu))
