@@ -307,7 +307,10 @@ oph_status topk_or_threshold_results(const oph_hit *d_in, uint64_t n_in, uint32_
  * S_l = sum_{j<=l} c_j M_j) is >= acc[l-1] stops Similar, <= rej[l-1] stops
  * NotSimilar (acc = UINT64_MAX / rej = -1: never).  weights[j] = c_{j+1}
  * (GOPH: 1).  *l0 = the level the collection scan ends at.  Host only; for
- * tests and diagnostics.  acc/rej hold nlev-1 entries, weights nlev. */
+ * tests and diagnostics.  acc/rej hold nlev-1 entries, weights nlev.  The
+ * planner itself works in 128 bits (HOPH 1:2 on |V| = 2^32: L = 45, weights up
+ * to 3^44); a plan with a value that does not fit these 64-bit outputs
+ * returns OPH_EOVERFLOW here (compare_hoph runs it regardless). */
 oph_status oph_plan_thresholds(uint32_t method, uint32_t nlev, uint32_t kprime, uint32_t a, uint32_t b,
                                uint32_t t_num, uint32_t t_den, double epsilon, uint64_t *acc, int64_t *rej,
                                uint32_t *l0, uint64_t *weights);

@@ -57,11 +57,14 @@ struct MinwiseArgs {
     uint8_t *flags;
 };
 
+typedef unsigned __int128 u128_t;
+typedef __int128 i128_t;
+
 // Survivor list (structure of arrays), one per level parity.
 struct SurvList {
     uint32_t *q;      // global query index
     uint32_t *s;      // local set index
-    uint64_t *state;  // M_c (GOPH) or S_l (HOPH)
+    u128_t *state;    // M_c (GOPH) or S_l (HOPH: up to D k' ~ 2^75 for the 1:2 split of 2^32)
     uint32_t *nmb;    // raw matched bins so far
 };
 
@@ -95,9 +98,9 @@ struct ScanArgs {
     uint32_t nbins_total;   // k for the final verdict's denominator
     uint32_t joint, t_num, t_den;
     uint32_t level;         // groups compared at the end of the scan
-    uint64_t w1;            // state = w1 * raw count (HOPH c_1, else 1)
-    uint64_t acc;           // Similar if state >= acc
-    int64_t rej;            // NotSimilar if state <= rej
+    u128_t w1;              // state = w1 * raw count (HOPH c_1, else 1)
+    uint32_t acc_cnt;       // Similar iff raw count >= acc_cnt (state >= acc <=> count >= ceil(acc / w1))
+    int32_t rej_cnt;        // NotSimilar iff raw count <= rej_cnt (-1: never)
     uint32_t tiles_per_cta;
     OutArgs out;
     SurvList surv;
@@ -149,8 +152,9 @@ struct ProbeArgs {
     uint32_t q_col0;        // global index of the chunk's first query
     uint32_t nq;            // queries in this pass
     uint32_t method, final_, level, joint, t_num, t_den;
-    uint64_t w1, acc;
-    int64_t rej;
+    u128_t w1;              // as ScanArgs
+    uint32_t acc_cnt;
+    int32_t rej_cnt;
     OutArgs out;
     SurvList surv;
     unsigned long long *surv_count;
@@ -171,10 +175,10 @@ struct LevelArgs {
     uint32_t level_last;    // last group processed by this launch (<= nlev)
     uint32_t nlev;          // n (GOPH) or L (HOPH)
     uint32_t kp, joint, t_num, t_den;
-    uint64_t acc[kMaxGroups];  // per-level thresholds, index l-1
-    int64_t rej[kMaxGroups];
-    uint64_t c[kMaxGroups]; // group weights (GOPH: 1)
-    unsigned __int128 lam;  // lcm(1..kp) for the HOPH final verdict
+    u128_t acc[kMaxGroups]; // per-level thresholds on the state, index l-1 (~0: never)
+    i128_t rej[kMaxGroups]; // (-1: never)
+    u128_t c[kMaxGroups];   // group weights (GOPH: 1)
+    u128_t lam;             // lcm(1..kp) for the HOPH final verdict
     SurvList in, out;
     const unsigned long long *count_in;
     unsigned long long *count_out;

@@ -131,9 +131,13 @@ struct Rule {
     }
 };
 
+// Per-level thresholds on the pair state (GOPH: M_c <= n k'; HOPH: S_l = sum c_j M_j,
+// up to D k' ~ 2^75 for the 1:2 split of 2^32): Similar iff state >= acc, NotSimilar
+// iff state <= rej.
+constexpr u128 kNeverAcc = ~(u128)0;
 struct LevelThr {
-    uint64_t acc;  // Similar iff state >= acc (UINT64_MAX: never)
-    int64_t rej;   // NotSimilar iff state <= rej (-1: never)
+    u128 acc;  // kNeverAcc: never
+    i128 rej;  // -1: never
 };
 
 // Compile one level: decide(state) is, by construction, Similar on an upward
@@ -141,44 +145,48 @@ struct LevelThr {
 // decreasing in the state, the lower tail increasing and the upper tail
 // decreasing in x).  Binary search both boundaries, then verify.
 template <class F>
-bool compile_level(F decide, uint64_t smax, bool exhaustive, LevelThr &out) {
-    out.acc = UINT64_MAX;
+bool compile_level(F decide, u128 smax, bool exhaustive, LevelThr &out) {
+    out.acc = kNeverAcc;
     out.rej = -1;
     if (decide(smax) == kSimilar) {
-        uint64_t lo = 0, hi = smax;
+        u128 lo = 0, hi = smax;
         while (lo < hi) {
-            const uint64_t mid = lo + (hi - lo) / 2;
+            const u128 mid = lo + (hi - lo) / 2;
             if (decide(mid) == kSimilar) hi = mid; else lo = mid + 1;
         }
         out.acc = lo;
     }
     if (decide(0) == kNotSimilar) {
-        uint64_t lo = 0, hi = smax;
+        u128 lo = 0, hi = smax;
         while (lo < hi) {
-            const uint64_t mid = lo + (hi - lo + 1) / 2;
+            const u128 mid = lo + (hi - lo + 1) / 2;
             if (decide(mid) == kNotSimilar) lo = mid; else hi = mid - 1;
         }
-        out.rej = (int64_t)lo;
+        out.rej = (i128)lo;
     }
-    auto check = [&](uint64_t s) {
+    auto check = [&](u128 s) {
         const Decision want = decide(s);
-        const Decision got = s >= out.acc ? kSimilar : ((int64_t)s <= out.rej ? kNotSimilar : kContinue);
+        const Decision got = s >= out.acc ? kSimilar : ((i128)s <= out.rej ? kNotSimilar : kContinue);
         return want == got;
     };
     if (exhaustive) {
-        for (uint64_t s = 0; s <= smax; s++)
+        for (u128 s = 0; s <= smax; s++)
             if (!check(s)) return false;
         return true;
     }
     std::mt19937_64 rng(12345);
-    for (uint64_t s = 0; s <= std::min<uint64_t>(smax, 2048); s++)
+    for (u128 s = 0; s <= std::min<u128>(smax, 2048); s++)
         if (!check(s)) return false;
     for (int d = -3; d <= 3; d++) {
-        if (out.acc != UINT64_MAX && (int64_t)out.acc + d >= 0 && out.acc + d <= smax && !check(out.acc + d)) return false;
-        if (out.rej >= 0 && out.rej + d >= 0 && (uint64_t)(out.rej + d) <= smax && !check(out.rej + d)) return false;
+        if (out.acc != kNeverAcc && (i128)out.acc + d >= 0 && (u128)((i128)out.acc + d) <= smax &&
+            !check((u128)((i128)out.acc + d)))
+            return false;
+        if (out.rej >= 0 && out.rej + d >= 0 && (u128)(out.rej + d) <= smax && !check((u128)(out.rej + d))) return false;
     }
-    for (int i = 0; i < 4096; i++)
-        if (!check(rng() % (smax + 1))) return false;
+    for (int i = 0; i < 4096; i++) {
+        const u128 r = ((u128)rng() << 64) | rng();
+        if (!check(r % (smax + 1))) return false;
+    }
     return check(smax);
 }
 
@@ -187,7 +195,7 @@ struct Plan {
     uint32_t nlev = 0;          // n or L
     uint32_t l0 = 0;            // level the scan ends at
     std::vector<LevelThr> thr;  // thr[l-1] for l = 1..nlev-1
-    std::vector<uint64_t> c;    // weights (GOPH: 1)
+    std::vector<u128> c;        // weights (GOPH: 1)
     u128 lam = 1;               // lcm(1..kp)
 };
 
@@ -230,7 +238,7 @@ Plan make_plan(uint32_t method, uint32_t nlev, uint32_t kp, uint32_t a, uint32_t
         const i128 ab = (i128)a + b;
         for (uint32_t j = 1; j < nlev; j++) {
             D *= ab;
-            if (D > ((i128)1 << 62)) { P.st = OPH_EINVAL; return P; }
+            if (D > ((i128)1 << 100)) { P.st = OPH_EINVAL; return P; }
         }
         for (uint32_t j = 1; j <= nlev; j++) {
             i128 w = 1;
@@ -241,33 +249,34 @@ Plan make_plan(uint32_t method, uint32_t nlev, uint32_t kp, uint32_t a, uint32_t
             } else {
                 for (uint32_t t = 1; t < nlev; t++) w *= b;
             }
-            P.c[j - 1] = (uint64_t)w;
+            P.c[j - 1] = (u128)w;
         }
-        if ((i128)t_num * D * kp >= ((i128)1 << 62)) { P.st = OPH_EINVAL; return P; }
+        // the rule's products (num * t_den, k' * t_num * den) stay below t_num t_den D k'
+        if ((i128)t_num * t_den * D * kp >= ((i128)1 << 120)) { P.st = OPH_EINVAL; return P; }
         // the final verdict compares sums over the common denominator lcm(1..k');
         // lam = 0 marks "too large for exact 128-bit arithmetic" (compare_hoph refuses)
         bool of = false;
         P.lam = lcm_upto(kp, of);
         if (of || (u128)t_den * P.lam * (u128)D >= (((u128)1) << 126)) P.lam = 0;
     }
-    P.thr.assign(nlev > 0 ? nlev - 1 : 0, LevelThr{UINT64_MAX, -1});
+    P.thr.assign(nlev > 0 ? nlev - 1 : 0, LevelThr{kNeverAcc, -1});
     P.l0 = nlev;
     i128 csum = 0;
     for (uint32_t l = 1; l < nlev; l++) {
-        csum += P.c[l - 1];
-        const uint64_t smax = (uint64_t)(csum * kp);
+        csum += (i128)P.c[l - 1];
+        const u128 smax = (u128)(csum * kp);
         LevelThr T;
         bool ok;
         if (method == OPH_METHOD_GOPH) {
             // M_ra = (n k' T - M_c) / (n - l) with T = t_num / t_den   (Alg. 1 line 11, R10)
-            auto dec = [&](uint64_t Mc) {
+            auto dec = [&](u128 Mc) {
                 return rule((i128)nlev * kp * t_num - (i128)Mc * t_den, (i128)t_den * (nlev - l));
             };
             ok = compile_level(dec, smax, true, T);
         } else {
             // x = P_r k' = (T D k' - S_l) / W_l, W_l = D - sum_{j<=l} c_j   (Alg. 2 line 10, R19)
             const i128 W = D - csum;
-            auto dec = [&](uint64_t S) { return rule((i128)t_num * D * kp - (i128)t_den * S, (i128)t_den * W); };
+            auto dec = [&](u128 S) { return rule((i128)t_num * D * kp - (i128)t_den * (i128)S, (i128)t_den * W); };
             ok = compile_level(dec, smax, smax <= (1u << 20), T);
         }
         if (!ok) { P.st = OPH_EINVAL; return P; }
@@ -350,7 +359,7 @@ size_t ws_fixed_bytes(uint64_t n_q, uint64_t n_sets, uint32_t nb) {
            align256(ceil_div(nb, 32) * (1ull << probe_log2W(pq)) * 32 * 4) + align256(n_sets * 4);
 }
 
-constexpr uint64_t kSurvBytes = 2 * (4 + 4 + 8 + 4);  // two lists, per entry
+constexpr uint64_t kSurvBytes = 2 * (4 + 4 + 16 + 4);  // two lists, per entry
 
 Ws carve_ws(void *base, uint64_t n_q, uint64_t n_sets, uint32_t nb, uint64_t cap) {
     Ws w{};
@@ -371,13 +380,13 @@ Ws carve_ws(void *base, uint64_t n_q, uint64_t n_sets, uint32_t nb, uint64_t cap
     for (int i = 0; i < 2; i++) {
         w.list[i].q = (uint32_t *)p; p += align256(cap * 4);
         w.list[i].s = (uint32_t *)p; p += align256(cap * 4);
-        w.list[i].state = (uint64_t *)p; p += align256(cap * 8);
+        w.list[i].state = (u128_t *)p; p += align256(cap * 16);
         w.list[i].nmb = (uint32_t *)p; p += align256(cap * 4);
     }
     return w;
 }
 
-size_t surv_region_bytes(uint64_t cap) { return 2 * (align256(cap * 4) * 3 + align256(cap * 8)); }
+size_t surv_region_bytes(uint64_t cap) { return 2 * (align256(cap * 4) * 3 + align256(cap * 16)); }
 
 // largest survivor capacity that fits in ws_bytes
 uint64_t cap_from_ws(size_t ws_bytes, size_t fixed) {
@@ -476,8 +485,16 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     s.out = out;
     s.w1 = 1;
     s.one = 1;
-    s.acc = UINT64_MAX;
-    s.rej = -1;
+    s.acc_cnt = UINT32_MAX;
+    s.rej_cnt = -1;
+    // the scan decides on the raw count of its groups: state = w1 * count, so
+    // state >= acc <=> count >= ceil(acc / w1) and state <= rej <=> count <= floor(rej / w1)
+    auto set_count_thresholds = [&](u128 w1, const LevelThr &T) {
+        s.w1 = w1;
+        s.acc_cnt = T.acc == kNeverAcc ? UINT32_MAX
+                                       : (uint32_t)std::min<u128>((T.acc + w1 - 1) / w1, (u128)UINT32_MAX);
+        s.rej_cnt = T.rej < 0 ? -1 : (int32_t)std::min<i128>(T.rej / (i128)w1, (i128)INT32_MAX);
+    };
     s.nbins_total = nb;
     if (method == OPH_METHOD_FULL || mw) {
         s.nscan = nb;
@@ -489,27 +506,20 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         s.level = plan.l0;
         s.final_ = plan.l0 == nlev;
         s.nw_load = (uint32_t)(s.final_ ? nw : ceil_div(s.nscan, 32));
-        if (!s.final_) {
-            s.acc = plan.thr[plan.l0 - 1].acc;
-            s.rej = plan.thr[plan.l0 - 1].rej;
-        }
+        if (!s.final_) set_count_thresholds(1, plan.thr[plan.l0 - 1]);
     } else {  // HOPH: the scan compares group 1
         s.nscan = kp;
         s.level = 1;
         s.final_ = nlev == 1;  // one group: the HOPH estimator is the OPH estimator of it
         s.nw_load = (uint32_t)ceil_div(kp, 32);
-        if (!s.final_) {
-            s.w1 = plan.c[0];
-            s.acc = plan.thr[0].acc;
-            s.rej = plan.thr[0].rej;
-        }
+        if (!s.final_) set_count_thresholds(plan.c[0], plan.thr[0]);
     }
     if (((size_t)std::min<uint32_t>(s.nscan, 512) + s.nw_load + 1) * 32 * 4 > 227 * 1024) return OPH_EINVAL;
 
     // PROBE applies to threshold results when a pair with no matched bin is
     // decided NotSimilar at the scanned level (final verdicts: N_mb = 0 is
     // never >= T > 0; otherwise the level must reject state 0)
-    const bool probe = p->strategy != OPH_STRATEGY_BRUTE && !out.dense && (s.final_ || s.rej >= 0);
+    const bool probe = p->strategy != OPH_STRATEGY_BRUTE && !out.dense && (s.final_ || s.rej_cnt >= 0);
 
     LevelArgs la{};
     if (levels) {
@@ -589,8 +599,8 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         pr.t_num = s.t_num;
         pr.t_den = s.t_den;
         pr.w1 = s.w1;
-        pr.acc = s.acc;
-        pr.rej = s.rej;
+        pr.acc_cnt = s.acc_cnt;
+        pr.rej_cnt = s.rej_cnt;
         pr.out = out;
         pr.surv = s.surv;
         pr.surv_count = s.surv_count;
@@ -911,11 +921,17 @@ oph_status oph_plan_thresholds(uint32_t method, uint32_t nlev, uint32_t kp, uint
     if (nlev == 0 || nlev > OPH_MAX_GROUPS || kp == 0 || t_den == 0 || t_num == 0 || t_num > t_den) return OPH_EINVAL;
     Plan P = make_plan(method, nlev, kp, a, b, t_num, t_den, eps);
     if (P.st != OPH_OK) return P.st;
+    // 64-bit introspection: plans whose states exceed 64 bits (the 1:2 split of 2^32) report OPH_EOVERFLOW
     for (uint32_t l = 1; l < nlev; l++) {
-        acc[l - 1] = P.thr[l - 1].acc;
-        rej[l - 1] = P.thr[l - 1].rej;
+        const LevelThr &T = P.thr[l - 1];
+        if ((T.acc != kNeverAcc && T.acc >= (u128)UINT64_MAX) || T.rej > (i128)INT64_MAX) return OPH_EOVERFLOW;
+        acc[l - 1] = T.acc == kNeverAcc ? UINT64_MAX : (uint64_t)T.acc;
+        rej[l - 1] = (int64_t)T.rej;
     }
-    for (uint32_t j = 0; j < nlev; j++) weights[j] = P.c[j];
+    for (uint32_t j = 0; j < nlev; j++) {
+        if (P.c[j] > (u128)UINT64_MAX) return OPH_EOVERFLOW;
+        weights[j] = (uint64_t)P.c[j];
+    }
     *l0 = P.l0;
     return OPH_OK;
 }

@@ -587,8 +587,7 @@ __global__ void __launch_bounds__(128, 3) scan_kernel(const __grid_constant__ Sc
 #pragma unroll
                 for (int q = 0; q < B; q++) {
                     const bool valid = sv && (qb0 + q < a.nq);
-                    const uint64_t st = a.w1 * cnt[j][q];
-                    const bool acc = st >= a.acc, rej = (int64_t)st <= a.rej;
+                    const bool acc = cnt[j][q] >= a.acc_cnt, rej = (int32_t)cnt[j][q] <= a.rej_cnt;
                     hit_mask |= (uint32_t)(valid && acc) << q;
                     dec_mask |= (uint32_t)(valid && (acc || rej)) << q;
                     surv_mask |= (uint32_t)(valid && !acc && !rej) << q;
@@ -615,7 +614,7 @@ __global__ void __launch_bounds__(128, 3) scan_kernel(const __grid_constant__ Sc
                         if (sp && idx < a.surv_cap) {  // past capacity: counted, the host redoes the chunk
                             a.surv.q[idx] = (uint32_t)(col0 + q);
                             a.surv.s[idx] = (uint32_t)s;
-                            a.surv.state[idx] = a.w1 * cnt[j][q];
+                            a.surv.state[idx] = a.w1 * cnt[j][q];  // S_1 = c_1 M_1 (GOPH: M_c)
                             a.surv.nmb[idx] = cnt[j][q];
                         }
                     }
@@ -1021,7 +1020,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
             uint32_t q = 0, m = 0, ex = 0, flags = 0, verdict = 0;
             bool surv = false;
             float est = -1.0f;
-            uint64_t st = 0;
+            u128_t st = 0;
             if (has) {
                 q = (x >> 16) - 1u;
                 m = x & 0xFFFFu;
@@ -1044,8 +1043,8 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
                     else est = (float)m / (float)den;
                 } else {
                     st = a.w1 * m;
-                    verdict = st >= a.acc;
-                    surv = !verdict && (int64_t)st > a.rej;
+                    verdict = m >= a.acc_cnt;
+                    surv = !verdict && (int32_t)m > a.rej_cnt;
                     flags = OPH_FLAG_EARLY;
                     if (verdict)
                         for (uint32_t w = 0; w * 32 < a.nscan; w++)
@@ -1111,7 +1110,7 @@ __global__ void __launch_bounds__(256) level_kernel(const __grid_constant__ Leve
         const unsigned long long i = base + (threadIdx.x & 31u);
         bool alive = i < n;
         uint32_t q = 0, s = 0, nmb = 0;
-        uint64_t st = 0;
+        u128_t st = 0;
         if (alive) {
             q = a.in.q[i];
             s = a.in.s[i];
@@ -1142,21 +1141,20 @@ __global__ void __launch_bounds__(256) level_kernel(const __grid_constant__ Leve
                     } else {
                         // HOPH estimator: sum_j c_j m_j / d_j over groups with d_j > 0, exact with
                         // the common denominator lam = lcm(1..kp) (R21, R22)
-                        unsigned __int128 num = 0;
-                        uint64_t csum = 0;
+                        u128_t num = 0, csum = 0;
                         for (uint32_t g = 0; g < a.nlev; g++) {
                             const uint32_t m = (g == l - 1) ? M : group_matches(a, q, s, g);
                             const uint32_t ex = group_excl(a, q, s, g);
                             ex_tot += ex;
                             const uint32_t d = a.kp - ex;
                             if (d == 0) continue;
-                            num += (unsigned __int128)a.c[g] * m * (a.lam / d);
+                            num += a.c[g] * m * (a.lam / d);  // m <= d: num <= D lam (planner-checked)
                             csum += a.c[g];
                         }
                         if (csum == 0) {
                             flags = OPH_FLAG_UNDEFINED;
                         } else {
-                            verdict = num * a.t_den >= (unsigned __int128)a.t_num * a.lam * csum;
+                            verdict = num * a.t_den >= (u128_t)a.t_num * a.lam * csum;
                             est = (float)((double)num / ((double)a.lam * (double)csum));
                         }
                     }
@@ -1167,7 +1165,7 @@ __global__ void __launch_bounds__(256) level_kernel(const __grid_constant__ Leve
                 break;
             }
             const bool acc = alive && st >= a.acc[l - 1];
-            const bool rej = alive && !acc && (int64_t)st <= a.rej[l - 1];
+            const bool rej = alive && !acc && (i128_t)st <= a.rej[l - 1];
             hist_add(a.res.hist, l, (acc || rej) ? 1u : 0u);
             const bool want = a.res.dense ? (acc || rej) : acc;
             if (__any_sync(0xFFFFFFFFu, want)) {

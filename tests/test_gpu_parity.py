@@ -280,13 +280,23 @@ def test_probe_overflow_falls_back_to_brute(method):
         assert (h["n_mb"], h["n_excl"], h["groups"], h["flags"]) == (wr["n_mb"], wr["n_excl"], wr["groups"], wr["flags"])
 
 
-@pytest.mark.parametrize("a,b,V,kp", [(1, 2, 1 << 20, 32), (2, 1, 1 << 20, 32), (3, 1, 1 << 16, 16), (1, 1, 100003, 16)])
+@pytest.mark.parametrize("a,b,V,kp", [(1, 2, 1 << 20, 32), (2, 1, 1 << 20, 32), (3, 1, 1 << 16, 16), (1, 1, 100003, 16),
+                                      (1, 2, 1 << 32, 32), (2, 1, 1 << 32, 32)])
 def test_hoph_split_ratios(a, b, V, kp):
     """(a:b)HOPH variants of P:801-803 (general nominal weights, binary-search
-    group lookup): sketches and dense records bit-exact, both empty modes."""
-    rng = np.random.default_rng(a * 10 + b)
-    sets = [rng.choice(V, size=int(rng.integers(0, 700)), replace=False) for _ in range(300)]
-    qsets = [sets[i] if i % 2 == 0 else rng.choice(V, size=400, replace=False) for i in range(40)]
+    group lookup): sketches and dense records bit-exact, both empty modes.  At
+    |V| = 2^32 the 1:2 split has L = 45 groups and weights up to 3^44, so the
+    pair state S_l needs 128 bits; its threshold lists are
+    checked for both scan strategies too."""
+    rng = np.random.default_rng(a * 10 + b + (V >> 31))
+
+    def draw(n):
+        if V <= 1 << 24:
+            return rng.choice(V, size=n, replace=False)
+        return np.unique(rng.integers(0, V, size=n, dtype=np.uint64))
+
+    sets = [draw(int(rng.integers(0, 700))) for _ in range(300)]
+    qsets = [sets[i] if i % 2 == 0 else draw(400) for i in range(40)]
     offs, ids = make_csr(sets)
     qoffs, qids = make_csr(qsets)
     hier = og.oph_hier_layout_make(V, a, b, kp)
@@ -299,8 +309,12 @@ def test_hoph_split_ratios(a, b, V, kp):
     assert (sh.numpy() == H).all() and (qh.numpy() == QH).all()
     for joint in (False, True):
         kw = dict(t_num=3, t_den=5, eps=1e-4, joint=joint)
-        assert_records_equal(gpu_dense("hoph", qh, sh, layout=hier, **kw),
-                             oracle_records("hoph", QH, H, kprime=kp, L=len(glay), a=a, b=b, **kw), f"hoph {a}:{b}")
+        want = oracle_records("hoph", QH, H, kprime=kp, L=len(glay), a=a, b=b, **kw)
+        assert_records_equal(gpu_dense("hoph", qh, sh, layout=hier, **kw), want, f"hoph {a}:{b}")
+        if V == 1 << 32:
+            for strategy in (og.OPH_STRATEGY_BRUTE, og.OPH_STRATEGY_PROBE):
+                hits = gpu_threshold_hits("hoph", qh, sh, layout=hier, strategy=strategy, **kw)
+                assert [(int(h["query"]), int(h["set_id"])) for h in hits] == oracle.threshold_list(want, 0)
 
 
 def test_empty_inputs():
