@@ -518,3 +518,30 @@ def test_exact_jaccard_pairs_vs_oracle():
     # the planted pairs carry their realised intersection / union (workloads: i = round(2sJ/(1+J)))
     for i, (q, s, pi, pu) in enumerate(w.planted):
         assert (int(inter[i]), int(union[i])) == (int(pi), int(pu))
+
+
+# ----------------------------------------------------------------------------- parameter sweeps
+@pytest.mark.parametrize("kprime", [8, 16, 32])
+@pytest.mark.parametrize("t_num,t_den", [(1, 2), (3, 5), (4, 5), (9, 10)])
+@pytest.mark.parametrize("eps", [1e-3, 1e-5])
+def test_tiny_parameter_sweep(tiny_run, kprime, t_num, t_den, eps):
+    """The paper's sweeps (GOPH group count n = k/k', T in [0.5, 0.9], eps in {1e-3, 1e-5}):
+    GOPH and HOPH dense records bit-exact with the oracle (tiny, k = 64)."""
+    r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    w = r["w"]
+    V = w.vocab_size
+    kw = dict(t_num=t_num, t_den=t_den, eps=eps)
+    lay = og.flat_layout(V, p["k"], kprime)
+    assert_records_equal(gpu_dense("goph", r["qo"], r["so"], layout=lay, **kw),
+                         oracle_records("goph", o["QF"], o["F"], k=p["k"], kprime=kprime, **kw),
+                         f"goph k'={kprime} T={t_num}/{t_den} eps={eps}")
+    hier = og.oph_hier_layout_make(V, 1, 1, kprime)
+    glay = oracle.hoph_layout(V, 1, 1, kprime)
+    seed = p["perm_seed"]
+    _, _, sh = gpu_build(w.offsets, w.ids, V, seed, hier=hier)
+    _, _, qh = gpu_build(w.q_offsets, w.q_ids, V, seed, hier=hier)
+    H = oracle.hoph_sketch(w.offsets, w.ids, V, glay, kprime, seed)
+    QH = oracle.hoph_sketch(w.q_offsets, w.q_ids, V, glay, kprime, seed)
+    assert_records_equal(gpu_dense("hoph", qh, sh, layout=hier, **kw),
+                         oracle_records("hoph", QH, H, kprime=kprime, L=len(glay), **kw),
+                         f"hoph k'={kprime} T={t_num}/{t_den} eps={eps}")
