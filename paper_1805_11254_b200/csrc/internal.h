@@ -183,6 +183,19 @@ struct LevelArgs {
     const unsigned long long *count_in;
     unsigned long long *count_out;
     OutArgs res;
+    // multi-level BRUTE scan (levels_kernel; states < 2^32): all groups of a query
+    // block in one pass, decided group by group
+    const uint32_t *QT;     // prepared queries, bin-major [nb][ldq]
+    uint64_t ldq;
+    uint32_t q_col0, nq;    // query columns [q_col0, q_col0 + nq)
+    // the counter of a pair is state << sh | raw matched bins (sh = 10 for HOPH, 0 for GOPH)
+    uint32_t sh;
+    uint32_t w32[kMaxGroups];    // c_l << sh | (sh ? 1 : 0) (GOPH: 1)
+    uint32_t acc32[kMaxGroups];  // Similar iff counter >= acc32 (= A_l << sh; UINT32_MAX: never)
+    uint32_t rej1[kMaxGroups];   // NotSimilar iff counter < rej1 (= (R_l + 1) << sh; 0: never)
+    uint64_t s_begin;
+    uint32_t tiles_per_cta;
+    uint32_t one;           // = 1, opaque to the compiler (see acc_eq)
 };
 
 struct PrepArgs {
@@ -213,6 +226,7 @@ cudaError_t launch_scan(const ScanArgs &a, uint32_t B, cudaStream_t st);
 cudaError_t launch_table(const TableArgs &a, cudaStream_t st);
 cudaError_t launch_probe(const ProbeArgs &a, cudaStream_t st);
 cudaError_t launch_level(const LevelArgs &a, cudaStream_t st);
+cudaError_t launch_levels_scan(const LevelArgs &a, cudaStream_t st);
 cudaError_t launch_jaccard(const JaccardArgs &a, cudaStream_t st);
 size_t select_temp_bytes(uint64_t n);
 cudaError_t run_select(const oph_hit *in, uint64_t n, uint32_t mode, uint32_t topk, uint32_t k_bins, oph_hit *out,

@@ -3,6 +3,7 @@
 // paper's GOPH / HOPH early-termination rules into exact per-level integer
 // thresholds.  No device arithmetic here.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -521,6 +522,15 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     // never >= T > 0; otherwise the level must reject state 0)
     const bool probe = p->strategy != OPH_STRATEGY_BRUTE && !out.dense && (s.final_ || s.rej_cnt >= 0);
 
+    // BRUTE scans of GOPH / HOPH decide every level in one pass (levels_kernel) when the
+    // pair states fit 32 bits and every group's query values fit shared memory; else
+    // the scan covers the first decidable level and survivors go through level_kernel
+    // (HOPH packs the raw matched-bin count into the counter's low 10 bits: records need it)
+    u128 state_max = 0;
+    for (uint32_t j = 0; levels && j < nlev; j++) state_max += plan.c[j] * kp;
+    const uint32_t msh = method == OPH_METHOD_HOPH ? 10u : 0u;
+    const bool multi = levels && (uint64_t)nlev * kp <= 512 && (state_max << msh) < (u128)UINT32_MAX &&
+                       !getenv("OPHGPU_NO_MULTI_LEVEL_SCAN");  // (the variable: A/B diagnostics only)
     LevelArgs la{};
     if (levels) {
         la.F = Sv->d_values;
@@ -544,6 +554,20 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         }
         la.lam = plan.lam;
         la.res = out;
+        // multi-level BRUTE scan (levels_kernel): states as u32 counters, thresholds on them
+        la.QT = w.QT;
+        la.ldq = w.ldq;
+        la.one = 1;
+        la.sh = msh;
+        for (uint32_t j = 0; j < nlev; j++)
+            la.w32[j] = multi ? (uint32_t)((plan.c[j] << msh) | (msh ? 1u : 0u)) : 0u;
+        for (uint32_t l = 1; l < nlev; l++) {
+            const LevelThr &T = plan.thr[l - 1];
+            const u128 A = T.acc == kNeverAcc ? (u128)UINT32_MAX : T.acc << msh;
+            la.acc32[l - 1] = A >= (u128)UINT32_MAX ? UINT32_MAX : (uint32_t)A;
+            const i128 R1 = T.rej < 0 ? 0 : (T.rej + 1) << msh;
+            la.rej1[l - 1] = R1 >= (i128)UINT32_MAX ? UINT32_MAX : (uint32_t)R1;
+        }
     }
 
     unsigned long long *ovf_count = w.counters + kMaxGroups + 2;
@@ -622,9 +646,17 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
                 return e;
             if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return e;
             if (ovf * 4 > n1) {
-                ScanArgs sr = s;
-                sr.s_begin = n1;
-                if ((e = launch_scan(sr, 32, stream)) != cudaSuccess) return e;
+                if (multi) {
+                    LevelArgs lm = la;
+                    lm.q_col0 = (uint32_t)q0;
+                    lm.nq = (uint32_t)nq;
+                    lm.s_begin = n1;
+                    if ((e = launch_levels_scan(lm, stream)) != cudaSuccess) return e;
+                } else {
+                    ScanArgs sr = s;
+                    sr.s_begin = n1;
+                    if ((e = launch_scan(sr, 32, stream)) != cudaSuccess) return e;
+                }
             } else {
                 pr.s_begin = n1;
                 pr.s_end = n_s;
@@ -648,7 +680,14 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         }
         if (levels || probe)
             if ((e = cudaMemsetAsync(w.counters, 0, (kMaxGroups + 3) * 8, stream)) != cudaSuccess) return e;
-        if (!probe) return launch_scan(s, 32, stream);
+        if (!probe) {
+            if (!multi) return launch_scan(s, 32, stream);
+            LevelArgs lm = la;
+            lm.q_col0 = (uint32_t)q0;
+            lm.nq = (uint32_t)nq;
+            lm.s_begin = 0;
+            return launch_levels_scan(lm, stream);
+        }
         const uint64_t pq = probe_pass(nq);
         for (uint64_t a0 = q0; a0 < q0 + nq; a0 += pq)
             if ((e = probe_pass_run(a0, std::min<uint64_t>(pq, q0 + nq - a0))) != cudaSuccess) return e;

@@ -402,15 +402,16 @@ constexpr uint32_t kScanChunk = 512;  // query bins held in shared memory at onc
 // pipe), `one` a runtime 1 the compiler cannot fold: 2 instructions split
 // over both integer pipes.  (The C++ form compiles to 3 instructions, a
 // predicated IADD puts both on the ALU pipe, which then bounds the scan.)
-__device__ __forceinline__ void acc_eq(uint32_t &c, uint32_t v, uint32_t q, uint32_t one) {
-    asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\t@p mad.lo.u32 %0, %0, %3, %3;\n}"
+__device__ __forceinline__ void acc_eq(uint32_t &c, uint32_t v, uint32_t q, uint32_t one, uint32_t inc) {
+    asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\t@p mad.lo.u32 %0, %0, %3, %4;\n}"
         : "+r"(c)
-        : "r"(v), "r"(q), "r"(one));
+        : "r"(v), "r"(q), "r"(one), "r"(inc));
 }
 
 template <int B, int SPT, int U>
 __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool active, const uint32_t *qs,
-                                          uint32_t b0, uint32_t nb, uint32_t (&cnt)[SPT][B], uint32_t one) {
+                                          uint32_t b0, uint32_t nb, uint32_t (&cnt)[SPT][B], uint32_t one,
+                                          uint32_t inc) {
     // software pipeline: the U bin rows of the next group are loaded while the
     // current group is compared, so HBM latency hides behind ~2*SPT*B*U instructions
     uint32_t b = 0;
@@ -436,10 +437,10 @@ __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool 
                 const uint4 x = q4[q];
 #pragma unroll
                 for (int j = 0; j < SPT; j++) {
-                    acc_eq(cnt[j][4 * q + 0], v[u][j], x.x, one);
-                    acc_eq(cnt[j][4 * q + 1], v[u][j], x.y, one);
-                    acc_eq(cnt[j][4 * q + 2], v[u][j], x.z, one);
-                    acc_eq(cnt[j][4 * q + 3], v[u][j], x.w, one);
+                    acc_eq(cnt[j][4 * q + 0], v[u][j], x.x, one, inc);
+                    acc_eq(cnt[j][4 * q + 1], v[u][j], x.y, one, inc);
+                    acc_eq(cnt[j][4 * q + 2], v[u][j], x.z, one, inc);
+                    acc_eq(cnt[j][4 * q + 3], v[u][j], x.w, one, inc);
                 }
             }
         }
@@ -460,10 +461,10 @@ __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool 
             const uint4 x = q4[q];
 #pragma unroll
             for (int j = 0; j < SPT; j++) {
-                acc_eq(cnt[j][4 * q + 0], v[j], x.x, one);
-                acc_eq(cnt[j][4 * q + 1], v[j], x.y, one);
-                acc_eq(cnt[j][4 * q + 2], v[j], x.z, one);
-                acc_eq(cnt[j][4 * q + 3], v[j], x.w, one);
+                acc_eq(cnt[j][4 * q + 0], v[j], x.x, one, inc);
+                acc_eq(cnt[j][4 * q + 1], v[j], x.y, one, inc);
+                acc_eq(cnt[j][4 * q + 2], v[j], x.z, one, inc);
+                acc_eq(cnt[j][4 * q + 3], v[j], x.w, one, inc);
             }
         }
     }
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(128, 3) scan_kernel(const __grid_constant__ Sc
 
         const uint32_t *Fp = a.F + s0;
         if (one_chunk) {
-            scan_bins<B, SPT, U>(Fp, a.ld, active, qs, 0, a.nscan, cnt, a.one);
+            scan_bins<B, SPT, U>(Fp, a.ld, active, qs, 0, a.nscan, cnt, a.one, a.one);
         } else {
             for (uint32_t c0 = 0; c0 < a.nscan; c0 += kScanChunk) {
                 const uint32_t cn = min(kScanChunk, a.nscan - c0);
@@ -522,7 +523,7 @@ __global__ void __launch_bounds__(128, 3) scan_kernel(const __grid_constant__ Sc
                 for (uint32_t i = threadIdx.x; i < cn * B; i += blockDim.x)
                     qs[i] = a.QT[(uint64_t)(c0 + i / B) * a.ldq + col0 + (i % B)];
                 __syncthreads();
-                scan_bins<B, SPT, U>(Fp, a.ld, active, qs, c0, cn, cnt, a.one);
+                scan_bins<B, SPT, U>(Fp, a.ld, active, qs, c0, cn, cnt, a.one, a.one);
             }
         }
 
@@ -1184,6 +1185,165 @@ __global__ void __launch_bounds__(256) level_kernel(const __grid_constant__ Leve
             a.out.nmb[idx] = nmb;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// K3'' multi-level BRUTE scan for GOPH / HOPH (Alg. 1 / Alg. 2 group by group in
+// registers): the query block's values of every group sit in shared memory; a
+// thread owns SPT sets x 32 queries whose counters ARE the pair states (each
+// matched bin of group l adds the group weight c_l, GOPH c = 1).  After each
+// group the undecided pairs are tested against the level's thresholds; a warp
+// stops as soon as none of its pairs is undecided.  Replaces the survivor
+// lists when the states fit 32 bits and the groups fit shared memory: a
+// high-similarity collection then costs at most one scan instead of per-pair
+// gathers at every level.  The HOPH final estimator (per-group counts) is
+// recomputed by gathers for the pairs that reach the last group.
+// ---------------------------------------------------------------------------
+// cnt[q] for a runtime q without demoting the register array to local memory
+template <int B>
+__device__ __forceinline__ uint32_t pick(const uint32_t (&cnt)[B], uint32_t q) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < B; i++) c = ((uint32_t)i == q) ? cnt[i] : c;
+    return c;
+}
+
+template <int SPT>
+__global__ void __launch_bounds__(128, 3) levels_kernel(const __grid_constant__ LevelArgs a) {
+    constexpr int B = 32, U = 4;
+    extern __shared__ __align__(16) uint32_t lsm[];
+    const uint32_t nbs = a.nlev * a.kp;  // every bin of every group
+    const uint32_t qb0 = blockIdx.x * B;
+    const uint64_t col0 = (uint64_t)a.q_col0 + qb0;
+    for (uint32_t i = threadIdx.x; i < nbs * B; i += blockDim.x)
+        lsm[i] = a.QT[(uint64_t)(i / B) * a.ldq + col0 + (i % B)];
+    __syncthreads();
+    const uint32_t qvalid = qb0 + B <= a.nq ? 0xFFFFFFFFu : ((1u << (a.nq - qb0)) - 1u);
+    const bool hoph = a.method == kHoph;
+    const uint32_t rawmask = a.sh ? (1u << a.sh) - 1u : 0xFFFFFFFFu;
+
+    const uint64_t tile_sets = 128ull * SPT;
+    const uint64_t ntiles = (a.n_sets - a.s_begin + tile_sets - 1) / tile_sets;
+    const uint64_t t_end = min(ntiles, (uint64_t)(blockIdx.y + 1) * a.tiles_per_cta);
+    for (uint64_t t = (uint64_t)blockIdx.y * a.tiles_per_cta; t < t_end; t++) {
+        const uint64_t s0 = a.s_begin + t * tile_sets + threadIdx.x * SPT;
+        const bool active = s0 < a.n_sets;
+        uint32_t cnt[SPT][B];
+        uint32_t alive[SPT];
+#pragma unroll
+        for (int j = 0; j < SPT; j++) {
+            alive[j] = (s0 + j < a.n_sets) ? qvalid : 0u;
+#pragma unroll
+            for (int q = 0; q < B; q++) cnt[j][q] = 0;
+        }
+        const uint32_t *Fp = a.F + s0;
+        for (uint32_t l = 1; l <= a.nlev; l++) {
+            uint32_t any = 0;
+#pragma unroll
+            for (int j = 0; j < SPT; j++) any |= alive[j];
+            if (!__any_sync(0xFFFFFFFFu, any != 0u)) break;  // every pair of this warp is decided
+            scan_bins<B, SPT, U>(Fp, a.ld, active, lsm + (size_t)(l - 1) * a.kp * B, (l - 1) * a.kp, a.kp, cnt,
+                                 a.one, a.w32[l - 1]);
+#pragma unroll
+            for (int j = 0; j < SPT; j++) {
+                const uint32_t s = (uint32_t)(s0 + j);
+                if (l < a.nlev) {
+                    // ---- early termination at level l (thresholds on the state)
+                    uint32_t accm = 0, decm = 0;
+#pragma unroll
+                    for (int q = 0; q < B; q++) {
+                        const bool acc = cnt[j][q] >= a.acc32[l - 1];
+                        const bool rej = cnt[j][q] < a.rej1[l - 1];
+                        accm |= (uint32_t)acc << q;
+                        decm |= (uint32_t)(acc || rej) << q;
+                    }
+                    accm &= alive[j];
+                    decm &= alive[j];
+                    hist_add(a.res.hist, l, __popc(decm));
+                    const uint32_t want = a.res.dense ? decm : accm;
+                    if (__any_sync(0xFFFFFFFFu, want != 0u)) {
+#pragma unroll 1
+                        for (int q = 0; q < B; q++) {
+                            const bool e = (want >> q) & 1u;
+                            const uint32_t qg = (uint32_t)(col0 + q);
+                            uint32_t ex = 0, nmb = 0;
+                            if (e) {
+                                for (uint32_t g = 0; g < l; g++) ex += group_excl(a, qg, s, g);
+                                nmb = pick<B>(cnt[j], q) & rawmask;  // matched bins over groups 1..l
+                            }
+                            emit(a.res, e, qg, s, nmb, ex, l, (accm >> q) & 1u, OPH_FLAG_EARLY, -1.0f);
+                        }
+                    }
+                    alive[j] &= ~decm;
+                } else {
+                    // ---- the last group: the final verdict (GOPH: Eq. 6 over all n k' bins;
+                    // HOPH: the nominal-weight estimator, exact over lam = lcm(1..k'))
+                    hist_add(a.res.hist, a.nlev, __popc(alive[j]));
+                    if (!__any_sync(0xFFFFFFFFu, alive[j] != 0u)) continue;
+#pragma unroll 1
+                    for (int q = 0; q < B; q++) {
+                        const bool al = (alive[j] >> q) & 1u;
+                        const uint32_t qg = (uint32_t)(col0 + q);
+                        uint32_t verdict = 0, flags = 0, ex_tot = 0, nmb = 0;
+                        float est = -1.0f;
+                        if (al) {
+                            if (!hoph) {
+                                nmb = pick<B>(cnt[j], q);
+                                for (uint32_t g = 0; g < a.nlev; g++) ex_tot += group_excl(a, qg, s, g);
+                                const uint32_t den = a.nb - ex_tot;
+                                if (den == 0) {
+                                    flags = OPH_FLAG_UNDEFINED;
+                                } else {
+                                    verdict = (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
+                                    est = (float)nmb / (float)den;
+                                }
+                            } else {
+                                u128_t num = 0, csum = 0;
+                                for (uint32_t g = 0; g < a.nlev; g++) {
+                                    const uint32_t m = group_matches(a, qg, s, g);
+                                    const uint32_t ex = group_excl(a, qg, s, g);
+                                    nmb += m;
+                                    ex_tot += ex;
+                                    const uint32_t d = a.kp - ex;
+                                    if (d == 0) continue;
+                                    num += a.c[g] * m * (a.lam / d);
+                                    csum += a.c[g];
+                                }
+                                if (csum == 0) {
+                                    flags = OPH_FLAG_UNDEFINED;
+                                } else {
+                                    verdict = num * a.t_den >= (u128_t)a.t_num * a.lam * csum;
+                                    est = (float)((double)num / ((double)a.lam * (double)csum));
+                                }
+                            }
+                        }
+                        emit(a.res, al, qg, s, nmb, ex_tot, a.nlev, verdict, flags, est);
+                    }
+                    alive[j] = 0;
+                }
+            }
+        }
+    }
+}
+
+cudaError_t launch_levels_scan(const LevelArgs &a0, cudaStream_t st) {
+    if (a0.n_sets <= a0.s_begin || a0.nq == 0) return cudaSuccess;
+    LevelArgs a = a0;
+    constexpr int SPT = 2;
+    const size_t smem = (size_t)a.nlev * a.kp * 32 * 4;
+    const uint64_t tile_sets = 128ull * SPT;
+    const uint32_t qblocks = (a.nq + 31) / 32;
+    const uint64_t ntiles = (a.n_sets - a.s_begin + tile_sets - 1) / tile_sets;
+    const uint64_t want_y = std::max<uint64_t>(1, (148ull * 3 * 4 + qblocks - 1) / qblocks);
+    uint64_t tpc = std::max<uint64_t>(1, (ntiles + want_y - 1) / want_y);
+    tpc = std::min<uint64_t>(tpc, 64);
+    a.tiles_per_cta = (uint32_t)tpc;
+    const uint64_t gy = (ntiles + tpc - 1) / tpc;
+    if (gy > 65535) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(levels_kernel<SPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    levels_kernel<SPT><<<dim3(qblocks, (unsigned)gy), 128, smem, st>>>(a);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
