@@ -520,3 +520,39 @@ def test_result_lists():
     recs["n_mb"][1] = [0, 5, 0, 0, 0]
     assert oracle.threshold_list(recs, 10) == [(0, 10), (0, 12), (0, 13), (0, 14), (1, 11)]
     assert oracle.topk_list(recs, 8, 2) == [(0, 2), (0, 3), (1, 1)]
+
+
+# ----------------------------------------------------------------------------- shingling (ingestion, 8(f) rank 3)
+def test_shingle_hash_known_answers():
+    """FNV-1a 64 and splitmix64 against their published test vectors."""
+    from oracle import shingle as sh
+    assert sh.fnv1a64(b"") == 0xCBF29CE484222325
+    assert sh.fnv1a64(b"a") == 0xAF63DC4C8601EC8C
+    assert sh.fnv1a64(b"foobar") == 0x85944171F73967E8
+    assert sh.splitmix64_stream(0, 3) == [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F]
+
+
+def test_shingle_tokenizer_and_spec_examples():
+    """Tokens == bytes.lower().split() (independent ASCII whitespace / case rules); SPEC examples."""
+    import random
+    from oracle import shingle as sh
+    rng = random.Random(3)
+    alphabet = b"abcXYZ \t\n\r\x0b\x0c01-'" + bytes([0xC3, 0xA9])
+    for _ in range(300):
+        text = bytes(rng.choice(alphabet) for _ in range(rng.randint(0, 60)))
+        assert sh.tokens(text) == text.lower().split()
+    V = 1 << 32
+    assert len(sh.shingle_text(b"a b a b", 2, V, 7)) == 2            # "a b", "b a"
+    assert sh.shingle_text(b"A\tB  a\nb", 2, V, 7) == sh.shingle_text(b"a b a b", 2, V, 7)
+    assert sh.shingle_text(b"one two", 3, V, 7) == []                  # fewer than w tokens
+    assert sh.shingle_text(b"", 1, V, 7) == []
+    doc = b"the quick brown fox jumps over the lazy dog the quick brown fox"
+    a = sh.shingle_text(doc, 3, V, 11)
+    assert a == sh.shingle_text(doc, 3, V, 11) and a == sorted(set(a))
+    assert len(sh.shingle_text(doc, 1, V, 11)) == len(set(doc.split()))  # w = 1: distinct tokens
+    # the id is the seeded chain mod |V| (spot check of the definition, small |V|)
+    toks = [b"x", b"y"]
+    h = 5
+    for t in toks:
+        h = sh.mix64(h + sh.GOLDEN + sh.fnv1a64(t))
+    assert sh.gram_id(toks, 1000, 5) == h % 1000
