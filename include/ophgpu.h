@@ -285,6 +285,30 @@ oph_status exact_jaccard_pairs(const oph_sets *queries, const oph_sets *sets, co
                                const uint32_t *d_set, uint64_t n_pairs, uint32_t *d_inter, uint32_t *d_union,
                                void *stream);
 
+/* Text shingling -- the ingestion step before oph_build_sketches (SPEC
+ * shingle_text; "convert the words of each document into a set of
+ * fingerprints").  Definition:
+ * tokens are maximal runs of non-whitespace bytes (ASCII space, \t, \n, \v,
+ * \f, \r) with ASCII letters lowercased; tok = FNV-1a 64 of a token; every w
+ * consecutive tokens of a document give h_0 = seed, h_i = mix64(h_{i-1} +
+ * 0x9E3779B97F4A7C15 + tok_i) (mix64 = the splitmix64 finalizer, mod 2^64),
+ * id = h_w mod vocab_size; a document's set is its distinct ids, sorted (a
+ * document with fewer than w tokens gets the empty set).
+ *   d_text [n_bytes] bytes, document d = bytes [d_doc_offsets[d],
+ *   d_doc_offsets[d+1]) with d_doc_offsets[0] = 0 and d_doc_offsets[n_docs]
+ *   = n_bytes (caller-owned device memory).
+ *   Output: the CSR collection oph_build_sketches takes: d_set_offsets
+ *   [n_docs + 1] and d_ids [ids_capacity]; *d_n_ids receives the total id
+ *   count (if it exceeds ids_capacity the ids are truncated; retry).
+ *   Workspace: shingle_workspace_size(n_bytes, n_docs).  Asynchronous, no
+ *   host synchronisation.  Errors: OPH_EINVAL (w == 0, vocab_size == 0 or >
+ *   2^32, NULL pointers, n_bytes >= 2^32), OPH_ENOMEM (workspace too small). */
+oph_status shingle_workspace_size(uint64_t n_bytes, uint64_t n_docs, size_t *bytes);
+oph_status shingle_text(const uint8_t *d_text, const uint64_t *d_doc_offsets, uint64_t n_docs, uint64_t n_bytes,
+                        uint32_t w, uint64_t vocab_size, uint64_t seed, uint64_t *d_set_offsets, uint32_t *d_ids,
+                        uint64_t ids_capacity, unsigned long long *d_n_ids, void *d_ws, size_t ws_bytes,
+                        void *stream);
+
 oph_status oph_select_workspace_size(uint64_t n_in, size_t *bytes);
 
 /* Result lists.  d_in: n_in records (n_in is a

@@ -89,7 +89,7 @@ _lib = None
 EXPORTS = ["oph_status_string", "oph_sketch_ld", "oph_hier_layout_make", "oph_build_sketches",
            "minwise_build_sketches", "oph_workspace_size", "compare_full", "compare_goph", "compare_hoph",
            "compare_minwise", "oph_select_workspace_size", "topk_or_threshold_results", "oph_plan_thresholds",
-           "exact_jaccard_pairs"]
+           "exact_jaccard_pairs", "shingle_workspace_size", "shingle_text"]
 
 
 def lib():
@@ -379,6 +379,29 @@ def exact_jaccard_pairs(queries: SetCollection, sets: SetCollection, query_idx, 
                                      _ptr(set_idx), c_u64(n), _ptr(inter), _ptr(union), _stream(stream)),
            "exact_jaccard_pairs")
     return inter[:n], union[:n]
+
+
+def shingle_text(text, doc_offsets, w: int, vocab_size: int, seed: int, ids_capacity: Optional[int] = None,
+                 ws: Optional[Workspace] = None, stream=None) -> SetCollection:
+    """Documents (uint8 device tensor of bytes + int64 device offsets [n_docs+1], offsets[0] = 0)
+    -> their shingle sets as a CSR SetCollection (include/ophgpu.h shingle_text)."""
+    torch = _torch()
+    n_docs = int(doc_offsets.numel()) - 1
+    n_bytes = int(text.numel())
+    nb = ctypes.c_size_t()
+    _check(lib().shingle_workspace_size(c_u64(n_bytes), c_u64(n_docs), ctypes.byref(nb)), "shingle_workspace_size")
+    buf = (ws or Workspace()).get(nb.value)
+    cap = ids_capacity if ids_capacity is not None else (n_bytes + n_docs) // 2 + 1
+    offsets = torch.zeros((n_docs + 1,), dtype=torch.int64, device="cuda")
+    ids = torch.zeros((max(1, cap),), dtype=torch.int32, device="cuda")
+    n_ids = torch.zeros((1,), dtype=torch.int64, device="cuda")
+    _check(lib().shingle_text(_ptr(text), _ptr(doc_offsets), c_u64(n_docs), c_u64(n_bytes), c_u32(w), c_u64(vocab_size),
+                              c_u64(seed), _ptr(offsets), _ptr(ids), c_u64(cap), _ptr(n_ids), _ptr(buf),
+                              ctypes.c_size_t(buf.numel()), _stream(stream)), "shingle_text")
+    n = int(n_ids.item())
+    if n > cap:
+        raise OphError(OPH_EOVERFLOW, f"shingle_text: {n} ids > capacity {cap}")
+    return SetCollection(offsets, ids[:n])
 
 
 def topk_or_threshold_results(res_in: Results, n_in: int, mode: int, out: Results, topk: int = 0, k_bins: int = 0,

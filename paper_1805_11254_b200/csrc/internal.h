@@ -218,6 +218,18 @@ struct JaccardArgs {
     uint32_t *inter, *uni;
 };
 
+struct ShingleArgs {
+    const uint8_t *text;
+    const uint64_t *doc_offsets;
+    uint64_t n_docs, n_bytes;
+    uint32_t w;
+    uint64_t V, seed;
+    uint64_t *set_offsets;
+    uint32_t *ids;
+    uint64_t ids_cap;
+    unsigned long long *n_ids;
+};
+
 // ---- launchers (ophgpu_kernels.cu); all return cudaGetLastError()
 cudaError_t launch_build(const BuildArgs &a, cudaStream_t st);
 cudaError_t launch_minwise(const MinwiseArgs &a, cudaStream_t st);
@@ -228,6 +240,8 @@ cudaError_t launch_probe(const ProbeArgs &a, cudaStream_t st);
 cudaError_t launch_level(const LevelArgs &a, cudaStream_t st);
 cudaError_t launch_levels_scan(const LevelArgs &a, cudaStream_t st);
 cudaError_t launch_jaccard(const JaccardArgs &a, cudaStream_t st);
+size_t shingle_temp_bytes(uint64_t n_bytes, uint64_t n_docs);
+cudaError_t run_shingle(const ShingleArgs &a, void *ws, size_t ws_bytes, cudaStream_t st);
 size_t select_temp_bytes(uint64_t n);
 cudaError_t run_select(const oph_hit *in, uint64_t n, uint32_t mode, uint32_t topk, uint32_t k_bins, oph_hit *out,
                        unsigned long long *n_out, void *ws, size_t ws_bytes, cudaStream_t st);

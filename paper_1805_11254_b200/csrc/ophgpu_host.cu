@@ -938,6 +938,36 @@ oph_status exact_jaccard_pairs(const oph_sets *queries, const oph_sets *sets, co
     return cuda_status(launch_jaccard(a, (cudaStream_t)stream));
 }
 
+oph_status shingle_workspace_size(uint64_t n_bytes, uint64_t n_docs, size_t *bytes) {
+    if (!bytes || n_bytes >= (1ull << 32) || n_docs >= (1ull << 32)) return OPH_EINVAL;
+    *bytes = shingle_temp_bytes(n_bytes, n_docs);
+    return OPH_OK;
+}
+
+oph_status shingle_text(const uint8_t *d_text, const uint64_t *d_doc_offsets, uint64_t n_docs, uint64_t n_bytes,
+                        uint32_t w, uint64_t vocab_size, uint64_t seed, uint64_t *d_set_offsets, uint32_t *d_ids,
+                        uint64_t ids_capacity, unsigned long long *d_n_ids, void *d_ws, size_t ws_bytes,
+                        void *stream) {
+    if (w == 0 || vocab_size == 0 || vocab_size > (1ull << 32) || n_bytes >= (1ull << 32) || n_docs >= (1ull << 32))
+        return OPH_EINVAL;
+    if (!d_doc_offsets || !d_set_offsets || !d_n_ids || (n_bytes && !d_text) || (ids_capacity && !d_ids))
+        return OPH_EINVAL;
+    if (ws_bytes < shingle_temp_bytes(n_bytes, n_docs) || !d_ws) return OPH_ENOMEM;
+    ShingleArgs a{};
+    a.text = d_text;
+    a.doc_offsets = d_doc_offsets;
+    a.n_docs = n_docs;
+    a.n_bytes = n_bytes;
+    a.w = w;
+    a.V = vocab_size;
+    a.seed = seed;
+    a.set_offsets = d_set_offsets;
+    a.ids = d_ids;
+    a.ids_cap = ids_capacity;
+    a.n_ids = d_n_ids;
+    return cuda_status(run_shingle(a, d_ws, ws_bytes, (cudaStream_t)stream));
+}
+
 oph_status oph_select_workspace_size(uint64_t n_in, size_t *bytes) {
     if (!bytes || n_in >= (1ull << 31)) return OPH_EINVAL;
     *bytes = select_temp_bytes(n_in);

@@ -1659,4 +1659,166 @@ cudaError_t run_select(const oph_hit *in, uint64_t n, uint32_t mode, uint32_t to
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Text shingling (ingestion before the OPH build):
+//   1. byte flags: token start = non-whitespace byte at a document start or
+//      after whitespace; exclusive scan -> token index
+//   2. token starts scattered; per token: document (binary search), FNV-1a 64
+//      of its lowercased bytes
+//   3. per w-gram start: seeded splitmix64 chain over w token hashes, id = h
+//      mod |V|, key = doc << 32 | id (grams crossing a document: key ~0)
+//   4. radix sort of the keys, unique, ids + per-document offsets
+// Sizes use the bound T = (n_bytes + n_docs) / 2 + 1 tokens, so nothing is
+// read back to the host.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool is_ws(uint8_t b) { return b == 32 || (b >= 9 && b <= 13); }
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+struct ShingleWs {
+    uint8_t *docstart;   // [n_bytes]
+    uint32_t *flag;      // [n_bytes + 1]: token-start flags
+    uint32_t *idx;       // [n_bytes + 1]: exclusive scan of flag (idx[n_bytes] = the token count)
+    uint64_t *tok_start; // [T]
+    uint32_t *tok_doc;   // [T]
+    uint64_t *tok_hash;  // [T]
+    uint64_t *k0, *k1;   // [T]
+    unsigned long long *n_unique;
+    void *cub;
+    size_t cub_bytes;
+};
+
+static uint64_t shingle_T(uint64_t n_bytes, uint64_t n_docs) { return (n_bytes + n_docs) / 2 + 1; }
+
+static size_t shingle_cub_bytes(uint64_t n_bytes, uint64_t T) {
+    size_t a = 0, b = 0, c = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, a, (uint32_t *)nullptr, (uint32_t *)nullptr, (int)(n_bytes + 1));
+    cub::DeviceRadixSort::SortKeys(nullptr, b, (uint64_t *)nullptr, (uint64_t *)nullptr, (int)T);
+    cub::DeviceSelect::Unique(nullptr, c, (uint64_t *)nullptr, (uint64_t *)nullptr, (unsigned long long *)nullptr,
+                              (int)T);
+    return std::max(a, std::max(b, c));
+}
+
+size_t shingle_temp_bytes(uint64_t n_bytes, uint64_t n_docs) {
+    const uint64_t T = shingle_T(n_bytes, n_docs);
+    return align_up(n_bytes + 1) + 2 * align_up(4 * (n_bytes + 1)) + align_up(8 * T) + align_up(4 * T) +
+           align_up(8 * T) * 3 + align_up(8) + align_up(shingle_cub_bytes(n_bytes, T));
+}
+
+__global__ void sh_docstart(const uint64_t *doc_offsets, uint64_t n_docs, uint64_t n_bytes, uint8_t *docstart) {
+    for (uint64_t d = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; d < n_docs; d += (uint64_t)gridDim.x * blockDim.x)
+        if (doc_offsets[d] < n_bytes) docstart[doc_offsets[d]] = 1;
+}
+
+__global__ void sh_flags(const uint8_t *text, const uint8_t *docstart, uint64_t n_bytes, uint32_t *flag) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p <= n_bytes;
+         p += (uint64_t)gridDim.x * blockDim.x)
+        flag[p] = p < n_bytes && !is_ws(text[p]) && (docstart[p] || p == 0 || is_ws(text[p - 1]));
+}
+
+__global__ void sh_scatter(const uint32_t *flag, uint64_t n_bytes, const uint32_t *idx, uint64_t *tok_start) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n_bytes;
+         p += (uint64_t)gridDim.x * blockDim.x)
+        if (flag[p]) tok_start[idx[p]] = p;
+}
+
+// per token: its document and the FNV-1a 64 of its lowercased bytes
+__global__ void sh_tokens(const __grid_constant__ ShingleArgs a, const uint32_t *idx, const uint64_t *tok_start,
+                          uint32_t *tok_doc, uint64_t *tok_hash) {
+    const uint64_t n_tok = idx[a.n_bytes];
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n_tok; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t p0 = tok_start[t];
+        uint64_t lo = 0, hi = a.n_docs;  // the last document with offsets[d] <= p0
+        while (lo + 1 < hi) {
+            const uint64_t m = (lo + hi) >> 1;
+            if (a.doc_offsets[m] <= p0) lo = m; else hi = m;
+        }
+        const uint64_t end = a.doc_offsets[lo + 1];
+        uint64_t h = 0xCBF29CE484222325ull;
+        for (uint64_t p = p0; p < end; p++) {
+            uint8_t b = a.text[p];
+            if (is_ws(b)) break;
+            if (b >= 65 && b <= 90) b += 32;
+            h = (h ^ b) * 0x100000001B3ull;
+        }
+        tok_doc[t] = (uint32_t)lo;
+        tok_hash[t] = h;
+    }
+}
+
+// per gram start t < T: key = doc << 32 | id, or ~0 (no gram: past the tokens or crossing a document)
+__global__ void sh_grams(const __grid_constant__ ShingleArgs a, const uint32_t *idx, const uint32_t *tok_doc,
+                         const uint64_t *tok_hash, uint64_t T, uint64_t *keys) {
+    const uint64_t n_tok = idx[a.n_bytes];
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < T; t += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t key = ~0ull;
+        if (t + a.w <= n_tok && tok_doc[t + a.w - 1] == tok_doc[t]) {
+            uint64_t h = a.seed;
+            for (uint32_t i = 0; i < a.w; i++) h = mix64(h + 0x9E3779B97F4A7C15ull + tok_hash[t + i]);
+            key = ((uint64_t)tok_doc[t] << 32) | (uint32_t)(h % a.V);
+        }
+        keys[t] = key;
+    }
+}
+
+// ids and per-document offsets from the sorted distinct keys (the last one may be ~0)
+__global__ void sh_output(const __grid_constant__ ShingleArgs a, const uint64_t *keys, const unsigned long long *n_unique) {
+    uint64_t n = *n_unique;
+    if (n && keys[n - 1] == ~0ull) n--;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    for (uint64_t i = tid; i < n && i < a.ids_cap; i += stride) a.ids[i] = (uint32_t)keys[i];
+    for (uint64_t d = tid; d <= a.n_docs; d += stride) {
+        uint64_t lo = 0, hi = n;  // first key with doc >= d
+        while (lo < hi) {
+            const uint64_t m = (lo + hi) >> 1;
+            if ((keys[m] >> 32) < d) lo = m + 1; else hi = m;
+        }
+        a.set_offsets[d] = d == a.n_docs ? n : lo;
+    }
+    if (tid == 0) *a.n_ids = n;
+}
+
+cudaError_t run_shingle(const ShingleArgs &a, void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (ws_bytes < shingle_temp_bytes(a.n_bytes, a.n_docs)) return cudaErrorInvalidValue;
+    const uint64_t T = shingle_T(a.n_bytes, a.n_docs);
+    char *p = (char *)ws;
+    ShingleWs w;
+    w.docstart = (uint8_t *)p; p += align_up(a.n_bytes + 1);
+    w.flag = (uint32_t *)p; p += align_up(4 * (a.n_bytes + 1));
+    w.idx = (uint32_t *)p; p += align_up(4 * (a.n_bytes + 1));
+    w.tok_start = (uint64_t *)p; p += align_up(8 * T);
+    w.tok_doc = (uint32_t *)p; p += align_up(4 * T);
+    w.tok_hash = (uint64_t *)p; p += align_up(8 * T);
+    w.k0 = (uint64_t *)p; p += align_up(8 * T);
+    w.k1 = (uint64_t *)p; p += align_up(8 * T);
+    w.n_unique = (unsigned long long *)p; p += align_up(8);
+    w.cub = p;
+    w.cub_bytes = align_up(shingle_cub_bytes(a.n_bytes, T));
+    const unsigned gb = (unsigned)std::min<uint64_t>((a.n_bytes + 256) / 256, 148ull * 32);
+    const unsigned gt = (unsigned)std::min<uint64_t>((T + 255) / 256, 148ull * 32);
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(w.docstart, 0, a.n_bytes + 1, st)) != cudaSuccess) return e;
+    sh_docstart<<<(unsigned)std::min<uint64_t>((a.n_docs + 255) / 256 + 1, 148ull * 8), 256, 0, st>>>(
+        a.doc_offsets, a.n_docs, a.n_bytes, w.docstart);
+    sh_flags<<<gb, 256, 0, st>>>(a.text, w.docstart, a.n_bytes, w.flag);
+    size_t tb = w.cub_bytes;
+    // idx[p] = token starts before p (idx[n_bytes] = the token count)
+    if ((e = cub::DeviceScan::ExclusiveSum(w.cub, tb, w.flag, w.idx, (int)(a.n_bytes + 1), st)) != cudaSuccess)
+        return e;
+    sh_scatter<<<gb, 256, 0, st>>>(w.flag, a.n_bytes, w.idx, w.tok_start);
+    sh_tokens<<<gt, 256, 0, st>>>(a, w.idx, w.tok_start, w.tok_doc, w.tok_hash);
+    sh_grams<<<gt, 256, 0, st>>>(a, w.idx, w.tok_doc, w.tok_hash, T, w.k0);
+    tb = w.cub_bytes;
+    if ((e = cub::DeviceRadixSort::SortKeys(w.cub, tb, w.k0, w.k1, (int)T, 0, 64, st)) != cudaSuccess) return e;
+    tb = w.cub_bytes;
+    if ((e = cub::DeviceSelect::Unique(w.cub, tb, w.k1, w.k0, w.n_unique, (int)T, st)) != cudaSuccess) return e;
+    sh_output<<<gt, 256, 0, st>>>(a, w.k0, w.n_unique);
+    return cudaGetLastError();
+}
+
 }  // namespace ophgpu

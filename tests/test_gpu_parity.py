@@ -545,3 +545,47 @@ def test_tiny_parameter_sweep(tiny_run, kprime, t_num, t_den, eps):
     assert_records_equal(gpu_dense("hoph", qh, sh, layout=hier, **kw),
                          oracle_records("hoph", QH, H, kprime=kprime, L=len(glay), **kw),
                          f"hoph k'={kprime} T={t_num}/{t_den} eps={eps}")
+
+
+# ----------------------------------------------------------------------------- shingling (ingestion)
+def _synthetic_docs(rng, n_docs):
+    words = [b"alpha", b"Beta", b"GAMMA", b"delta", b"eps", b"x", b"don't", b"e-mail", b"42", bytes([0xC3, 0xA9, 0x74])]
+    seps = [b" ", b"  ", b"\t", b"\n", b"\r\n", b" \x0b ", b"\x0c"]
+    docs = []
+    for d in range(n_docs):
+        n = int(rng.integers(0, 40)) if d % 7 else int(rng.integers(0, 3))  # some empty / short documents
+        parts = []
+        if rng.random() < 0.3:
+            parts.append(seps[int(rng.integers(len(seps)))])                # leading whitespace
+        for _ in range(n):
+            parts.append(words[int(rng.integers(len(words)))])
+            parts.append(seps[int(rng.integers(len(seps)))])
+        docs.append(b"".join(parts))
+    return docs
+
+
+@pytest.mark.parametrize("w,V", [(1, 1 << 32), (3, 1 << 32), (5, 1 << 20), (2, 1000003)])
+def test_shingle_text_vs_oracle(w, V):
+    """GPU shingling == the oracle's CSR bit-exact (ids strictly increasing per document), and the
+    result feeds the OPH build (end to end: text -> sets -> sketches == oracle sketches)."""
+    import torch
+    from oracle import shingle as osh
+    rng = np.random.default_rng(w * 31 + (V & 0xFF))
+    docs = _synthetic_docs(rng, 600)
+    text = b"".join(docs)
+    offs = np.zeros(len(docs) + 1, dtype=np.int64)
+    np.cumsum([len(d) for d in docs], out=offs[1:])
+    t = torch.from_numpy(np.frombuffer(text, dtype=np.uint8).copy()).cuda()
+    o = torch.from_numpy(offs).cuda()
+    sets = og.shingle_text(t, o, w, V, seed=1234)
+    want_off, want_ids = osh.shingle_docs(docs, w, V, 1234)
+    got_off = sets.offsets.cpu().numpy().astype(np.uint64)
+    got_ids = sets.ids.cpu().numpy().view(np.uint32)
+    assert (got_off == want_off).all()
+    assert (got_ids == want_ids).all()
+    assert want_off[-1] > 0
+    if V >= 4096:
+        hier = og.oph_hier_layout_make(V, 1, 1, 16)
+        flat = og.flat_layout(V, 64, 16)
+        so, _ = og.oph_build_sketches(sets, V, 9, flat=flat, hier=hier)
+        assert (so.numpy() == oracle.oph_sketch(want_off, want_ids, V, 64, 9)).all()
