@@ -4,12 +4,17 @@
 //                                             SURVEY 8(a) a1-a3
 //   K2 minwise_kernel   MinWise sketches, k keyed permutations        a4
 //   -- prep_kernel      query preparation: empty remap + both layouts        a5
-//   K3 scan_kernel      streaming compare of a register-resident query block
-//                       against set tiles; full OPH / MinWise / the first
-//                       decidable GOPH level / HOPH level 1               a6-a9
+//   K3 scan_kernel      BRUTE: streaming compare of a register-resident query
+//                       block against set tiles; full OPH / MinWise / the
+//                       first decidable GOPH level / HOPH level 1          a6-a9
+//   K3' table_kernel +  PROBE: hash join of the collection with per-bin Bloom
+//       join_kernel     filters in shared memory + exact L2 tables           a6-a9
+//   K3'' levels_kernel  BRUTE GOPH / HOPH decided group by group in one pass a7-a8
 //   K4 level_kernel     one GOPH/HOPH level over the compacted survivors;
 //                       the last level applies the final verdict            a7-a8
 //   K6 run_select       threshold / top-k result lists (CUB radix sort)     a10
+//   -- jaccard_kernel   exact Jaccard of hit pairs (quality check)
+//   -- sh_* kernels     text shingling (ingestion before K1)
 //
 // All decisions are exact integer arithmetic against thresholds the host
 // planner compiled from the paper's rules (R23); no floating
@@ -1503,7 +1508,6 @@ cudaError_t launch_probe(const ProbeArgs &a0, cudaStream_t st) {
     const uint64_t waves = (n + 148ull * Rmax - 1) / (148ull * Rmax);
     const uint32_t R = (uint32_t)((((n + 148 * waves - 1) / (148 * waves)) + kJoinTile - 1) / kJoinTile * kJoinTile);
     a.R = R;
-    a.nst = 0;
     const size_t smem = join_layout(W, R).total;
     if (smem > kSmemMax) return cudaErrorInvalidConfiguration;
     const bool mw = a.method == kMinwise;
