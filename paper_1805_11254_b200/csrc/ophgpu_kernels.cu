@@ -119,6 +119,33 @@ __device__ __forceinline__ void build_one(const BuildArgs &a, const RangeBins *g
     }
 }
 
+// The common layout in 32-bit arithmetic (FAST): psi a plain bijection (|V| = 2^w,
+// no cycle walking), flat bins of 2^fsh values (bin = p >> fsh), and the 1:1
+// HOPH split of 2^log2V with L <= 32 groups, taken from the left-aligned
+// t = p << (32 - log2V): g = min(leading ones of t, L - 1); dropping the g ones
+// and the 0 after them (L - 1 ones for the last group) leaves the position inside
+// the group, left-aligned in y, whose top log2kp bits are the bin and the next
+// log2V - sc - log2kp bits the offset.  so_j / sh_j: this set's smem rows.
+template <bool W32>
+__device__ __forceinline__ void build_one_fast(const BuildArgs &a, uint32_t *so_j, uint32_t *sh_j, uint32_t id) {
+    const uint32_t p = psi_pass<W32>(a.psi.kappa, a.psi.mu, a.psi.mask, a.psi.shift, id);
+    {
+        const uint32_t bin = p >> a.flat.shift, off = p & ((1u << a.flat.shift) - 1u);
+        uint32_t *slot = so_j + bin;
+        if (off < *slot) atomicMin(slot, off);
+    }
+    {
+        const uint32_t t = p << (32u - a.log2V);
+        const uint32_t g = min((uint32_t)__clz(~t), a.L - 1u);
+        const uint32_t sc = g + (g + 1u < a.L ? 1u : 0u);
+        const uint32_t y = t << sc;
+        const uint32_t bin = y >> (32u - a.log2kp);
+        const uint32_t off = __funnelshift_rc(y << a.log2kp, 0u, 32u - a.log2V + sc + a.log2kp);
+        uint32_t *hslot = sh_j + g * a.kp + bin;
+        if (off < *hslot) atomicMin(hslot, off);
+    }
+}
+
 // write-out of SB sets' sketches (smem rows of `stride` words, stride = 1 mod 32
 // so that a lane per bin reads the SB sets conflict-free): a warp takes 32
 // consecutive bins; each lane stores its bin's SB values as 128-bit stores of 4
@@ -129,6 +156,27 @@ __device__ __forceinline__ void write_sketch(const uint32_t *src, uint32_t strid
                                              uint32_t *dst, uint32_t *dst_mask, uint64_t ld, uint64_t s0) {
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const bool full = nloc == SB && SB % 4 == 0;
+    if (full && nbins % 32u == 0 && ld < (1ull << 32)) {  // the common tile: straight-line code, 32-bit ld
+        const uint32_t ldw = (uint32_t)ld;
+        for (uint32_t b0 = warp * 32u; b0 < nbins; b0 += nwarps * 32u) {
+            const uint32_t b = b0 + lane;
+            uint32_t v[SB];
+#pragma unroll
+            for (int j = 0; j < SB; j++) v[j] = src[j * stride + b];
+            uint32_t *d = dst + (uint64_t)b * ldw + s0;
+#pragma unroll
+            for (int q = 0; q < SB / 4; q++)
+                *reinterpret_cast<uint4 *>(d + 4 * q) = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            uint32_t mine = 0;
+#pragma unroll
+            for (int j = 0; j < SB; j++) {
+                const uint32_t m = __ballot_sync(0xFFFFFFFFu, v[j] == kEmpty);
+                mine = lane == (uint32_t)j ? m : mine;
+            }
+            if (lane < SB) dst_mask[(uint64_t)(b0 >> 5) * ldw + s0 + lane] = mine;
+        }
+        return;
+    }
     for (uint32_t b0 = warp * 32u; b0 < nbins; b0 += nwarps * 32u) {  // warp-uniform
         const uint32_t b = b0 + lane;
         const bool in = b < nbins;
@@ -157,13 +205,14 @@ __device__ __forceinline__ void write_sketch(const uint32_t *src, uint32_t strid
     }
 }
 
-template <bool W32, int SB>
+template <bool W32, int SB, bool FAST>
 __global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ BuildArgs a) {
     extern __shared__ __align__(16) uint32_t smem_u32[];
     // group table in shared memory: lanes index it divergently, which would
     // serialise on the constant cache if read from the kernel parameters
     __shared__ RangeBins grp[kMaxGroups];
     __shared__ uint64_t offs[33];
+    __shared__ uint32_t loffs[33];  // offsets relative to the tile's first element
     // row strides = 1 mod 32: the write-out reads the SB sets of one bin conflict-free
     const uint32_t kst = (a.k + 31u) / 32u * 32u + 1u;
     const uint32_t nbh = a.L * a.kp;
@@ -175,6 +224,8 @@ __global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ Buil
     const uint64_t s0 = (uint64_t)blockIdx.x * SB;
     const uint32_t nloc = (uint32_t)min((uint64_t)SB, a.n_sets - s0);
     for (uint32_t i = threadIdx.x; i <= nloc; i += blockDim.x) offs[i] = a.offsets[s0 + i];
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i <= nloc; i += blockDim.x) loffs[i] = (uint32_t)(offs[i] - offs[0]);
     if (a.do_hier && !a.hier_pow2_halves)
         for (uint32_t i = threadIdx.x; i < a.L; i += blockDim.x) grp[i] = a.grp[i];
     {
@@ -185,8 +236,29 @@ __global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ Buil
     __syncthreads();
 
     const uint64_t e0 = offs[0], e1 = offs[nloc];
-    constexpr int kU = 4;  // ids in flight per thread
+    constexpr int kU = FAST ? 8 : 4;  // ids in flight per thread
     uint32_t j = 0;
+    if (FAST) {
+        const uint32_t n = (uint32_t)(e1 - e0);
+        const uint32_t *ids = a.ids + e0;
+        uint32_t *so_j = so, *sh_j = sh;
+        for (uint32_t e = threadIdx.x; e < n; e += kU * blockDim.x) {
+            uint32_t id[kU];
+#pragma unroll
+            for (int u = 0; u < kU; u++) id[u] = e + u * blockDim.x < n ? __ldg(ids + e + u * blockDim.x) : 0u;
+#pragma unroll
+            for (int u = 0; u < kU; u++) {
+                const uint32_t eu = e + u * blockDim.x;
+                if (eu >= n) break;
+                if (loffs[j + 1] <= eu) {  // the set owning element eu (empty sets are skipped)
+                    do j++; while (loffs[j + 1] <= eu);
+                    so_j = so + j * kst;
+                    sh_j = sh + j * hst;
+                }
+                build_one_fast<W32>(a, so_j, sh_j, id[u]);
+            }
+        }
+    } else
     for (uint64_t e = e0 + threadIdx.x; e < e1; e += kU * blockDim.x) {
         uint32_t id[kU];
 #pragma unroll
@@ -1412,7 +1484,11 @@ cudaError_t launch_jaccard(const JaccardArgs &a, cudaStream_t st) {
 template <int SB>
 static cudaError_t launch_build_sb(const BuildArgs &a, size_t smem, cudaStream_t st) {
     const uint64_t grid = (a.n_sets + SB - 1) / SB;
-    auto kern = a.psi.mask == 0xFFFFFFFFu ? build_kernel<true, SB> : build_kernel<false, SB>;
+    const bool fast = a.do_flat && a.flat.pow2 && a.flat.start == 0 && a.psi.pow2 && !a.psi.identity && a.do_hier &&
+                      a.hier_pow2_halves && a.L <= 32 && a.log2kp >= 1;
+    const bool w32 = a.psi.mask == 0xFFFFFFFFu;
+    auto kern = fast ? (w32 ? build_kernel<true, SB, true> : build_kernel<false, SB, true>)
+                     : (w32 ? build_kernel<true, SB, false> : build_kernel<false, SB, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)grid, 256, smem, st>>>(a);
