@@ -457,9 +457,12 @@ def run_ours(args):
     peaks, peak_src = load_peaks()
     f_sm = peaks.get("sm_max_mhz", 1965.0) * 1e6
     # ALU pipe (IADD3/LOP3/SHF/min): 16 lanes/clk/SMSP (B300_MICROARCH "rt_SMSP=2"), 148 SM x 4 SMSP;
-    # one psi evaluation + running min needs >= 9.5 ALU-pipe lane-ops at w = 32
+    # one psi evaluation + running min is 9.5 ALU-pipe lane-ops at w = 32 and 10 at w < 32 (the
+    # SASS of minwise_kernel)
     alu_lanes = 148 * 4 * 16 * f_sm
-    psi_peak = alu_lanes / 9.5
+    w_bits = max(1, (V - 1).bit_length())
+    psi_ops = 9.5 if w_bits >= 32 else 10.0
+    psi_peak = alu_lanes / psi_ops
     hbm = peaks["hbm_gbs"] * 1e9
     nnz = int(w.offsets[-1])
     nw_k, nw_h = (k + 31) // 32, (L * hkp + 31) // 32
@@ -483,7 +486,7 @@ def run_ours(args):
     b, a_, pk, u, _ = kern[dom]
     roof = {"kernel": dom, "bound": b, "achieved": a_, "peak": pk, "unit": u, "frac": a_ / pk,
             "traffic": traffic.get(dom), "peak_source": peak_src if b == "hbm" else
-            "derived: 148 SM x 4 SMSP x 16 ALU lanes x sm_max_mhz / 9.5 ALU ops per psi (DESIGN.md)"}
+            f"derived: 148 SM x 4 SMSP x 16 ALU lanes x sm_max_mhz / {psi_ops} ALU ops per psi (DESIGN.md)"}
     per_kernel = {n: {"ms": phase_ms[n], "bound": v[0], "achieved": v[1], "peak": v[2], "unit": v[3],
                       "frac": v[1] / v[2], "bytes": v[4]} for n, v in kern.items()}
     # the PROBE collection scans on their own (CUPTI device time of the join kernels over the

@@ -21,6 +21,7 @@ struct PsiParams {
     uint32_t mu[4];     // odd
     uint32_t identity;  // psi(x) = x
     uint32_t pow2;      // |V| == 2^w: no cycle walking
+    uint32_t hmul, hsh; // w < 32: 2^(32-w) and 32 - w + shift (see psi_pass)
 };
 
 // One range [start, start+len) cut into nb bins by the floor rule.
@@ -55,6 +56,7 @@ struct MinwiseArgs {
     uint32_t k, w;
     uint32_t *mw;
     uint8_t *flags;
+    uint32_t hmul, hsh;  // w < 32: 2^(32-w) and 32 - w + ceil(w/2) (set by launch_minwise)
 };
 
 typedef unsigned __int128 u128_t;

@@ -41,6 +41,8 @@ PsiParams make_psi(uint64_t V, uint64_t seed, uint32_t kind) {
     P.V = V;
     P.mask = (uint32_t)mask;
     P.shift = (w + 1) / 2;
+    P.hmul = w >= 32 ? 1u : (1u << (32 - w));
+    P.hsh = (w >= 32 ? 0u : 32u - w) + P.shift;
     uint64_t st = seed;
     for (int r = 0; r < 4; r++) {
         P.kappa[r] = (uint32_t)(splitmix64_next(st) & mask);

@@ -29,24 +29,31 @@ namespace ophgpu {
 // psi: keyed 4-round bijection of [0, 2^w), cycle-walked into [0, |V|)
 // (DESIGN.md section 4).  W32: w == 32, the mask is a no-op.
 // ---------------------------------------------------------------------------
+// w < 32: one round is y = ((x ^ kappa) mu) mod 2^w, x' = y ^ (y >> s).  The bits
+// of the 32-bit product above w only reach higher bits through later products,
+// so they may stay; only the shift must not pull them down: y >> s =
+// (P 2^(32-w) mod 2^32) >> (32 - w + s), an IMAD (the FMA pipe, idle in the
+// MinWise build) and one SHF instead of an AND and a SHF on the ALU pipe.  The
+// value is masked to w bits once, at the end.  hmul = 2^(32-w) and hsh =
+// 32 - w + s come in as runtime values so the multiply stays an IMAD.
 template <bool W32>
 __device__ __forceinline__ uint32_t psi_pass(const uint32_t (&kappa)[4], const uint32_t (&mu)[4], uint32_t mask,
-                                             uint32_t shift, uint32_t x) {
+                                             uint32_t shift, uint32_t hmul, uint32_t hsh, uint32_t x) {
 #pragma unroll
     for (int r = 0; r < 4; r++) {
         x = (x ^ kappa[r]) * mu[r];
-        if (!W32) x &= mask;
-        x ^= x >> shift;
+        if (W32) x ^= x >> shift;
+        else x ^= (x * hmul) >> hsh;
     }
-    return x;
+    return W32 ? x : (x & mask);
 }
 
 template <bool W32>
 __device__ __forceinline__ uint32_t psi(const PsiParams &P, uint32_t x) {
     if (P.identity) return x;
-    x = psi_pass<W32>(P.kappa, P.mu, P.mask, P.shift, x);
+    x = psi_pass<W32>(P.kappa, P.mu, P.mask, P.shift, P.hmul, P.hsh, x);
     if (!P.pow2)
-        while ((uint64_t)x >= P.V) x = psi_pass<W32>(P.kappa, P.mu, P.mask, P.shift, x);
+        while ((uint64_t)x >= P.V) x = psi_pass<W32>(P.kappa, P.mu, P.mask, P.shift, P.hmul, P.hsh, x);
     return x;
 }
 
@@ -128,7 +135,7 @@ __device__ __forceinline__ void build_one(const BuildArgs &a, const RangeBins *g
 // log2V - sc - log2kp bits the offset.  so_j / sh_j: this set's smem rows.
 template <bool W32>
 __device__ __forceinline__ void build_one_fast(const BuildArgs &a, uint32_t *so_j, uint32_t *sh_j, uint32_t id) {
-    const uint32_t p = psi_pass<W32>(a.psi.kappa, a.psi.mu, a.psi.mask, a.psi.shift, id);
+    const uint32_t p = psi_pass<W32>(a.psi.kappa, a.psi.mu, a.psi.mask, a.psi.shift, a.psi.hmul, a.psi.hsh, id);
     {
         const uint32_t bin = p >> a.flat.shift, off = p & ((1u << a.flat.shift) - 1u);
         uint32_t *slot = so_j + bin;
@@ -329,9 +336,9 @@ __global__ void __launch_bounds__(256) minwise_kernel(const __grid_constant__ Mi
                     const uint64_t lo = max(offs[j], c0), hi = min(offs[j + 1], c0 + cn);
                     uint32_t m = mn[j];
                     for (uint64_t e = lo; e < hi; e++) {
-                        uint32_t x = psi_pass<W32>(kappa, mu, mask, shift, ids[e - c0]);
+                        uint32_t x = psi_pass<W32>(kappa, mu, mask, shift, a.hmul, a.hsh, ids[e - c0]);
                         if (!pow2)
-                            while ((uint64_t)x >= a.V) x = psi_pass<W32>(kappa, mu, mask, shift, x);
+                            while ((uint64_t)x >= a.V) x = psi_pass<W32>(kappa, mu, mask, shift, a.hmul, a.hsh, x);
                         m = min(m, x);
                     }
                     mn[j] = m;
@@ -1516,8 +1523,11 @@ cudaError_t launch_minwise(const MinwiseArgs &a, cudaStream_t st) {
     if (a.n_sets == 0) return cudaSuccess;
     const uint64_t grid = (a.n_sets + kMwSets - 1) / kMwSets;
     const uint32_t threads = a.k >= 256 ? 256 : ((a.k + 31) / 32) * 32;
-    if (a.w >= 32) minwise_kernel<true><<<(unsigned)grid, threads, 0, st>>>(a);
-    else minwise_kernel<false><<<(unsigned)grid, threads, 0, st>>>(a);
+    MinwiseArgs b = a;
+    b.hmul = 1u << (32 - std::min<uint32_t>(a.w, 32));  // (w = 32: unused)
+    b.hsh = (32 - std::min<uint32_t>(a.w, 32)) + (a.w + 1) / 2;
+    if (a.w >= 32) minwise_kernel<true><<<(unsigned)grid, threads, 0, st>>>(b);
+    else minwise_kernel<false><<<(unsigned)grid, threads, 0, st>>>(b);
     return cudaGetLastError();
 }
 
