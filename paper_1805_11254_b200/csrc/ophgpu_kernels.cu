@@ -293,10 +293,9 @@ __global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ Buil
 // splitmix64 stream, R30) and keeps 8 running minima in registers; the
 // sets' ids are staged through shared memory in chunks.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kMwSets = 8;
 constexpr uint32_t kMwChunk = 8192;
 
-template <bool W32>
+template <bool W32, uint32_t kMwSets>
 __global__ void __launch_bounds__(256) minwise_kernel(const __grid_constant__ MinwiseArgs a) {
     __shared__ uint64_t offs[kMwSets + 1];
     __shared__ uint32_t ids[kMwChunk];
@@ -1521,13 +1520,21 @@ cudaError_t launch_build(const BuildArgs &a, cudaStream_t st) {
 
 cudaError_t launch_minwise(const MinwiseArgs &a, cudaStream_t st) {
     if (a.n_sets == 0) return cudaSuccess;
-    const uint64_t grid = (a.n_sets + kMwSets - 1) / kMwSets;
+    // 8 sets per CTA (ids staged once for 8 x k evaluations); a small collection (the
+    // queries) one set per CTA, so that it still covers the 148 SMs
+    const uint32_t sets = a.n_sets >= 148ull * 8 * 4 ? 8u : 1u;
+    const uint64_t grid = (a.n_sets + sets - 1) / sets;
     const uint32_t threads = a.k >= 256 ? 256 : ((a.k + 31) / 32) * 32;
     MinwiseArgs b = a;
     b.hmul = 1u << (32 - std::min<uint32_t>(a.w, 32));  // (w = 32: unused)
     b.hsh = (32 - std::min<uint32_t>(a.w, 32)) + (a.w + 1) / 2;
-    if (a.w >= 32) minwise_kernel<true><<<(unsigned)grid, threads, 0, st>>>(b);
-    else minwise_kernel<false><<<(unsigned)grid, threads, 0, st>>>(b);
+    if (sets == 8) {
+        if (a.w >= 32) minwise_kernel<true, 8><<<(unsigned)grid, threads, 0, st>>>(b);
+        else minwise_kernel<false, 8><<<(unsigned)grid, threads, 0, st>>>(b);
+    } else {
+        if (a.w >= 32) minwise_kernel<true, 1><<<(unsigned)grid, threads, 0, st>>>(b);
+        else minwise_kernel<false, 1><<<(unsigned)grid, threads, 0, st>>>(b);
+    }
     return cudaGetLastError();
 }
 
