@@ -1016,7 +1016,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
             if ((sb + 1) * kJoinTile <= nset && (rb + 1) * kJoinRPT <= rows) {  // full tile (warp-uniform): no checks
 #pragma unroll
                 for (int r = 0; r < (int)kJoinRPT; r++) {
-                    const uint4 x = __ldg(reinterpret_cast<const uint4 *>(Fs + (uint64_t)((uint32_t)r) * ldb));
+                    const uint4 x = __ldcs(reinterpret_cast<const uint4 *>(Fs + (uint64_t)((uint32_t)r) * ldb));
                     v[0 * kJoinRPT + r] = x.x;
                     v[1 * kJoinRPT + r] = x.y;
                     v[2 * kJoinRPT + r] = x.z;
