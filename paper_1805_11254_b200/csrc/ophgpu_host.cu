@@ -531,8 +531,9 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     u128 state_max = 0;
     for (uint32_t j = 0; levels && j < nlev; j++) state_max += plan.c[j] * kp;
     const uint32_t msh = method == OPH_METHOD_HOPH ? 10u : 0u;
-    // (OPHGPU_NO_MULTI_LEVEL_SCAN set: the survivor path always; A/B diagnostics only, read once)
-    static const bool no_multi = getenv("OPHGPU_NO_MULTI_LEVEL_SCAN") != nullptr;
+    // (OPHGPU_NO_MULTI_LEVEL_SCAN set: the survivor path always -- A/B diagnostics and the
+    // parity test of that path)
+    const bool no_multi = getenv("OPHGPU_NO_MULTI_LEVEL_SCAN") != nullptr;
     const bool multi =
         levels && (uint64_t)nlev * kp <= 512 && (state_max << msh) < (u128)UINT32_MAX && !no_multi;
     LevelArgs la{};

@@ -589,3 +589,20 @@ def test_shingle_text_vs_oracle(w, V):
         flat = og.flat_layout(V, 64, 16)
         so, _ = og.oph_build_sketches(sets, V, 9, flat=flat, hier=hier)
         assert (so.numpy() == oracle.oph_sketch(want_off, want_ids, V, 64, 9)).all()
+
+
+@pytest.mark.parametrize("method", ["goph", "hoph"])
+def test_tiny_survivor_path_dense(tiny_run, method, monkeypatch):
+    """The BRUTE survivor-list path (first decidable level + level_kernel), which levels_kernel
+    replaces whenever the states fit 32 bits, stays bit-exact: forced on tiny, dense records."""
+    monkeypatch.setenv("OPHGPU_NO_MULTI_LEVEL_SCAN", "1")
+    r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    if method == "goph":
+        lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+        g = gpu_dense("goph", r["qo"], r["so"], layout=lay, **kw)
+        want = oracle_records("goph", o["QF"], o["F"], k=p["k"], kprime=p["kprime"], **kw)
+    else:
+        g = gpu_dense("hoph", r["qh"], r["sh"], layout=r["hier"], **kw)
+        want = oracle_records("hoph", o["QH"], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw)
+    assert_records_equal(g, want, f"tiny {method} survivor path")
