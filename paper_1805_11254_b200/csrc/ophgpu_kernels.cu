@@ -1572,10 +1572,15 @@ static cudaError_t launch_scan_t(const ScanArgs &a0, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_scan(const ScanArgs &a, uint32_t B, cudaStream_t st) {
+// query block B: 32 queries per thread block of registers, fewer when the chunk has
+// fewer queries (4 / 8 / 16: less wasted work, fewer registers, more CTAs per SM --
+// the small-B end of the HBM-bound -> ALU-bound crossover)
+cudaError_t launch_scan(const ScanArgs &a, uint32_t, cudaStream_t st) {
     if (a.n_sets <= a.s_begin || a.nq == 0) return cudaSuccess;
-    (void)B;
     if (a.set_list) return launch_scan_t<32, 1, true>(a, st);
+    if (a.nq <= 4) return launch_scan_t<4, 2, false>(a, st);
+    if (a.nq <= 8) return launch_scan_t<8, 2, false>(a, st);
+    if (a.nq <= 16) return launch_scan_t<16, 2, false>(a, st);
     return launch_scan_t<32, 2, false>(a, st);
 }
 
