@@ -553,10 +553,17 @@ __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool 
     }
 }
 
+// B >= 16: 3 CTAs/SM (<= 168 registers): 4 spills into the compare loop and 2 CTAs/SM
+// leaves HBM latency exposed (measured on image-like: 294 / 190 / 227 ms for 4 / 3 / 2).
+// B <= 8 (HBM-bound): 8 / 7 CTAs/SM (<= 64 / 72 registers, no spills); the strip read needs
+// ~32 warps per SM to reach the copy bandwidth (scripts/access_bench.cu: 12 / 24 / 32
+// warps per SM stream 3.1-3.9 / 5.1-5.8 / 6.2-6.7 TB/s whatever the loads in flight)
+template <int B>
+constexpr int scan_min_ctas() {
+    return B <= 4 ? 8 : (B <= 8 ? 7 : 3);
+}
 template <int B, int SPT, bool LIST>
-// 3 CTAs/SM (<= 168 registers): 4 spills into the compare loop and 2 CTAs/SM leaves
-// HBM latency exposed (measured on image-like: 294 / 190 / 227 ms for 4 / 3 / 2)
-__global__ void __launch_bounds__(128, 3) scan_kernel(const __grid_constant__ ScanArgs a) {
+__global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __grid_constant__ ScanArgs a) {
     static_assert(!LIST || SPT == 1, "list mode scans one gathered set per thread");
     constexpr int U = 4;  // bins in flight per thread
     extern __shared__ __align__(16) uint32_t sm[];
@@ -1557,10 +1564,13 @@ static cudaError_t launch_scan_t(const ScanArgs &a0, cudaStream_t st) {
         a.tiles_per_cta = 1;
     } else {
         const uint64_t ntiles = (a.n_sets - a.s_begin + tile_sets - 1) / tile_sets;
-        // aim for >= 4 waves of CTAs over 148 SMs, otherwise longest tile runs per CTA
+        // aim for >= 4 waves of CTAs over 148 SMs, otherwise longest tile runs per CTA;
+        // HBM-bound small blocks: one tile per CTA (the hardware's CTA scheduler balances
+        // the tail; a tile is 128 SPT sets x every bin, ~0.1 ms at 8 CTAs/SM)
         const uint64_t want_y = std::max<uint64_t>(1, (148ull * 4 * 4 + qblocks - 1) / qblocks);
-        uint64_t tpc = std::max<uint64_t>(1, (ntiles + want_y - 1) / want_y);
+        uint64_t tpc = B <= 8 ? 1 : std::max<uint64_t>(1, (ntiles + want_y - 1) / want_y);
         tpc = std::min<uint64_t>(tpc, 64);
+        if ((ntiles + tpc - 1) / tpc > 65535) tpc = (ntiles + 65534) / 65535;
         a.tiles_per_cta = (uint32_t)tpc;
         gy = (ntiles + tpc - 1) / tpc;
     }

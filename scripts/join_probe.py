@@ -27,7 +27,11 @@ so, sh = og.oph_build_sketches(sets, V, seed, flat=flat, hier=hier)
 qo, qh = og.oph_build_sketches(qs, V, seed, flat=flat, hier=hier)
 prm = og.params(p["t_num"], p["t_den"], p["eps"], strategy=args.strategy)
 res = og.Results(1 << 22)
-fn = {"full": lambda: og.compare_full(qo, so, flat, prm, res),
+if args.method == "minwise":
+    mw = og.minwise_build_sketches(sets, V, seed, p["mw_k"])
+    qmw = og.minwise_build_sketches(qs, V, seed, p["mw_k"])
+fn = {"minwise": lambda: og.compare_minwise(qmw, mw, prm, res),
+      "full": lambda: og.compare_full(qo, so, flat, prm, res),
       "goph": lambda: og.compare_goph(qo, so, flat, prm, res),
       "hoph": lambda: og.compare_hoph(qh, sh, hier, prm, res)}[args.method]
 torch.cuda.synchronize()

@@ -132,6 +132,27 @@ def test_tiny_threshold_lists(tiny_run, method, strategy):
         assert (h["n_mb"], h["n_excl"], h["groups"], h["flags"]) == (wr["n_mb"], wr["n_excl"], wr["groups"], wr["flags"])
 
 
+@pytest.mark.parametrize("nq", [1, 3, 4, 5, 8, 9, 16, 17, 33])
+@pytest.mark.parametrize("method", ["full", "goph", "hoph", "minwise"])
+def test_tiny_query_blocks(tiny_run, method, nq):
+    """Dense records for 1 .. 33 queries: every register query block of the BRUTE
+    scan (4 / 8 / 16 / 32 queries, the 4- and 8-query blocks at 8 / 7 CTAs per SM)
+    and its partial last block; 33 adds a second 32-query block of one query."""
+    r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    if method in ("full", "goph"):
+        lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+        g = gpu_dense(method, subview(r["qo"], nq), r["so"], layout=lay, **kw)
+        want = oracle_records(method, o["QF"][:nq], o["F"], k=p["k"], kprime=p["kprime"], **kw)
+    elif method == "hoph":
+        g = gpu_dense(method, subview(r["qh"], nq), r["sh"], layout=r["hier"], **kw)
+        want = oracle_records(method, o["QH"][:nq], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw)
+    else:
+        g = gpu_dense(method, subview(r["qmw"], nq), r["mw"], **kw)
+        want = oracle_records(method, o["QMW"][0][:nq], o["MW"][0], qflags=o["QMW"][1][:nq], sflags=o["MW"][1], **kw)
+    assert_records_equal(g, want, f"tiny {method} nq={nq}")
+
+
 @pytest.mark.parametrize("method", ["full", "minwise"])
 def test_tiny_topk(tiny_run, method):
     r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
