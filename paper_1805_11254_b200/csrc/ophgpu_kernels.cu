@@ -553,14 +553,17 @@ __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool 
     }
 }
 
-// B >= 16: 3 CTAs/SM (<= 168 registers): 4 spills into the compare loop and 2 CTAs/SM
-// leaves HBM latency exposed (measured on image-like: 294 / 190 / 227 ms for 4 / 3 / 2).
-// B <= 8 (HBM-bound): 8 / 7 CTAs/SM (<= 64 / 72 registers, no spills); the strip read needs
-// ~32 warps per SM to reach the copy bandwidth (scripts/access_bench.cu: 12 / 24 / 32
-// warps per SM stream 3.1-3.9 / 5.1-5.8 / 6.2-6.7 TB/s whatever the loads in flight)
+// CTAs per SM by query block (no spills at any of them):
+//   B = 32: 3 (<= 168 registers): 4 spills into the compare loop and 2 leaves HBM
+//           latency exposed (image-like: 294 / 190 / 227 ms for 4 / 3 / 2)
+//   B = 16: 5 (96 registers; 1,168 -> 928 us on image-like at Q = 16)
+//   B = 8 / 4 (HBM-bound): 7 / 8 (72 / 64 registers): the bin-major strip read needs
+//           ~32 warps per SM to reach the copy bandwidth (scripts/access_bench.cu:
+//           12 / 24 / 32 warps per SM stream 3.1-3.9 / 5.1-5.8 / 6.2-6.7 TB/s,
+//           whatever the loads in flight per thread)
 template <int B>
 constexpr int scan_min_ctas() {
-    return B <= 4 ? 8 : (B <= 8 ? 7 : 3);
+    return B <= 4 ? 8 : (B <= 8 ? 7 : (B <= 16 ? 5 : 3));
 }
 template <int B, int SPT, bool LIST>
 __global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __grid_constant__ ScanArgs a) {
