@@ -553,17 +553,71 @@ __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool 
     }
 }
 
-// CTAs per SM by query block (no spills at any of them):
-//   B = 32: 3 (<= 168 registers): 4 spills into the compare loop and 2 leaves HBM
-//           latency exposed (image-like: 294 / 190 / 227 ms for 4 / 3 / 2)
-//   B = 16: 5 (96 registers; 1,168 -> 928 us on image-like at Q = 16)
+// The same scan with two 16-bit counters per register (query 2i in the low half,
+// 2i + 1 in the high half; nscan <= 65535, so a half never carries): the predicated
+// IMAD adds 1 or 1 << 16, still 2 instructions per compare, half the counter
+// registers -- more CTAs per SM at every query block.
+template <int B, int SPT, int U>
+__device__ __forceinline__ void scan_bins_packed(const uint32_t *Fp, uint64_t ld, bool active, const uint32_t *qs,
+                                                 uint32_t b0, uint32_t nb, uint32_t (&cp)[SPT][B / 2], uint32_t one,
+                                                 uint32_t hi) {
+    uint32_t b = 0;
+    uint32_t v[U][SPT];
+    auto load_group = [&](uint32_t bb, uint32_t (&dst)[U][SPT]) {
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (active && bb + u < nb) load_vals<SPT>(Fp + (uint64_t)(b0 + bb + u) * ld, dst[u]);
+            else
+#pragma unroll
+                for (int j = 0; j < SPT; j++) dst[u][j] = kEmpty;
+        }
+    };
+    auto compare_row = [&](const uint32_t (&vr)[SPT], uint32_t row) {
+        const uint4 *q4 = reinterpret_cast<const uint4 *>(qs + (size_t)row * B);
+#pragma unroll
+        for (int q = 0; q < B / 4; q++) {
+            const uint4 x = q4[q];
+#pragma unroll
+            for (int j = 0; j < SPT; j++) {
+                acc_eq(cp[j][2 * q + 0], vr[j], x.x, one, one);
+                acc_eq(cp[j][2 * q + 1], vr[j], x.z, one, one);
+                acc_eq(cp[j][2 * q + 0], vr[j], x.y, one, hi);
+                acc_eq(cp[j][2 * q + 1], vr[j], x.w, one, hi);
+            }
+        }
+    };
+    if (U <= nb) load_group(0, v);
+    for (; b + U <= nb; b += U) {
+        uint32_t vn[U][SPT];
+        load_group(b + U, vn);  // past the end: fills kEmpty, never read
+#pragma unroll
+        for (int u = 0; u < U; u++) compare_row(v[u], b + u);
+#pragma unroll
+        for (int u = 0; u < U; u++)
+#pragma unroll
+            for (int j = 0; j < SPT; j++) v[u][j] = vn[u][j];
+    }
+    for (; b < nb; b++) {
+        uint32_t vr[SPT];
+        if (active) load_vals<SPT>(Fp + (uint64_t)(b0 + b) * ld, vr);
+        else
+#pragma unroll
+            for (int j = 0; j < SPT; j++) vr[j] = kEmpty;
+        compare_row(vr, b);
+    }
+}
+
+// CTAs per SM by query block (packed counters, scan_bins_packed):
+//   B = 32: 4 (128 registers, 48 B of spills outside the compare loop; 1,862 us on
+//           image-like at Q = 32 vs 2,013 at 3 CTAs; unpacked 3 CTAs: 1,871)
+//   B = 16: 5 (96 registers; 1,168 -> 913 us on image-like at Q = 16)
 //   B = 8 / 4 (HBM-bound): 7 / 8 (72 / 64 registers): the bin-major strip read needs
 //           ~32 warps per SM to reach the copy bandwidth (scripts/access_bench.cu:
 //           12 / 24 / 32 warps per SM stream 3.1-3.9 / 5.1-5.8 / 6.2-6.7 TB/s,
 //           whatever the loads in flight per thread)
 template <int B>
 constexpr int scan_min_ctas() {
-    return B <= 4 ? 8 : (B <= 8 ? 7 : (B <= 16 ? 5 : 3));
+    return B <= 4 ? 8 : (B <= 8 ? 7 : (B <= 16 ? 5 : 4));
 }
 template <int B, int SPT, bool LIST>
 __global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __grid_constant__ ScanArgs a) {
@@ -600,15 +654,16 @@ __global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __g
         const uint64_t i0 = t * tile_sets + threadIdx.x * SPT;
         const bool active = i0 < n_items;
         const uint64_t s0 = LIST ? (active ? a.set_list[i0] : 0ull) : a.s_begin + i0;
-        uint32_t cnt[SPT][B];
+        uint32_t cp[SPT][B / 2];  // packed counters (scan_bins_packed)
 #pragma unroll
         for (int j = 0; j < SPT; j++)
 #pragma unroll
-            for (int q = 0; q < B; q++) cnt[j][q] = 0;
+            for (int q = 0; q < B / 2; q++) cp[j][q] = 0;
+        const uint32_t hi = a.one << 16;
 
         const uint32_t *Fp = a.F + s0;
         if (one_chunk) {
-            scan_bins<B, SPT, U>(Fp, a.ld, active, qs, 0, a.nscan, cnt, a.one, a.one);
+            scan_bins_packed<B, SPT, U>(Fp, a.ld, active, qs, 0, a.nscan, cp, a.one, hi);
         } else {
             for (uint32_t c0 = 0; c0 < a.nscan; c0 += kScanChunk) {
                 const uint32_t cn = min(kScanChunk, a.nscan - c0);
@@ -616,11 +671,12 @@ __global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __g
                 for (uint32_t i = threadIdx.x; i < cn * B; i += blockDim.x)
                     qs[i] = a.QT[(uint64_t)(c0 + i / B) * a.ldq + col0 + (i % B)];
                 __syncthreads();
-                scan_bins<B, SPT, U>(Fp, a.ld, active, qs, c0, cn, cnt, a.one, a.one);
+                scan_bins_packed<B, SPT, U>(Fp, a.ld, active, qs, c0, cn, cp, a.one, hi);
             }
         }
 
         // ---------------- epilogue: decisions and emission, one set column at a time
+#define CNT(j, q) ((cp[j][(q) >> 1] >> (((q) & 1) * 16)) & 0xFFFFu)
 #pragma unroll
         for (int j = 0; j < SPT; j++) {
             const uint64_t s = s0 + j;
@@ -651,7 +707,7 @@ __global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __g
                         den = a.nbins_total - ex[q];
                         undef = den == 0;
                     }
-                    const uint32_t verdict = !undef && (uint64_t)cnt[j][q] * a.t_den >= (uint64_t)a.t_num * den;
+                    const uint32_t verdict = !undef && (uint64_t)CNT(j, q) * a.t_den >= (uint64_t)a.t_num * den;
                     hit_mask |= (uint32_t)(valid && verdict) << q;
                     dec_mask |= (uint32_t)valid << q;
                 }
@@ -670,9 +726,9 @@ __global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __g
                             undef = den == 0;
                         }
                         const uint32_t verdict = (hit_mask >> q) & 1u;
-                        const float est = undef ? -1.0f : (float)cnt[j][q] / (float)den;
+                        const float est = undef ? -1.0f : (float)CNT(j, q) / (float)den;
                         // an empty MinWise set has no sketch: nothing is compared
-                        const uint32_t nmb = (a.method == kMinwise && undef) ? 0u : cnt[j][q];
+                        const uint32_t nmb = (a.method == kMinwise && undef) ? 0u : CNT(j, q);
                         emit(a.out, valid, (uint32_t)(col0 + q), s, nmb,
                              a.method == kMinwise ? 0u : ex[q], a.level, verdict, undef ? OPH_FLAG_UNDEFINED : 0u, est);
                     }
@@ -681,7 +737,7 @@ __global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __g
 #pragma unroll
                 for (int q = 0; q < B; q++) {
                     const bool valid = sv && (qb0 + q < a.nq);
-                    const bool acc = cnt[j][q] >= a.acc_cnt, rej = (int32_t)cnt[j][q] <= a.rej_cnt;
+                    const bool acc = CNT(j, q) >= a.acc_cnt, rej = (int32_t)CNT(j, q) <= a.rej_cnt;
                     hit_mask |= (uint32_t)(valid && acc) << q;
                     dec_mask |= (uint32_t)(valid && (acc || rej)) << q;
                     surv_mask |= (uint32_t)(valid && !acc && !rej) << q;
@@ -696,7 +752,7 @@ __global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __g
                         if (e)
                             for (uint32_t w = 0; w < a.nw_load; w++)
                                 ex += popc_masked(qe[w * B + q], __ldg(a.E + (uint64_t)w * a.ld + s), a.joint, w, a.nscan);
-                        emit(a.out, (dec_mask >> q) & 1u, (uint32_t)(col0 + q), s, cnt[j][q], ex, a.level,
+                        emit(a.out, (dec_mask >> q) & 1u, (uint32_t)(col0 + q), s, CNT(j, q), ex, a.level,
                              (hit_mask >> q) & 1u, OPH_FLAG_EARLY, -1.0f);
                     }
                 }
@@ -708,8 +764,8 @@ __global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __g
                         if (sp && idx < a.surv_cap) {  // past capacity: counted, the host redoes the chunk
                             a.surv.q[idx] = (uint32_t)(col0 + q);
                             a.surv.s[idx] = (uint32_t)s;
-                            a.surv.state[idx] = a.w1 * cnt[j][q];  // S_1 = c_1 M_1 (GOPH: M_c)
-                            a.surv.nmb[idx] = cnt[j][q];
+                            a.surv.state[idx] = a.w1 * CNT(j, q);  // S_1 = c_1 M_1 (GOPH: M_c)
+                            a.surv.nmb[idx] = CNT(j, q);
                         }
                     }
                 }
@@ -717,6 +773,8 @@ __global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __g
         }
     }
 }
+
+#undef CNT
 
 // ---------------------------------------------------------------------------
 // K3' PROBE: the same scan as a hash join, streaming the collection once per
