@@ -479,6 +479,29 @@ __device__ __forceinline__ void load_vals(const uint32_t *p, uint32_t (&v)[SPT])
     }
 }
 
+// dst[i] = src[(row0 + i / B) * ldq + col0 + i % B] for i < rows * B: a query block's
+// columns of the prepared bin-major query matrix into shared memory, 8 loads in
+// flight per thread (the copy is on every CTA's critical path before its first tile)
+template <int B>
+__device__ __forceinline__ void load_query_block(uint32_t *dst, const uint32_t *src, uint64_t ldq, uint64_t row0,
+                                                 uint64_t col0, uint32_t rows) {
+    constexpr int kIn = 8;
+    const uint32_t n = rows * B;
+    for (uint32_t i0 = 0; i0 < n; i0 += kIn * blockDim.x) {
+        uint32_t t[kIn];
+#pragma unroll
+        for (int u = 0; u < kIn; u++) {
+            const uint32_t i = i0 + u * blockDim.x + threadIdx.x;
+            t[u] = i < n ? __ldg(src + (row0 + i / B) * ldq + col0 + (i % B)) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kIn; u++) {
+            const uint32_t i = i0 + u * blockDim.x + threadIdx.x;
+            if (i < n) dst[i] = t[u];
+        }
+    }
+}
+
 constexpr uint32_t kScanChunk = 512;  // query bins held in shared memory at once
 
 // c += (v == q) as ISETP (ALU pipe) + predicated IMAD c = c*one + one (FMA
@@ -634,11 +657,9 @@ __global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __g
     const uint64_t col0 = (uint64_t)a.q_col0 + qb0;     // column in the prepared arrays
     const bool one_chunk = a.nscan <= kScanChunk;
     if (one_chunk)
-        for (uint32_t i = threadIdx.x; i < a.nscan * B; i += blockDim.x)
-            qs[i] = a.QT[(uint64_t)(i / B) * a.ldq + col0 + (i % B)];
+        load_query_block<B>(qs, a.QT, a.ldq, 0, col0, a.nscan);
     if (a.E)
-        for (uint32_t i = threadIdx.x; i < a.nw_load * B; i += blockDim.x)
-            qe[i] = a.QE[(uint64_t)(i / B) * a.ldq + col0 + (i % B)];
+        load_query_block<B>(qe, a.QE, a.ldq, 0, col0, a.nw_load);
     if (a.method == kMinwise)
         for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) qf[i] = a.qflags[col0 + i];
     __syncthreads();
@@ -668,8 +689,7 @@ __global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __g
             for (uint32_t c0 = 0; c0 < a.nscan; c0 += kScanChunk) {
                 const uint32_t cn = min(kScanChunk, a.nscan - c0);
                 __syncthreads();
-                for (uint32_t i = threadIdx.x; i < cn * B; i += blockDim.x)
-                    qs[i] = a.QT[(uint64_t)(c0 + i / B) * a.ldq + col0 + (i % B)];
+                load_query_block<B>(qs, a.QT, a.ldq, c0, col0, cn);
                 __syncthreads();
                 scan_bins_packed<B, SPT, U>(Fp, a.ld, active, qs, c0, cn, cp, a.one, hi);
             }
@@ -1366,8 +1386,7 @@ __global__ void __launch_bounds__(128, 3) levels_kernel(const __grid_constant__ 
     const uint32_t nbs = a.nlev * a.kp;  // every bin of every group
     const uint32_t qb0 = blockIdx.x * B;
     const uint64_t col0 = (uint64_t)a.q_col0 + qb0;
-    for (uint32_t i = threadIdx.x; i < nbs * B; i += blockDim.x)
-        lsm[i] = a.QT[(uint64_t)(i / B) * a.ldq + col0 + (i % B)];
+    load_query_block<B>(lsm, a.QT, a.ldq, 0, col0, nbs);
     __syncthreads();
     const uint32_t qvalid = qb0 + B <= a.nq ? 0xFFFFFFFFu : ((1u << (a.nq - qb0)) - 1u);
     const bool hoph = a.method == kHoph;
