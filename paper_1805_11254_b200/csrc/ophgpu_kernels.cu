@@ -581,19 +581,13 @@ __device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool 
 // IMAD adds 1 or 1 << 16, still 2 instructions per compare, half the counter
 // registers -- more CTAs per SM at every query block.
 template <int B, int SPT, int U>
-__device__ __forceinline__ void scan_bins_packed(const uint32_t *Fp, uint64_t ld, bool active, const uint32_t *qs,
-                                                 uint32_t b0, uint32_t nb, uint32_t (&cp)[SPT][B / 2], uint32_t one,
-                                                 uint32_t hi) {
-    uint32_t b = 0;
-    uint32_t v[U][SPT];
-    auto load_group = [&](uint32_t bb, uint32_t (&dst)[U][SPT]) {
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            if (active && bb + u < nb) load_vals<SPT>(Fp + (uint64_t)(b0 + bb + u) * ld, dst[u]);
-            else
-#pragma unroll
-                for (int j = 0; j < SPT; j++) dst[u][j] = kEmpty;
-        }
+__device__ __forceinline__ void scan_bins_packed(const uint32_t *Fp, uint32_t ldb, const uint32_t *qs, uint32_t b0,
+                                                 uint32_t nb, uint32_t (&cp)[SPT][B / 2], uint32_t one, uint32_t hi) {
+    // Fp points at a readable column of every row (the caller clamps threads past the
+    // last set), so no load is predicated: row r is one IMAD.WIDE.U32 off the base
+    const char *base = reinterpret_cast<const char *>(Fp);
+    auto load_row = [&](uint32_t r, uint32_t (&dst)[SPT]) {
+        load_vals<SPT>(reinterpret_cast<const uint32_t *>(base + (uint64_t)(b0 + r) * ldb), dst);
     };
     auto compare_row = [&](const uint32_t (&vr)[SPT], uint32_t row) {
         const uint4 *q4 = reinterpret_cast<const uint4 *>(qs + (size_t)row * B);
@@ -609,23 +603,30 @@ __device__ __forceinline__ void scan_bins_packed(const uint32_t *Fp, uint64_t ld
             }
         }
     };
-    if (U <= nb) load_group(0, v);
-    for (; b + U <= nb; b += U) {
-        uint32_t vn[U][SPT];
-        load_group(b + U, vn);  // past the end: fills kEmpty, never read
+    uint32_t b = 0;
+    if (U <= nb) {
+        // software pipeline: the U rows of the next group load while this group compares
+        uint32_t v[U][SPT];
+#pragma unroll
+        for (int u = 0; u < U; u++) load_row(u, v[u]);
+        for (; b + 2 * U <= nb; b += U) {
+            uint32_t vn[U][SPT];
+#pragma unroll
+            for (int u = 0; u < U; u++) load_row(b + U + u, vn[u]);
+#pragma unroll
+            for (int u = 0; u < U; u++) compare_row(v[u], b + u);
+#pragma unroll
+            for (int u = 0; u < U; u++)
+#pragma unroll
+                for (int j = 0; j < SPT; j++) v[u][j] = vn[u][j];
+        }
 #pragma unroll
         for (int u = 0; u < U; u++) compare_row(v[u], b + u);
-#pragma unroll
-        for (int u = 0; u < U; u++)
-#pragma unroll
-            for (int j = 0; j < SPT; j++) v[u][j] = vn[u][j];
+        b += U;
     }
     for (; b < nb; b++) {
         uint32_t vr[SPT];
-        if (active) load_vals<SPT>(Fp + (uint64_t)(b0 + b) * ld, vr);
-        else
-#pragma unroll
-            for (int j = 0; j < SPT; j++) vr[j] = kEmpty;
+        load_row(b, vr);
         compare_row(vr, b);
     }
 }
@@ -682,16 +683,18 @@ __global__ void __launch_bounds__(128, scan_min_ctas<B>()) scan_kernel(const __g
             for (int q = 0; q < B / 2; q++) cp[j][q] = 0;
         const uint32_t hi = a.one << 16;
 
-        const uint32_t *Fp = a.F + s0;
+        // threads past the last item read (and never use) the row's last SPT columns
+        const uint32_t *Fp = a.F + (active ? s0 : a.ld - SPT);
+        const uint32_t ldb = (uint32_t)(a.ld * 4u);  // < 2^32 (launcher)
         if (one_chunk) {
-            scan_bins_packed<B, SPT, U>(Fp, a.ld, active, qs, 0, a.nscan, cp, a.one, hi);
+            scan_bins_packed<B, SPT, U>(Fp, ldb, qs, 0, a.nscan, cp, a.one, hi);
         } else {
             for (uint32_t c0 = 0; c0 < a.nscan; c0 += kScanChunk) {
                 const uint32_t cn = min(kScanChunk, a.nscan - c0);
                 __syncthreads();
                 load_query_block<B>(qs, a.QT, a.ldq, c0, col0, cn);
                 __syncthreads();
-                scan_bins_packed<B, SPT, U>(Fp, a.ld, active, qs, c0, cn, cp, a.one, hi);
+                scan_bins_packed<B, SPT, U>(Fp, ldb, qs, c0, cn, cp, a.one, hi);
             }
         }
 
@@ -1654,7 +1657,7 @@ static cudaError_t launch_scan_t(const ScanArgs &a0, cudaStream_t st) {
         a.tiles_per_cta = (uint32_t)tpc;
         gy = (ntiles + tpc - 1) / tpc;
     }
-    if (gy > 65535) return cudaErrorInvalidConfiguration;
+    if (gy > 65535 || a.ld * 4 > 0xFFFFFFFFull) return cudaErrorInvalidConfiguration;
     cudaError_t e =
         cudaFuncSetAttribute(scan_kernel<B, SPT, LIST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
