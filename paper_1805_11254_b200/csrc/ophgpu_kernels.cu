@@ -515,64 +515,53 @@ __device__ __forceinline__ void acc_eq(uint32_t &c, uint32_t v, uint32_t q, uint
 }
 
 template <int B, int SPT, int U>
-__device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint64_t ld, bool active, const uint32_t *qs,
-                                          uint32_t b0, uint32_t nb, uint32_t (&cnt)[SPT][B], uint32_t one,
-                                          uint32_t inc) {
-    // software pipeline: the U bin rows of the next group are loaded while the
-    // current group is compared, so HBM latency hides behind ~2*SPT*B*U instructions
-    uint32_t b = 0;
-    uint32_t v[U][SPT];
-    auto load_group = [&](uint32_t bb, uint32_t (&dst)[U][SPT]) {
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            if (active && bb + u < nb) load_vals<SPT>(Fp + (uint64_t)(b0 + bb + u) * ld, dst[u]);
-            else
-#pragma unroll
-                for (int j = 0; j < SPT; j++) dst[u][j] = kEmpty;
-        }
+__device__ __forceinline__ void scan_bins(const uint32_t *Fp, uint32_t ldb, const uint32_t *qs, uint32_t b0,
+                                          uint32_t nb, uint32_t (&cnt)[SPT][B], uint32_t one, uint32_t inc) {
+    // Fp points at a readable column of every row (the caller clamps threads past the
+    // last set), so no load is predicated; software pipeline: the U rows of the next
+    // group load while this group compares (HBM latency behind ~2*SPT*B*U instructions)
+    const char *base = reinterpret_cast<const char *>(Fp);
+    auto load_row = [&](uint32_t r, uint32_t (&dst)[SPT]) {
+        load_vals<SPT>(reinterpret_cast<const uint32_t *>(base + (uint64_t)(b0 + r) * ldb), dst);
     };
-    if (U <= nb) load_group(0, v);
-    for (; b + U <= nb; b += U) {
-        uint32_t vn[U][SPT];
-        load_group(b + U, vn);  // past the end: fills kEmpty, never read
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const uint4 *q4 = reinterpret_cast<const uint4 *>(qs + (size_t)(b + u) * B);
-#pragma unroll
-            for (int q = 0; q < B / 4; q++) {
-                const uint4 x = q4[q];
-#pragma unroll
-                for (int j = 0; j < SPT; j++) {
-                    acc_eq(cnt[j][4 * q + 0], v[u][j], x.x, one, inc);
-                    acc_eq(cnt[j][4 * q + 1], v[u][j], x.y, one, inc);
-                    acc_eq(cnt[j][4 * q + 2], v[u][j], x.z, one, inc);
-                    acc_eq(cnt[j][4 * q + 3], v[u][j], x.w, one, inc);
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++)
-#pragma unroll
-            for (int j = 0; j < SPT; j++) v[u][j] = vn[u][j];
-    }
-    for (; b < nb; b++) {
-        uint32_t v[SPT];
-        if (active) load_vals<SPT>(Fp + (uint64_t)(b0 + b) * ld, v);
-        else
-#pragma unroll
-            for (int j = 0; j < SPT; j++) v[j] = kEmpty;
-        const uint4 *q4 = reinterpret_cast<const uint4 *>(qs + (size_t)b * B);
+    auto compare_row = [&](const uint32_t (&vr)[SPT], uint32_t row) {
+        const uint4 *q4 = reinterpret_cast<const uint4 *>(qs + (size_t)row * B);
 #pragma unroll
         for (int q = 0; q < B / 4; q++) {
             const uint4 x = q4[q];
 #pragma unroll
             for (int j = 0; j < SPT; j++) {
-                acc_eq(cnt[j][4 * q + 0], v[j], x.x, one, inc);
-                acc_eq(cnt[j][4 * q + 1], v[j], x.y, one, inc);
-                acc_eq(cnt[j][4 * q + 2], v[j], x.z, one, inc);
-                acc_eq(cnt[j][4 * q + 3], v[j], x.w, one, inc);
+                acc_eq(cnt[j][4 * q + 0], vr[j], x.x, one, inc);
+                acc_eq(cnt[j][4 * q + 1], vr[j], x.y, one, inc);
+                acc_eq(cnt[j][4 * q + 2], vr[j], x.z, one, inc);
+                acc_eq(cnt[j][4 * q + 3], vr[j], x.w, one, inc);
             }
         }
+    };
+    uint32_t b = 0;
+    if (U <= nb) {
+        uint32_t v[U][SPT];
+#pragma unroll
+        for (int u = 0; u < U; u++) load_row(u, v[u]);
+        for (; b + 2 * U <= nb; b += U) {
+            uint32_t vn[U][SPT];
+#pragma unroll
+            for (int u = 0; u < U; u++) load_row(b + U + u, vn[u]);
+#pragma unroll
+            for (int u = 0; u < U; u++) compare_row(v[u], b + u);
+#pragma unroll
+            for (int u = 0; u < U; u++)
+#pragma unroll
+                for (int j = 0; j < SPT; j++) v[u][j] = vn[u][j];
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) compare_row(v[u], b + u);
+        b += U;
+    }
+    for (; b < nb; b++) {
+        uint32_t vr[SPT];
+        load_row(b, vr);
+        compare_row(vr, b);
     }
 }
 
@@ -1409,14 +1398,16 @@ __global__ void __launch_bounds__(128, 3) levels_kernel(const __grid_constant__ 
 #pragma unroll
             for (int q = 0; q < B; q++) cnt[j][q] = 0;
         }
-        const uint32_t *Fp = a.F + s0;
+        // threads past the last set read (and never use) the row's last SPT columns
+        const uint32_t *Fp = a.F + (active ? s0 : a.ld - SPT);
+        const uint32_t ldb = (uint32_t)(a.ld * 4u);  // < 2^32 (launcher)
         for (uint32_t l = 1; l <= a.nlev; l++) {
             uint32_t any = 0;
 #pragma unroll
             for (int j = 0; j < SPT; j++) any |= alive[j];
             if (!__any_sync(0xFFFFFFFFu, any != 0u)) break;  // every pair of this warp is decided
-            scan_bins<B, SPT, U>(Fp, a.ld, active, lsm + (size_t)(l - 1) * a.kp * B, (l - 1) * a.kp, a.kp, cnt,
-                                 a.one, a.w32[l - 1]);
+            scan_bins<B, SPT, U>(Fp, ldb, lsm + (size_t)(l - 1) * a.kp * B, (l - 1) * a.kp, a.kp, cnt, a.one,
+                                 a.w32[l - 1]);
 #pragma unroll
             for (int j = 0; j < SPT; j++) {
                 const uint32_t s = (uint32_t)(s0 + j);
@@ -1512,7 +1503,7 @@ cudaError_t launch_levels_scan(const LevelArgs &a0, cudaStream_t st) {
     tpc = std::min<uint64_t>(tpc, 64);
     a.tiles_per_cta = (uint32_t)tpc;
     const uint64_t gy = (ntiles + tpc - 1) / tpc;
-    if (gy > 65535) return cudaErrorInvalidConfiguration;
+    if (gy > 65535 || a.ld * 4 > 0xFFFFFFFFull) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(levels_kernel<SPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     levels_kernel<SPT><<<dim3(qblocks, (unsigned)gy), 128, smem, st>>>(a);
