@@ -4,7 +4,8 @@
 
 Tiny config: builds (OPH, HOPH, MinWise), every compare in dense and in
 threshold mode with both scan strategies (PROBE incl. its BRUTE list fallback
-and the survivor levels), threshold and top-k selection."""
+and the survivor levels), threshold and top-k selection, the 4 / 8 / 16-query scan blocks, exact Jaccard
+pairs and text shingling."""
 import os
 import sys
 
@@ -50,6 +51,25 @@ def main():
                 out = og.Results(max(n, 1))
                 og.topk_or_threshold_results(r, n, og.OPH_SELECT_THRESHOLD, out)
                 og.topk_or_threshold_results(r, n, og.OPH_SELECT_TOPK, out, topk=3, k_bins=p["mw_k"])
+    # small query blocks of the BRUTE scan (4 / 8 / 16 queries per register block)
+    import dataclasses
+    prm = og.params(p["t_num"], p["t_den"], p["eps"], strategy=og.OPH_STRATEGY_BRUTE)
+    for nq in (3, 8, 13):
+        q = dataclasses.replace(qo, n_sets=nq)
+        for fn in (og.compare_full, og.compare_goph):
+            r = og.Results(nq * so.n_sets, dense=True)
+            fn(q, so, flat, prm, r)
+            total += r.n()
+    # exact Jaccard of some pairs, and the text shingling front end
+    qi = torch.arange(0, 64, dtype=torch.int32, device="cuda") % w.n_queries
+    si = (torch.arange(0, 64, dtype=torch.int32, device="cuda") * 31) % w.n_sets
+    inter, union = og.exact_jaccard_pairs(qs, sets, qi, si)
+    total += int(inter.sum().item())
+    docs = [b"the quick brown fox jumps over the lazy dog", b"", b"  a b  ", b"Lorem ipsum dolor sit amet, consectetur"]
+    text = torch.tensor(list(b"".join(docs)), dtype=torch.uint8, device="cuda")
+    offs = torch.tensor(np.cumsum([0] + [len(d) for d in docs]), dtype=torch.int64, device="cuda")
+    sh_sets = og.shingle_text(text, offs, 3, 1 << 20, 7)
+    total += int(sh_sets.n_sets)
     torch.cuda.synchronize()
     print("sanitize_run ok", total)
 
