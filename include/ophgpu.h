@@ -121,7 +121,22 @@ typedef struct {
     double epsilon;
     uint32_t empty_mode; /* OPH_EMPTY_EITHER | OPH_EMPTY_JOINT */
     uint32_t strategy;   /* OPH_STRATEGY_*: how the collection scan finds matched bins (results identical) */
+    uint32_t variant;    /* OPH_VARIANT_*: the filter rule (compare_goph only; 0 elsewhere) */
 } oph_params;
+
+/* Filter rule of compare_goph.
+ *   PAPER       : Algorithm 1 as read in DESIGN.md R10-R16: the
+ *                 binomial trials of a group are its k' bins.
+ *   EMPTY_AWARE : the empty-aware variant (DESIGN.md
+ *                 E1-E4): the trials are the pair's non-excluded bins (known
+ *                 from the empty masks before any value is compared);
+ *                 M_ra = k' (T D - M_c) / R with D the pair's non-excluded
+ *                 bins, R those not yet compared; Algorithm 1's tests on M_ra
+ *                 unchanged; R = 0 completes the comparison with the full-OPH
+ *                 verdict.  Identical to PAPER when no bin is excluded.  Runs
+ *                 as one register scan over all groups: needs n k' <= 512
+ *                 (OPH_EINVAL otherwise); the strategy field is ignored. */
+enum { OPH_VARIANT_PAPER = 0, OPH_VARIANT_EMPTY_AWARE = 1 };
 
 /* Collection-scan strategies; every strategy returns
  * identical results.

@@ -161,7 +161,8 @@ def compare_full(Q, S, *, t_num, t_den, joint=False, groups=0):
     return out
 
 
-def compare_goph(Q, S, *, n, kprime, t_num, t_den, eps, joint=False, trace=False):
+def compare_goph(Q, S, *, n, kprime, t_num, t_den, eps, joint=False, trace=False, empty_aware=False):
+    """Algorithm 1 (O9); empty_aware: the empty-aware variant (O9e, E1-E4)."""
     Q = np.ascontiguousarray(Q, dtype=np.uint32)
     S = np.ascontiguousarray(S, dtype=np.uint32)
     assert Q.shape[1] == S.shape[1] == n * kprime
@@ -171,7 +172,8 @@ def compare_goph(Q, S, *, n, kprime, t_num, t_den, eps, joint=False, trace=False
     out = _recs(Q.shape[0], S.shape[0])
     tr = np.zeros((Q.shape[0], S.shape[0], n, 2), dtype=np.int64) if trace else None
     lib().orc_compare_goph(_p(Q), _u64(Q.shape[0]), _p(S), _u64(S.shape[0]), _u32(n), _u32(kprime),
-                           ctypes.c_int(int(joint)), _u32(t_num), _u32(t_den), _p(lo), _p(up), _p(out), _p(tr))
+                           ctypes.c_int(int(joint)), _u32(t_num), _u32(t_den), _p(lo), _p(up), _p(out), _p(tr),
+                           ctypes.c_int(int(empty_aware)))
     return (out, tr) if trace else out
 
 

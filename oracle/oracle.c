@@ -347,6 +347,64 @@ static void pair_goph(const uint32_t *q, const uint32_t *s, uint32_t n, uint32_t
 }
 
 /* ------------------------------------------------------------------------ */
+/* O9e empty-aware GOPH (readings E1-E4).
+ *     Algorithm 1 with the binomial trials taken to be the non-excluded bins.
+ *     D = k - N_excl over all n k' bins (the empty masks are known before any
+ *     value is compared, E1); after l groups D_c = non-excluded bins compared,
+ *     R = D - D_c the remaining trials, need = T D - M_c the matches still
+ *     needed for the full-OPH verdict (Eq. 6).  Alg. 1's tests (lines 13-26,
+ *     R11-R16) run unchanged on the requirement per group of k' trials,
+ *     M_ra = k' need / R (E2); with no excluded bin D = n k', R = (n - l) k'
+ *     and M_ra is Alg. 1's (n k' T - M_c) / (n - l) exactly.  R = 0 (every
+ *     remaining bin excluded) completes the comparison: the full-OPH verdict
+ *     and estimate, groups = l (E3).  The last group: the full-OPH verdict.  */
+/* ------------------------------------------------------------------------ */
+static void pair_goph_e(const uint32_t *q, const uint32_t *s, uint32_t n, uint32_t kp, int joint,
+                        uint32_t t_num, uint32_t t_den, const uint8_t *lower_le, const uint8_t *upper_le,
+                        orc_rec *r, int64_t *trace)
+{
+    memset(r, 0, sizeof(*r));
+    const uint32_t k = n * kp;
+    uint32_t excl_all = 0;
+    for (uint32_t b = 0; b < k; b++) excl_all += bin_excluded(q[b], s[b], joint);
+    const int64_t D = (int64_t)k - excl_all; /* E1: the pair's trials */
+    int64_t M_c = 0;
+    uint32_t excl_c = 0;
+    for (uint32_t l = 1; l <= n; l++) {
+        for (uint32_t b = (l - 1) * kp; b < l * kp; b++) {
+            M_c += bin_matched(q[b], s[b]);
+            excl_c += bin_excluded(q[b], s[b], joint);
+        }
+        r->groups = l;
+        const int64_t D_c = (int64_t)l * kp - excl_c;
+        const int64_t R = D - D_c;
+        if (l == n || R == 0) { /* E3: nothing left to compare -- the full-OPH verdict (Eq. 6) */
+            oph_verdict((uint32_t)M_c, excl_all, k, t_num, t_den, r);
+            return;
+        }
+        /* E2: M_ra = k' (T D - M_c) / R = num / den with T = t_num / t_den */
+        int64_t num = (int64_t)kp * ((int64_t)t_num * D - M_c * (int64_t)t_den);
+        int64_t den = (int64_t)t_den * R;
+        if (trace) { trace[2 * (l - 1)] = num; trace[2 * (l - 1) + 1] = den; }
+        r->n_mb = (uint32_t)M_c;
+        r->n_excl = excl_c;
+        r->estimate = -1.0;
+        r->flags = ORC_EARLY;
+        /* Alg. 1 lines 13-26 on M_ra, exactly as pair_goph */
+        if (num <= 0) { r->verdict = 1; return; }
+        if (num > (int64_t)kp * den) { r->verdict = 0; return; }
+        if (num * (int64_t)t_den < (int64_t)kp * t_num * den) {
+            int64_t m = num / den;
+            if (lower_le[m]) { r->verdict = 1; return; }
+        } else {
+            int64_t m = (num + den - 1) / den;
+            if (upper_le[m]) { r->verdict = 0; return; }
+        }
+        r->flags = 0;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* O10 HOPH comparison: Algorithm 2 with the mass balance of
  *     nominal group weights (R19, R21).  Weights w_j = r(1-r)^(j-1) for j<L,
  *     w_L = (1-r)^(L-1), r = a/(a+b) (Lemma 3 with l = L), held as
@@ -525,15 +583,15 @@ void orc_compare_full(const uint32_t *Q, uint64_t n_q, const uint32_t *S, uint64
 
 void orc_compare_goph(const uint32_t *Q, uint64_t n_q, const uint32_t *S, uint64_t n_s, uint32_t n,
                       uint32_t kp, int joint, uint32_t t_num, uint32_t t_den, const uint8_t *lower_le,
-                      const uint8_t *upper_le, orc_rec *out, int64_t *trace)
+                      const uint8_t *upper_le, orc_rec *out, int64_t *trace, int empty_aware)
 {
     uint64_t k = (uint64_t)n * kp;
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t qi = 0; qi < (int64_t)n_q; qi++)
         for (uint64_t si = 0; si < n_s; si++) {
             uint64_t pi = (uint64_t)qi * n_s + si;
-            pair_goph(Q + (uint64_t)qi * k, S + si * k, n, kp, joint, t_num, t_den, lower_le, upper_le,
-                      &out[pi], trace ? trace + 2 * n * pi : NULL);
+            (empty_aware ? pair_goph_e : pair_goph)(Q + (uint64_t)qi * k, S + si * k, n, kp, joint, t_num, t_den,
+                                                    lower_le, upper_le, &out[pi], trace ? trace + 2 * n * pi : NULL);
         }
 }
 

@@ -32,6 +32,7 @@ OPH_SELECT_THRESHOLD, OPH_SELECT_TOPK = 0, 1
 OPH_METHOD_FULL, OPH_METHOD_GOPH, OPH_METHOD_HOPH, OPH_METHOD_MINWISE = range(4)
 OPH_FLAG_UNDEFINED, OPH_FLAG_EARLY = 1, 2
 OPH_STRATEGY_AUTO, OPH_STRATEGY_BRUTE, OPH_STRATEGY_PROBE = 0, 1, 2
+OPH_VARIANT_PAPER, OPH_VARIANT_EMPTY_AWARE = 0, 1
 OPH_EMPTY = 0xFFFFFFFF
 MAX_GROUPS = 64
 
@@ -66,7 +67,8 @@ class oph_sketches(ctypes.Structure):
 
 
 class oph_params(ctypes.Structure):
-    _fields_ = [("t_num", c_u32), ("t_den", c_u32), ("epsilon", c_dbl), ("empty_mode", c_u32), ("strategy", c_u32)]
+    _fields_ = [("t_num", c_u32), ("t_den", c_u32), ("epsilon", c_dbl), ("empty_mode", c_u32), ("strategy", c_u32),
+                ("variant", c_u32)]
 
 
 class oph_results(ctypes.Structure):
@@ -151,8 +153,10 @@ def flat_layout(vocab_size: int, k: int, kprime: int) -> oph_flat_layout:
     return oph_flat_layout(vocab_size, k, kprime)
 
 
-def params(t_num: int, t_den: int, epsilon: float, joint: bool = False, strategy: int = 0) -> oph_params:
-    return oph_params(t_num, t_den, epsilon, OPH_EMPTY_JOINT if joint else OPH_EMPTY_EITHER, strategy)
+def params(t_num: int, t_den: int, epsilon: float, joint: bool = False, strategy: int = 0,
+           variant: int = 0) -> oph_params:
+    """Filter parameters; variant = OPH_VARIANT_EMPTY_AWARE selects the empty-aware GOPH rule."""
+    return oph_params(t_num, t_den, epsilon, OPH_EMPTY_JOINT if joint else OPH_EMPTY_EITHER, strategy, variant)
 
 
 def plan_thresholds(method: int, nlev: int, kprime: int, t_num: int, t_den: int, epsilon: float, a: int = 1, b: int = 1):

@@ -197,6 +197,11 @@ struct LevelArgs {
     uint64_t s_begin;
     uint32_t tiles_per_cta;
     uint32_t one;           // = 1, opaque to the compiler (see acc_eq)
+    // empty-aware GOPH (levels_e_kernel, E1-E4)
+    uint32_t eaware;
+    const uint32_t *QE;     // query empty masks, bin-major [nw][ldq]
+    uint32_t ma1;           // #{m : P(X <= m) <= eps}, X ~ Bin(k', T) (0: never Similar by the tail)
+    uint32_t mr1;           // min{m : P(X >= m) <= eps} - 1
 };
 
 struct PrepArgs {

@@ -410,7 +410,10 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     oph_status st;
     if ((st = check_view(Qv, !mw, mw)) || (st = check_view(Sv, !mw, mw)) || (st = check_params(p))) return st;
     if (!res || !res->d_hits || !res->d_count || res->mode > OPH_RES_DENSE) return OPH_EINVAL;
-    if (p->strategy > OPH_STRATEGY_PROBE) return OPH_EINVAL;
+    if (p->strategy > OPH_STRATEGY_PROBE || p->variant > OPH_VARIANT_EMPTY_AWARE) return OPH_EINVAL;
+    // the empty-aware GOPH rule (E1-E4) runs as one register scan of every group
+    const bool ea = p->variant == OPH_VARIANT_EMPTY_AWARE;
+    if (ea && method != OPH_METHOD_GOPH) return OPH_EINVAL;
     if (Qv->seed != Sv->seed || Qv->vocab_size != Sv->vocab_size || Qv->n_bins != Sv->n_bins) return OPH_EINCOMPAT;
     const uint32_t nb = Qv->n_bins;
     const uint32_t nw = (uint32_t)ceil_div(nb, 32);
@@ -428,13 +431,14 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         plan = make_plan(method, nlev, kp, a, b, p->t_num, p->t_den, p->epsilon);
         if (plan.st != OPH_OK) return plan.st;
         if (method == OPH_METHOD_HOPH && nlev > 1 && plan.lam == 0) return OPH_EINVAL;
+        if (ea && (uint64_t)nlev * kp > 512) return OPH_EINVAL;
     }
 
     const size_t fixed = ws_fixed_bytes(n_q, n_s, nb);
     uint64_t chunk = ceil_div(n_q, 32) * 32;
     uint64_t cap = 0;
-    const bool levels = (method == OPH_METHOD_GOPH || method == OPH_METHOD_HOPH) && plan.l0 < nlev;
-    if (levels) {
+    const bool levels = (method == OPH_METHOD_GOPH || method == OPH_METHOD_HOPH) && (plan.l0 < nlev || ea);
+    if (levels && !ea) {  // (the empty-aware scan decides in registers: no survivor lists)
         cap = cap_from_ws(ws_bytes, fixed);
         const uint64_t fit = (cap / n_s) / 32 * 32;
         if (fit < 32) return OPH_ENOMEM;
@@ -522,7 +526,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     // PROBE applies to threshold results when a pair with no matched bin is
     // decided NotSimilar at the scanned level (final verdicts: N_mb = 0 is
     // never >= T > 0; otherwise the level must reject state 0)
-    const bool probe = p->strategy != OPH_STRATEGY_BRUTE && !out.dense && (s.final_ || s.rej_cnt >= 0);
+    const bool probe = p->strategy != OPH_STRATEGY_BRUTE && !out.dense && (s.final_ || s.rej_cnt >= 0) && !ea;
 
     // BRUTE scans of GOPH / HOPH decide every level in one pass (levels_kernel) when the
     // pair states fit 32 bits and every group's query values fit shared memory; else
@@ -535,7 +539,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     // parity test of that path)
     const bool no_multi = getenv("OPHGPU_NO_MULTI_LEVEL_SCAN") != nullptr;
     const bool multi =
-        levels && (uint64_t)nlev * kp <= 512 && (state_max << msh) < (u128)UINT32_MAX && !no_multi;
+        levels && (uint64_t)nlev * kp <= 512 && (((state_max << msh) < (u128)UINT32_MAX && !no_multi) || ea);
     LevelArgs la{};
     if (levels) {
         la.F = Sv->d_values;
@@ -559,6 +563,25 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         }
         la.lam = plan.lam;
         la.res = out;
+        if (ea) {
+            // Alg. 1's tail tests on M_ra reduce to two integers: floor(M_ra) <= m_a <=> M_ra < ma1
+            // and ceil(M_ra) >= m_r <=> M_ra > mr1 (lower_le / upper_le are monotone)
+            std::vector<uint8_t> lo, up;
+            const oph_status ts = small_prob_tables(kp, p->t_num, p->t_den, p->epsilon, lo, up);
+            if (ts != OPH_OK) return ts;
+            uint32_t ma1 = 0, mr = kp + 1;
+            while (ma1 <= kp && lo[ma1]) ma1++;
+            while (mr > 0 && up[mr - 1]) mr--;
+            for (uint32_t m = 0; m <= kp; m++)
+                if (lo[m] != (m < ma1)) return OPH_EINVAL;
+            for (uint32_t m = 0; m <= kp + 1; m++)
+                if (up[m] != (m >= mr)) return OPH_EINVAL;
+            if (mr == 0) return OPH_EINVAL;  // P(X >= 0) = 1 > eps
+            la.eaware = 1;
+            la.QE = w.QE;
+            la.ma1 = ma1;
+            la.mr1 = mr - 1;
+        }
         // multi-level BRUTE scan (levels_kernel): states as u32 counters, thresholds on them
         la.QT = w.QT;
         la.ldq = w.ldq;
@@ -717,7 +740,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         for (uint64_t a0 = q0; a0 < q1; a0 += chunk) {
             cudaError_t e = scan_chunk(a0, std::min<uint64_t>(chunk, q1 - a0));
             if (e != cudaSuccess) return e;
-            if (levels && (e = level_chunk()) != cudaSuccess) return e;
+            if (levels && !ea && (e = level_chunk()) != cudaSuccess) return e;
         }
         return cudaSuccess;
     };

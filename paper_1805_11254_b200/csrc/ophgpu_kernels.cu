@@ -1490,11 +1490,135 @@ __global__ void __launch_bounds__(128, 3) levels_kernel(const __grid_constant__ 
     }
 }
 
+// ---------------------------------------------------------------------------
+// K3e empty-aware GOPH (E1-E4): Alg. 1 with the
+// binomial trials taken to be the pair's non-excluded bins.  The same register
+// scan as levels_kernel; a pair's state packs three 10-bit fields,
+//   D << 20 | D_c << 10 | M_c   (nb <= 512, so no field carries),
+// D = non-excluded bins over all groups (from the empty masks, before any value
+// is compared), D_c = non-excluded bins compared so far, M_c = matched bins (the
+// scan adds 1 per match).  After group l < n with R = D - D_c remaining trials:
+//   R = 0      -> the full-OPH verdict now (E3);
+//   else M_ra = k' (T D - M_c) / R = num / den, and Alg. 1's tests on it:
+//     Similar    if num <= 0, or num < k' t_num R and floor(M_ra) <= m_a
+//                (num < ma1 den, ma1 = m_a + 1 = #{m : P(X <= m) <= eps})
+//     NotSimilar if num > k' den, or num >= k' t_num R and ceil(M_ra) >= m_r
+//                (num > (m_r - 1) den, m_r = min{m : P(X >= m) <= eps})
+// (all products < 2^51 in int64); the last group: the full-OPH verdict.
+// ---------------------------------------------------------------------------
+template <int SPT>
+__global__ void __launch_bounds__(128, 3) levels_e_kernel(const __grid_constant__ LevelArgs a) {
+    constexpr int B = 32, U = 4;
+    extern __shared__ __align__(16) uint32_t lsm[];
+    const uint32_t nbs = a.nlev * a.kp;  // every bin of every group
+    uint32_t *qm = lsm + (size_t)nbs * B;  // [nw][B] query empty masks
+    const uint32_t qb0 = blockIdx.x * B;
+    const uint64_t col0 = (uint64_t)a.q_col0 + qb0;
+    load_query_block<B>(lsm, a.QT, a.ldq, 0, col0, nbs);
+    load_query_block<B>(qm, a.QE, a.ldq, 0, col0, a.nw);
+    __syncthreads();
+    const uint32_t qvalid = qb0 + B <= a.nq ? 0xFFFFFFFFu : ((1u << (a.nq - qb0)) - 1u);
+    const int64_t kp = a.kp, tn = a.t_num, td = a.t_den;
+
+    const uint64_t tile_sets = 128ull * SPT;
+    const uint64_t ntiles = (a.n_sets - a.s_begin + tile_sets - 1) / tile_sets;
+    const uint64_t t_end = min(ntiles, (uint64_t)(blockIdx.y + 1) * a.tiles_per_cta);
+    for (uint64_t t = (uint64_t)blockIdx.y * a.tiles_per_cta; t < t_end; t++) {
+        const uint64_t s0 = a.s_begin + t * tile_sets + threadIdx.x * SPT;
+        const bool active = s0 < a.n_sets;
+        uint32_t cnt[SPT][B];
+        uint32_t alive[SPT];
+        // D of every pair: nb minus the excluded bins over all groups (E1)
+#pragma unroll
+        for (int j = 0; j < SPT; j++) {
+            const uint64_t s = s0 + j;
+            alive[j] = (s < a.n_sets) ? qvalid : 0u;
+#pragma unroll
+            for (int q = 0; q < B; q++) cnt[j][q] = a.nb << 20;
+            for (uint32_t w = 0; w < a.nw; w++) {
+                const uint32_t es = s < a.n_sets ? __ldg(a.E + (uint64_t)w * a.ld + s) : 0u;
+#pragma unroll
+                for (int q = 0; q < B; q++) cnt[j][q] -= popc_masked(qm[w * B + q], es, a.joint, w, a.nb) << 20;
+            }
+        }
+        const uint32_t *Fp = a.F + (active ? s0 : a.ld - SPT);
+        const uint32_t ldb = (uint32_t)(a.ld * 4u);  // < 2^32 (launcher)
+        for (uint32_t l = 1; l <= a.nlev; l++) {
+            uint32_t any = 0;
+#pragma unroll
+            for (int j = 0; j < SPT; j++) any |= alive[j];
+            if (!__any_sync(0xFFFFFFFFu, any != 0u)) break;  // every pair of this warp is decided
+            scan_bins<B, SPT, U>(Fp, ldb, lsm + (size_t)(l - 1) * a.kp * B, (l - 1) * a.kp, a.kp, cnt, a.one, a.one);
+            // D_c += the group's non-excluded bins
+            const uint32_t lo = (l - 1) * a.kp, hi = l * a.kp;
+            for (uint32_t w = lo / 32; w * 32 < hi; w++) {
+                const uint32_t b0 = max(lo, 32 * w), b1 = min(hi, 32 * w + 32);
+                const uint32_t gm = (b1 - b0 == 32 ? 0xFFFFFFFFu : ((1u << (b1 - b0)) - 1u)) << (b0 - 32 * w);
+                const uint32_t nbw = __popc(gm);
+#pragma unroll
+                for (int j = 0; j < SPT; j++) {
+                    const uint64_t s = s0 + j;
+                    const uint32_t es = s < a.n_sets ? __ldg(a.E + (uint64_t)w * a.ld + s) : 0u;
+#pragma unroll
+                    for (int q = 0; q < B; q++) {
+                        const uint32_t x = a.joint ? (qm[w * B + q] & es) : (qm[w * B + q] | es);
+                        cnt[j][q] += (nbw - __popc(x & gm)) << 10;
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < SPT; j++) {
+                const uint32_t s = (uint32_t)(s0 + j);
+                uint32_t accm = 0, decm = 0, donem = 0;  // Similar / decided / complete (E3)
+#pragma unroll
+                for (int q = 0; q < B; q++) {
+                    const uint32_t v = cnt[j][q];
+                    const int64_t M = v & 1023u, Dc = (v >> 10) & 1023u, D = v >> 20;
+                    const int64_t R = D - Dc;
+                    bool acc, dec, done = false;
+                    if (l == a.nlev || R == 0) {  // the full-OPH verdict
+                        acc = D > 0 && M * td >= tn * D;
+                        dec = done = true;
+                    } else {
+                        const int64_t num = kp * (tn * D - td * M), den = td * R;
+                        acc = num <= 0 || (num < kp * tn * R && num < (int64_t)a.ma1 * den);
+                        dec = acc || num > kp * den || (num >= kp * tn * R && num > (int64_t)a.mr1 * den);
+                    }
+                    accm |= (uint32_t)acc << q;
+                    decm |= (uint32_t)dec << q;
+                    donem |= (uint32_t)done << q;
+                }
+                accm &= alive[j];
+                decm &= alive[j];
+                hist_add(a.res.hist, l, __popc(decm));
+                const uint32_t want = a.res.dense ? decm : accm;
+                if (__any_sync(0xFFFFFFFFu, want != 0u)) {
+#pragma unroll 1
+                    for (int q = 0; q < B; q++) {
+                        const bool e = (want >> q) & 1u;
+                        const uint32_t v = pick<B>(cnt[j], q);
+                        const uint32_t M = v & 1023u, Dc = (v >> 10) & 1023u, D = v >> 20;
+                        uint32_t flags = OPH_FLAG_EARLY, ex = l * a.kp - Dc;
+                        float est = -1.0f;
+                        if ((donem >> q) & 1u) {  // complete: the full-OPH record
+                            ex = a.nb - D;
+                            flags = D == 0 ? OPH_FLAG_UNDEFINED : 0u;
+                            if (D) est = (float)M / (float)D;
+                        }
+                        emit(a.res, e, (uint32_t)(col0 + q), s, M, ex, l, (accm >> q) & 1u, flags, est);
+                    }
+                }
+                alive[j] &= ~decm;
+            }
+        }
+    }
+}
+
 cudaError_t launch_levels_scan(const LevelArgs &a0, cudaStream_t st) {
     if (a0.n_sets <= a0.s_begin || a0.nq == 0) return cudaSuccess;
     LevelArgs a = a0;
     constexpr int SPT = 2;
-    const size_t smem = (size_t)a.nlev * a.kp * 32 * 4;
+    const size_t smem = ((size_t)a.nlev * a.kp + (a.eaware ? a.nw : 0)) * 32 * 4;
     const uint64_t tile_sets = 128ull * SPT;
     const uint32_t qblocks = (a.nq + 31) / 32;
     const uint64_t ntiles = (a.n_sets - a.s_begin + tile_sets - 1) / tile_sets;
@@ -1504,9 +1628,10 @@ cudaError_t launch_levels_scan(const LevelArgs &a0, cudaStream_t st) {
     a.tiles_per_cta = (uint32_t)tpc;
     const uint64_t gy = (ntiles + tpc - 1) / tpc;
     if (gy > 65535 || a.ld * 4 > 0xFFFFFFFFull) return cudaErrorInvalidConfiguration;
-    cudaError_t e = cudaFuncSetAttribute(levels_kernel<SPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = a.eaware ? levels_e_kernel<SPT> : levels_kernel<SPT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    levels_kernel<SPT><<<dim3(qblocks, (unsigned)gy), 128, smem, st>>>(a);
+    kern<<<dim3(qblocks, (unsigned)gy), 128, smem, st>>>(a);
     return cudaGetLastError();
 }
 

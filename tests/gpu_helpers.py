@@ -21,10 +21,10 @@ def gpu_build(offsets, ids, V, seed, k=None, kprime=None, hier=None, identity=Fa
 def gpu_dense(method, q, s, *, layout=None, t_num, t_den, eps=1e-4, joint=False, survivor_capacity=0):
     """Dense per-pair records [n_q, n_s] from the GPU."""
     res = og.Results(q.n_sets * s.n_sets, dense=True)
-    prm = og.params(t_num, t_den, eps, joint)
+    prm = og.params(t_num, t_den, eps, joint, variant=og.OPH_VARIANT_EMPTY_AWARE if method == "goph_e" else 0)
     if method == "full":
         og.compare_full(q, s, layout, prm, res)
-    elif method == "goph":
+    elif method in ("goph", "goph_e"):
         og.compare_goph(q, s, layout, prm, res, survivor_capacity=survivor_capacity)
     elif method == "hoph":
         og.compare_hoph(q, s, layout, prm, res, survivor_capacity=survivor_capacity)
@@ -55,10 +55,11 @@ def gpu_threshold_hits(method, q, s, *, layout=None, t_num, t_den, eps=1e-4, joi
                        set_id_base=0, survivor_capacity=0, strategy=og.OPH_STRATEGY_AUTO):
     """Sorted threshold hit list from the GPU (compare + topk_or_threshold_results)."""
     res = og.Results(capacity)
-    prm = og.params(t_num, t_den, eps, joint, strategy)
+    prm = og.params(t_num, t_den, eps, joint, strategy,
+                    variant=og.OPH_VARIANT_EMPTY_AWARE if method == "goph_e" else 0)
     if method == "full":
         og.compare_full(q, s, layout, prm, res, set_id_base=set_id_base)
-    elif method == "goph":
+    elif method in ("goph", "goph_e"):
         og.compare_goph(q, s, layout, prm, res, set_id_base=set_id_base, survivor_capacity=survivor_capacity)
     elif method == "hoph":
         og.compare_hoph(q, s, layout, prm, res, set_id_base=set_id_base, survivor_capacity=survivor_capacity)
@@ -77,8 +78,9 @@ def oracle_records(method, Q, S, *, t_num, t_den, eps=1e-4, joint=False, k=None,
                    qflags=None, sflags=None):
     if method == "full":
         return oracle.compare_full(Q, S, t_num=t_num, t_den=t_den, joint=joint, groups=k // kprime)
-    if method == "goph":
-        return oracle.compare_goph(Q, S, n=k // kprime, kprime=kprime, t_num=t_num, t_den=t_den, eps=eps, joint=joint)
+    if method in ("goph", "goph_e"):
+        return oracle.compare_goph(Q, S, n=k // kprime, kprime=kprime, t_num=t_num, t_den=t_den, eps=eps, joint=joint,
+                                   empty_aware=method == "goph_e")
     if method == "hoph":
         return oracle.compare_hoph(Q, S, L=L, kprime=kprime, a=a, b=b, t_num=t_num, t_den=t_den, eps=eps, joint=joint)
     if method == "minwise":

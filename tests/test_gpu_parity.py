@@ -153,6 +153,72 @@ def test_tiny_query_blocks(tiny_run, method, nq):
     assert_records_equal(g, want, f"tiny {method} nq={nq}")
 
 
+# ----------------------------------------------------------------------------- empty-aware GOPH (E1-E4)
+@pytest.mark.parametrize("joint", [False, True])
+def test_tiny_goph_empty_aware(tiny_run, joint):
+    """The empty-aware GOPH rule (OPH_VARIANT_EMPTY_AWARE): dense records,
+    threshold list and termination histogram == the oracle's (O9e)."""
+    r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"], joint=joint)
+    lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+    want = oracle_records("goph_e", o["QF"], o["F"], k=p["k"], kprime=p["kprime"], **kw)
+    g = gpu_dense("goph_e", r["qo"], r["so"], layout=lay, **kw)
+    assert_records_equal(g, want, f"tiny goph_e joint={joint}")
+    hits = gpu_threshold_hits("goph_e", r["qo"], r["so"], layout=lay, set_id_base=7, **kw)
+    assert [(int(h["query"]), int(h["set_id"])) for h in hits] == oracle.threshold_list(want, 7)
+    res = og.Results(1 << 20, stop_hist=True)
+    og.compare_goph(r["qo"], r["so"], lay, og.params(p["t_num"], p["t_den"], p["eps"], joint,
+                                                     variant=og.OPH_VARIANT_EMPTY_AWARE), res)
+    assert np.array_equal(res.hist()[: p["k"] // p["kprime"] + 1],
+                          np.bincount(want["groups"].ravel(), minlength=p["k"] // p["kprime"] + 1))
+    # the variant finds at least the planted near-duplicates the paper rule finds
+    paper = oracle_records("goph", o["QF"], o["F"], k=p["k"], kprime=p["kprime"], **kw)
+    assert want["verdict"].sum() >= paper["verdict"].sum()
+
+
+@pytest.mark.parametrize("V,k,kp,seed", [(1000003, 48, 16, 3), (4097, 96, 32, 4), (1 << 20, 512, 32, 5),
+                                         (300, 30, 10, 6), (2, 1, 1, 8)])
+def test_goph_empty_aware_ragged(V, k, kp, seed):
+    """Ragged shapes for the variant: k not a multiple of 32, k' = 10, empty
+    sets, a set and query count that are not multiples of a tile / block,
+    many empty bins (sets of 0-60 ids); T = 1/2, eps = 1e-3."""
+    rng = np.random.default_rng(seed)
+    nset, nq = 517, 45
+    sets_l = [np.sort(rng.choice(V, size=min(V, int(rng.integers(0, 60))), replace=False)) for _ in range(nset)]
+    qs_l = [np.sort(rng.choice(V, size=min(V, int(rng.integers(0, 60))), replace=False)) for _ in range(nq)]
+    for i in range(0, nq, 3):  # near-duplicates so some pairs reach late groups
+        qs_l[i] = sets_l[i * 7 % nset]
+    offs, ids = make_csr(sets_l)
+    qoffs, qids = make_csr(qs_l)
+    _, so, _ = gpu_build(offs, ids, V, seed, k=k, kprime=kp)
+    _, qo, _ = gpu_build(qoffs, qids, V, seed, k=k, kprime=kp)
+    F = oracle.oph_sketch(offs, ids, V, k, seed)
+    QF = oracle.oph_sketch(qoffs, qids, V, k, seed)
+    lay = og.flat_layout(V, k, kp)
+    for joint in (False, True):
+        kw = dict(t_num=1, t_den=2, eps=1e-3, joint=joint)
+        want = oracle_records("goph_e", QF, F, k=k, kprime=kp, **kw)
+        assert_records_equal(gpu_dense("goph_e", qo, so, layout=lay, **kw), want, f"goph_e V={V} k={k} joint={joint}")
+
+
+def test_goph_empty_aware_invalid(tiny_run):
+    """The variant is a GOPH rule: other methods refuse it, and so does a GOPH
+    layout with n k' > 512 (the register scan holds every group)."""
+    r, p = tiny_run, tiny_run["p"]
+    prm = og.params(p["t_num"], p["t_den"], p["eps"], variant=og.OPH_VARIANT_EMPTY_AWARE)
+    lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+    with pytest.raises(RuntimeError):
+        og.compare_full(r["qo"], r["so"], lay, prm, og.Results(1 << 16))
+    with pytest.raises(RuntimeError):
+        og.compare_hoph(r["qh"], r["sh"], r["hier"], prm, og.Results(1 << 16))
+    w = text_like(seed=3, n_sets=300, n_queries=10)
+    big = og.flat_layout(w.vocab_size, 1024, 32)
+    _, so, _ = gpu_build(w.offsets, w.ids, w.vocab_size, 1, k=1024, kprime=32)
+    _, qo, _ = gpu_build(w.q_offsets, w.q_ids, w.vocab_size, 1, k=1024, kprime=32)
+    with pytest.raises(RuntimeError):
+        og.compare_goph(qo, so, big, prm, og.Results(1 << 16))
+
+
 @pytest.mark.parametrize("method", ["full", "minwise"])
 def test_tiny_topk(tiny_run, method):
     r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
@@ -376,7 +442,7 @@ def test_text_sketches_full_collection(text_run):
 
 
 @pytest.mark.parametrize("strategy", [og.OPH_STRATEGY_AUTO, og.OPH_STRATEGY_BRUTE])
-@pytest.mark.parametrize("method", ["full", "goph", "hoph"])
+@pytest.mark.parametrize("method", ["full", "goph", "hoph", "goph_e"])
 def test_text_full_size_sampled_queries(text_run, method, strategy):
     """All 1,000 queries x 200,000 sets in the bench launch configuration
     (threshold mode); the hit lists of 8 sampled queries == the oracle's, and

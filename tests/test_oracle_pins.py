@@ -252,6 +252,89 @@ def test_goph_example1(golden):
     assert float(binomial.upper_tail(85, 100, 3, 5)) == pytest.approx(g["upper_85"], rel=1e-5)
 
 
+# ---- O9e empty-aware GOPH (E1-E4)
+def test_goph_e_example1_without_empties(golden):
+    """E2 reduces to Alg. 1 when no bin is excluded: Example 1 gives
+    the same M_ra 59.4, 66.25, 74.28, 85 and NotSimilar after group 4."""
+    g = golden("example1.json")
+    q, s = _goph_pair(g["matches"] + [0] * 6, g["kprime"], g["n"])
+    r, tr = oracle.compare_goph(q, s, n=g["n"], kprime=g["kprime"], t_num=g["t_num"], t_den=g["t_den"],
+                                eps=g["eps"], trace=True, empty_aware=True)
+    assert (r[0, 0]["groups"], r[0, 0]["verdict"], r[0, 0]["flags"]) == (g["groups_compared"], 0, oracle.EARLY)
+    for l, (printed, tol) in enumerate(g["m_ra_printed"]):
+        assert abs(tr[0, 0, l, 0] / tr[0, 0, l, 1] - printed) <= tol + 1e-12
+
+
+def test_goph_e_example1_excluded_tail(golden):
+    """Example 1's counts (65, 5 matched of 100 in groups 1-2) with every bin of
+    groups 5-10 empty on the set side (EitherEmpty): D = 400 trials.  Group 1:
+    R = 300, M_ra = 100 (0.6*400 - 65)/300 = 58.33 < 60, P(X <= 58) = 0.38 > eps:
+    continue.  Group 2: R = 200, M_ra = 100 (240 - 70)/200 = 85 >= 60 and
+    P(X >= 85) = 5.0732e-8 <= eps (the paper's printed tail): NotSimilar
+    after 2 groups -- Alg. 1 itself needs 4 (M_ra 66.25 at group 2)."""
+    g = golden("example1.json")
+    kp, n = g["kprime"], g["n"]
+    q, s = _goph_pair(g["matches"] + [0] * 6, kp, n)
+    s[0, 4 * kp:] = oracle.EMPTY
+    r, tr = oracle.compare_goph(q, s, n=n, kprime=kp, t_num=g["t_num"], t_den=g["t_den"], eps=g["eps"],
+                                trace=True, empty_aware=True)
+    assert Fraction(int(tr[0, 0, 0, 0]), int(tr[0, 0, 0, 1])) == Fraction(175, 3)
+    assert Fraction(int(tr[0, 0, 1, 0]), int(tr[0, 0, 1, 1])) == 85
+    assert float(binomial.upper_tail(85, 100, 3, 5)) == pytest.approx(g["upper_85"], rel=1e-5)
+    assert (r[0, 0]["groups"], r[0, 0]["verdict"], r[0, 0]["flags"]) == (2, 0, oracle.EARLY)
+    assert (r[0, 0]["n_mb"], r[0, 0]["n_excl"]) == (70, 0)
+    r0 = oracle.compare_goph(q, s, n=n, kprime=kp, t_num=g["t_num"], t_den=g["t_den"], eps=g["eps"])
+    assert r0[0, 0]["groups"] == 4
+
+
+def test_goph_e_reduces_to_alg1_without_empties():
+    """No excluded bin: the variant's records and M_ra traces equal Alg. 1's
+    (E2) on random per-group match counts, four parameter sets."""
+    rng = np.random.default_rng(55)
+    for kp, n, tn, td, eps in [(16, 4, 7, 10, 1e-4), (32, 8, 7, 10, 1e-4), (32, 8, 4, 5, 1e-3), (10, 6, 1, 2, 1e-2)]:
+        Q, S = [], []
+        for _ in range(200):
+            q, s = _goph_pair(rng.binomial(kp, rng.uniform(0, 1), size=n).tolist(), kp, n)
+            Q.append(q[0]); S.append(s[0])
+        Q, S = np.array(Q), np.array(S)
+        for joint in (False, True):
+            kw = dict(n=n, kprime=kp, t_num=tn, t_den=td, eps=eps, joint=joint, trace=True)
+            a, ta = oracle.compare_goph(Q, S, **kw)
+            b, tb = oracle.compare_goph(Q, S, empty_aware=True, **kw)
+            assert np.array_equal(a, b)
+            d = np.arange(len(Q))
+            # per stop level, the traced M_ra agree as rationals (the variant's are scaled by k')
+            for l in range(n - 1):
+                live = a["groups"][d, d] > l
+                assert np.array_equal(ta[d, d, l, 0][live] * tb[d, d, l, 1][live],
+                                      tb[d, d, l, 0][live] * ta[d, d, l, 1][live])
+
+
+def test_goph_e_final_and_complete_are_full_oph():
+    """E3: a pair the variant does not stop early (flags without EARLY) carries
+    the full-OPH record (Eq. 6) -- at the last group, or earlier when every
+    remaining bin is excluded; both empty modes, random sketches with empties."""
+    rng = np.random.default_rng(56)
+    n, kp = 8, 16
+    Q = rng.integers(0, 2, size=(40, n * kp)).astype(np.uint32)
+    S = rng.integers(0, 2, size=(60, n * kp)).astype(np.uint32)
+    Q[rng.random(Q.shape) < 0.3] = oracle.EMPTY
+    S[rng.random(S.shape) < 0.3] = oracle.EMPTY
+    S[:20, 5 * kp:] = oracle.EMPTY            # groups 6-8 empty on the set side
+    Q[:10, 3 * kp:] = oracle.EMPTY            # groups 4-8 empty on the query side
+    for joint in (False, True):
+        full = oracle.compare_full(Q, S, t_num=1, t_den=2, joint=joint)
+        e = oracle.compare_goph(Q, S, n=n, kprime=kp, t_num=1, t_den=2, eps=1e-3, joint=joint, empty_aware=True)
+        done = (e["flags"] & oracle.EARLY) == 0
+        assert done.any() and (~done).any()
+        for f in ("n_mb", "n_excl", "verdict", "flags"):
+            assert np.array_equal(e[f][done], full[f][done]), f
+        assert np.array_equal(e["estimate"][done], full["estimate"][done])
+        if not joint:  # EitherEmpty: queries 0-9 x sets 0-19 have no trial past group 3
+            assert (e["groups"][:10, :20] <= 3).all()
+            assert done[:10, :20].any()
+
+
 def test_goph_degenerate_traces():
     """S:347-348 (A.2): identical sketches -> Similar at the first l where
     lower(floor((600-100l)/(10-l))) <= 1e-4 (= group 4); zero matches ->
