@@ -560,6 +560,28 @@ def run_ours(args):
         og.compare_goph(qo, so, flat, prm_j, jr[1], set_id_base=base, ws=ws[1], survivor_capacity=surv_cap)
         og.compare_hoph(qh, sh, hier, prm_j, jr[2], set_id_base=base, ws=ws[2], survivor_capacity=surv_cap)
         quality["joint_empty"] = {m: score(jr[i], jr[i].n()) for i, m in enumerate(("full", "goph", "hoph"))}
+        # the empty-aware GOPH rule (E1-E4): not part of the timed
+        # step; its quality in both empty modes, device time per call and termination histogram
+        variants = {}
+        for joint, key in ((False, "either_empty"), (True, "joint_empty")):
+            prm_e = og.params(p["t_num"], p["t_den"], p["eps"], joint=joint, variant=og.OPH_VARIANT_EMPTY_AWARE)
+            er = og.Results(cap, stop_hist=True)
+            og.compare_goph(qo, so, flat, prm_e, er, set_id_base=base, ws=ws[1])
+            torch.cuda.synchronize()
+            quality[key]["goph_empty_aware"] = score(er, er.n())
+            h = er.hist().astype(np.float64)
+            times = []
+            for _ in range(3):
+                er.reset()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                og.compare_goph(qo, so, flat, prm_e, er, set_id_base=base, ws=ws[1])
+                e1.record()
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1))
+            variants[key] = {"ms_per_call": float(np.median(times)),
+                             "mean_bins_compared": float((h * np.arange(len(h))).sum() / max(1.0, h.sum()) * kp)}
+        quality["goph_empty_aware_runs"] = variants
 
     # ---------------- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None

@@ -1504,9 +1504,11 @@ __global__ void __launch_bounds__(128, 3) levels_kernel(const __grid_constant__ 
 //                (num < ma1 den, ma1 = m_a + 1 = #{m : P(X <= m) <= eps})
 //     NotSimilar if num > k' den, or num >= k' t_num R and ceil(M_ra) >= m_r
 //                (num > (m_r - 1) den, m_r = min{m : P(X >= m) <= eps})
-// (all products < 2^51 in int64); the last group: the full-OPH verdict.
+// (all products < 2^51 in int64; I = int32_t when the host has bounded them below
+// 2^31 -- T with a small denominator, the common case); the last group: the
+// full-OPH verdict.
 // ---------------------------------------------------------------------------
-template <int SPT>
+template <int SPT, typename I>
 __global__ void __launch_bounds__(128, 3) levels_e_kernel(const __grid_constant__ LevelArgs a) {
     constexpr int B = 32, U = 4;
     extern __shared__ __align__(16) uint32_t lsm[];
@@ -1518,7 +1520,7 @@ __global__ void __launch_bounds__(128, 3) levels_e_kernel(const __grid_constant_
     load_query_block<B>(qm, a.QE, a.ldq, 0, col0, a.nw);
     __syncthreads();
     const uint32_t qvalid = qb0 + B <= a.nq ? 0xFFFFFFFFu : ((1u << (a.nq - qb0)) - 1u);
-    const int64_t kp = a.kp, tn = a.t_num, td = a.t_den;
+    const I kp = (I)a.kp, tn = (I)a.t_num, td = (I)a.t_den, ma1 = (I)a.ma1, mr1 = (I)a.mr1;
 
     const uint64_t tile_sets = 128ull * SPT;
     const uint64_t ntiles = (a.n_sets - a.s_begin + tile_sets - 1) / tile_sets;
@@ -1573,16 +1575,16 @@ __global__ void __launch_bounds__(128, 3) levels_e_kernel(const __grid_constant_
 #pragma unroll
                 for (int q = 0; q < B; q++) {
                     const uint32_t v = cnt[j][q];
-                    const int64_t M = v & 1023u, Dc = (v >> 10) & 1023u, D = v >> 20;
-                    const int64_t R = D - Dc;
+                    const I M = (I)(v & 1023u), Dc = (I)((v >> 10) & 1023u), D = (I)(v >> 20);
+                    const I R = D - Dc;
                     bool acc, dec, done = false;
                     if (l == a.nlev || R == 0) {  // the full-OPH verdict
                         acc = D > 0 && M * td >= tn * D;
                         dec = done = true;
                     } else {
-                        const int64_t num = kp * (tn * D - td * M), den = td * R;
-                        acc = num <= 0 || (num < kp * tn * R && num < (int64_t)a.ma1 * den);
-                        dec = acc || num > kp * den || (num >= kp * tn * R && num > (int64_t)a.mr1 * den);
+                        const I num = kp * (tn * D - td * M), den = td * R;
+                        acc = num <= 0 || (num < kp * tn * R && num < ma1 * den);
+                        dec = acc || num > kp * den || (num >= kp * tn * R && num > mr1 * den);
                     }
                     accm |= (uint32_t)acc << q;
                     decm |= (uint32_t)dec << q;
@@ -1628,7 +1630,10 @@ cudaError_t launch_levels_scan(const LevelArgs &a0, cudaStream_t st) {
     a.tiles_per_cta = (uint32_t)tpc;
     const uint64_t gy = (ntiles + tpc - 1) / tpc;
     if (gy > 65535 || a.ld * 4 > 0xFFFFFFFFull) return cudaErrorInvalidConfiguration;
-    auto kern = a.eaware ? levels_e_kernel<SPT> : levels_kernel<SPT>;
+    // the empty-aware rule in 32-bit arithmetic when every product is < 2^31
+    // (|num|, k' den, ma1 den, k' t_num R <= k' max(t_num, t_den) 512 (k' + 1))
+    const bool e32 = (uint64_t)a.kp * std::max(a.t_num, a.t_den) * 512ull * (a.kp + 1ull) < (1ull << 31);
+    auto kern = !a.eaware ? levels_kernel<SPT> : (e32 ? levels_e_kernel<SPT, int32_t> : levels_e_kernel<SPT, int64_t>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<dim3(qblocks, (unsigned)gy), 128, smem, st>>>(a);
