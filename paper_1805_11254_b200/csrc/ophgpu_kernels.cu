@@ -879,7 +879,11 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 
 constexpr int kJoinWarps = 28;
 constexpr int kJoinThreads = 32 * kJoinWarps;
-constexpr uint32_t kJoinQCap = 256;  // candidate queue per warp (4-B entries)
+// candidate queue per warp (4-B entries).  Small on purpose: the verification re-reads
+// each candidate's value, which is still in L2 only if the flush follows within a few
+// tiles (text-like full OPH / MinWise join: 256 entries 90 / 116 us, 128 77 / 87, 64 66 / 74,
+// 32 68 / 79), and a 64-entry flush needs 2 loads in flight per lane, not 8
+constexpr uint32_t kJoinQCap = 64;
 constexpr uint32_t kJoinSPL = 4;                  // sets per lane (one 16-B load per bin row)
 constexpr uint32_t kJoinRPT = 8;                  // bin rows per tile
 constexpr uint32_t kJoinVals = kJoinSPL * kJoinRPT;  // values per lane per tile (mask bits)
@@ -1092,11 +1096,12 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
             const uint32_t sb = t / RB, rb = t % RB;
             const uint32_t sl = sb * kJoinTile + lane * kJoinSPL;
             const char *Fs = reinterpret_cast<const char *>(Fj + (uint64_t)(rb * kJoinRPT) * a.ld + s_lo + sl);
-            // row r at Fs + r * ldb: one IMAD.WIDE.U32 per row (ldb < 2^32, checked by the launcher)
+            // row r at Fs + r * ldb: one IMAD.WIDE.U32 per row (ldb < 2^32, checked by the launcher);
+            // default caching (an evict-first hint made the verification re-reads miss L2)
             if ((sb + 1) * kJoinTile <= nset && (rb + 1) * kJoinRPT <= rows) {  // full tile (warp-uniform): no checks
 #pragma unroll
                 for (int r = 0; r < (int)kJoinRPT; r++) {
-                    const uint4 x = __ldcs(reinterpret_cast<const uint4 *>(Fs + (uint64_t)((uint32_t)r) * ldb));
+                    const uint4 x = __ldg(reinterpret_cast<const uint4 *>(Fs + (uint64_t)((uint32_t)r) * ldb));
                     v[0 * kJoinRPT + r] = x.x;
                     v[1 * kJoinRPT + r] = x.y;
                     v[2 * kJoinRPT + r] = x.z;
