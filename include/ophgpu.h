@@ -133,9 +133,12 @@ typedef struct {
  *                 M_ra = k' (T D - M_c) / R with D the pair's non-excluded
  *                 bins, R those not yet compared; Algorithm 1's tests on M_ra
  *                 unchanged; R = 0 completes the comparison with the full-OPH
- *                 verdict.  Identical to PAPER when no bin is excluded.  Runs
- *                 as one register scan over all groups: needs n k' <= 512
- *                 (OPH_EINVAL otherwise); the strategy field is ignored. */
+ *                 verdict.  Identical to PAPER when no bin is excluded.  Needs
+ *                 n k' <= 512 (OPH_EINVAL otherwise).  A pair with no matched
+ *                 bin is never Similar under it (E5), so threshold results
+ *                 without a termination histogram take the PROBE join (AUTO /
+ *                 PROBE) and decide only the listed pairs; dense records, a
+ *                 histogram or BRUTE run one register scan over all groups. */
 enum { OPH_VARIANT_PAPER = 0, OPH_VARIANT_EMPTY_AWARE = 1 };
 
 /* Collection-scan strategies; every strategy returns

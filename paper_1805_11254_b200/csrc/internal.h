@@ -244,6 +244,7 @@ cudaError_t launch_scan(const ScanArgs &a, uint32_t B, cudaStream_t st);
 cudaError_t launch_table(const TableArgs &a, cudaStream_t st);
 cudaError_t launch_probe(const ProbeArgs &a, cudaStream_t st);
 cudaError_t launch_level(const LevelArgs &a, cudaStream_t st);
+cudaError_t launch_level_e(const LevelArgs &a, cudaStream_t st);  // empty-aware rule over a survivor list
 cudaError_t launch_levels_scan(const LevelArgs &a, cudaStream_t st);
 cudaError_t launch_jaccard(const JaccardArgs &a, cudaStream_t st);
 size_t shingle_temp_bytes(uint64_t n_bytes, uint64_t n_docs);

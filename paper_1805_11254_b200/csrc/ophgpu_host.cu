@@ -438,7 +438,12 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     uint64_t chunk = ceil_div(n_q, 32) * 32;
     uint64_t cap = 0;
     const bool levels = (method == OPH_METHOD_GOPH || method == OPH_METHOD_HOPH) && (plan.l0 < nlev || ea);
-    if (levels && !ea) {  // (the empty-aware scan decides in registers: no survivor lists)
+    // the empty-aware rule with threshold results and no histogram: the join lists every pair
+    // with a matched bin (no other pair can be Similar, E5) and level_e_kernel
+    // decides those survivors; otherwise the register scan decides every pair (no lists)
+    const bool ea_probe = ea && p->strategy != OPH_STRATEGY_BRUTE && res->mode != OPH_RES_DENSE && !res->d_stop_hist;
+    const uint32_t surv_l = ea ? 1u : plan.l0;  // counter / list parity of the scan's survivors
+    if (levels && (!ea || ea_probe)) {
         cap = cap_from_ws(ws_bytes, fixed);
         const uint64_t fit = (cap / n_s) / 32 * 32;
         if (fit < 32) return OPH_ENOMEM;
@@ -508,6 +513,13 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         s.final_ = 1;
         s.level = mw ? 0 : nb / kp;
         s.nw_load = mw ? 0 : nw;
+    } else if (ea_probe) {  // list every pair with a matched bin as a survivor
+        s.nscan = nb;
+        s.level = 1;
+        s.final_ = 0;
+        s.nw_load = nw;
+        s.acc_cnt = UINT32_MAX;
+        s.rej_cnt = 0;
     } else if (method == OPH_METHOD_GOPH) {
         s.nscan = plan.l0 * kp;
         s.level = plan.l0;
@@ -526,7 +538,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     // PROBE applies to threshold results when a pair with no matched bin is
     // decided NotSimilar at the scanned level (final verdicts: N_mb = 0 is
     // never >= T > 0; otherwise the level must reject state 0)
-    const bool probe = p->strategy != OPH_STRATEGY_BRUTE && !out.dense && (s.final_ || s.rej_cnt >= 0) && !ea;
+    const bool probe = ea ? ea_probe : p->strategy != OPH_STRATEGY_BRUTE && !out.dense && (s.final_ || s.rej_cnt >= 0);
 
     // BRUTE scans of GOPH / HOPH decide every level in one pass (levels_kernel) when the
     // pair states fit 32 bits and every group's query values fit shared memory; else
@@ -703,8 +715,8 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         s.nq = (uint32_t)nq;
         s.surv_cap = cap;
         if (levels) {
-            s.surv = w.list[plan.l0 % 2];
-            s.surv_count = w.counters + plan.l0;
+            s.surv = w.list[surv_l % 2];
+            s.surv_count = w.counters + surv_l;
         }
         if (levels || probe)
             if ((e = cudaMemsetAsync(w.counters, 0, (kMaxGroups + 3) * 8, stream)) != cudaSuccess) return e;
@@ -722,7 +734,13 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         return cudaSuccess;
     };
     // later levels, kLevelsPerLaunch per launch, survivors compacted between launches
+    // (empty-aware rule: one launch decides every listed pair)
     auto level_chunk = [&]() -> cudaError_t {
+        if (ea) {
+            la.in = w.list[surv_l % 2];
+            la.count_in = w.counters + surv_l;
+            return launch_level_e(la, stream);
+        }
         for (uint32_t l = plan.l0 + 1; l <= nlev; l += kLevelsPerLaunch) {
             const uint32_t l_last = std::min(nlev, l + kLevelsPerLaunch - 1);
             la.level = l;
@@ -740,7 +758,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         for (uint64_t a0 = q0; a0 < q1; a0 += chunk) {
             cudaError_t e = scan_chunk(a0, std::min<uint64_t>(chunk, q1 - a0));
             if (e != cudaSuccess) return e;
-            if (levels && !ea && (e = level_chunk()) != cudaSuccess) return e;
+            if (levels && (!ea || probe) && (e = level_chunk()) != cudaSuccess) return e;
         }
         return cudaSuccess;
     };
@@ -754,7 +772,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         if (e == cudaSuccess) e = scan_chunk(0, n_q);
         unsigned long long n_surv = 0;
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(&n_surv, w.counters + plan.l0, sizeof(n_surv), cudaMemcpyDeviceToHost, stream);
+            e = cudaMemcpyAsync(&n_surv, w.counters + surv_l, sizeof(n_surv), cudaMemcpyDeviceToHost, stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
         if (e != cudaSuccess) return OPH_ECUDA;
         if (n_surv <= cap) {

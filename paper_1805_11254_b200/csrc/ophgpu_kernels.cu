@@ -1838,6 +1838,60 @@ cudaError_t launch_probe(const ProbeArgs &a0, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// The empty-aware rule (E1-E4) for listed pairs (the join's pairs with a matched bin,
+// E5): one thread per pair walks the groups from the first, gathering each group's
+// values and masks, and stops at the pair's decision -- the same arithmetic as
+// levels_e_kernel in int64.
+__global__ void __launch_bounds__(256) level_e_kernel(const __grid_constant__ LevelArgs a) {
+    const unsigned long long n = *a.count_in;
+    const int64_t kp = a.kp, tn = a.t_num, td = a.t_den;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    // warp-uniform trip counts: emit() appends with full-warp ballots
+    for (unsigned long long base = blockIdx.x * (unsigned long long)blockDim.x + (threadIdx.x & ~31u); base < n;
+         base += stride) {
+        const unsigned long long i = base + (threadIdx.x & 31u);
+        bool alive = i < n;
+        uint32_t q = 0, s = 0, ex = 0;
+        int64_t D = 0, M = 0, Dc = 0;
+        if (alive) {
+            q = a.in.q[i];
+            s = a.in.s[i];
+            uint32_t ex_all = 0;
+            for (uint32_t w = 0; w < a.nw; w++)
+                ex_all += popc_masked(__ldg(a.QEM + (uint64_t)q * a.nw + w), __ldg(a.E + (uint64_t)w * a.ld + s),
+                                      a.joint, w, a.nb);
+            D = (int64_t)a.nb - ex_all;
+        }
+        for (uint32_t l = 1; l <= a.nlev; l++) {
+            if (!__any_sync(0xFFFFFFFFu, alive)) break;
+            bool dec = false, acc = false, done = false;
+            if (alive) {
+                M += group_matches(a, q, s, l - 1);
+                const uint32_t e = group_excl(a, q, s, l - 1);
+                ex += e;
+                Dc += kp - e;
+                const int64_t R = D - Dc;
+                if (l == a.nlev || R == 0) {  // the full-OPH verdict
+                    acc = D > 0 && M * td >= tn * D;
+                    dec = done = true;
+                } else {
+                    const int64_t num = kp * (tn * D - td * M), den = td * R;
+                    acc = num <= 0 || (num < kp * tn * R && num < (int64_t)a.ma1 * den);
+                    dec = acc || num > kp * den || (num >= kp * tn * R && num > (int64_t)a.mr1 * den);
+                }
+            }
+            emit(a.res, dec, q, s, (uint32_t)M, done ? (uint32_t)(a.nb - D) : ex, l, acc,
+                 done ? (D == 0 ? OPH_FLAG_UNDEFINED : 0u) : OPH_FLAG_EARLY, (done && D) ? (float)M / (float)D : -1.0f);
+            alive = alive && !dec;
+        }
+    }
+}
+
+cudaError_t launch_level_e(const LevelArgs &a, cudaStream_t st) {
+    level_e_kernel<<<148 * 2, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_level(const LevelArgs &a, cudaStream_t st) {
     // grid-stride over a device-side count: one CTA per SM covers sparse
     // survivor lists cheaply and still fills the chip for dense ones

@@ -199,6 +199,14 @@ def test_goph_empty_aware_ragged(V, k, kp, seed):
         kw = dict(t_num=1, t_den=2, eps=1e-3, joint=joint)
         want = oracle_records("goph_e", QF, F, k=k, kprime=kp, **kw)
         assert_records_equal(gpu_dense("goph_e", qo, so, layout=lay, **kw), want, f"goph_e V={V} k={k} joint={joint}")
+        # threshold lists through the join + listed-pair path (E5) and through the register scan
+        for strategy in (og.OPH_STRATEGY_PROBE, og.OPH_STRATEGY_BRUTE):
+            hits = gpu_threshold_hits("goph_e", qo, so, layout=lay, strategy=strategy, **kw)
+            assert [(int(h["query"]), int(h["set_id"])) for h in hits] == oracle.threshold_list(want)
+            for h in hits:
+                wr = want[h["query"], h["set_id"]]
+                assert (h["n_mb"], h["n_excl"], h["groups"], h["flags"]) == \
+                    (wr["n_mb"], wr["n_excl"], wr["groups"], wr["flags"])
 
 
 def test_goph_empty_aware_invalid(tiny_run):
@@ -317,7 +325,7 @@ def test_threshold_and_epsilon_extremes(tiny_run, tn, td, eps):
                          oracle_records("hoph", o["QH"][:40], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw), "hoph")
 
 
-@pytest.mark.parametrize("method", ["full", "goph", "hoph", "minwise"])
+@pytest.mark.parametrize("method", ["full", "goph", "hoph", "minwise", "goph_e"])
 def test_probe_overflow_falls_back_to_brute(method):
     """40 identical queries (plus 20 others): every set near them matches more
     than 4 distinct queries, so PROBE hands those sets to the BRUTE list
