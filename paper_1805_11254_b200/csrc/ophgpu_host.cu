@@ -741,8 +741,10 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
             la.count_in = w.counters + surv_l;
             return launch_level_e(la, stream);
         }
-        for (uint32_t l = plan.l0 + 1; l <= nlev; l += kLevelsPerLaunch) {
-            const uint32_t l_last = std::min(nlev, l + kLevelsPerLaunch - 1);
+        // the first launch compacts after kLevelsPerLaunch levels; the few survivors left
+        // then finish every remaining level in one launch (HOPH text-like: 2 launches, not 7)
+        for (uint32_t l = plan.l0 + 1, first = 1; l <= nlev; first = 0) {
+            const uint32_t l_last = first ? std::min(nlev, l + kLevelsPerLaunch - 1) : nlev;
             la.level = l;
             la.level_last = l_last;
             la.in = w.list[(l - 1) % 2];
@@ -751,6 +753,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
             la.count_out = w.counters + l_last;
             cudaError_t e = launch_level(la, stream);
             if (e != cudaSuccess) return e;
+            l = l_last + 1;
         }
         return cudaSuccess;
     };

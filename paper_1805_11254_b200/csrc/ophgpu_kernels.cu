@@ -1247,6 +1247,18 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
 __device__ __forceinline__ uint32_t group_matches(const LevelArgs &a, uint32_t q, uint32_t s, uint32_t g) {
     const uint32_t *qp = a.QM + (uint64_t)q * a.nb + (uint64_t)g * a.kp;
     const uint32_t *fp = a.F + (uint64_t)g * a.kp * a.ld + s;
+    if (a.kp == 32) {  // the configs' k': every load of the group in flight at once (one latency per group)
+        uint32_t f[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) f[i] = __ldg(fp + (uint64_t)i * a.ld);
+        uint32_t m = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4 *>(qp) + i);  // nb, k' multiples of 4: 16-B aligned
+            m += (f[4 * i] == x.x) + (f[4 * i + 1] == x.y) + (f[4 * i + 2] == x.z) + (f[4 * i + 3] == x.w);
+        }
+        return m;
+    }
     uint32_t m = 0;
 #pragma unroll 8
     for (uint32_t i = 0; i < a.kp; i++) m += (__ldg(fp + (uint64_t)i * a.ld) == __ldg(qp + i));
@@ -1264,6 +1276,25 @@ __device__ __forceinline__ uint32_t group_excl(const LevelArgs &a, uint32_t q, u
         const uint32_t width = b1 - b0;
         const uint32_t mask = (width == 32 ? 0xFFFFFFFFu : ((1u << width) - 1u)) << (b0 - 32 * w);
         ex += __popc(x & mask);
+    }
+    return ex;
+}
+
+// excluded bins among bins [0, nbins) of a pair (= the sum of group_excl over the
+// groups they cover): every mask word's pair of loads issued before any is used
+__device__ __forceinline__ uint32_t excl_prefix(const LevelArgs &a, uint32_t q, uint32_t s, uint32_t nbins) {
+    const uint32_t nw = (nbins + 31) / 32;
+    uint32_t ex = 0;
+    for (uint32_t w0 = 0; w0 < nw; w0 += 8) {
+        uint32_t qm[8], sm[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const bool in = w0 + u < nw;
+            qm[u] = in ? __ldg(a.QEM + (uint64_t)q * a.nw + w0 + u) : 0u;
+            sm[u] = in ? __ldg(a.E + (uint64_t)(w0 + u) * a.ld + s) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) ex += popc_masked(qm[u], sm[u], a.joint, w0 + u, nbins);
     }
     return ex;
 }
@@ -1299,7 +1330,7 @@ __global__ void __launch_bounds__(256) level_kernel(const __grid_constant__ Leve
                 float est = -1.0f;
                 if (alive) {
                     if (a.method == kGoph) {
-                        for (uint32_t g = 0; g < a.nlev; g++) ex_tot += group_excl(a, q, s, g);
+                        ex_tot = excl_prefix(a, q, s, a.nb);
                         const uint32_t den = a.nb - ex_tot;
                         if (den == 0) {
                             flags = OPH_FLAG_UNDEFINED;
@@ -1338,9 +1369,7 @@ __global__ void __launch_bounds__(256) level_kernel(const __grid_constant__ Leve
             hist_add(a.res.hist, l, (acc || rej) ? 1u : 0u);
             const bool want = a.res.dense ? (acc || rej) : acc;
             if (__any_sync(0xFFFFFFFFu, want)) {
-                uint32_t ex = 0;
-                if (want)
-                    for (uint32_t g = 0; g < l; g++) ex += group_excl(a, q, s, g);
+                const uint32_t ex = want ? excl_prefix(a, q, s, l * a.kp) : 0u;
                 emit(a.res, acc || rej, q, s, nmb, ex, l, acc ? 1u : 0u, OPH_FLAG_EARLY, -1.0f);
             }
             alive = alive && !acc && !rej;
@@ -1437,7 +1466,7 @@ __global__ void __launch_bounds__(128, 3) levels_kernel(const __grid_constant__ 
                             const uint32_t qg = (uint32_t)(col0 + q);
                             uint32_t ex = 0, nmb = 0;
                             if (e) {
-                                for (uint32_t g = 0; g < l; g++) ex += group_excl(a, qg, s, g);
+                                ex = excl_prefix(a, qg, s, l * a.kp);
                                 nmb = pick<B>(cnt[j], q) & rawmask;  // matched bins over groups 1..l
                             }
                             emit(a.res, e, qg, s, nmb, ex, l, (accm >> q) & 1u, OPH_FLAG_EARLY, -1.0f);
@@ -1458,7 +1487,7 @@ __global__ void __launch_bounds__(128, 3) levels_kernel(const __grid_constant__ 
                         if (al) {
                             if (!hoph) {
                                 nmb = pick<B>(cnt[j], q);
-                                for (uint32_t g = 0; g < a.nlev; g++) ex_tot += group_excl(a, qg, s, g);
+                                ex_tot = excl_prefix(a, qg, s, a.nb);
                                 const uint32_t den = a.nb - ex_tot;
                                 if (den == 0) {
                                     flags = OPH_FLAG_UNDEFINED;
