@@ -147,11 +147,13 @@ enum { OPH_VARIANT_PAPER = 0, OPH_VARIANT_EMPTY_AWARE = 1 };
  *          bin are decided NotSimilar at the scanned level), else BRUTE.  It
  *          probes a leading sample (1/16 of the sets, >= 16384) first and
  *          scans the rest with BRUTE if more than a quarter of the sample
- *          matched more than 4 distinct queries (one host synchronisation
- *          per call).
+ *          matched more than 4 distinct queries (one host synchronisation).
+ *          The decision is remembered per (collection buffer, n_sets, bins,
+ *          method, pass size), so repeated calls on a collection neither
+ *          sample nor synchronise; it affects speed only, never results.
  *   BRUTE: every (query, set, bin) equality is tested (register-blocked
  *          query tiles; cost ~ Q N bins; best when most pairs share bins).
- *   PROBE: a hash join in passes of <= 1024 queries, each one stream over
+ *   PROBE: a hash join in passes of <= 4096 queries, each one stream over
  *          the scanned collection bins: per bin, the pass's query values go
  *          into an exact hash table and a Bloom filter; every set bin tests
  *          the filter (held in shared memory) and the rare positives are

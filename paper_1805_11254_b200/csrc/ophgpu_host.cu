@@ -292,6 +292,18 @@ Plan make_plan(uint32_t method, uint32_t nlev, uint32_t kp, uint32_t a, uint32_t
     return P;
 }
 
+// AUTO's per-collection decision cache (see probe_pass_run)
+struct AutoKey {
+    uintptr_t F;
+    uint64_t n_sets;
+    uint32_t nscan, method, nq;
+    bool operator<(const AutoKey &o) const {
+        return std::tie(F, n_sets, nscan, method, nq) < std::tie(o.F, o.n_sets, o.nscan, o.method, o.nq);
+    }
+};
+std::mutex g_auto_mu;
+std::map<AutoKey, int> g_auto;
+
 // ---------------------------------------------------------------- validation
 oph_status check_sets(const oph_sets *s) {
     if (!s || (s->n_sets && (!s->d_offsets || !s->d_ids)) || s->n_sets >= (1ull << 32)) return OPH_EINVAL;
@@ -674,18 +686,36 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         // AUTO probes a leading sample of the sets first; when more than a quarter of it
         // matches too many distinct queries (a high-similarity collection), the rest goes
         // to BRUTE as one contiguous scan instead of the list fallback
-        const uint64_t n1 = p->strategy == OPH_STRATEGY_AUTO
-                                ? std::min<uint64_t>(n_s, std::max<uint64_t>(16384, ceil_div(n_s / 16, 256) * 256))
-                                : n_s;
+        // The decision is only a speed heuristic (every strategy returns the same results), so
+        // it is remembered per (collection buffer, size, bins, method, pass size): a repeated call
+        // on the same collection skips the sample's host synchronisation -- a probe decision
+        // becomes one join over every set.
+        uint64_t n1 = p->strategy == OPH_STRATEGY_AUTO
+                          ? std::min<uint64_t>(n_s, std::max<uint64_t>(16384, ceil_div(n_s / 16, 256) * 256))
+                          : n_s;
+        const AutoKey akey{(uintptr_t)Sv->d_values, n_s, s.nscan, method | (ea ? 16u : 0u), (uint32_t)nq};
+        int cached = -1;  // -1 unknown, 0 probe the rest, 1 BRUTE the rest
+        if (n1 < n_s) {
+            std::lock_guard<std::mutex> g(g_auto_mu);
+            auto it = g_auto.find(akey);
+            if (it != g_auto.end()) cached = it->second;
+        }
+        if (cached == 0) n1 = n_s;
         pr.s_begin = 0;
         pr.s_end = n1;
         if ((e = launch_probe(pr, stream)) != cudaSuccess) return e;
         if (n1 < n_s) {
-            unsigned long long ovf = 0;
-            if ((e = cudaMemcpyAsync(&ovf, ovf_count, sizeof(ovf), cudaMemcpyDeviceToHost, stream)) != cudaSuccess)
-                return e;
-            if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return e;
-            if (ovf * 4 > n1) {
+            bool brute_rest = cached == 1;
+            if (cached < 0) {
+                unsigned long long ovf = 0;
+                if ((e = cudaMemcpyAsync(&ovf, ovf_count, sizeof(ovf), cudaMemcpyDeviceToHost, stream)) != cudaSuccess)
+                    return e;
+                if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return e;
+                brute_rest = ovf * 4 > n1;
+                std::lock_guard<std::mutex> g(g_auto_mu);
+                g_auto[akey] = brute_rest ? 1 : 0;
+            }
+            if (brute_rest) {
                 if (multi) {
                     LevelArgs lm = la;
                     lm.q_col0 = (uint32_t)q0;
