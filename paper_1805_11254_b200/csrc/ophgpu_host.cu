@@ -455,7 +455,22 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     // decides those survivors; otherwise the register scan decides every pair (no lists)
     const bool ea_probe = ea && p->strategy != OPH_STRATEGY_BRUTE && res->mode != OPH_RES_DENSE && !res->d_stop_hist;
     const uint32_t surv_l = ea ? 1u : plan.l0;  // counter / list parity of the scan's survivors
-    if (levels && (!ea || ea_probe)) {
+    // BRUTE scans of GOPH / HOPH decide every level in one pass (levels_kernel) when the
+    // pair states fit 32 bits and every group's query values fit shared memory; else
+    // the scan covers the first decidable level and survivors go through level_kernel
+    // (HOPH packs the raw matched-bin count into the counter's low 10 bits: records need it)
+    u128 state_max = 0;
+    for (uint32_t j = 0; levels && j < nlev; j++) state_max += plan.c[j] * kp;
+    const uint32_t msh = method == OPH_METHOD_HOPH ? 10u : 0u;
+    // (OPHGPU_NO_MULTI_LEVEL_SCAN set: the survivor path always -- A/B diagnostics and the
+    // parity test of that path)
+    const bool no_multi = getenv("OPHGPU_NO_MULTI_LEVEL_SCAN") != nullptr;
+    const bool multi =
+        levels && (uint64_t)nlev * kp <= 512 && (((state_max << msh) < (u128)UINT32_MAX && !no_multi) || ea);
+    // the multi-level scan of a BRUTE or dense call produces no survivor lists: all
+    // queries in one chunk (survivor-sized chunks cut its grid into small launches)
+    const bool no_lists = multi && !ea_probe && (p->strategy == OPH_STRATEGY_BRUTE || res->mode == OPH_RES_DENSE);
+    if (levels && (!ea || ea_probe) && !no_lists) {
         cap = cap_from_ws(ws_bytes, fixed);
         const uint64_t fit = (cap / n_s) / 32 * 32;
         if (fit < 32) return OPH_ENOMEM;
@@ -552,18 +567,6 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     // never >= T > 0; otherwise the level must reject state 0)
     const bool probe = ea ? ea_probe : p->strategy != OPH_STRATEGY_BRUTE && !out.dense && (s.final_ || s.rej_cnt >= 0);
 
-    // BRUTE scans of GOPH / HOPH decide every level in one pass (levels_kernel) when the
-    // pair states fit 32 bits and every group's query values fit shared memory; else
-    // the scan covers the first decidable level and survivors go through level_kernel
-    // (HOPH packs the raw matched-bin count into the counter's low 10 bits: records need it)
-    u128 state_max = 0;
-    for (uint32_t j = 0; levels && j < nlev; j++) state_max += plan.c[j] * kp;
-    const uint32_t msh = method == OPH_METHOD_HOPH ? 10u : 0u;
-    // (OPHGPU_NO_MULTI_LEVEL_SCAN set: the survivor path always -- A/B diagnostics and the
-    // parity test of that path)
-    const bool no_multi = getenv("OPHGPU_NO_MULTI_LEVEL_SCAN") != nullptr;
-    const bool multi =
-        levels && (uint64_t)nlev * kp <= 512 && (((state_max << msh) < (u128)UINT32_MAX && !no_multi) || ea);
     LevelArgs la{};
     if (levels) {
         la.F = Sv->d_values;

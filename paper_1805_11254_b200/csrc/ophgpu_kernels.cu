@@ -309,7 +309,8 @@ __global__ void __launch_bounds__(256) minwise_kernel(const __grid_constant__ Mi
     const bool pow2 = a.V == (1ull << a.w);
     const uint64_t gamma = 0x9E3779B97F4A7C15ull;
 
-    for (uint32_t i0 = 0; i0 < a.k; i0 += blockDim.x) {  // uniform over the CTA
+    // permutations i0 + threadIdx.x; grid.y > 1 splits them over CTAs (small collections)
+    for (uint32_t i0 = blockIdx.y * blockDim.x; i0 < a.k; i0 += blockDim.x * gridDim.y) {  // uniform over the CTA
         const uint32_t i = i0 + threadIdx.x;
         uint32_t kappa[4], mu[4];
         {
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(256) minwise_kernel(const __grid_constant__ Mi
                 if (j < nloc) a.mw[(uint64_t)i * a.ld + s0 + j] = (offs[j] == offs[j + 1]) ? kEmpty : mn[j];
         }
     }
-    if (threadIdx.x < nloc) a.flags[s0 + threadIdx.x] = (offs[threadIdx.x] == offs[threadIdx.x + 1]) ? 1 : 0;
+    if (blockIdx.y == 0 && threadIdx.x < nloc) a.flags[s0 + threadIdx.x] = (offs[threadIdx.x] == offs[threadIdx.x + 1]) ? 1 : 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -1766,10 +1767,17 @@ cudaError_t launch_build(const BuildArgs &a, cudaStream_t st) {
 cudaError_t launch_minwise(const MinwiseArgs &a, cudaStream_t st) {
     if (a.n_sets == 0) return cudaSuccess;
     // 8 sets per CTA (ids staged once for 8 x k evaluations); a small collection (the
-    // queries) one set per CTA, so that it still covers the 148 SMs
+    // queries) one set per CTA with its k permutations split over CTAs of 64 threads,
+    // so that it covers the 148 SMs and the largest set's work is spread (the query
+    // build sits on the step's critical path: text-like 176 us with 256-thread CTAs)
     const uint32_t sets = a.n_sets >= 148ull * 8 * 4 ? 8u : 1u;
     const uint64_t grid = (a.n_sets + sets - 1) / sets;
-    const uint32_t threads = a.k >= 256 ? 256 : ((a.k + 31) / 32) * 32;
+    uint32_t threads = a.k >= 256 ? 256 : ((a.k + 31) / 32) * 32;
+    uint32_t gy = 1;
+    if (sets == 1 && threads > 64) {
+        threads = 64;
+        gy = (a.k + 63) / 64;
+    }
     MinwiseArgs b = a;
     b.hmul = 1u << (32 - std::min<uint32_t>(a.w, 32));  // (w = 32: unused)
     b.hsh = (32 - std::min<uint32_t>(a.w, 32)) + (a.w + 1) / 2;
@@ -1777,8 +1785,8 @@ cudaError_t launch_minwise(const MinwiseArgs &a, cudaStream_t st) {
         if (a.w >= 32) minwise_kernel<true, 8><<<(unsigned)grid, threads, 0, st>>>(b);
         else minwise_kernel<false, 8><<<(unsigned)grid, threads, 0, st>>>(b);
     } else {
-        if (a.w >= 32) minwise_kernel<true, 1><<<(unsigned)grid, threads, 0, st>>>(b);
-        else minwise_kernel<false, 1><<<(unsigned)grid, threads, 0, st>>>(b);
+        if (a.w >= 32) minwise_kernel<true, 1><<<dim3((unsigned)grid, gy), threads, 0, st>>>(b);
+        else minwise_kernel<false, 1><<<dim3((unsigned)grid, gy), threads, 0, st>>>(b);
     }
     return cudaGetLastError();
 }
