@@ -149,8 +149,9 @@ enum { OPH_VARIANT_PAPER = 0, OPH_VARIANT_EMPTY_AWARE = 1 };
  *          scans the rest with BRUTE if more than a quarter of the sample
  *          matched more than 4 distinct queries (one host synchronisation).
  *          The decision is remembered per (collection buffer, n_sets, bins,
- *          method, pass size), so repeated calls on a collection neither
- *          sample nor synchronise; it affects speed only, never results.
+ *          method), so repeated calls on a collection neither sample nor
+ *          synchronise (a BRUTE decision makes later calls BRUTE outright);
+ *          it affects speed only, never results.
  *   BRUTE: every (query, set, bin) equality is tested (register-blocked
  *          query tiles; cost ~ Q N bins; best when most pairs share bins).
  *   PROBE: a hash join in passes of <= 4096 queries, each one stream over

@@ -296,9 +296,9 @@ Plan make_plan(uint32_t method, uint32_t nlev, uint32_t kp, uint32_t a, uint32_t
 struct AutoKey {
     uintptr_t F;
     uint64_t n_sets;
-    uint32_t nscan, method, nq;
+    uint32_t nb, method;
     bool operator<(const AutoKey &o) const {
-        return std::tie(F, n_sets, nscan, method, nq) < std::tie(o.F, o.n_sets, o.nscan, o.method, o.nq);
+        return std::tie(F, n_sets, nb, method) < std::tie(o.F, o.n_sets, o.nb, o.method);
     }
 };
 std::mutex g_auto_mu;
@@ -453,7 +453,16 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     // the empty-aware rule with threshold results and no histogram: the join lists every pair
     // with a matched bin (no other pair can be Similar, E5) and level_e_kernel
     // decides those survivors; otherwise the register scan decides every pair (no lists)
-    const bool ea_probe = ea && p->strategy != OPH_STRATEGY_BRUTE && res->mode != OPH_RES_DENSE && !res->d_stop_hist;
+    // AUTO with a remembered BRUTE decision for this collection runs as BRUTE outright
+    // (no sample join, no survivor-sized query chunks)
+    const AutoKey akey{(uintptr_t)Sv->d_values, n_s, nb, method | (ea ? 16u : 0u)};
+    uint32_t strategy = p->strategy;
+    if (strategy == OPH_STRATEGY_AUTO) {
+        std::lock_guard<std::mutex> g(g_auto_mu);
+        auto it = g_auto.find(akey);
+        if (it != g_auto.end() && it->second == 1) strategy = OPH_STRATEGY_BRUTE;
+    }
+    const bool ea_probe = ea && strategy != OPH_STRATEGY_BRUTE && res->mode != OPH_RES_DENSE && !res->d_stop_hist;
     const uint32_t surv_l = ea ? 1u : plan.l0;  // counter / list parity of the scan's survivors
     // BRUTE scans of GOPH / HOPH decide every level in one pass (levels_kernel) when the
     // pair states fit 32 bits and every group's query values fit shared memory; else
@@ -469,7 +478,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         levels && (uint64_t)nlev * kp <= 512 && (((state_max << msh) < (u128)UINT32_MAX && !no_multi) || ea);
     // the multi-level scan of a BRUTE or dense call produces no survivor lists: all
     // queries in one chunk (survivor-sized chunks cut its grid into small launches)
-    const bool no_lists = multi && !ea_probe && (p->strategy == OPH_STRATEGY_BRUTE || res->mode == OPH_RES_DENSE);
+    const bool no_lists = multi && !ea_probe && (strategy == OPH_STRATEGY_BRUTE || res->mode == OPH_RES_DENSE);
     if (levels && (!ea || ea_probe) && !no_lists) {
         cap = cap_from_ws(ws_bytes, fixed);
         const uint64_t fit = (cap / n_s) / 32 * 32;
@@ -565,7 +574,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     // PROBE applies to threshold results when a pair with no matched bin is
     // decided NotSimilar at the scanned level (final verdicts: N_mb = 0 is
     // never >= T > 0; otherwise the level must reject state 0)
-    const bool probe = ea ? ea_probe : p->strategy != OPH_STRATEGY_BRUTE && !out.dense && (s.final_ || s.rej_cnt >= 0);
+    const bool probe = ea ? ea_probe : strategy != OPH_STRATEGY_BRUTE && !out.dense && (s.final_ || s.rej_cnt >= 0);
 
     LevelArgs la{};
     if (levels) {
@@ -693,10 +702,9 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         // it is remembered per (collection buffer, size, bins, method, pass size): a repeated call
         // on the same collection skips the sample's host synchronisation -- a probe decision
         // becomes one join over every set.
-        uint64_t n1 = p->strategy == OPH_STRATEGY_AUTO
+        uint64_t n1 = strategy == OPH_STRATEGY_AUTO
                           ? std::min<uint64_t>(n_s, std::max<uint64_t>(16384, ceil_div(n_s / 16, 256) * 256))
                           : n_s;
-        const AutoKey akey{(uintptr_t)Sv->d_values, n_s, s.nscan, method | (ea ? 16u : 0u), (uint32_t)nq};
         int cached = -1;  // -1 unknown, 0 probe the rest, 1 BRUTE the rest
         if (n1 < n_s) {
             std::lock_guard<std::mutex> g(g_auto_mu);
