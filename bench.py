@@ -316,16 +316,27 @@ def run_ours(args):
         mark(4)
         og.compare_hoph(qh, sh, hier, prm, res[2], set_id_base=base, ws=ws[2], survivor_capacity=surv_cap)
         mark(5)
+        # ---- a10 for the OPH family while the MinWise side stream is still busy (one GPU:
+        # nothing to gather): read their three hit counts (syncs this stream only) and sort
+        early = world == 1 and not serial
+        if early:
+            n3 = [int(x) for x in counts[:3].cpu()]
+            assert max(n3) <= cap, f"hit buffer overflow {n3}"
+            for i in range(3):
+                og.topk_or_threshold_results(res[i], n3[i], og.OPH_SELECT_THRESHOLD, outs[i], ws=ws[4])
         join = torch.cuda.Event()
         join.record(side)
         stream.wait_event(join)
         mark(6)
-        # ---- a10: gather (N > 1) and sort the four hit lists
+        # ---- a10: gather (N > 1) and sort the (remaining) hit lists
         n4 = [int(x) for x in counts.cpu()]  # one device->host read of the four hit counts
         assert max(n4) <= cap, f"hit buffer overflow {n4}"
         total = []
         for i in range(4):
             src, n = res[i], n4[i]
+            if early and i < 3:
+                total.append(n)
+                continue
             if world > 1:
                 allh, cnts = odist.gather_hits(res[i].hits, n4[i])
                 n = int(sum(cnts))
