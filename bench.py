@@ -289,15 +289,27 @@ def run_ours(args):
         fork = torch.cuda.Event()
         fork.record(stream)
         side.wait_event(fork)
-        # ---- side stream: a4 MinWise build (collection + queries), a9 MinWise scoring
+        qmw_ready = torch.cuda.Event()
+        # ---- side stream: a4 MinWise build (collection; the queries' on the main stream, which
+        # is idle meanwhile, so the side stream's critical path is the collection build), a9
         with torch.cuda.stream(side):
             mark(9, side)
             og.minwise_build_sketches(sets, V, seed, mwk, out=mw)
             mark(10, side)
+        if not serial:
             if rank == 0:
                 og.minwise_build_sketches(qsets, V, seed, mwk, out=qmw)
             if world > 1:
                 odist.broadcast_tensors([qmw.values, qmw.flags])
+            qmw_ready.record(stream)
+        with torch.cuda.stream(side):
+            if serial:
+                if rank == 0:
+                    og.minwise_build_sketches(qsets, V, seed, mwk, out=qmw)
+                if world > 1:
+                    odist.broadcast_tensors([qmw.values, qmw.flags])
+            else:
+                side.wait_event(qmw_ready)
             mark(11, side)
             og.compare_minwise(qmw, mw, prm, res[3], set_id_base=base, ws=ws[3])
             mark(12, side)
