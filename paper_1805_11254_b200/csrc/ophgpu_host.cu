@@ -724,6 +724,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
                 if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return e;
                 brute_rest = ovf * 4 > n1;
                 std::lock_guard<std::mutex> g(g_auto_mu);
+                if (g_auto.size() >= 4096) g_auto.clear();  // bounded: stale buffers age out
                 g_auto[akey] = brute_rest ? 1 : 0;
             }
             if (brute_rest) {
