@@ -375,6 +375,45 @@ def test_probe_overflow_falls_back_to_brute(method):
         assert (h["n_mb"], h["n_excl"], h["groups"], h["flags"]) == (wr["n_mb"], wr["n_excl"], wr["groups"], wr["flags"])
 
 
+@pytest.mark.parametrize("similar", [False, True])
+def test_auto_decision_cache(similar):
+    """AUTO samples the first 1/16 of a > 16,384-set collection once and remembers its
+    decision for the buffer: the first call, the repeated calls (cached probe -> one join
+    over every set; cached BRUTE -> BRUTE outright) and explicit BRUTE / PROBE return the
+    same hit lists, equal to the oracle's for the sampled queries.  `similar`: every set
+    shares most of its ids with the queries (the sample overflows the join's lists)."""
+    rng = np.random.default_rng(77 + similar)
+    V, k, kp, n_sets, nq = 1 << 20, 64, 16, 40_000, 40
+    base = [rng.choice(V, size=80, replace=False) for _ in range(4)]
+    sets_l = []
+    for i in range(n_sets):
+        if similar:
+            b = base[i % 4]
+            keep = b[rng.random(80) < 0.85]
+            sets_l.append(np.unique(np.concatenate([keep, rng.choice(V, size=10, replace=False)])))
+        else:
+            sets_l.append(np.unique(rng.choice(V, size=int(rng.integers(40, 120)), replace=False)))
+    qs_l = [base[i % 4] if similar else sets_l[i * 997 % n_sets] for i in range(nq)]
+    offs, ids = make_csr(sets_l)
+    qoffs, qids = make_csr([np.sort(q) for q in qs_l])
+    _, so, sh = gpu_build(offs, ids, V, 5, k=k, kprime=kp)
+    _, qo, _ = gpu_build(qoffs, qids, V, 5, k=k, kprime=kp)
+    lay = og.flat_layout(V, k, kp)
+    kw = dict(t_num=7, t_den=10, eps=1e-4)
+    for method in ("full", "goph"):
+        runs = [gpu_threshold_hits(method, qo, so, layout=lay, strategy=st, capacity=1 << 22,
+                                   survivor_capacity=32 * n_sets, **kw)
+                for st in (og.OPH_STRATEGY_AUTO, og.OPH_STRATEGY_AUTO, og.OPH_STRATEGY_AUTO,
+                           og.OPH_STRATEGY_BRUTE, og.OPH_STRATEGY_PROBE)]
+        lists = [[(int(h["query"]), int(h["set_id"])) for h in r] for r in runs]
+        assert all(x == lists[0] for x in lists[1:]), method
+        F = oracle.oph_sketch(offs, ids, V, k, 5)
+        QF = oracle.oph_sketch(qoffs, qids, V, k, 5)
+        want = oracle_records(method, QF[:2], F, k=k, kprime=kp, **kw)
+        assert [x for x in lists[0] if x[0] < 2] == oracle.threshold_list(want)
+        assert len(lists[0]) > 0
+
+
 @pytest.mark.parametrize("a,b,V,kp", [(1, 2, 1 << 20, 32), (2, 1, 1 << 20, 32), (3, 1, 1 << 16, 16), (1, 1, 100003, 16),
                                       (1, 2, 1 << 32, 32), (2, 1, 1 << 32, 32)])
 def test_hoph_split_ratios(a, b, V, kp):
