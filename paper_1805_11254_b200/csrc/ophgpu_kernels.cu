@@ -23,6 +23,10 @@
 
 #include "internal.h"
 
+#ifndef EA_B
+#define EA_B 16  // queries per thread block of the empty-aware register scan (image-like: 32 208 ms, 16 136, 8 151)
+#endif
+
 namespace ophgpu {
 
 // ---------------------------------------------------------------------------
@@ -1543,9 +1547,9 @@ __global__ void __launch_bounds__(128, 3) levels_kernel(const __grid_constant__ 
 // 2^31 -- T with a small denominator, the common case); the last group: the
 // full-OPH verdict.
 // ---------------------------------------------------------------------------
-template <int SPT, typename I>
+template <int SPT, typename I, int B>
 __global__ void __launch_bounds__(128, 3) levels_e_kernel(const __grid_constant__ LevelArgs a) {
-    constexpr int B = 32, U = 4;
+    constexpr int U = 4;
     extern __shared__ __align__(16) uint32_t lsm[];
     const uint32_t nbs = a.nlev * a.kp;  // every bin of every group
     uint32_t *qm = lsm + (size_t)nbs * B;  // [nw][B] query empty masks
@@ -1554,7 +1558,8 @@ __global__ void __launch_bounds__(128, 3) levels_e_kernel(const __grid_constant_
     load_query_block<B>(lsm, a.QT, a.ldq, 0, col0, nbs);
     load_query_block<B>(qm, a.QE, a.ldq, 0, col0, a.nw);
     __syncthreads();
-    const uint32_t qvalid = qb0 + B <= a.nq ? 0xFFFFFFFFu : ((1u << (a.nq - qb0)) - 1u);
+    const uint32_t qvalid =
+        qb0 + B <= a.nq ? (B == 32 ? 0xFFFFFFFFu : ((1u << (B & 31)) - 1u)) : ((1u << (a.nq - qb0)) - 1u);
     const I kp = (I)a.kp, tn = (I)a.t_num, td = (I)a.t_den, ma1 = (I)a.ma1, mr1 = (I)a.mr1;
 
     const uint64_t tile_sets = 128ull * SPT;
@@ -1655,9 +1660,14 @@ cudaError_t launch_levels_scan(const LevelArgs &a0, cudaStream_t st) {
     if (a0.n_sets <= a0.s_begin || a0.nq == 0) return cudaSuccess;
     LevelArgs a = a0;
     constexpr int SPT = 2;
-    const size_t smem = ((size_t)a.nlev * a.kp + (a.eaware ? a.nw : 0)) * 32 * 4;
-    const uint64_t tile_sets = 128ull * SPT;
-    const uint32_t qblocks = (a.nq + 31) / 32;
+    // the empty-aware scan: 1 set x EB queries per thread -- a pair's stop group depends on its
+    // own empty bins, and a warp stops only when all of its pairs have (fewer pairs per warp:
+    // image-like 344 ms at 2 x 32, 208 at 1 x 32, 136 at 1 x 16)
+    constexpr int EB = EA_B;
+    const uint32_t qb = a.eaware ? EB : 32u;
+    const size_t smem = ((size_t)a.nlev * a.kp + (a.eaware ? a.nw : 0)) * qb * 4;
+    const uint64_t tile_sets = 128ull * (a.eaware ? 1 : SPT);
+    const uint32_t qblocks = (a.nq + qb - 1) / qb;
     const uint64_t ntiles = (a.n_sets - a.s_begin + tile_sets - 1) / tile_sets;
     const uint64_t want_y = std::max<uint64_t>(1, (148ull * 3 * 4 + qblocks - 1) / qblocks);
     uint64_t tpc = std::max<uint64_t>(1, (ntiles + want_y - 1) / want_y);
@@ -1668,7 +1678,8 @@ cudaError_t launch_levels_scan(const LevelArgs &a0, cudaStream_t st) {
     // the empty-aware rule in 32-bit arithmetic when every product is < 2^31
     // (|num|, k' den, ma1 den, k' t_num R <= k' max(t_num, t_den) 512 (k' + 1))
     const bool e32 = (uint64_t)a.kp * std::max(a.t_num, a.t_den) * 512ull * (a.kp + 1ull) < (1ull << 31);
-    auto kern = !a.eaware ? levels_kernel<SPT> : (e32 ? levels_e_kernel<SPT, int32_t> : levels_e_kernel<SPT, int64_t>);
+    auto kern = !a.eaware ? levels_kernel<SPT>
+                          : (e32 ? levels_e_kernel<1, int32_t, EB> : levels_e_kernel<1, int64_t, EB>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<dim3(qblocks, (unsigned)gy), 128, smem, st>>>(a);

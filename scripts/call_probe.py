@@ -15,6 +15,7 @@ ap.add_argument("--config", default="image")
 ap.add_argument("--methods", default="goph,hoph")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--strategy", type=int, default=og.OPH_STRATEGY_AUTO)
+ap.add_argument("--variant", type=int, default=0, help="1: the empty-aware GOPH rule")
 args = ap.parse_args()
 w = text_like() if args.config == "text" else gen_gpu.image_like()
 p = w.params
@@ -26,12 +27,13 @@ qs = og.SetCollection.from_numpy(w.q_offsets, w.q_ids)
 so, sh = og.oph_build_sketches(sets, V, seed, flat=flat, hier=hier)
 qo, qh = og.oph_build_sketches(qs, V, seed, flat=flat, hier=hier)
 prm = og.params(p["t_num"], p["t_den"], p["eps"], strategy=args.strategy)
+prm_e = og.params(p["t_num"], p["t_den"], p["eps"], strategy=args.strategy, variant=args.variant)
 res = og.Results(1 << 24)
 ws = og.Workspace()
 cap = min(((qo.n_sets + 31) // 32) * 32 * so.n_sets, 1 << 26)
 for m in args.methods.split(","):
     fn = {"full": lambda: og.compare_full(qo, so, flat, prm, res, ws=ws),
-          "goph": lambda: og.compare_goph(qo, so, flat, prm, res, ws=ws, survivor_capacity=cap),
+          "goph": lambda: og.compare_goph(qo, so, flat, prm_e, res, ws=ws, survivor_capacity=cap),
           "hoph": lambda: og.compare_hoph(qh, sh, hier, prm, res, ws=ws, survivor_capacity=cap)}[m]
     ts = []
     for r in range(args.reps):
