@@ -17,7 +17,12 @@ ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--strategy", type=int, default=og.OPH_STRATEGY_AUTO)
 ap.add_argument("--variant", type=int, default=0, help="1: the empty-aware GOPH rule")
 args = ap.parse_args()
-w = text_like() if args.config == "text" else gen_gpu.image_like()
+if args.config == "text":
+    w = text_like()
+elif args.config.startswith("sweep"):
+    w = gen_gpu.sweep(float(args.config[5:]))
+else:
+    w = gen_gpu.image_like()
 p = w.params
 V, seed = w.vocab_size, p["perm_seed"]
 hier = og.oph_hier_layout_make(V, 1, 1, p["hoph_kprime"])
