@@ -1411,7 +1411,8 @@ __device__ __forceinline__ uint32_t pick(const uint32_t (&cnt)[B], uint32_t q) {
 }
 
 template <int SPT>
-__global__ void __launch_bounds__(128, 3) levels_kernel(const __grid_constant__ LevelArgs a) {
+// 4 CTAs/SM (128 registers, no spills; image-like GOPH / HOPH 67.7 / 11.8 -> 63.9 / 11.1 ms vs 3)
+__global__ void __launch_bounds__(128, 4) levels_kernel(const __grid_constant__ LevelArgs a) {
     constexpr int B = 32, U = 4;
     extern __shared__ __align__(16) uint32_t lsm[];
     const uint32_t nbs = a.nlev * a.kp;  // every bin of every group
@@ -1669,7 +1670,7 @@ cudaError_t launch_levels_scan(const LevelArgs &a0, cudaStream_t st) {
     const uint64_t tile_sets = 128ull * (a.eaware ? 1 : SPT);
     const uint32_t qblocks = (a.nq + qb - 1) / qb;
     const uint64_t ntiles = (a.n_sets - a.s_begin + tile_sets - 1) / tile_sets;
-    const uint64_t want_y = std::max<uint64_t>(1, (148ull * 3 * 4 + qblocks - 1) / qblocks);
+    const uint64_t want_y = std::max<uint64_t>(1, (148ull * 4 * 4 + qblocks - 1) / qblocks);
     uint64_t tpc = std::max<uint64_t>(1, (ntiles + want_y - 1) / want_y);
     tpc = std::min<uint64_t>(tpc, 64);
     a.tiles_per_cta = (uint32_t)tpc;
