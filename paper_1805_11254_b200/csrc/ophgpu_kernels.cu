@@ -1410,8 +1410,8 @@ __device__ __forceinline__ uint32_t pick(const uint32_t (&cnt)[B], uint32_t q) {
     return c;
 }
 
-template <int SPT>
 // 4 CTAs/SM (128 registers, no spills; image-like GOPH / HOPH 67.7 / 11.8 -> 63.9 / 11.1 ms vs 3)
+template <int SPT>
 __global__ void __launch_bounds__(128, 4) levels_kernel(const __grid_constant__ LevelArgs a) {
     constexpr int B = 32, U = 4;
     extern __shared__ __align__(16) uint32_t lsm[];
