@@ -480,11 +480,11 @@ def run_ours(args):
     peaks, peak_src = load_peaks()
     f_sm = peaks.get("sm_max_mhz", 1965.0) * 1e6
     # ALU pipe (IADD3/LOP3/SHF/min): 16 lanes/clk/SMSP (B300_MICROARCH "rt_SMSP=2"), 148 SM x 4 SMSP;
-    # one psi evaluation + running min is 9.5 ALU-pipe lane-ops at w = 32 and 10 at w < 32 (the
-    # SASS of minwise_kernel)
+    # one psi evaluation + running min is 9.5 ALU-pipe lane-ops at both widths (the SASS of
+    # minwise_kernel: 5 LOP3 + 4 SHF + half a 3-input VIMNMX3)
     alu_lanes = 148 * 4 * 16 * f_sm
     w_bits = max(1, (V - 1).bit_length())
-    psi_ops = 9.5 if w_bits >= 32 else 10.0
+    psi_ops = 9.5
     psi_peak = alu_lanes / psi_ops
     hbm = peaks["hbm_gbs"] * 1e9
     nnz = int(w.offsets[-1])
