@@ -542,6 +542,80 @@ def test_hoph_unbiased_joint_empty_dense():
     assert abs(ests.mean() - float(Jt)) < 3 * se
 
 
+def _hoph_r22_pair():
+    """3 groups of k' = 4 (1:1: c = [2, 1, 1], D = 4); group 2 is empty on both
+    sides, so it is excluded in either empty mode."""
+    q = _sk([1, 2, 3, 4, None, None, None, None, 5, 6, 7, 8])
+    s = _sk([1, 2, 3, 4, None, None, None, None, 5, 0, 7, None])
+    return np.array(q, dtype=np.uint32), np.array(s, dtype=np.uint32)
+
+
+@pytest.mark.parametrize("joint", [False, True])
+def test_hoph_drop_renormalise_hand_example(joint):
+    """R22 (S:416 'groups whose every bin is excluded are dropped and the
+    remaining weights renormalized'): with group 2 fully excluded the
+    estimate is (c1 m1/d1 + c3 m3/d3) / (c1 + c3), derived by hand:
+      EitherEmpty: g1 m=4 of d=4, g3 m=2 of d=3 -> (2*1 + 1*2/3) / 3 = 8/9
+      JointEmpty : g1 m=4 of d=4, g3 m=2 of d=4 -> (2*1 + 1*1/2) / 3 = 5/6
+    (dividing by D = 4 instead would give 2/3 -- NotSimilar at T = 7/10 -- and
+    5/8).  The filter path (compare_hoph, eps tiny) ends in the same record: the
+    raw state S_2 = 8 keeps x = (T D k' - S_l) / W_l at 1.6 and 3.2, inside
+    (0, k'], so only the last group decides; every group excluded -> UNDEFINED,
+    NotSimilar."""
+    q, s = _hoph_r22_pair()
+    want = Fraction(5, 6) if joint else Fraction(8, 9)
+    r = oracle.hoph_estimate(q, s, L=3, kprime=4, a=1, b=1, t_num=7, t_den=10, joint=joint)
+    assert r["flags"] == 0
+    assert r["estimate"] == pytest.approx(float(want), abs=1e-15)
+    assert r["verdict"] == (want >= Fraction(7, 10))
+    assert r["n_mb"] == 6
+    assert r["n_excl"] == (4 if joint else 5)  # EitherEmpty 0 + 4 + 1; JointEmpty 0 + 4 + 0
+    f = oracle.compare_hoph(q[None], s[None], L=3, kprime=4, a=1, b=1, t_num=7, t_den=10, eps=1e-300,
+                            joint=joint)[0, 0]
+    assert f["groups"] == 3 and f["flags"] == 0
+    assert f["estimate"] == pytest.approx(float(want), abs=1e-15)
+    assert f["verdict"] == r["verdict"]
+    e = np.full(12, E, dtype=np.uint32)
+    u = oracle.hoph_estimate(e, s, L=3, kprime=4, a=1, b=1, t_num=7, t_den=10, joint=False)
+    assert u["flags"] & oracle.UNDEFINED and u["verdict"] == 0
+
+
+def test_hoph_drop_renormalise_unbiased_sparse():
+    """Lemma 3 with R22: JointEmpty, |V| = 2^16, k' = 16, L = 12 and a
+    union of only 24 elements, so the deep groups hold no element of the
+    union and are dropped in essentially every permutation.  Given the union's
+    positions, every kept group's M_j / d_j is unbiased for J (which union
+    elements are shared is exchangeable), so the renormalised mean is J within
+    3 s.e. over 6000 permutations.  The same draws re-weighted with the
+    dropped groups' weight left in the denominator (the "divide by D" misreading)
+    miss J by more than 3 s.e., so this test would catch that mutant."""
+    rng = np.random.default_rng(2222)
+    V, kp = 1 << 16, 16
+    lay = oracle.hoph_layout(V, 1, 1, kp)
+    L = len(lay)
+    assert L == 12
+    c, D = oracle.hoph_weights(1, 1, L)
+    A, B, Jt = _pair_with_union(24, 0.5, V, rng)
+    offs, ids = make_csr([A, B])
+    ests, mutant, dropped = [], [], 0
+    for seed in range(6000):
+        H = oracle.hoph_sketch(offs, ids, V, lay, kp, seed)
+        ests.append(oracle.hoph_estimate(H[0], H[1], L=L, kprime=kp, a=1, b=1, t_num=1, t_den=2,
+                                         joint=True)["estimate"])
+        g0, g1 = H[0].reshape(L, kp), H[1].reshape(L, kp)
+        both = (g0 == E) & (g1 == E)
+        m = ((g0 == g1) & (g0 != E)).sum(1)
+        d = kp - both.sum(1)
+        keep = d > 0
+        dropped += int((~keep).any())
+        mutant.append(float(sum(c[j] * m[j] / d[j] for j in range(L) if keep[j]) / D))
+    ests, mutant = np.array(ests), np.array(mutant)
+    se = ests.std(ddof=1) / np.sqrt(len(ests))
+    assert dropped >= 0.99 * len(ests)
+    assert abs(ests.mean() - float(Jt)) < 3 * se
+    assert abs(mutant.mean() - float(Jt)) > 3 * (mutant.std(ddof=1) / np.sqrt(len(mutant)))
+
+
 # --------------------------------------------------------------------- MinWise
 def test_minwise_properties():
     """S:283 full vocabulary -> all fingerprints 0; S:292 disjoint sets -> 0
