@@ -323,7 +323,8 @@ oph_status exact_jaccard_pairs(const oph_sets *queries, const oph_sets *sets, co
  *   count (if it exceeds ids_capacity the ids are truncated; retry).
  *   Workspace: shingle_workspace_size(n_bytes, n_docs).  Asynchronous, no
  *   host synchronisation.  Errors: OPH_EINVAL (w == 0, vocab_size == 0 or >
- *   2^32, NULL pointers, n_bytes >= 2^32), OPH_ENOMEM (workspace too small). */
+ *   2^32, NULL pointers, n_bytes + n_docs >= 2^31 - 2: the library's scans and
+ *   sorts count items in 32-bit ints), OPH_ENOMEM (workspace too small). */
 oph_status shingle_workspace_size(uint64_t n_bytes, uint64_t n_docs, size_t *bytes);
 oph_status shingle_text(const uint8_t *d_text, const uint64_t *d_doc_offsets, uint64_t n_docs, uint64_t n_bytes,
                         uint32_t w, uint64_t vocab_size, uint64_t seed, uint64_t *d_set_offsets, uint32_t *d_ids,

@@ -133,6 +133,17 @@ def _stream(stream):
     return c_vp(s.cuda_stream)
 
 
+def _on(stream):
+    """Make `stream` current for the binding's own temporaries (outputs,
+    default workspaces, zero-fills, count reads): they are then allocated,
+    filled and released in the order of the kernels the call enqueues on that
+    stream.  A caller-owned Workspace / Results must be usable on `stream`."""
+    import contextlib
+    if stream is None:
+        return contextlib.nullcontext()
+    return _torch().cuda.stream(stream)
+
+
 def _ptr(t):
     return c_vp(t.data_ptr()) if t is not None else None
 
@@ -228,7 +239,7 @@ def _alloc_sketch(n_bins: int, n_sets: int, with_empty: bool):
     return vals, emp, ld
 
 
-def oph_build_sketches(sets: SetCollection, vocab_size: int, seed: int, flat: Optional[oph_flat_layout] = None,
+def _oph_build_sketches_impl(sets: SetCollection, vocab_size: int, seed: int, flat: Optional[oph_flat_layout] = None,
                        hier: Optional[oph_hier_layout] = None, identity: bool = False, stream=None,
                        out_oph: Optional[Sketches] = None, out_hoph: Optional[Sketches] = None):
     """OPH and/or HOPH sketches of every set (one psi evaluation per element).
@@ -255,7 +266,7 @@ def oph_build_sketches(sets: SetCollection, vocab_size: int, seed: int, flat: Op
     return so, sh
 
 
-def minwise_build_sketches(sets: SetCollection, vocab_size: int, seed: int, k: int, stream=None,
+def _minwise_build_sketches_impl(sets: SetCollection, vocab_size: int, seed: int, k: int, stream=None,
                            out: Optional[Sketches] = None) -> Sketches:
     torch = _torch()
     n = sets.n_sets
@@ -334,7 +345,7 @@ def _ws(ws, method, q: Sketches, s: Sketches, survivor_capacity):
     return buf
 
 
-def compare_full(q: Sketches, s: Sketches, layout: oph_flat_layout, prm: oph_params, res: Results,
+def _compare_full_impl(q: Sketches, s: Sketches, layout: oph_flat_layout, prm: oph_params, res: Results,
                  set_id_base: int = 0, ws: Optional[Workspace] = None, stream=None):
     buf = _ws(ws, OPH_METHOD_FULL, q, s, 0)
     _check(lib().compare_full(ctypes.byref(q.c()), ctypes.byref(s.c()), c_u32(set_id_base), ctypes.byref(layout),
@@ -342,7 +353,7 @@ def compare_full(q: Sketches, s: Sketches, layout: oph_flat_layout, prm: oph_par
                               _stream(stream)), "compare_full")
 
 
-def compare_goph(q: Sketches, s: Sketches, layout: oph_flat_layout, prm: oph_params, res: Results,
+def _compare_goph_impl(q: Sketches, s: Sketches, layout: oph_flat_layout, prm: oph_params, res: Results,
                  set_id_base: int = 0, ws: Optional[Workspace] = None, survivor_capacity: int = 0, stream=None):
     buf = _ws(ws, OPH_METHOD_GOPH, q, s, survivor_capacity)
     _check(lib().compare_goph(ctypes.byref(q.c()), ctypes.byref(s.c()), c_u32(set_id_base), ctypes.byref(layout),
@@ -350,7 +361,7 @@ def compare_goph(q: Sketches, s: Sketches, layout: oph_flat_layout, prm: oph_par
                               _stream(stream)), "compare_goph")
 
 
-def compare_hoph(q: Sketches, s: Sketches, layout: oph_hier_layout, prm: oph_params, res: Results,
+def _compare_hoph_impl(q: Sketches, s: Sketches, layout: oph_hier_layout, prm: oph_params, res: Results,
                  set_id_base: int = 0, ws: Optional[Workspace] = None, survivor_capacity: int = 0, stream=None):
     buf = _ws(ws, OPH_METHOD_HOPH, q, s, survivor_capacity)
     _check(lib().compare_hoph(ctypes.byref(q.c()), ctypes.byref(s.c()), c_u32(set_id_base), ctypes.byref(layout),
@@ -358,7 +369,7 @@ def compare_hoph(q: Sketches, s: Sketches, layout: oph_hier_layout, prm: oph_par
                               _stream(stream)), "compare_hoph")
 
 
-def compare_minwise(q: Sketches, s: Sketches, prm: oph_params, res: Results, set_id_base: int = 0,
+def _compare_minwise_impl(q: Sketches, s: Sketches, prm: oph_params, res: Results, set_id_base: int = 0,
                     ws: Optional[Workspace] = None, stream=None):
     buf = _ws(ws, OPH_METHOD_MINWISE, q, s, 0)
     _check(lib().compare_minwise(ctypes.byref(q.c()), ctypes.byref(s.c()), c_u32(set_id_base), ctypes.byref(prm),
@@ -372,7 +383,7 @@ def oph_select_workspace_size(n_in: int) -> int:
     return int(out.value)
 
 
-def exact_jaccard_pairs(queries: SetCollection, sets: SetCollection, query_idx, set_idx, stream=None):
+def _exact_jaccard_pairs_impl(queries: SetCollection, sets: SetCollection, query_idx, set_idx, stream=None):
     """|Q_a n S_b| and |Q_a u S_b| for pairs (query_idx[i], set_idx[i]) (int32/uint32
     device tensors; set_idx local to `sets`) -> (inter, union) uint32-as-int32 tensors."""
     torch = _torch()
@@ -385,7 +396,7 @@ def exact_jaccard_pairs(queries: SetCollection, sets: SetCollection, query_idx, 
     return inter[:n], union[:n]
 
 
-def shingle_text(text, doc_offsets, w: int, vocab_size: int, seed: int, ids_capacity: Optional[int] = None,
+def _shingle_text_impl(text, doc_offsets, w: int, vocab_size: int, seed: int, ids_capacity: Optional[int] = None,
                  ws: Optional[Workspace] = None, stream=None) -> SetCollection:
     """Documents (uint8 device tensor of bytes + int64 device offsets [n_docs+1], offsets[0] = 0)
     -> their shingle sets as a CSR SetCollection (include/ophgpu.h shingle_text)."""
@@ -408,7 +419,7 @@ def shingle_text(text, doc_offsets, w: int, vocab_size: int, seed: int, ids_capa
     return SetCollection(offsets, ids[:n])
 
 
-def topk_or_threshold_results(res_in: Results, n_in: int, mode: int, out: Results, topk: int = 0, k_bins: int = 0,
+def _topk_or_threshold_results_impl(res_in: Results, n_in: int, mode: int, out: Results, topk: int = 0, k_bins: int = 0,
                               ws: Optional[Workspace] = None, stream=None):
     """Sort (threshold) or select per-query top-k from the first n_in records
     of res_in into out (out.count receives the number written)."""
@@ -417,3 +428,28 @@ def topk_or_threshold_results(res_in: Results, n_in: int, mode: int, out: Result
     _check(lib().topk_or_threshold_results(_ptr(res_in.hits), c_u64(n_in), c_u32(mode), c_u32(topk), c_u32(k_bins),
                                            _ptr(out.hits), _ptr(out.count), _ptr(buf), ctypes.c_size_t(buf.numel()),
                                            _stream(stream)), "topk_or_threshold_results")
+
+
+# --------------------------------------------------------------------------- stream-safe entry points
+# Every public call runs with `stream` current (see _on): a caller passing a
+# non-current stream gets temporaries ordered with the kernels on that stream.
+def _with_stream(impl):
+    import functools
+
+    @functools.wraps(impl)
+    def call(*args, stream=None, **kw):
+        with _on(stream):
+            return impl(*args, stream=stream, **kw)
+    call.__name__ = call.__qualname__ = impl.__name__[1:-len("_impl")]
+    return call
+
+
+oph_build_sketches = _with_stream(_oph_build_sketches_impl)
+minwise_build_sketches = _with_stream(_minwise_build_sketches_impl)
+compare_full = _with_stream(_compare_full_impl)
+compare_goph = _with_stream(_compare_goph_impl)
+compare_hoph = _with_stream(_compare_hoph_impl)
+compare_minwise = _with_stream(_compare_minwise_impl)
+exact_jaccard_pairs = _with_stream(_exact_jaccard_pairs_impl)
+shingle_text = _with_stream(_shingle_text_impl)
+topk_or_threshold_results = _with_stream(_topk_or_threshold_results_impl)

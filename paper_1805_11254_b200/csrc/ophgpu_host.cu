@@ -784,13 +784,18 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
             return launch_level_e(la, stream);
         }
         // the first launch compacts after kLevelsPerLaunch levels; the few survivors left
-        // then finish every remaining level in one launch (HOPH text-like: 2 launches, not 7)
+        // then finish every remaining level in one launch (HOPH text-like: 2 launches, not 7).
+        // The lists ping-pong explicitly: a launch reads list[cur] and appends to the other
+        // one (input and output must never alias: the grid-stride walk of the input runs
+        // concurrently with other warps' appends).
+        uint32_t cur = surv_l % 2;  // the scan appended its survivors to list[surv_l % 2]
         for (uint32_t l = plan.l0 + 1, first = 1; l <= nlev; first = 0) {
             const uint32_t l_last = first ? std::min(nlev, l + kLevelsPerLaunch - 1) : nlev;
             la.level = l;
             la.level_last = l_last;
-            la.in = w.list[(l - 1) % 2];
-            la.out = w.list[l_last % 2];
+            la.in = w.list[cur];
+            la.out = w.list[cur ^ 1u];
+            cur ^= 1u;
             la.count_in = w.counters + (l - 1);
             la.count_out = w.counters + l_last;
             cudaError_t e = launch_level(la, stream);
@@ -1029,8 +1034,14 @@ oph_status exact_jaccard_pairs(const oph_sets *queries, const oph_sets *sets, co
     return cuda_status(launch_jaccard(a, (cudaStream_t)stream));
 }
 
+// CUB's scan / sort / unique take int item counts: n_bytes + 1 bytes and
+// (n_bytes + n_docs) / 2 + 1 tokens must stay below 2^31 - 1
+static bool shingle_sizes_ok(uint64_t n_bytes, uint64_t n_docs) {
+    return n_bytes + n_docs < (1ull << 31) - 2;
+}
+
 oph_status shingle_workspace_size(uint64_t n_bytes, uint64_t n_docs, size_t *bytes) {
-    if (!bytes || n_bytes >= (1ull << 32) || n_docs >= (1ull << 32)) return OPH_EINVAL;
+    if (!bytes || !shingle_sizes_ok(n_bytes, n_docs)) return OPH_EINVAL;
     *bytes = shingle_temp_bytes(n_bytes, n_docs);
     return OPH_OK;
 }
@@ -1039,7 +1050,7 @@ oph_status shingle_text(const uint8_t *d_text, const uint64_t *d_doc_offsets, ui
                         uint32_t w, uint64_t vocab_size, uint64_t seed, uint64_t *d_set_offsets, uint32_t *d_ids,
                         uint64_t ids_capacity, unsigned long long *d_n_ids, void *d_ws, size_t ws_bytes,
                         void *stream) {
-    if (w == 0 || vocab_size == 0 || vocab_size > (1ull << 32) || n_bytes >= (1ull << 32) || n_docs >= (1ull << 32))
+    if (w == 0 || vocab_size == 0 || vocab_size > (1ull << 32) || !shingle_sizes_ok(n_bytes, n_docs))
         return OPH_EINVAL;
     if (!d_doc_offsets || !d_set_offsets || !d_n_ids || (n_bytes && !d_text) || (ids_capacity && !d_ids))
         return OPH_EINVAL;

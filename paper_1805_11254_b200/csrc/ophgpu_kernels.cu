@@ -486,7 +486,10 @@ struct VecT<4> {
 
 template <int SPT>
 __device__ __forceinline__ void load_vals(const uint32_t *p, uint32_t (&v)[SPT]) {
-    if constexpr (SPT == 2) {
+    static_assert(SPT == 1 || SPT == 2 || SPT == 4, "sets per thread: 1, 2 or 4");
+    if constexpr (SPT == 1) {
+        v[0] = __ldg(p);  // a gathered (list-mode) set: only 4-byte aligned
+    } else if constexpr (SPT == 2) {
         const uint2 x = __ldg(reinterpret_cast<const uint2 *>(p));
         v[0] = x.x;
         v[1] = x.y;

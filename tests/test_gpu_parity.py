@@ -740,3 +740,43 @@ def test_tiny_survivor_path_dense(tiny_run, method, monkeypatch):
         g = gpu_dense("hoph", r["qh"], r["sh"], layout=r["hier"], **kw)
         want = oracle_records("hoph", o["QH"], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw)
     assert_records_equal(g, want, f"tiny {method} survivor path")
+
+
+def test_survivor_lists_many_late_pairs(monkeypatch):
+    """Regression (ping-pong of the survivor lists): GOPH with the survivor-list path forced
+    (OPHGPU_NO_MULTI_LEVEL_SCAN) on a collection whose pairs sit near T, so that far more
+    than one grid stride of level_kernel (296 x 256 = 75,776 threads) survives past the
+    first survivor launch (levels l0+1 .. l0+4).  The first launch must read one list and
+    append to the other; hit list and termination histogram == the oracle's."""
+    monkeypatch.setenv("OPHGPU_NO_MULTI_LEVEL_SCAN", "1")
+    from workloads.gen import _uniform_sampler, plant_duplicate, sample_sets
+    rng = np.random.default_rng(77)
+    V, k, kp, tn, td, eps = 1 << 20, 512, 32, 7, 10, 1e-4
+    draw = _uniform_sampler(V)
+    _, hub = sample_sets(rng, np.array([800]), V, draw)
+    qs = [plant_duplicate(rng, hub, 0.98, V, draw)[0] for _ in range(64)]
+    ss = [plant_duplicate(rng, hub, float(rng.uniform(0.64, 0.86)), V, draw)[0] for _ in range(3000)]
+    qo_, qi_ = make_csr(qs)
+    so_, si_ = make_csr(ss)
+    _, qo, _ = gpu_build(qo_, qi_, V, 5, k=k, kprime=kp)
+    _, so, _ = gpu_build(so_, si_, V, 5, k=k, kprime=kp)
+    lay = og.flat_layout(V, k, kp)
+    l0 = og.plan_thresholds(og.OPH_METHOD_GOPH, k // kp, kp, tn, td, eps)[2]
+    res = og.Results(1 << 20, stop_hist=True)
+    og.compare_goph(qo, so, lay, og.params(tn, td, eps, strategy=og.OPH_STRATEGY_BRUTE), res,
+                    survivor_capacity=64 * 3000)
+    hist = res.hist().astype(np.int64)
+    QF = oracle.oph_sketch(qo_, qi_, V, k, 5)
+    F = oracle.oph_sketch(so_, si_, V, k, 5)
+    want = oracle_records("goph", QF, F, t_num=tn, t_den=td, eps=eps, k=k, kprime=kp)
+    assert hist[l0 + 5:].sum() > 75_776, hist  # the case the bug needs
+    assert (hist == np.bincount(want["groups"].ravel(), minlength=len(hist))).all()
+    n = res.n()
+    out = og.Results(max(n, 1))
+    og.topk_or_threshold_results(res, n, og.OPH_SELECT_THRESHOLD, out)
+    got = out.numpy(n)
+    wl = oracle.threshold_list(want)
+    assert list(zip(got["query"].tolist(), got["set_id"].tolist())) == wl
+    sel = want[got["query"].astype(np.int64), got["set_id"].astype(np.int64)]
+    for f in ("n_mb", "n_excl", "groups", "verdict", "flags"):
+        assert (got[f].astype(np.int64) == sel[f].astype(np.int64)).all(), f
