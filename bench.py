@@ -1,29 +1,42 @@
 #!/usr/bin/env python
-"""bench.py -- one step of the whole OPH/GOPH/HOPH hot path (SURVEY 8(a) rows
-a1-a10) on the text-like workload (BASELINE.json configs[1]), timed on the
-device; prints ONE JSON line (rank 0).
+"""bench.py -- the OPH / GOPH / HOPH hot path (SURVEY 8(a) rows a1-a3, a5-a8,
+a10) on BASELINE.json's image-like workload (configs[2]: 10^6 sets x 4,096
+queries, k = 512, the largest single-GPU config), timed on the device; rank 0
+prints ONE JSON line.
 
-A step, per GPU (rank r owns a text-like shard of 200,000 sets, set IDs
-offset by r*200,000; the 1,000 queries are the same on every rank):
-  a1-a3  oph_build_sketches     OPH (k=256) + HOPH (1:1, k'=32, L=27) of the shard
-  a4     minwise_build_sketches MinWise (k=256) of the shard
-  a5     query sketches (rank 0) + NCCL broadcast; query prep inside compare_*
-  a6-a9  compare_full / compare_goph / compare_hoph / compare_minwise (threshold)
-  a10    hit lists gathered to rank 0 and sorted (topk_or_threshold_results)
+A step, per GPU (rank r owns its own shard of the config's collection, set
+IDs offset by r * N; the queries are the same on every rank):
+  a1-a3  oph_build_sketches   OPH (k) + HOPH (1:1, k') sketches of the shard
+  a5     query sketches (rank 0) + broadcast; query prep inside compare_*
+  a6-a8  compare_full / compare_goph / compare_hoph (threshold hit lists)
+  a10    one device->host read of the hit counts; hit lists gathered to
+         rank 0 (N > 1) and sorted (topk_or_threshold_results)
 
-value = 3 * Q * N_total / step time: query x set comparisons per second of
-the three OPH-family methods the metric names (every pair is scored by each
-of full OPH, GOPH and HOPH in a step; MinWise and the sketch builds are
-inside the timed step but not counted).
+value = 3 * Q * N_total / step time: query x set comparisons per second of the
+three OPH-family methods the metric names (every pair is scored by each of
+full OPH, GOPH and HOPH in a step).
 
-`--impl reference` times the CPU oracle (the reference arm of this tier) on
-a bounded sample of the same workload on the host cores.
+The MinWise baseline (rows a4, a9: k permutations, then scoring) is timed as
+its own leg right after, with the same K / W: `baseline_minwise` in the line,
+and `speedup_vs_minwise` = the paper's headline comparison ("HOPH is
+five to seven times faster than MinWise"), build + score and score only.
+
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+(one process per GPU, 127.0.0.1).  --dist-backend gloo stages the two
+collectives through host memory, so N ranks can share one GPU (a test of the
+N > 1 step; the numbers of such a run are not scaling numbers).
+--scaling strong (scale config only) splits the 8 shards of the 10^7-set
+collection over the ranks instead of giving each rank its own shard.
+
+`--impl reference` times the CPU oracle (the reference arm of this tier) on a
+bounded sample of the same workload on the host cores.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,10 +50,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "query×set sketch comparisons/sec (HOPH, GOPH, full OPH) + sketches/sec; % HBM peak"
 UNIT = "comparisons/s"
+CONFIG_NAMES = ["image-like", "text-like", "scale", "sweep-0.2", "sweep-0.5", "sweep-0.9", "tiny"]
 
-# CPU sample of the workload for the oracle legs (about 10 s of CPU work)
-CPU_SAMPLE_SETS = 20_000
-CPU_SAMPLE_QUERIES = 32
+# bounded CPU samples of each workload for the oracle legs (about 5-10 s of CPU work each)
+CPU_SAMPLE = {"image-like": (2048, 16), "text-like": (20_000, 32), "scale": (20_000, 32),
+              "sweep-0.2": (2048, 16), "sweep-0.5": (2048, 16), "sweep-0.9": (2048, 16), "tiny": (2000, 100)}
 
 
 def load_peaks():
@@ -48,8 +62,19 @@ def load_peaks():
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return d, "measured"
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+        return d, "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # --------------------------------------------------------------------------- clocks
@@ -106,77 +131,39 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# --------------------------------------------------------------------------- oracle (CPU) legs
-def cpu_sample_step(w, n_sets: int, n_q: int):
-    """The whole path on a bounded sample, with the CPU oracle: sketches of
-    n_sets sets and n_q queries, the four comparisons, threshold lists."""
-    import oracle
-    p = w.params
-    V, seed = w.vocab_size, p["perm_seed"]
-    offs = w.offsets[: n_sets + 1]
-    qoffs = w.q_offsets[: n_q + 1]
-    lay = oracle.hoph_layout(V, p["a"], p["b"], p["hoph_kprime"])
-    F = oracle.oph_sketch(offs, w.ids, V, p["k"], seed)
-    H = oracle.hoph_sketch(offs, w.ids, V, lay, p["hoph_kprime"], seed)
-    MW, fl = oracle.minwise_sketch(offs, w.ids, V, p["mw_k"], seed)
-    QF = oracle.oph_sketch(qoffs, w.q_ids, V, p["k"], seed)
-    QH = oracle.hoph_sketch(qoffs, w.q_ids, V, lay, p["hoph_kprime"], seed)
-    QMW, qfl = oracle.minwise_sketch(qoffs, w.q_ids, V, p["mw_k"], seed)
-    kw = dict(t_num=p["t_num"], t_den=p["t_den"])
-    r1 = oracle.compare_full(QF, F, groups=p["k"] // p["kprime"], **kw)
-    r2 = oracle.compare_goph(QF, F, n=p["k"] // p["kprime"], kprime=p["kprime"], eps=p["eps"], **kw)
-    r3 = oracle.compare_hoph(QH, H, L=len(lay), kprime=p["hoph_kprime"], a=p["a"], b=p["b"], eps=p["eps"], **kw)
-    r4 = oracle.compare_minwise(QMW, qfl, MW, fl, **kw)
-    return sum(len(oracle.threshold_list(r)) for r in (r1, r2, r3, r4))
+# --------------------------------------------------------------------------- workloads
+def concat_workloads(ws):
+    """One collection from several shards (strong scaling: a rank owns several of the 8
+    scale shards); queries from the first (they are the same in every shard)."""
+    import dataclasses
+    offs, ids, planted, base, nnz = [np.zeros(1, dtype=np.uint64)], [], [], 0, 0
+    for w in ws:
+        offs.append(w.offsets[1:] + np.uint64(nnz))
+        ids.append(w.ids)
+        pl = w.planted.copy()
+        pl[:, 1] += base
+        planted.append(pl)
+        base += w.n_sets
+        nnz += int(w.offsets[-1])
+    return dataclasses.replace(ws[0], offsets=np.concatenate(offs), ids=np.concatenate(ids),
+                               planted=np.concatenate(planted))
 
 
-def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
-    import oracle
-    from workloads import text_like
-    oracle.build()
-    w = text_like()
-    n_s, n_q = CPU_SAMPLE_SETS, CPU_SAMPLE_QUERIES
-    for _ in range(args.warmup):
-        cpu_sample_step(w, n_s, n_q)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        cpu_sample_step(w, n_s, n_q)
-        times.append(time.perf_counter() - t0)
-    t = sum(times) / len(times)
-    value = 3 * n_q * n_s / t
-    sample = (f"text-like: first {n_s} of 200,000 sets x first {n_q} of 1,000 queries; whole path "
-              f"(OPH/HOPH/MinWise sketches of the sample, full/GOPH/HOPH/MinWise scoring, threshold lists)")
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": "text-like", "sample_sets": n_s, "sample_queries": n_q},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-                             "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-    return 0
-
-
-# --------------------------------------------------------------------------- GPU arm
-CONFIG_NAMES = ["text-like", "image-like", "scale", "sweep-0.2", "sweep-0.5", "sweep-0.9", "tiny"]
-
-
-def make_workload(config: str, rank: int):
-    """(workload of this rank's shard, scan strategy, hit capacity per method,
-    survivor-capacity limit).  Every rank scores the same queries against its
-    own independent shard (weak scaling).  Strategy: PROBE where background
-    similarity is low (text-like law), BRUTE where every set shares bins with
-    the queries (Zipf image words, the sweep's hub)."""
+def make_workload(config: str, rank: int, world: int, scaling: str):
+    """(workload of this rank, scan strategy, hit capacity per method, survivor-capacity
+    limit).  Weak scaling: every rank scores the same queries against its own shard.
+    Strategy: PROBE where background similarity is low (text-like law), BRUTE where every
+    set shares bins with the queries (Zipf image words, the sweep's hub)."""
     import paper_1805_11254_b200 as og
     from workloads import gen_gpu, text_like, tiny
+    if config == "scale":  # configs[3]: 8 shards x 1.25M sets, 16,384 queries, T = 0.8
+        shards = range(rank, 8, world) if scaling == "strong" else [rank]
+        w = concat_workloads([gen_gpu.scale_shard(shard=s) for s in shards])
+        return w, og.OPH_STRATEGY_PROBE, 1 << 24, 1 << 28
+    if scaling == "strong":
+        raise SystemExit("--scaling strong applies to the scale config (the 8-shard collection) only")
     if config == "text-like":
         return text_like(shard=rank), og.OPH_STRATEGY_PROBE, 1 << 22, 1 << 28
-    if config == "scale":  # configs[3]: 8 shards x 1.25M sets, 16,384 queries, T = 0.8
-        return gen_gpu.scale_shard(shard=rank), og.OPH_STRATEGY_PROBE, 1 << 23, 1 << 28
     if config == "image-like":
         return gen_gpu.image_like(shard=rank), og.OPH_STRATEGY_BRUTE, 1 << 23, 1 << 28
     if config.startswith("sweep-"):
@@ -188,14 +175,80 @@ def make_workload(config: str, rank: int):
     raise ValueError(config)
 
 
-def count_launches(step_fn):
-    """Kernel launches of one step and their device times, from the CUDA profiler
-    (CUPTI) over one extra, untimed step: (launch count, {kernel: [count, total us]})."""
+# --------------------------------------------------------------------------- oracle (CPU) legs
+def cpu_sample_step(w, n_sets: int, n_q: int):
+    """The OPH-family path on a bounded sample with the CPU oracle: OPH + HOPH
+    sketches of n_sets sets and n_q queries, full / GOPH / HOPH scoring,
+    threshold lists (the rows `value` counts)."""
+    import oracle
+    p = w.params
+    V, seed = w.vocab_size, p["perm_seed"]
+    offs = w.offsets[: n_sets + 1]
+    qoffs = w.q_offsets[: n_q + 1]
+    lay = oracle.hoph_layout(V, p["a"], p["b"], p["hoph_kprime"])
+    F = oracle.oph_sketch(offs, w.ids, V, p["k"], seed)
+    H = oracle.hoph_sketch(offs, w.ids, V, lay, p["hoph_kprime"], seed)
+    QF = oracle.oph_sketch(qoffs, w.q_ids, V, p["k"], seed)
+    QH = oracle.hoph_sketch(qoffs, w.q_ids, V, lay, p["hoph_kprime"], seed)
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"])
+    r1 = oracle.compare_full(QF, F, groups=p["k"] // p["kprime"], **kw)
+    r2 = oracle.compare_goph(QF, F, n=p["k"] // p["kprime"], kprime=p["kprime"], eps=p["eps"], **kw)
+    r3 = oracle.compare_hoph(QH, H, L=len(lay), kprime=p["hoph_kprime"], a=p["a"], b=p["b"], eps=p["eps"], **kw)
+    return sum(len(oracle.threshold_list(r)) for r in (r1, r2, r3))
+
+
+def cpu_workload(config: str):
+    """The workload the oracle legs sample: the same generator and seed as the GPU arm's
+    rank 0 (image-like / sweep / scale are drawn with torch on the GPU)."""
+    from workloads import text_like, tiny
+    if config == "text-like":
+        return text_like()
+    if config == "tiny":
+        return tiny()
+    w, _, _, _ = make_workload(config, 0, 1, "weak")
+    return w
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    w = cpu_workload(args.config)
+    n_s, n_q = CPU_SAMPLE[args.config]
+    n_s, n_q = min(n_s, w.n_sets), min(n_q, w.n_queries)
+    for _ in range(args.warmup):
+        cpu_sample_step(w, n_s, n_q)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_sample_step(w, n_s, n_q)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    value = 3 * n_q * n_s / t
+    sample = (f"{args.config}: first {n_s} of {w.n_sets} sets x first {n_q} of {w.n_queries} queries; the "
+              f"OPH-family path (OPH/HOPH sketches of the sample, full/GOPH/HOPH scoring, threshold lists)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": args.config, "sample_sets": n_s, "sample_queries": n_q},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "cpu": cpu_model(),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU arm
+def profile_kernels(fn):
+    """Kernel launches of fn() and their device times, from the CUDA profiler (CUPTI),
+    untimed: (launch count, {kernel: [count, total us]})."""
     try:
         import torch
         from torch.profiler import ProfilerActivity, profile
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
-            step_fn()
+            fn()
             torch.cuda.synchronize()
         n = 0
         per = {}
@@ -214,48 +267,75 @@ def count_launches(step_fn):
         return None, {}
 
 
+def ubench_peaks():
+    """Measured ALU / issue peaks (scripts/ubench.cu, committed under profiles/)."""
+    p = os.path.join(ROOT, "profiles", "ubench_r02.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return None
+
+
+def ncu_traffic(config: str):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(config, {})
+    return {}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     import paper_1805_11254_b200 as og
     from paper_1805_11254_b200 import dist as odist
-    from workloads import text_like
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
     og.build()
     og.lib()
 
-    w, strategy, cap, surv_limit = make_workload(args.config, rank)
+    w, strategy, cap, surv_limit = make_workload(args.config, rank, world, args.scaling)
     p = w.params
     V, seed = w.vocab_size, p["perm_seed"]
     N, Q = w.n_sets, w.n_queries
-    N_total = N * world
-    base = rank * N
+    if args.scaling == "strong":
+        # every rank owns several of the 8 shards: set IDs from the ranks' actual sizes
+        sizes = [N]
+        if world > 1:
+            nt = torch.tensor([N], dtype=torch.int64, device="cuda")
+            allv = [torch.zeros_like(nt) for _ in range(world)]
+            odist.all_gather(allv, nt)
+            sizes = [int(x.item()) for x in allv]
+        N_total = sum(sizes)
+        base = sum(sizes[:rank])
+    else:
+        N_total = N * world
+        base = rank * N
     k, kp, hkp, mwk = p["k"], p["kprime"], p["hoph_kprime"], p["mw_k"]
     flat = og.flat_layout(V, k, kp)
     hier = og.oph_hier_layout_make(V, p["a"], p["b"], hkp)
     L = hier.L
     prm = og.params(p["t_num"], p["t_den"], p["eps"], strategy=strategy)
-    # the OPH family runs on a high-priority stream; the MinWise baseline (one long ALU-bound
-    # kernel of short CTAs) on a normal-priority side stream fills the SMs around it
-    lo_prio, hi_prio = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
-        else (0, -1)
-    stream = torch.cuda.Stream(priority=hi_prio)
+    stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
 
     # resident inputs
     sets = og.SetCollection.from_numpy(w.offsets, w.ids)
     qsets = og.SetCollection.from_numpy(w.q_offsets, w.q_ids)
     so, sh = og.oph_build_sketches(sets, V, seed, flat=flat, hier=hier)
-    mw = og.minwise_build_sketches(sets, V, seed, mwk)
     qo, qh = og.oph_build_sketches(qsets, V, seed, flat=flat, hier=hier)
-    qmw = og.minwise_build_sketches(qsets, V, seed, mwk)
+    mw = og.minwise_build_sketches(sets, V, seed, mwk) if not args.no_minwise else None
+    qmw = og.minwise_build_sketches(qsets, V, seed, mwk) if not args.no_minwise else None
     counts = torch.zeros((4,), dtype=torch.int64, device="cuda")
     # termination-level histograms of the four scorings (include/ophgpu.h d_stop_hist), per step
     hists = torch.zeros((4, og.OPH_STOP_HIST_LEN), dtype=torch.int64, device="cuda")
@@ -269,161 +349,165 @@ def run_ours(args):
     ws = [og.Workspace() for _ in range(5)]
     outs = [og.Results(cap * (world if rank == 0 else 1)) for _ in range(4)]
     merged = [og.Results(cap * world) for _ in range(4)] if world > 1 else None
+    hit_bytes = og.HIT_DTYPE.itemsize
 
-    side_stream = torch.cuda.Stream(priority=lo_prio)  # MinWise (the baseline) beside the OPH family
+    def mark(ev, i):
+        if ev is not None:
+            ev[i].record(stream)
 
-    def step(ev=None, inputs=None, sets=sets, qsets=qsets, serial=False):
-        """One pass of rows a1-a10.  Stream `stream`: OPH/HOPH build, query
-        sketches, full OPH / GOPH / HOPH; stream `side`: the MinWise build and
-        scoring (ALU-bound) overlapping the OPH family (memory/latency-bound).
-        ev[j] marks phase boundaries on the stream that runs the phase.
-        serial=True runs everything on one stream (per-kernel timing)."""
-        side = stream if serial else side_stream
+    def select(idx, n4):
+        """a10: gather (N > 1) and sort method idx's hit list; returns the list length on rank 0."""
+        n = n4[idx]
+        src = res[idx]
+        if world > 1:
+            allh, cnts = odist.gather_hits(res[idx].hits, n)
+            n = int(sum(cnts))
+            if rank != 0:
+                return n
+            merged[idx].hits[: allh.numel()].copy_(allh)
+            src = merged[idx]
+        og.topk_or_threshold_results(src, n, og.OPH_SELECT_THRESHOLD, outs[idx], ws=ws[4])
+        return n
 
-        def mark(i, st=stream):
-            if ev is not None:
-                ev[i].record(st)
-        mark(0)
-        counts.zero_()
-        hists.zero_()
-        fork = torch.cuda.Event()
-        fork.record(stream)
-        side.wait_event(fork)
-        qmw_ready = torch.cuda.Event()
-        # ---- side stream: a4 MinWise build (collection; the queries' on the main stream, which
-        # is idle meanwhile, so the side stream's critical path is the collection build), a9
-        with torch.cuda.stream(side):
-            mark(9, side)
-            og.minwise_build_sketches(sets, V, seed, mwk, out=mw)
-            mark(10, side)
-        if not serial:
-            if rank == 0:
-                og.minwise_build_sketches(qsets, V, seed, mwk, out=qmw)
-            if world > 1:
-                odist.broadcast_tensors([qmw.values, qmw.flags])
-            qmw_ready.record(stream)
-        with torch.cuda.stream(side):
-            if serial:
-                if rank == 0:
-                    og.minwise_build_sketches(qsets, V, seed, mwk, out=qmw)
-                if world > 1:
-                    odist.broadcast_tensors([qmw.values, qmw.flags])
-            else:
-                side.wait_event(qmw_ready)
-            mark(11, side)
-            og.compare_minwise(qmw, mw, prm, res[3], set_id_base=base, ws=ws[3])
-            mark(12, side)
-        # ---- main stream: a1-a3 OPH+HOPH build, a5 queries, a6-a8 scoring
-        mark(8)
+    def step(ev=None, sets=sets, qsets=qsets):
+        """One OPH-family pass (rows a1-a3, a5-a8, a10); ev[i] marks phase boundaries."""
+        mark(ev, 0)
+        counts[:3].zero_()
+        hists[:3].zero_()
         og.oph_build_sketches(sets, V, seed, flat=flat, hier=hier, out_oph=so, out_hoph=sh)
-        mark(1)
+        mark(ev, 1)
         if rank == 0:
             og.oph_build_sketches(qsets, V, seed, flat=flat, hier=hier, out_oph=qo, out_hoph=qh)
         if world > 1:
             odist.broadcast_tensors([qo.values, qo.empty, qh.values, qh.empty])
-        mark(2)
+        mark(ev, 2)
         og.compare_full(qo, so, flat, prm, res[0], set_id_base=base, ws=ws[0])
-        mark(3)
+        mark(ev, 3)
         og.compare_goph(qo, so, flat, prm, res[1], set_id_base=base, ws=ws[1], survivor_capacity=surv_cap)
-        mark(4)
+        mark(ev, 4)
         og.compare_hoph(qh, sh, hier, prm, res[2], set_id_base=base, ws=ws[2], survivor_capacity=surv_cap)
-        mark(5)
-        # ---- a10 for the OPH family while the MinWise side stream is still busy (one GPU:
-        # nothing to gather): read their three hit counts (syncs this stream only) and sort
-        early = world == 1 and not serial
-        if early:
-            n3 = [int(x) for x in counts[:3].cpu()]
-            assert max(n3) <= cap, f"hit buffer overflow {n3}"
-            for i in range(3):
-                og.topk_or_threshold_results(res[i], n3[i], og.OPH_SELECT_THRESHOLD, outs[i], ws=ws[4])
-        join = torch.cuda.Event()
-        join.record(side)
-        stream.wait_event(join)
-        mark(6)
-        # ---- a10: gather (N > 1) and sort the (remaining) hit lists
-        n4 = [int(x) for x in counts.cpu()]  # one device->host read of the four hit counts
+        mark(ev, 5)
+        n4 = [int(x) for x in counts[:3].cpu()]  # one device->host read of the three hit counts
         assert max(n4) <= cap, f"hit buffer overflow {n4}"
-        total = []
-        for i in range(4):
-            src, n = res[i], n4[i]
-            if early and i < 3:
-                total.append(n)
-                continue
-            if world > 1:
-                allh, cnts = odist.gather_hits(res[i].hits, n4[i])
-                n = int(sum(cnts))
-                if rank != 0:
-                    continue
-                merged[i].hits[: allh.numel()].copy_(allh)
-                src = merged[i]
-            if rank == 0:
-                og.topk_or_threshold_results(src, n, og.OPH_SELECT_THRESHOLD, outs[i], ws=ws[4])
-                total.append(n)
-        mark(7)
+        total = [select(i, n4) for i in range(3)]
+        mark(ev, 6)
         return total
 
-    # phases: (name, start event, end event); 0..7 on the main stream, 9..12 on the side stream
-    phase_ev = [("build_oph_hoph", 8, 1),("query_sketches_oph_hoph", 1, 2), ("compare_full", 2, 3),
-                ("compare_goph", 3, 4), ("compare_hoph", 4, 5), ("join_minwise", 5, 6), ("select", 6, 7),
-                ("build_minwise", 9, 10), ("query_sketches_minwise", 10, 11), ("compare_minwise", 11, 12)]
+    def step_mw(ev=None, sets=sets, qsets=qsets):
+        """One MinWise-baseline pass (rows a4, a9, a10)."""
+        mark(ev, 0)
+        counts[3:].zero_()
+        hists[3:].zero_()
+        og.minwise_build_sketches(sets, V, seed, mwk, out=mw)
+        mark(ev, 1)
+        if rank == 0:
+            og.minwise_build_sketches(qsets, V, seed, mwk, out=qmw)
+        if world > 1:
+            odist.broadcast_tensors([qmw.values, qmw.flags])
+        mark(ev, 2)
+        og.compare_minwise(qmw, mw, prm, res[3], set_id_base=base, ws=ws[3])
+        mark(ev, 3)
+        n = int(counts[3:].cpu()[0])
+        assert n <= cap, f"hit buffer overflow {n}"
+        tot = select(3, [0, 0, 0, n])
+        mark(ev, 4)
+        return tot
 
-    # warm-up (also JIT-free: the .so is prebuilt)
+    phase_ev = [("build_oph_hoph", 0, 1), ("query_sketches_oph_hoph", 1, 2), ("compare_full", 2, 3),
+                ("compare_goph", 3, 4), ("compare_hoph", 4, 5), ("select", 5, 6)]
+    phase_mw = [("build_minwise", 0, 1), ("query_sketches_minwise", 1, 2), ("compare_minwise", 2, 3),
+                ("select_minwise", 3, 4)]
+
+    def timed(fn, K, n_ev, clocks=None):
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(K)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if clocks is not None:
+            clocks.start()
+            time.sleep(0.3)
+        t0.record(stream)
+        out = None
+        for i in range(K):
+            out = fn(evs[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        clk = clocks.stop() if clocks is not None else None
+        if world > 1:
+            dist.barrier()
+        ms = t0.elapsed_time(t1) / K
+        if world > 1:
+            ms = odist.max_over_ranks(ms, device="cuda")
+        return ms, evs, out, clk
+
+    # warm-up
     for _ in range(args.warmup):
         step()
+        if mw is not None:
+            step_mw()
     torch.cuda.synchronize()
-    # (the profiled step runs every call on one stream, so per-kernel device times are not
-    # inflated by the MinWise side stream sharing the SMs)
-    launches, kernel_us = (None, {}) if args.no_launch_count else count_launches(lambda: step(serial=True))
 
-    # ---------------- timed region: device inputs resident in HBM
+    # per-phase kernel lists (CUPTI, untimed): launch counts and device times of one step
+    phase_kernels = {}
+    launches = None
+    if not args.no_launch_count:
+        calls = {
+            "build_oph_hoph": lambda: og.oph_build_sketches(sets, V, seed, flat=flat, hier=hier, out_oph=so,
+                                                            out_hoph=sh),
+            "compare_full": lambda: og.compare_full(qo, so, flat, prm, res[0], set_id_base=base, ws=ws[0]),
+            "compare_goph": lambda: og.compare_goph(qo, so, flat, prm, res[1], set_id_base=base, ws=ws[1],
+                                                    survivor_capacity=surv_cap),
+            "compare_hoph": lambda: og.compare_hoph(qh, sh, hier, prm, res[2], set_id_base=base, ws=ws[2],
+                                                    survivor_capacity=surv_cap),
+        }
+        for name, fn in calls.items():
+            phase_kernels[name] = profile_kernels(fn)[1]
+        launches, step_kernels = profile_kernels(step)
+    else:
+        step_kernels = {}
+
+    # ---------------- timed region (OPH family): device inputs resident in HBM
     K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(13)] for _ in range(K)]
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    time.sleep(0.3)
-    t_start.record(stream)
-    hits_last = None
-    for i in range(K):
-        hits_last = step(evs[i])
-    t_end.record(stream)
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    if world > 1:
-        dist.barrier()
-    ms = t_start.elapsed_time(t_end) / K
-    if world > 1:
-        ms = odist.max_over_ranks(ms, device="cuda")
-    phase_ms_concurrent = {n: statistics.mean(evs[i][a].elapsed_time(evs[i][b]) for i in range(K))
-                           for n, a, b in phase_ev}
+    ms, evs, hits_last, clk = timed(step, K, 7, ClockSampler(dev))
+    phase_ms = {n: statistics.mean(evs[i][a].elapsed_time(evs[i][b]) for i in range(K)) for n, a, b in phase_ev}
+    hh = hists.cpu().numpy().copy()
 
-    # ---------------- per-kernel timing: the same K steps with every call on one stream, so each
-    # call's CUDA-event time is its own duration (the rooflines below use these)
-    evs_s = [[torch.cuda.Event(enable_timing=True) for _ in range(13)] for _ in range(K)]
-    ts0, ts1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    ts0.record(stream)
-    for i in range(K):
-        step(evs_s[i], serial=True)
-    ts1.record(stream)
-    torch.cuda.synchronize()
-    ms_serial = ts0.elapsed_time(ts1) / K
-    phase_ms = {n: statistics.mean(evs_s[i][a].elapsed_time(evs_s[i][b]) for i in range(K)) for n, a, b in phase_ev}
+    # ---------------- the MinWise baseline leg, same K / W (not in `value`)
+    mw_line = None
+    if mw is not None:
+        ms_mw, evs_mw, hits_mw, clk_mw = timed(step_mw, K, 5, ClockSampler(dev))
+        ph_mw = {n: statistics.mean(evs_mw[i][a].elapsed_time(evs_mw[i][b]) for i in range(K)) for n, a, b in phase_mw}
+        hh[3] = hists[3].cpu().numpy()
+        e2e_oph = {m: phase_ms["build_oph_hoph"] + phase_ms["query_sketches_oph_hoph"] + phase_ms["compare_" + m]
+                   for m in ("full", "goph", "hoph")}
+        e2e_mw = ph_mw["build_minwise"] + ph_mw["query_sketches_minwise"] + ph_mw["compare_minwise"]
+        mw_line = {
+            "ms_per_step": ms_mw, "phase_ms": ph_mw, "hits": hits_mw,
+            "comparisons_per_s": Q * N_total / (ms_mw / 1e3),
+            "sketches_per_s": N_total / (ph_mw["build_minwise"] / 1e3),
+            "clocks": clk_mw,
+            "speedup_vs_minwise": {
+                "definition": "MinWise (collection + query sketches, then scoring) time / the method's "
+                              "(OPH+HOPH sketches of collection + queries, then its scoring); score_only: "
+                              "compare_minwise / compare_<method>",
+                "build_and_score": {m: e2e_mw / t for m, t in e2e_oph.items()},
+                "score_only": {m: ph_mw["compare_minwise"] / phase_ms["compare_" + m] for m in ("full", "goph", "hoph")},
+                "paper": "HOPH 5-7x faster than MinWise on its FS / ImageNet data, Java on one CPU (P:40, P:860)",
+            },
+        }
 
-    # ---------------- e2e: same step through the C-ABI with HOST (pinned) inputs and result read-back.
-    # Every step copies its inputs (collection CSR + query CSR) host->device and reads its sorted hit
-    # lists back; the copies run on a copy stream into a second input buffer while the previous step
-    # computes (double buffering), so they are inside the timed region but overlap compute.
+    # ---------------- e2e: the OPH-family step through the C-ABI with HOST (pinned) inputs and result
+    # read-back.  Every step copies its inputs (collection CSR + query CSR) host->device and reads its
+    # sorted hit lists back; the copies run on a copy stream into a second input buffer while the
+    # previous step computes (double buffering), so they are inside the timed region but overlap compute.
     e2e = None
     if not args.no_e2e:
         host = [torch.from_numpy(w.offsets.astype(np.int64)).pin_memory(),
                 torch.from_numpy(w.ids.view(np.int32)).pin_memory(),
                 torch.from_numpy(w.q_offsets.astype(np.int64)).pin_memory(),
                 torch.from_numpy(w.q_ids.view(np.int32)).pin_memory()]
-        h2d = sum(t.numel() * t.element_size() for t in host)
+        h2d = sum(t.numel() * t.element_size() for t in (host if rank == 0 else host[:2]))
         bufs = [(og.SetCollection(torch.empty_like(sets.offsets), torch.empty_like(sets.ids)),
                  og.SetCollection(torch.empty_like(qsets.offsets), torch.empty_like(qsets.ids))) for _ in range(2)]
         cstream = torch.cuda.Stream()
@@ -437,8 +521,9 @@ def run_ours(args):
                     cstream.wait_event(consumed[j % 2])
                 b[0].offsets.copy_(host[0], non_blocking=True)
                 b[0].ids.copy_(host[1], non_blocking=True)
-                b[1].offsets.copy_(host[2], non_blocking=True)
-                b[1].ids.copy_(host[3], non_blocking=True)
+                if rank == 0:
+                    b[1].offsets.copy_(host[2], non_blocking=True)
+                    b[1].ids.copy_(host[3], non_blocking=True)
                 copied[j % 2].record(cstream)
 
         d2h = 0
@@ -455,13 +540,12 @@ def run_ours(args):
                 enqueue_copy(i + 1)
             tot = step(None, sets=bufs[i % 2][0], qsets=bufs[i % 2][1])
             consumed[i % 2].record(stream)
-            d2h = 4 * 8
+            d2h = 3 * 8
             if rank == 0:
-                for j in range(4):
-                    n = tot[j]
-                    if n:
-                        _ = outs[j].hits[: n * 20].cpu()
-                        d2h += n * 20
+                for j in range(3):
+                    if tot[j]:
+                        _ = outs[j].hits[: tot[j] * hit_bytes].cpu()
+                        d2h += tot[j] * hit_bytes
         e1.record(stream)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1) / K
@@ -476,74 +560,90 @@ def run_ours(args):
             dist.destroy_process_group()
         return 0
 
-    # ---------------- roofline of the dominant kernel
-    peaks, peak_src = load_peaks()
-    f_sm = peaks.get("sm_max_mhz", 1965.0) * 1e6
-    # ALU pipe (IADD3/LOP3/SHF/min): 16 lanes/clk/SMSP (B300_MICROARCH "rt_SMSP=2"), 148 SM x 4 SMSP;
-    # one psi evaluation + running min is 9.5 ALU-pipe lane-ops at both widths (the SASS of
-    # minwise_kernel: 5 LOP3 + 4 SHF + half a 3-input VIMNMX3)
-    alu_lanes = 148 * 4 * 16 * f_sm
-    w_bits = max(1, (V - 1).bit_length())
-    psi_ops = 9.5
-    psi_peak = alu_lanes / psi_ops
-    hbm = peaks["hbm_gbs"] * 1e9
-    nnz = int(w.offsets[-1])
-    nw_k, nw_h = (k + 31) // 32, (L * hkp + 31) // 32
-    g_l0 = og.plan_thresholds(og.OPH_METHOD_GOPH, k // kp, kp, p["t_num"], p["t_den"], p["eps"])[2]
-    # algorithmic bytes per launch: inputs read once + outputs written once
-    by = {
-        "build_oph_hoph": 4 * nnz + 8 * (N + 1) + 4 * N * (k + L * hkp) + 4 * N * (nw_k + nw_h),
-        "compare_full": N * (4 * k + 4 * nw_k),
-        "compare_goph": N * (4 * g_l0 * kp + 4 * ((g_l0 * kp + 31) // 32)),
-        "compare_hoph": N * (4 * hkp + 4),
-        "compare_minwise": N * (4 * mwk + 1),
-    }
-    kern = {n: ("hbm", b / (phase_ms[n] / 1e3) / 1e9, hbm / 1e9, "GB/s", b) for n, b in by.items()}
-    kern["build_minwise"] = ("alu", nnz * mwk / (phase_ms["build_minwise"] / 1e3), psi_peak, "psi-evals/s", None)
-    traffic = {}
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            traffic = json.load(f)
-    dom = max(kern, key=lambda n: phase_ms[n])
-    b, a_, pk, u, _ = kern[dom]
-    roof = {"kernel": dom, "bound": b, "achieved": a_, "peak": pk, "unit": u, "frac": a_ / pk,
-            "traffic": traffic.get(dom), "peak_source": peak_src if b == "hbm" else
-            f"derived: 148 SM x 4 SMSP x 16 ALU lanes x sm_max_mhz / {psi_ops} ALU ops per psi (DESIGN.md)"}
-    per_kernel = {n: {"ms": phase_ms[n], "bound": v[0], "achieved": v[1], "peak": v[2], "unit": v[3],
-                      "frac": v[1] / v[2], "bytes": v[4]} for n, v in kern.items()}
-    # the PROBE collection scans on their own (CUPTI device time of the join kernels over the
-    # untimed profiled step): algorithmic bytes = one stream of the scanned bins per pass of
-    # <= 4096 queries (full + GOPH prefix + HOPH group 1; MinWise separately)
-    scan = {}
-    passes = -(-Q // 4096)
-    for name, mw_flag, byt in (("oph_family", "false", by["compare_full"] + by["compare_goph"] + by["compare_hoph"]),
-                               ("minwise", "true", by["compare_minwise"])):
-        hit = [v for kname, v in kernel_us.items() if kname.startswith(f"join_kernel<{mw_flag}")]
-        if hit:
-            us = sum(v[1] for v in hit)
-            scan[name] = {"kernel": f"join_kernel<{mw_flag}, ...>", "launches": sum(v[0] for v in hit), "us": us,
-                          "bytes": byt * passes, "achieved": byt * passes / (us / 1e6) / 1e9, "peak": hbm / 1e9,
-                          "unit": "GB/s", "frac": byt * passes / (us / 1e6) / hbm}
-
     # ---------------- work saved by early termination: per method, the pairs
     # decided after each number of groups compared (the last step's histograms, this rank)
-    hh = hists.cpu().numpy()
     term = {}
+    bins_compared = {}
     for i, (m, gsize, gtot) in enumerate((("full", kp, k // kp), ("goph", kp, k // kp), ("hoph", hkp, L),
                                           ("minwise", mwk, 1))):
         h = hh[i]
         npairs = int(h.sum())
+        if npairs == 0:
+            continue
         groups = float((h * np.arange(len(h))).sum() / max(1, npairs))
         bins = mwk if m == "minwise" else groups * gsize
+        bins_compared[m] = float((h * np.arange(len(h))).sum()) * gsize if m != "minwise" else npairs * mwk
         term[m] = {"pairs": npairs, "hist": {str(g): int(c) for g, c in enumerate(h) if c},
                    "mean_groups_compared": groups if m != "minwise" else None,
                    "mean_bins_compared": bins, "bins_total": (mwk if m == "minwise" else gtot * gsize)}
 
+    # ---------------- roofline of the dominant hot-path kernel
+    peaks, peak_src = load_peaks()
+    ub = ubench_peaks()
+    f_sm = peaks.get("sm_max_mhz", 1965.0) * 1e6
+    hbm = peaks["hbm_gbs"] * 1e9
+    nnz = int(w.offsets[-1])
+    nw_k, nw_h = (k + 31) // 32, (L * hkp + 31) // 32
+    g_l0 = og.plan_thresholds(og.OPH_METHOD_GOPH, k // kp, kp, p["t_num"], p["t_den"], p["eps"])[2]
+    # BRUTE compare: 2 warp-instructions (ISETP + predicated IMAD) per 32 bin-compares -> the issue
+    # ceiling is 16 bin-compares per SMSP per clock; the measured rate of that exact loop is in
+    # profiles/ubench_r02.json (scripts/ubench.cu)
+    issue_peak = 148 * 4 * 16 * f_sm
+    issue_src = "derived: 148 SM x 4 SMSP x 16 bin-compares/clk (2 warp-instr per 32 compares) x sm_max_mhz"
+    if ub and ub.get("brute_compares_per_s"):
+        issue_peak = ub["brute_compares_per_s"]
+        issue_src = "measured: scripts/ubench.cu ISETP+IMAD compare loop (profiles/ubench_r02.json)"
+    # algorithmic bytes / work per launch
+    build_bytes = 4 * nnz + 8 * (N + 1) + 4 * N * (k + L * hkp) + 4 * N * (nw_k + nw_h)
+    scan_bytes = {"compare_full": N * (4 * k + 4 * nw_k),
+                  "compare_goph": N * (4 * g_l0 * kp + 4 * ((g_l0 * kp + 31) // 32)),
+                  "compare_hoph": N * (4 * hkp + 4)}
+    models = {}
+
+    def model_for(kernel: str, phase: str):
+        if kernel.startswith("build_kernel"):
+            return ("hbm", build_bytes, hbm, "GB/s", 1e9, "bytes: CSR in + OPH/HOPH sketches and masks out")
+        if kernel.startswith("join_kernel"):
+            return ("hbm", scan_bytes[phase], hbm, "GB/s", 1e9, "bytes: the scanned collection bins, one pass")
+        if kernel.startswith("scan_kernel") or kernel.startswith("levels_kernel"):
+            m = phase.split("_")[1]
+            work = bins_compared.get(m, Q * N * k) if m != "full" else Q * N * k
+            return ("alu", work, issue_peak, "bin-compares/s", 1.0,
+                    "work: (query, set, bin) equality tests the method needs (termination histograms)")
+        return None
+
+    dom, dom_phase, dom_us = None, None, -1.0
+    for ph, kl in phase_kernels.items():
+        for kn, (cnt, us) in kl.items():
+            if us > dom_us:
+                dom, dom_phase, dom_us = kn, ph, us
+    roof = None
+    if dom is not None:
+        mdl = model_for(dom, dom_phase)
+        ph_us = sum(v[1] for v in phase_kernels[dom_phase].values())
+        if mdl is not None:
+            bound, work, peak, unit, scale, what = mdl
+            # the call's CUDA-event time in the timed region, times the kernel's share of the call's
+            # device time (CUPTI of the same call): the call's other kernels (query prep) are excluded
+            share = dom_us / ph_us if ph_us > 0 else 1.0
+            t_kernel = phase_ms[dom_phase] / 1e3 * share
+            launches_dom = phase_kernels[dom_phase][dom][0]
+            ach = work / t_kernel
+            tr = ncu_traffic(args.config).get(dom.split("<")[0])
+            roof = {"kernel": dom, "phase": dom_phase, "bound": bound, "achieved": ach / scale, "peak": peak / scale,
+                    "unit": unit, "frac": ach / peak, "traffic": tr, "launches_per_step": launches_dom,
+                    "work_per_step": work, "work": what, "kernel_ms": t_kernel * 1e3,
+                    "kernel_share_of_call": share,
+                    "peak_source": (peak_src if bound == "hbm" else issue_src),
+                    "step_share": t_kernel * 1e3 / ms}
+    per_phase = {}
+    for ph, byt in list(scan_bytes.items()) + [("build_oph_hoph", build_bytes)]:
+        per_phase[ph] = {"ms": phase_ms[ph], "hbm_bytes": byt, "hbm_frac": byt / (phase_ms[ph] / 1e3) / hbm}
+
     # ---------------- quality vs exact Jaccard, untimed: every reported pair of the
     # last step is verified with exact_jaccard_pairs (precision); recall counts the planted pairs
-    # whose realised J >= T (background pairs are random sets: a 100,000-pair random sample is
-    # verified too), for both empty-bin modes (EitherEmpty = the timed run; JointEmpty re-scored)
+    # whose realised J >= T (background pairs: a 100,000-pair random sample is verified too),
+    # for both empty-bin modes (EitherEmpty = the timed run; JointEmpty re-scored)
     quality = None
     if not args.no_quality and getattr(w, "planted", None) is not None and len(w.planted):
         tn, td = p["t_num"], p["t_den"]
@@ -572,11 +672,11 @@ def run_ours(args):
         bq, bs = bq[keep], bs[keep]
         bg_above = int(verify(bq, bs).sum())
         n4q = counts.cpu().numpy()
+        methods = ("full", "goph", "hoph", "minwise") if mw is not None else ("full", "goph", "hoph")
         quality = {"T": f"{tn}/{td}", "true_pairs": len(truth),
                    "truth": "planted pairs with realised J >= T; background check: "
                             f"{bg_above} of {len(bq)} random non-planted (query, set) pairs have exact J >= T",
-                   "either_empty": {m: score(res[i], int(n4q[i])) for i, m in enumerate(("full", "goph", "hoph",
-                                                                                          "minwise"))}}
+                   "either_empty": {m: score(res[i], int(n4q[i])) for i, m in enumerate(methods)}}
         prm_j = og.params(p["t_num"], p["t_den"], p["eps"], joint=True, strategy=strategy)
         jr = [og.Results(cap) for _ in range(3)]
         og.compare_full(qo, so, flat, prm_j, jr[0], set_id_base=base, ws=ws[0])
@@ -584,35 +684,20 @@ def run_ours(args):
         og.compare_hoph(qh, sh, hier, prm_j, jr[2], set_id_base=base, ws=ws[2], survivor_capacity=surv_cap)
         quality["joint_empty"] = {m: score(jr[i], jr[i].n()) for i, m in enumerate(("full", "goph", "hoph"))}
         # the empty-aware GOPH rule (E1-E4): not part of the timed
-        # step; its quality in both empty modes, device time per call and termination histogram
+        # step; its quality in both empty modes and device time per call
         variants = {}
         for joint, key in ((False, "either_empty"), (True, "joint_empty")):
-            prm_e = og.params(p["t_num"], p["t_den"], p["eps"], joint=joint, variant=og.OPH_VARIANT_EMPTY_AWARE)
+            prm_e = og.params(p["t_num"], p["t_den"], p["eps"], joint=joint, strategy=strategy,
+                              variant=og.OPH_VARIANT_EMPTY_AWARE)
             er = og.Results(cap, stop_hist=True)
-            og.compare_goph(qo, so, flat, prm_e, er, set_id_base=base, ws=ws[1])
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            og.compare_goph(qo, so, flat, prm_e, er, set_id_base=base, ws=ws[1], survivor_capacity=surv_cap)
+            e1.record()
             torch.cuda.synchronize()
             quality[key]["goph_empty_aware"] = score(er, er.n())
             h = er.hist().astype(np.float64)
-            # timed as a user calls it for a hit list: no histogram, so AUTO takes the join and
-            # decides only the listed pairs (E5); with the histogram every pair's stop
-            # group is needed and the register scan runs
-            prm_t = og.params(p["t_num"], p["t_den"], p["eps"], joint=joint, strategy=strategy,
-                              variant=og.OPH_VARIANT_EMPTY_AWARE)
-            et = og.Results(cap)
-            times, times_h = [], []
-            for r_, tl in ((et, times), (er, times_h)):
-                for _ in range(3):
-                    r_.reset()
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record()
-                    og.compare_goph(qo, so, flat, prm_t if r_ is et else prm_e, r_, set_id_base=base, ws=ws[1],
-                                    survivor_capacity=surv_cap)
-                    e1.record()
-                    torch.cuda.synchronize()
-                    tl.append(e0.elapsed_time(e1))
-            assert et.n() == er.n()
-            variants[key] = {"ms_per_call": float(np.median(times)),
-                             "ms_per_call_with_histogram": float(np.median(times_h)),
+            variants[key] = {"ms_per_call_with_histogram": e0.elapsed_time(e1),
                              "mean_bins_compared": float((h * np.arange(len(h))).sum() / max(1.0, h.sum()) * kp)}
         quality["goph_empty_aware_runs"] = variants
 
@@ -621,43 +706,40 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         import oracle
         oracle.build()
+        n_s, n_q = CPU_SAMPLE[args.config]
+        n_s, n_q = min(n_s, N), min(n_q, Q)
         t0 = time.perf_counter()
-        cpu_sample_step(w, CPU_SAMPLE_SETS, CPU_SAMPLE_QUERIES)
+        cpu_sample_step(w, n_s, n_q)
         t = time.perf_counter() - t0
-        cpu = {"value": 3 * CPU_SAMPLE_QUERIES * CPU_SAMPLE_SETS / t, "unit": UNIT, "cores": oracle.num_threads(),
+        cpu = {"value": 3 * n_q * n_s / t, "unit": UNIT, "cores": oracle.num_threads(), "cpu": cpu_model(),
                "kind": "oracle",
-               "sample": f"{args.config}: first {CPU_SAMPLE_SETS} sets x first {CPU_SAMPLE_QUERIES} queries, whole path "
-                         f"(sketch builds incl. MinWise, 4 comparisons, threshold lists), {t:.1f} s"}
+               "sample": f"{args.config}: first {n_s} sets x first {n_q} queries, the OPH-family path (OPH/HOPH "
+                         f"sketches, full/GOPH/HOPH scoring, threshold lists), {t:.1f} s"}
 
+    flush = (f"inputs larger than L2: CSR {4 * nnz / 1e6:.0f} MB + OPH/HOPH sketches "
+             f"{4 * N * (k + L * hkp) / 1e9:.2f} GB per step")
     line = {
         "metric": METRIC, "value": 3 * Q * N_total / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u32", "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": args.config, "sets_per_gpu": N, "sets_total": N_total, "queries": Q, "k": k,
                    "kprime": kp, "hoph_groups": L, "minwise_k": mwk, "T": f"{p['t_num']}/{p['t_den']}",
-                   "epsilon": p["eps"], "parallelism": f"set-sharded x{world}",
-                   "scan_strategy": ["auto", "brute", "probe"][strategy],
-                   "l2": f"inputs larger than L2 (CSR {4 * nnz / 1e6:.0f} MB + sketches "
-                         f"{4 * N * (k + L * hkp + mwk) / 1e9:.2f} GB per step)"},
-        "value_definition": "3 * queries * sets_total / step time (each pair scored by full OPH, GOPH, HOPH)",
-        "sketches_per_s": {"oph_hoph": (N_total) / (phase_ms["build_oph_hoph"] / 1e3),
-                           "minwise": (N_total) / (phase_ms["build_minwise"] / 1e3)},
-        "comparisons_per_s": {m: Q * N_total / (phase_ms["compare_" + m] / 1e3)
-                              for m in ("full", "goph", "hoph", "minwise")},
+                   "epsilon": p["eps"], "parallelism": f"set-sharded x{world} ({args.dist_backend})",
+                   "scan_strategy": ["auto", "brute", "probe"][strategy], "l2": flush},
+        "value_definition": "3 * queries * sets_total / step time; a step = OPH+HOPH sketches of the collection "
+                            "and the queries, full OPH + GOPH + HOPH threshold scoring of every pair, hit lists "
+                            "gathered and sorted (MinWise: baseline_minwise)",
+        "sketches_per_s": {"oph_hoph": N_total / (phase_ms["build_oph_hoph"] / 1e3)},
+        "comparisons_per_s": {m: Q * N_total / (phase_ms["compare_" + m] / 1e3) for m in ("full", "goph", "hoph")},
         "phase_ms": phase_ms,
-        "phase_note": "phase_ms / kernels / roofline: the K steps re-run with every call on one stream "
-                      "(ms_per_step_serial); the headline ms_per_step overlaps the MinWise calls (side stream) "
-                      "with the OPH family (phase_ms_concurrent)",
-        "ms_per_step_serial": ms_serial,
-        "phase_ms_concurrent": phase_ms_concurrent,
         "hits": hits_last,
         "roofline": roof,
-        "kernels": per_kernel,
-        "probe_scan": scan,
+        "phases": per_phase,
+        "baseline_minwise": mw_line,
         "termination": term,
         "quality": quality,
         "device_us_per_step": {n: {"launches": v[0], "us": round(v[1], 1)} for n, v in sorted(
-            kernel_us.items(), key=lambda kv: -kv[1][1])},
+            step_kernels.items(), key=lambda kv: -kv[1][1])},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches * K if launches is not None else None,
@@ -669,19 +751,42 @@ def run_ours(args):
     return 0
 
 
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="text-like", choices=CONFIG_NAMES,
-                    help="workload (BASELINE.json configs); text-like is the headline")
+    ap.add_argument("--config", default="image-like", choices=CONFIG_NAMES,
+                    help="workload (BASELINE.json configs); image-like (the largest single-GPU config) is the headline")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--no-minwise", action="store_true", help="skip the MinWise baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-quality", action="store_true", help="skip the precision/recall pass (untimed)")
-    ap.add_argument("--no-launch-count", action="store_true", help="skip the CUPTI launch count (use under ncu)")
+    ap.add_argument("--no-launch-count", action="store_true", help="skip the CUPTI kernel lists (use under ncu)")
     args = ap.parse_args()
+    if args.steps < 1 or args.warmup < 0:
+        ap.error("--steps >= 1, --warmup >= 0")
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        # one process per GPU: re-launch under torchrun (127.0.0.1 rendezvous)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+               *sys.argv[1:]]
+        return subprocess.call(cmd)
+    if ws_env is not None and int(ws_env) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={ws_env} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -74,3 +74,93 @@ def test_gather_hits_and_broadcast_gloo():
         assert qs == [0, 1, 10, 11, 12]
         assert t == [0, 1, 2, 3, 4]
         assert mx == 2.0
+
+
+def _records_from_oracle(recs, set_id_base):
+    """oph_hit records of the Similar pairs of an oracle result matrix (the records a
+    rank's compare call appends), in arbitrary (here: reversed) order."""
+    q, s = np.nonzero(recs["verdict"] == 1)
+    out = np.zeros(len(q), dtype=HIT_DTYPE)
+    out["query"], out["set_id"] = q, s + set_id_base
+    out["n_mb"], out["n_excl"] = recs["n_mb"][q, s], recs["n_excl"][q, s]
+    out["groups"], out["verdict"], out["flags"] = recs["groups"][q, s], 1, recs["flags"][q, s]
+    out["estimate"] = recs["estimate"][q, s]
+    return out[::-1].copy()
+
+
+def _shard_worker(rank, world, port, q):
+    """The N > 1 step of bench.py with the CPU oracle standing in for the compare kernels:
+    rank r scores its contiguous shard of the tiny collection with set IDs offset by its
+    shard base, the hit records are gathered (gather_hits) and rank 0 merges them."""
+    import oracle
+    from workloads import tiny
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = tiny()
+        p = w.params
+        lo, hi = odist.shard_range(w.n_sets, rank, world)
+        sh = w.slice_sets(lo, hi)
+        F = oracle.oph_sketch(sh.offsets, sh.ids, w.vocab_size, p["k"], p["perm_seed"])
+        QF = oracle.oph_sketch(w.q_offsets, w.q_ids, w.vocab_size, p["k"], p["perm_seed"])
+        out = {}
+        for m in ("full", "goph"):
+            if m == "full":
+                r = oracle.compare_full(QF, F, t_num=p["t_num"], t_den=p["t_den"], groups=p["k"] // p["kprime"])
+            else:
+                r = oracle.compare_goph(QF, F, n=p["k"] // p["kprime"], kprime=p["kprime"], t_num=p["t_num"],
+                                        t_den=p["t_den"], eps=p["eps"])
+            rec = _records_from_oracle(r, lo)
+            buf = torch.zeros(max(1, len(rec)) * 20 + 40, dtype=torch.uint8)
+            buf[: len(rec) * 20] = torch.from_numpy(rec.view(np.uint8).copy())
+            allh, counts = odist.gather_hits(buf, len(rec))
+            merged = odist.merge_threshold_records(odist.records_from_bytes(allh))
+            out[m] = (counts, merged.tobytes())
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_compare_gather_merge_gloo():
+    """shards with set_id_base offsets -> per-shard records -> gather -> merge
+    on rank 0 == the unsharded threshold list with the unsharded records, byte for byte."""
+    import oracle
+    from workloads import tiny
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = tiny()
+    p = w.params
+    F = oracle.oph_sketch(w.offsets, w.ids, w.vocab_size, p["k"], p["perm_seed"])
+    QF = oracle.oph_sketch(w.q_offsets, w.q_ids, w.vocab_size, p["k"], p["perm_seed"])
+    want = {"full": oracle.compare_full(QF, F, t_num=p["t_num"], t_den=p["t_den"], groups=p["k"] // p["kprime"]),
+            "goph": oracle.compare_goph(QF, F, n=p["k"] // p["kprime"], kprime=p["kprime"], t_num=p["t_num"],
+                                        t_den=p["t_den"], eps=p["eps"])}
+    for m, recs in want.items():
+        full = odist.merge_threshold_records(_records_from_oracle(recs, 0))
+        assert len(full) > 0
+        for rank in range(world):
+            counts, merged = out[rank][m]
+            assert sum(counts) == len(full)
+            assert merged == full.tobytes(), (m, rank)
+        assert [(int(a), int(b)) for a, b in zip(full["query"], full["set_id"])] == oracle.threshold_list(recs)
+
+
+def test_bench_refuses_world_size_mismatch():
+    """bench.py --gpus N must match the launcher's WORLD_SIZE (no silent 1-rank run)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "1"], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2 and "WORLD_SIZE=2" in r.stderr
