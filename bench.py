@@ -53,8 +53,9 @@ UNIT = "comparisons/s"
 CONFIG_NAMES = ["image-like", "text-like", "scale", "sweep-0.2", "sweep-0.5", "sweep-0.9", "tiny"]
 
 # bounded CPU samples of each workload for the oracle legs (about 5-10 s of CPU work each)
-CPU_SAMPLE = {"image-like": (2048, 16), "text-like": (20_000, 32), "scale": (20_000, 32),
-              "sweep-0.2": (2048, 16), "sweep-0.5": (2048, 16), "sweep-0.9": (2048, 16), "tiny": (2000, 100)}
+CPU_SAMPLE = {"image-like": (100_000, 64), "text-like": (100_000, 64), "scale": (100_000, 64),
+              "sweep-0.2": (100_000, 64), "sweep-0.5": (100_000, 64), "sweep-0.9": (100_000, 64),
+              "tiny": (2000, 100)}
 
 
 def load_peaks():
