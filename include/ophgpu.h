@@ -161,8 +161,21 @@ enum { OPH_VARIANT_PAPER = 0, OPH_VARIANT_EMPTY_AWARE = 1 };
  *          verified in the table, so only matching (query, set, bin) triples
  *          cost more than a filter test (cost ~ N bins + matches; best for
  *          low background similarity).  Sets matching more than 4 distinct
- *          queries are re-scanned by BRUTE. */
-enum { OPH_STRATEGY_AUTO = 0, OPH_STRATEGY_BRUTE = 1, OPH_STRATEGY_PROBE = 2 };
+ *          queries are re-scanned by BRUTE.
+ *   BITMAP: a value-indexed bitmap join in blocks of 1024 queries: per block, a
+ *          table over the |V| bin positions maps a value to the bitmask of the
+ *          queries holding it in that bin (built from the query sketches);
+ *          per (set, bin) a warp looks the set's value up and adds the mask to
+ *          bit-sliced per-query counters (carry-save adders), so 32 equality
+ *          tests cost ~3 lane-instructions; GOPH / HOPH thresholds are applied
+ *          to the bit-sliced states level by level (no survivor lists).
+ *          Applies to compare_full, compare_goph (Algorithm 1) and compare_hoph
+ *          with the 1:1 split (L <= 20) when |V| <= 2^23 and at most 1023
+ *          bins are compared; needs the workspace of oph_workspace_size_for.
+ *          AUTO uses it wherever it would otherwise scan BRUTE (and the
+ *          workspace is large enough); an explicit BITMAP request outside its
+ *          domain fails with OPH_EINVAL (OPH_ENOMEM: workspace too small). */
+enum { OPH_STRATEGY_AUTO = 0, OPH_STRATEGY_BRUTE = 1, OPH_STRATEGY_PROBE = 2, OPH_STRATEGY_BITMAP = 3 };
 
 /* One scored pair (20 bytes).
  *   full OPH : n_mb = N_mb, n_excl = excluded bins, over all k bins (Eq. 1-4)
@@ -251,6 +264,14 @@ oph_status minwise_build_sketches(const oph_sets *sets, uint64_t vocab_size, uin
  * 32 * n_sets is correct and larger capacities only save launches. */
 oph_status oph_workspace_size(uint32_t method, uint64_t n_queries, uint64_t n_sets, uint32_t n_bins,
                               uint64_t survivor_capacity, size_t *bytes);
+
+/* Workspace bytes for a compare_* call on these views and parameters: the
+ * bytes of oph_workspace_size plus, when the BITMAP strategy can apply
+ * (|V| <= 2^23, n_bins <= 1023, not MinWise), its per-block table (|V| x 4 B)
+ * and row masks ((1 + n_bins x 1024) x 128 B).  A workspace of only
+ * oph_workspace_size bytes keeps every other strategy. */
+oph_status oph_workspace_size_for(uint32_t method, const oph_sketches *queries, const oph_sketches *sets,
+                                  const oph_params *params, uint64_t survivor_capacity, size_t *bytes);
 
 /* Full-OPH scoring of every (query, set) pair (Eq. 1-6):
  * N_mb = #bins equal and both non-empty (R5), N_excl per empty_mode (R6),

@@ -31,7 +31,7 @@ OPH_RES_THRESHOLD, OPH_RES_DENSE = 0, 1
 OPH_SELECT_THRESHOLD, OPH_SELECT_TOPK = 0, 1
 OPH_METHOD_FULL, OPH_METHOD_GOPH, OPH_METHOD_HOPH, OPH_METHOD_MINWISE = range(4)
 OPH_FLAG_UNDEFINED, OPH_FLAG_EARLY = 1, 2
-OPH_STRATEGY_AUTO, OPH_STRATEGY_BRUTE, OPH_STRATEGY_PROBE = 0, 1, 2
+OPH_STRATEGY_AUTO, OPH_STRATEGY_BRUTE, OPH_STRATEGY_PROBE, OPH_STRATEGY_BITMAP = 0, 1, 2, 3
 OPH_VARIANT_PAPER, OPH_VARIANT_EMPTY_AWARE = 0, 1
 OPH_EMPTY = 0xFFFFFFFF
 MAX_GROUPS = 64
@@ -89,7 +89,7 @@ _lib = None
 
 # every symbol include/ophgpu.h declares
 EXPORTS = ["oph_status_string", "oph_sketch_ld", "oph_hier_layout_make", "oph_build_sketches",
-           "minwise_build_sketches", "oph_workspace_size", "compare_full", "compare_goph", "compare_hoph",
+           "minwise_build_sketches", "oph_workspace_size", "oph_workspace_size_for", "compare_full", "compare_goph", "compare_hoph",
            "compare_minwise", "oph_select_workspace_size", "topk_or_threshold_results", "oph_plan_thresholds",
            "exact_jaccard_pairs", "shingle_workspace_size", "shingle_text"]
 
@@ -337,8 +337,18 @@ def oph_workspace_size(method: int, n_queries: int, n_sets: int, n_bins: int, su
     return int(out.value)
 
 
-def _ws(ws, method, q: Sketches, s: Sketches, survivor_capacity):
-    nbytes = oph_workspace_size(method, q.n_sets, s.n_sets, q.n_bins, survivor_capacity)
+def oph_workspace_size_for(method: int, q: Sketches, s: Sketches, prm: oph_params, survivor_capacity: int = 0) -> int:
+    out = ctypes.c_size_t()
+    _check(lib().oph_workspace_size_for(c_u32(method), ctypes.byref(q.c()), ctypes.byref(s.c()), ctypes.byref(prm),
+                                        c_u64(survivor_capacity), ctypes.byref(out)), "oph_workspace_size_for")
+    return int(out.value)
+
+
+def _ws(ws, method, q: Sketches, s: Sketches, survivor_capacity, prm=None):
+    if prm is not None:
+        nbytes = oph_workspace_size_for(method, q, s, prm, survivor_capacity)
+    else:
+        nbytes = oph_workspace_size(method, q.n_sets, s.n_sets, q.n_bins, survivor_capacity)
     if ws is None:
         ws = Workspace()
     buf = ws.get(nbytes)
@@ -347,7 +357,7 @@ def _ws(ws, method, q: Sketches, s: Sketches, survivor_capacity):
 
 def _compare_full_impl(q: Sketches, s: Sketches, layout: oph_flat_layout, prm: oph_params, res: Results,
                  set_id_base: int = 0, ws: Optional[Workspace] = None, stream=None):
-    buf = _ws(ws, OPH_METHOD_FULL, q, s, 0)
+    buf = _ws(ws, OPH_METHOD_FULL, q, s, 0, prm)
     _check(lib().compare_full(ctypes.byref(q.c()), ctypes.byref(s.c()), c_u32(set_id_base), ctypes.byref(layout),
                               ctypes.byref(prm), ctypes.byref(res.c()), _ptr(buf), ctypes.c_size_t(buf.numel()),
                               _stream(stream)), "compare_full")
@@ -355,7 +365,7 @@ def _compare_full_impl(q: Sketches, s: Sketches, layout: oph_flat_layout, prm: o
 
 def _compare_goph_impl(q: Sketches, s: Sketches, layout: oph_flat_layout, prm: oph_params, res: Results,
                  set_id_base: int = 0, ws: Optional[Workspace] = None, survivor_capacity: int = 0, stream=None):
-    buf = _ws(ws, OPH_METHOD_GOPH, q, s, survivor_capacity)
+    buf = _ws(ws, OPH_METHOD_GOPH, q, s, survivor_capacity, prm)
     _check(lib().compare_goph(ctypes.byref(q.c()), ctypes.byref(s.c()), c_u32(set_id_base), ctypes.byref(layout),
                               ctypes.byref(prm), ctypes.byref(res.c()), _ptr(buf), ctypes.c_size_t(buf.numel()),
                               _stream(stream)), "compare_goph")
@@ -363,7 +373,7 @@ def _compare_goph_impl(q: Sketches, s: Sketches, layout: oph_flat_layout, prm: o
 
 def _compare_hoph_impl(q: Sketches, s: Sketches, layout: oph_hier_layout, prm: oph_params, res: Results,
                  set_id_base: int = 0, ws: Optional[Workspace] = None, survivor_capacity: int = 0, stream=None):
-    buf = _ws(ws, OPH_METHOD_HOPH, q, s, survivor_capacity)
+    buf = _ws(ws, OPH_METHOD_HOPH, q, s, survivor_capacity, prm)
     _check(lib().compare_hoph(ctypes.byref(q.c()), ctypes.byref(s.c()), c_u32(set_id_base), ctypes.byref(layout),
                               ctypes.byref(prm), ctypes.byref(res.c()), _ptr(buf), ctypes.c_size_t(buf.numel()),
                               _stream(stream)), "compare_hoph")
@@ -371,7 +381,7 @@ def _compare_hoph_impl(q: Sketches, s: Sketches, layout: oph_hier_layout, prm: o
 
 def _compare_minwise_impl(q: Sketches, s: Sketches, prm: oph_params, res: Results, set_id_base: int = 0,
                     ws: Optional[Workspace] = None, stream=None):
-    buf = _ws(ws, OPH_METHOD_MINWISE, q, s, 0)
+    buf = _ws(ws, OPH_METHOD_MINWISE, q, s, 0, prm)
     _check(lib().compare_minwise(ctypes.byref(q.c()), ctypes.byref(s.c()), c_u32(set_id_base), ctypes.byref(prm),
                                  ctypes.byref(res.c()), _ptr(buf), ctypes.c_size_t(buf.numel()), _stream(stream)),
            "compare_minwise")

@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libophgpu.so")
 SOURCES = ["ophgpu_host.cu", "ophgpu_kernels.cu"]
-DEPS = SOURCES + ["internal.h"]
+DEPS = SOURCES + ["internal.h", "bitjoin.cuh"]
 HEADER = os.path.join(os.path.dirname(HERE), "include", "ophgpu.h")
 
 NVCC_FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

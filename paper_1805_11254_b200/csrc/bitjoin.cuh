@@ -1,0 +1,382 @@
+// K7 BITMAP: the collection scan as a value-indexed bitmap join (included by
+// ophgpu_kernels.cu).
+//
+// The counts every method needs are N_mb(q, s) = #{b : F[b][s] == Q'[q][b]}
+// over the bins of the groups compared.  For a block of up to 1024 queries:
+//   * every bin value is a position p = start(b) + value in [0, |V|) (the
+//     bins tile the universe: the floor rule of P:158 / S:38 for the flat
+//     layout, the group ranges of P:466 for HOPH), so one table idx[p] of
+//     |V| entries (|V| <= 2^23) maps a collection value to the row of the
+//     queries holding that value in that bin (0 = none: row 0 is all zeros);
+//   * row r is a 1024-bit mask of those queries (32 words, lane = word).
+// A warp scores one set against the block: per bin it looks up the set's
+// value, broadcasts the row index and every lane adds its word of the row to
+// a bit-sliced counter of its 32 queries (carry-save adders, 16 bins per
+// batch: ~2.6 LOP3 per lane per bin), i.e. 32 equality tests per lane-word
+// instead of 32 ISETP + 32 IMAD per lane in the BRUTE scan.  The bit-sliced
+// counts ARE the paper's states: GOPH's M_c (Alg. 1 line 9) and HOPH's
+// T_l = S_l / 2^(L-1-l) = 2 T_(l-1) + M_l for the 1:1 weights c_j =
+// 2^(L-1-j) (R21).  Level thresholds compiled by the planner are applied as
+// bit-sliced comparisons with constants; the rare decided / candidate pairs
+// are extracted bit by bit and emitted with the same records as every other
+// strategy (bit-exact, R23).
+// ---------------------------------------------------------------------------
+
+constexpr uint32_t kBitQB = 1024;     // queries per block: 32 lanes x 32 bits
+constexpr uint32_t kBitMaxBins = 1023;  // bins scanned: counts fit 10 bit slices
+constexpr uint32_t kBitCS = 10;       // count slices: ones, twos, fours, eights, hi[6]
+constexpr uint32_t kBitTS = 24;       // HOPH T_l slices (L <= 20)
+constexpr int kBitWarps = 8;          // warps per CTA = consecutive sets per CTA tile
+
+// bin b -> (first position, width) of its value range
+__device__ __forceinline__ void bit_bin_range(const BitArgs &a, uint32_t b, uint32_t &start, uint32_t &width) {
+    const uint32_t r = b / a.bins_per_range, i = b - r * a.bins_per_range;
+    const RangeBins &R = a.ranges[r];
+    const uint64_t s0 = (uint64_t)i * R.len / a.bins_per_range;
+    const uint64_t s1 = (uint64_t)(i + 1) * R.len / a.bins_per_range;
+    start = (uint32_t)(R.start + s0);
+    width = (uint32_t)(s1 - s0);
+}
+
+// ---- per query block: the value -> row table and the rows
+// claim: the first (bin, query) holding a value takes a fresh row (rows are zeroed by
+// their claimer; row 0 is the shared all-zero row of "no query has this value")
+__global__ void bit_claim_kernel(const __grid_constant__ BitArgs a) {
+    const uint64_t n = (uint64_t)a.nscan * a.nqb;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = (uint32_t)(i / a.nqb), q = (uint32_t)(i % a.nqb);
+        const uint32_t v = a.QT[(uint64_t)b * a.ldq + a.qb0 + q];
+        uint32_t st, wd;
+        bit_bin_range(a, b, st, wd);
+        if (v >= wd) continue;  // the query-side empty bin (kQueryEmpty) matches nothing
+        uint32_t *slot = a.idx + st + v;
+        if (atomicCAS(slot, 0u, 0xFFFFFFFFu) == 0u) {
+            const uint32_t r = atomicAdd(a.nrows, 1u) + 1u;  // row 0 stays the zero row
+            uint4 *row = reinterpret_cast<uint4 *>(a.rows + (uint64_t)r * 32);
+#pragma unroll
+            for (int w = 0; w < 8; w++) row[w] = make_uint4(0, 0, 0, 0);
+            atomicExch(slot, r);
+        }
+    }
+}
+
+__global__ void bit_fill_kernel(const __grid_constant__ BitArgs a) {
+    const uint64_t n = (uint64_t)a.nscan * a.nqb;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = (uint32_t)(i / a.nqb), q = (uint32_t)(i % a.nqb);
+        const uint32_t v = a.QT[(uint64_t)b * a.ldq + a.qb0 + q];
+        uint32_t st, wd;
+        bit_bin_range(a, b, st, wd);
+        if (v >= wd) continue;
+        const uint32_t r = a.idx[st + v];
+        atomicOr(a.rows + (uint64_t)r * 32 + (q >> 5), 1u << (q & 31u));
+    }
+}
+
+// max over each word's 32 queries of the query's empty bins (the filter bound of the
+// final verdict, see bit_final)
+__global__ void bit_maxeq_kernel(const __grid_constant__ BitArgs a) {
+    const uint32_t q = threadIdx.x;  // one CTA of 1024 threads
+    uint32_t e = 0;
+    if (q < a.nqb) {
+        const uint32_t qg = a.qb0 + q;
+        for (uint32_t w = 0; w < a.nw; w++)
+            e += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + w), 0u, 0, w, a.nbins_total);
+    }
+    const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, e);
+    if ((q & 31u) == 0) a.max_eq[q >> 5] = m;
+}
+
+// ---- bit-sliced arithmetic (bit j of every slice word = query 32 lane + j)
+// (h, l) = full adder of three words: l = a ^ b ^ c, h = majority
+__device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b, uint32_t c) {
+    const uint32_t u = a ^ b;
+    h = (a & b) | (u & c);
+    l = u ^ c;
+}
+
+// add 16 input words (one per bin) to the count: c[0..3] = ones, twos, fours, eights
+// (the count mod 16, Harley-Seal), c[4..9] = count >> 4 (ripple add of the sixteens)
+__device__ __forceinline__ void csa16(uint32_t (&c)[kBitCS], const uint32_t (&x)[16]) {
+    uint32_t twosA, twosB, foursA, foursB, eightsA, eightsB, sixteens;
+    csa(twosA, c[0], c[0], x[0], x[1]);
+    csa(twosB, c[0], c[0], x[2], x[3]);
+    csa(foursA, c[1], c[1], twosA, twosB);
+    csa(twosA, c[0], c[0], x[4], x[5]);
+    csa(twosB, c[0], c[0], x[6], x[7]);
+    csa(foursB, c[1], c[1], twosA, twosB);
+    csa(eightsA, c[2], c[2], foursA, foursB);
+    csa(twosA, c[0], c[0], x[8], x[9]);
+    csa(twosB, c[0], c[0], x[10], x[11]);
+    csa(foursA, c[1], c[1], twosA, twosB);
+    csa(twosA, c[0], c[0], x[12], x[13]);
+    csa(twosB, c[0], c[0], x[14], x[15]);
+    csa(foursB, c[1], c[1], twosA, twosB);
+    csa(eightsB, c[2], c[2], foursA, foursB);
+    csa(sixteens, c[3], c[3], eightsA, eightsB);
+#pragma unroll
+    for (int i = 4; i < (int)kBitCS; i++) {
+        const uint32_t t = c[i] & sixteens;
+        c[i] ^= sixteens;
+        sixteens = t;
+    }
+}
+
+// bits whose NS-slice number is >= A (A may differ per lane; A >= 2^NS: none)
+template <int NS>
+__device__ __forceinline__ uint32_t sliced_ge(const uint32_t *c, uint32_t A) {
+    if (A >> NS) return 0u;
+    uint32_t gt = 0u, eq = 0xFFFFFFFFu;
+#pragma unroll
+    for (int i = NS - 1; i >= 0; i--) {
+        const uint32_t ai = 0u - ((A >> i) & 1u);
+        gt |= eq & c[i] & ~ai;
+        eq &= ~(c[i] ^ ai);
+    }
+    return gt | eq;
+}
+
+// the value of bit j of an NS-slice number
+template <int NS>
+__device__ __forceinline__ uint32_t sliced_get(const uint32_t *c, uint32_t j) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int i = 0; i < NS; i++) v |= ((c[i] >> j) & 1u) << i;
+    return v;
+}
+
+// matched bins of group g for query qg vs set s (query-major prepared values QM, as
+// level_kernel's group_matches)
+__device__ __forceinline__ uint32_t bit_group_matches(const BitArgs &a, uint32_t qg, uint64_t s, uint32_t g) {
+    const uint32_t *qp = a.QM + (uint64_t)qg * a.nb + (uint64_t)g * a.kp;
+    const uint32_t *fp = a.F + (uint64_t)g * a.kp * a.ld + s;
+    uint32_t m = 0;
+#pragma unroll 8
+    for (uint32_t i = 0; i < a.kp; i++) m += (__ldg(fp + (uint64_t)i * a.ld) == __ldg(qp + i));
+    return m;
+}
+
+// excluded bins of a pair among bins [b0, b1) (query-major masks QEM, set masks E)
+__device__ __forceinline__ uint32_t bit_excl(const BitArgs &a, uint32_t qg, uint64_t s, uint32_t b0, uint32_t b1) {
+    uint32_t ex = 0;
+    for (uint32_t w = b0 / 32; w * 32 < b1; w++) {
+        const uint32_t qm = __ldg(a.QEM + (uint64_t)qg * a.nw + w), sm = __ldg(a.E + (uint64_t)w * a.ld + s);
+        uint32_t x = a.joint ? (qm & sm) : (qm | sm);
+        const uint32_t lo = max(b0, 32 * w), hi = min(b1, 32 * w + 32);
+        const uint32_t width = hi - lo;
+        x &= (width == 32 ? 0xFFFFFFFFu : ((1u << width) - 1u)) << (lo - 32 * w);
+        ex += __popc(x);
+    }
+    return ex;
+}
+
+// HOPH final estimator of one pair (R21, R22), exact over lam = lcm(1..k'), as in
+// levels_kernel: groups with no usable bin dropped, weights renormalised
+__device__ void bit_hoph_final(const BitArgs &a, uint32_t qg, uint64_t s, uint32_t &nmb, uint32_t &ex_tot,
+                               uint32_t &verdict, uint32_t &flags, float &est) {
+    u128_t num = 0, csum = 0;
+    nmb = ex_tot = 0;
+    for (uint32_t g = 0; g < a.nlev; g++) {
+        const uint32_t m = bit_group_matches(a, qg, s, g);
+        const uint32_t ex = bit_excl(a, qg, s, g * a.kp, (g + 1) * a.kp);
+        nmb += m;
+        ex_tot += ex;
+        const uint32_t d = a.kp - ex;
+        if (d == 0) continue;
+        num += a.c[g] * m * (a.lam / d);
+        csum += a.c[g];
+    }
+    verdict = 0;
+    est = -1.0f;
+    flags = 0;
+    if (csum == 0) {
+        flags = OPH_FLAG_UNDEFINED;
+    } else {
+        verdict = num * a.t_den >= (u128_t)a.t_num * a.lam * csum;
+        est = (float)((double)num / ((double)a.lam * (double)csum));
+    }
+}
+
+// MODE 0: a count over the scanned bins (FULL: one level, the final verdict; GOPH:
+// levels of k' bins with thresholds on M_c).  MODE 1: HOPH 1:1, per-group counts
+// folded into T_l = 2 T_(l-1) + M_l, thresholds on T_l, the HOPH estimator at L.
+template <int MODE>
+__global__ void __launch_bounds__(32 * kBitWarps, 3) bit_scan_kernel(const __grid_constant__ BitArgs a) {
+    __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
+    for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
+        uint32_t st, wd;
+        bit_bin_range(a, b, st, wd);
+        s_start[b] = st;
+        s_width[b] = wd;
+    }
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    // this lane's word of the block: queries qb0 + 32 lane + j
+    const uint32_t qw0 = 32u * lane;
+    const uint32_t qvalid = qw0 >= a.nqb ? 0u : (a.nqb - qw0 >= 32u ? 0xFFFFFFFFu : ((1u << (a.nqb - qw0)) - 1u));
+    const uint32_t max_eq = a.max_eq[lane];
+    const uint32_t *rows_lane = a.rows + lane;
+    const uint32_t nlev_scan = MODE == 1 ? a.nlev : (a.method == kGoph ? a.nlev : 1u);
+    const uint32_t bins_per_level = MODE == 1 || a.method == kGoph ? a.kp : a.nscan;
+    const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
+
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t s = a.s_begin + tile * kBitWarps + warp;
+        if (s >= a.n_sets) continue;  // warp-uniform
+        const uint32_t *Fs = a.F + s;
+        uint32_t c[kBitCS];
+#pragma unroll
+        for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;
+        uint32_t T[MODE == 1 ? kBitTS : 1];
+#pragma unroll
+        for (int i = 0; i < (MODE == 1 ? (int)kBitTS : 1); i++) T[i] = 0u;
+        uint32_t alive = qvalid;
+
+        // row of (bin b, this set): the set's value of bin b, looked up in idx (lanes 0-15
+        // hold bins b0 + lane); rows are then broadcast by shuffle
+        auto lookup = [&](uint32_t b0, uint32_t nbat) -> uint32_t {
+            uint32_t r = 0;
+            if (lane < nbat) {
+                const uint32_t b = b0 + lane;
+                const uint32_t v = __ldg(Fs + (uint64_t)b * a.ld);
+                if (v < s_width[b]) r = __ldg(a.idx + s_start[b] + v);
+            }
+            return r;
+        };
+        for (uint32_t l = 1; l <= nlev_scan; l++) {
+            if (!__any_sync(0xFFFFFFFFu, alive != 0u)) break;  // every pair of this set is decided
+            const uint32_t lb0 = (l - 1) * bins_per_level;
+            const uint32_t lb1 = min(lb0 + bins_per_level, a.nscan);
+            if (MODE == 1) {
+#pragma unroll
+                for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;  // M_l: this group's count
+            }
+            uint32_t rn = lookup(lb0, min(16u, lb1 - lb0));
+            for (uint32_t b0 = lb0; b0 < lb1; b0 += 16) {
+                const uint32_t nbat = min(16u, lb1 - b0);
+                const uint32_t rc = rn;
+                uint32_t x[16];
+#pragma unroll
+                for (int u = 0; u < 16; u++) {
+                    const uint32_t r = __shfl_sync(0xFFFFFFFFu, rc, u);
+                    x[u] = __ldg(rows_lane + (uint64_t)r * 32);  // r = 0 (no row, or past nbat): zero row
+                }
+                if (b0 + 16 < lb1) rn = lookup(b0 + 16, min(16u, lb1 - b0 - 16));
+                csa16(c, x);
+            }
+            // ---- decisions at the end of level l
+            const bool last = l == (MODE == 1 ? a.nlev : nlev_scan);
+            uint32_t acc = 0u, dec = 0u;
+            if (MODE == 1) {
+                // T_l = 2 T_(l-1) + M_l (bit-sliced shift, then ripple add of the 6-bit M_l)
+#pragma unroll
+                for (int i = (int)kBitTS - 1; i >= 1; i--) T[i] = T[i - 1];
+                T[0] = 0u;
+                uint32_t carry = 0u;
+#pragma unroll
+                for (int i = 0; i < (int)kBitTS; i++) {
+                    const uint32_t m = i < 6 ? c[i] : 0u;  // M_l <= 32: slices 1 .. 32
+                    const uint32_t t = T[i];
+                    T[i] = t ^ m ^ carry;
+                    carry = (t & m) | ((t ^ m) & carry);
+                }
+            }
+            if (!last && a.thr_on[l - 1]) {
+                const uint32_t A = a.acc_cnt[l - 1];
+                const int32_t R = a.rej_cnt[l - 1];
+                if (MODE == 1) {
+                    acc = sliced_ge<kBitTS>(T, A);
+                    dec = acc | (R >= 0 ? ~sliced_ge<kBitTS>(T, (uint32_t)R + 1u) : 0u);
+                } else {
+                    acc = sliced_ge<kBitCS>(c, A);
+                    dec = acc | (R >= 0 ? ~sliced_ge<kBitCS>(c, (uint32_t)R + 1u) : 0u);
+                }
+                acc &= alive;
+                dec &= alive;
+                hist_add(a.out.hist, l, __popc(dec));
+                uint32_t want = a.out.dense ? dec : acc;
+                while (__any_sync(0xFFFFFFFFu, want != 0u)) {
+                    const bool has = want != 0u;
+                    const uint32_t j = has ? __ffs(want) - 1 : 0u;
+                    want &= want - 1u;
+                    const uint32_t qg = a.qb0 + qw0 + j;
+                    uint32_t nmb = 0, ex = 0;
+                    if (has) {
+                        if (MODE == 1) {
+                            for (uint32_t g = 0; g < l; g++) nmb += bit_group_matches(a, qg, s, g);
+                        } else {
+                            nmb = sliced_get<kBitCS>(c, j);
+                        }
+                        ex = bit_excl(a, qg, s, 0, l * a.kp);
+                    }
+                    emit(a.out, has, qg, s, nmb, ex, l, (acc >> j) & 1u, OPH_FLAG_EARLY, -1.0f);
+                }
+                alive &= ~dec;
+            }
+            if (!last) continue;
+            // ---- the final verdict of every pair still alive
+            hist_add(a.out.hist, MODE == 1 ? a.nlev : a.level_final, __popc(alive));
+            if (MODE == 1) {
+                uint32_t want = alive;
+                while (__any_sync(0xFFFFFFFFu, want != 0u)) {
+                    const bool has = want != 0u;
+                    const uint32_t j = has ? __ffs(want) - 1 : 0u;
+                    want &= want - 1u;
+                    const uint32_t qg = a.qb0 + qw0 + j;
+                    uint32_t nmb = 0, ex = 0, verdict = 0, flags = 0;
+                    float est = -1.0f;
+                    if (has) bit_hoph_final(a, qg, s, nmb, ex, verdict, flags, est);
+                    emit(a.out, has, qg, s, nmb, ex, a.nlev, verdict, flags, est);
+                }
+            } else {
+                // full-OPH verdict (Eq. 6): den = k - N_excl >= k - (max_q |Eq| + |Es|) (EitherEmpty)
+                // or k - min(max_q |Eq|, |Es|) (JointEmpty), so a pair can only be Similar if
+                // N_mb >= ceil(t_num den_min / t_den): the candidates, verified exactly
+                const uint32_t es_w = lane < a.nw ? __ldg(a.E + (uint64_t)lane * a.ld + s) : 0u;
+                const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, a.nbins_total));
+                const uint32_t k = a.nbins_total;
+                uint32_t den_min = a.joint ? k - min(max_eq, es) : k - min(k, max_eq + es);
+                const uint32_t theta =
+                    a.out.dense ? 0u : (uint32_t)(((uint64_t)a.t_num * den_min + a.t_den - 1) / a.t_den);
+                uint32_t want = sliced_ge<kBitCS>(c, theta) & alive;
+                while (__any_sync(0xFFFFFFFFu, want != 0u)) {
+                    const bool has = want != 0u;
+                    const uint32_t j = has ? __ffs(want) - 1 : 0u;
+                    want &= want - 1u;
+                    const uint32_t qg = a.qb0 + qw0 + j;
+                    uint32_t ex = 0;
+                    for (uint32_t w = 0; w < a.nw; w++) {
+                        const uint32_t sw = __shfl_sync(0xFFFFFFFFu, es_w, w);
+                        if (has) ex += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + w), sw, a.joint, w, k);
+                    }
+                    const uint32_t nmb = sliced_get<kBitCS>(c, j);
+                    const uint32_t den = k - ex;
+                    const bool undef = den == 0;
+                    const uint32_t verdict = !undef && (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
+                    emit(a.out, has, qg, s, nmb, ex, a.level_final, verdict, undef ? OPH_FLAG_UNDEFINED : 0u,
+                         undef ? -1.0f : (float)nmb / (float)den);
+                }
+            }
+            alive = 0u;
+        }
+    }
+}
+
+cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
+    cudaError_t e;
+    // the value -> row table of this block: clear, claim rows, set the bits
+    if ((e = cudaMemsetAsync(a.idx, 0, (size_t)a.vpos * 4, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(a.nrows, 0, 4, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(a.rows, 0, 128, st)) != cudaSuccess) return e;  // the zero row
+    const uint64_t n = (uint64_t)a.nscan * a.nqb;
+    const unsigned g = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    bit_claim_kernel<<<g, 256, 0, st>>>(a);
+    bit_fill_kernel<<<g, 256, 0, st>>>(a);
+    bit_maxeq_kernel<<<1, 1024, 0, st>>>(a);
+    // the scan: 8 consecutive sets per CTA tile, grid-stride; 3 CTAs per SM
+    const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
+    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * 3 * 8);
+    if (a.mode_hoph) bit_scan_kernel<1><<<grid, 32 * kBitWarps, 0, st>>>(a);
+    else bit_scan_kernel<0><<<grid, 32 * kBitWarps, 0, st>>>(a);
+    return cudaGetLastError();
+}

@@ -204,6 +204,33 @@ struct LevelArgs {
     uint32_t mr1;           // min{m : P(X >= m) <= eps} - 1
 };
 
+// BITMAP strategy (bitjoin.cuh): one block of <= 1024 queries against the collection
+struct BitArgs {
+    const uint32_t *F, *E;  // collection values [nb][ld], masks [nw][ld]
+    uint64_t n_sets, ld, s_begin;  // sets [s_begin, n_sets) are scanned
+    const uint32_t *QT;     // prepared queries, bin-major [nb][ldq]
+    uint64_t ldq;
+    const uint32_t *QM;     // prepared queries, query-major [n_q][nb]
+    const uint32_t *QEM;    // query masks, query-major [n_q][nw]
+    uint32_t nb, nw, nscan, kp, nlev, nbins_total;
+    uint32_t qb0, nqb;      // this block: query columns [qb0, qb0 + nqb), nqb <= 1024
+    uint32_t method, mode_hoph, joint, t_num, t_den, level_final;
+    // value ranges of the bins: bin b = range b / bins_per_range, floor rule inside it
+    uint32_t bins_per_range;
+    RangeBins ranges[kMaxGroups];
+    uint32_t thr_on[kMaxGroups];    // level l (index l-1) has a threshold
+    uint32_t acc_cnt[kMaxGroups];   // Similar iff state >= acc_cnt (GOPH: M_c; HOPH: T_l)
+    int32_t rej_cnt[kMaxGroups];    // NotSimilar iff state <= rej_cnt (-1: never)
+    u128_t c[kMaxGroups];           // HOPH weights (final estimator)
+    u128_t lam;                     // lcm(1..kp)
+    uint32_t *idx;                  // [vpos] position -> row (0: the zero row)
+    uint64_t vpos;                  // |V|
+    uint32_t *rows;                 // [1 + rows][32] query bitmasks
+    uint32_t *nrows;                // rows claimed
+    uint32_t *max_eq;               // [32] per query word: max empty bins of its queries
+    OutArgs out;
+};
+
 struct PrepArgs {
     const uint32_t *values;  // caller's query sketches [nb][ld_in]
     const uint32_t *empty;   // [nw][ld_in] or null
@@ -247,6 +274,7 @@ cudaError_t launch_level(const LevelArgs &a, cudaStream_t st);
 cudaError_t launch_level_e(const LevelArgs &a, cudaStream_t st);  // empty-aware rule over a survivor list
 cudaError_t launch_levels_scan(const LevelArgs &a, cudaStream_t st);
 cudaError_t launch_jaccard(const JaccardArgs &a, cudaStream_t st);
+cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st);
 size_t shingle_temp_bytes(uint64_t n_bytes, uint64_t n_docs);
 cudaError_t run_shingle(const ShingleArgs &a, void *ws, size_t ws_bytes, cudaStream_t st);
 size_t select_temp_bytes(uint64_t n);

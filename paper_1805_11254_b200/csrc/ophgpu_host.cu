@@ -403,6 +403,14 @@ Ws carve_ws(void *base, uint64_t n_q, uint64_t n_sets, uint32_t nb, uint64_t cap
 
 size_t surv_region_bytes(uint64_t cap) { return 2 * (align256(cap * 4) * 3 + align256(cap * 16)); }
 
+// BITMAP strategy (bitjoin.cuh): domain and workspace region (after the fixed part)
+constexpr uint64_t kBitMaxV = 1ull << 23;
+constexpr uint32_t kBitMaxNb = 1023;
+bool bitmap_sizes_ok(uint64_t V, uint32_t nb) { return V <= kBitMaxV && nb <= kBitMaxNb; }
+size_t bitmap_region_bytes(uint64_t V, uint32_t nb) {
+    return align256(V * 4) + align256((1 + (uint64_t)nb * 1024) * 128) + align256(4) + align256(32 * 4);
+}
+
 // largest survivor capacity that fits in ws_bytes
 uint64_t cap_from_ws(size_t ws_bytes, size_t fixed) {
     if (ws_bytes <= fixed) return 0;
@@ -414,6 +422,98 @@ uint64_t cap_from_ws(size_t ws_bytes, size_t fixed) {
     return lo;
 }
 
+// ---------------------------------------------------------------- the BITMAP driver
+// Query prep, then per block of 1024 queries: the value -> row table (bit_claim / bit_fill)
+// and one scan of the collection deciding every level (bit_scan_kernel).  No host
+// synchronisation, no survivor lists.
+oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketches *Sv, uint32_t set_id_base,
+                      uint32_t nb, uint32_t nw, uint32_t nlev, uint32_t kp, const Plan &plan, const oph_params *p,
+                      oph_results *res, void *d_ws, size_t fixed, cudaStream_t stream) {
+    const uint64_t n_q = Qv->n_sets, n_s = Sv->n_sets, V = Qv->vocab_size;
+    Ws w = carve_ws(d_ws, n_q, n_s, nb, 0);
+    char *bp = (char *)d_ws + fixed;
+    BitArgs ba{};
+    ba.idx = (uint32_t *)bp; bp += align256(V * 4);
+    ba.rows = (uint32_t *)bp; bp += align256((1 + (uint64_t)nb * 1024) * 128);
+    ba.nrows = (uint32_t *)bp; bp += align256(4);
+    ba.max_eq = (uint32_t *)bp;
+    ba.vpos = V;
+
+    PrepArgs pa{};
+    pa.values = Qv->d_values;
+    pa.empty = Qv->d_empty;
+    pa.ld_in = Qv->ld;
+    pa.n_q = (uint32_t)n_q;
+    pa.nb = nb;
+    pa.nw = nw;
+    pa.remap = 1;
+    pa.QT = w.QT;
+    pa.QE = w.QE;
+    pa.QM = w.QM;
+    pa.QEM = w.QEM;
+    pa.qflags = w.qflags;
+    pa.ldq = w.ldq;
+    if (launch_prep(pa, stream) != cudaSuccess) return OPH_ECUDA;
+
+    ba.F = Sv->d_values;
+    ba.E = Sv->d_empty;
+    ba.n_sets = n_s;
+    ba.ld = Sv->ld;
+    ba.s_begin = 0;
+    ba.QT = w.QT;
+    ba.ldq = w.ldq;
+    ba.QM = w.QM;
+    ba.QEM = w.QEM;
+    ba.nb = nb;
+    ba.nw = nw;
+    ba.nscan = nb;
+    ba.kp = kp;
+    ba.nbins_total = nb;
+    ba.method = method;
+    ba.mode_hoph = method == OPH_METHOD_HOPH;
+    ba.joint = p->empty_mode == OPH_EMPTY_JOINT;
+    ba.t_num = p->t_num;
+    ba.t_den = p->t_den;
+    ba.nlev = method == OPH_METHOD_FULL ? 1 : nlev;
+    ba.level_final = method == OPH_METHOD_FULL ? nb / kp : nlev;
+    ba.out.hits = res->d_hits;
+    ba.out.cap = res->capacity;
+    ba.out.count = res->d_count;
+    ba.out.dense = res->mode == OPH_RES_DENSE;
+    ba.out.set_id_base = set_id_base;
+    ba.out.n_sets = n_s;
+    ba.out.hist = res->d_stop_hist;
+    // the bins' value ranges: flat = one range of nb bins; HOPH = nlev group ranges of kp bins
+    if (method == OPH_METHOD_HOPH) {
+        oph_hier_layout lay;
+        if (oph_hier_layout_make(V, 1, 1, kp, &lay) != OPH_OK || lay.L != nlev) return OPH_EINCOMPAT;
+        ba.bins_per_range = kp;
+        for (uint32_t g = 0; g < nlev; g++) ba.ranges[g] = make_range(lay.start[g], lay.len[g], kp);
+        for (uint32_t j = 0; j < nlev; j++) ba.c[j] = plan.c[j];
+        ba.lam = plan.lam;
+    } else {
+        ba.bins_per_range = nb;
+        ba.ranges[0] = make_range(0, V, nb);
+    }
+    // level thresholds on the bit-sliced states: GOPH M_c as compiled; HOPH S_l = 2^(L-1-l) T_l,
+    // so S_l >= A <=> T_l >= ceil(A / 2^(L-1-l)) and S_l <= R <=> T_l <= floor(R / 2^(L-1-l))
+    for (uint32_t l = 1; method != OPH_METHOD_FULL && l < nlev; l++) {
+        const LevelThr &T = plan.thr[l - 1];
+        const uint32_t sh = method == OPH_METHOD_HOPH ? nlev - 1 - l : 0;
+        const u128 div = (u128)1 << sh;
+        u128 A = T.acc == kNeverAcc ? (u128)UINT32_MAX : (T.acc + div - 1) / div;
+        ba.acc_cnt[l - 1] = A >= (u128)UINT32_MAX ? UINT32_MAX : (uint32_t)A;
+        ba.rej_cnt[l - 1] = T.rej < 0 ? -1 : (int32_t)std::min<i128>(T.rej / (i128)div, (i128)INT32_MAX);
+        ba.thr_on[l - 1] = ba.acc_cnt[l - 1] != UINT32_MAX || ba.rej_cnt[l - 1] >= 0;
+    }
+    for (uint64_t q0 = 0; q0 < n_q; q0 += 1024) {
+        ba.qb0 = (uint32_t)q0;
+        ba.nqb = (uint32_t)std::min<uint64_t>(1024, n_q - q0);
+        if (launch_bit_block(ba, stream) != cudaSuccess) return OPH_ECUDA;
+    }
+    return OPH_OK;
+}
+
 // ---------------------------------------------------------------- the compare driver
 oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketches *Sv, uint32_t set_id_base,
                        uint32_t k_or_L, uint32_t kp, uint32_t a, uint32_t b, const oph_params *p, oph_results *res,
@@ -422,7 +522,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     oph_status st;
     if ((st = check_view(Qv, !mw, mw)) || (st = check_view(Sv, !mw, mw)) || (st = check_params(p))) return st;
     if (!res || !res->d_hits || !res->d_count || res->mode > OPH_RES_DENSE) return OPH_EINVAL;
-    if (p->strategy > OPH_STRATEGY_PROBE || p->variant > OPH_VARIANT_EMPTY_AWARE) return OPH_EINVAL;
+    if (p->strategy > OPH_STRATEGY_BITMAP || p->variant > OPH_VARIANT_EMPTY_AWARE) return OPH_EINVAL;
     // the empty-aware GOPH rule (E1-E4) runs as one register scan of every group
     const bool ea = p->variant == OPH_VARIANT_EMPTY_AWARE;
     if (ea && method != OPH_METHOD_GOPH) return OPH_EINVAL;
@@ -447,6 +547,35 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     }
 
     const size_t fixed = ws_fixed_bytes(n_q, n_s, nb);
+
+    // BITMAP (bitjoin.cuh): full OPH, GOPH (Algorithm 1) and HOPH with power-of-two weights
+    // (the 1:1 split: T_l = S_l / 2^(L-1-l) in <= 24 bit slices), |V| <= 2^23, <= 1023 bins
+    {
+        const bool dom = !mw && !ea && bitmap_sizes_ok(Qv->vocab_size, nb) &&
+                         (method != OPH_METHOD_HOPH || (a == 1 && b == 1 && nlev >= 2 && nlev <= 20 && plan.lam));
+        const bool fits = ws_bytes >= fixed + bitmap_region_bytes(Qv->vocab_size, nb);
+        bool use = false;
+        if (p->strategy == OPH_STRATEGY_BITMAP) {
+            if (!dom) return OPH_EINVAL;
+            if (!fits) return OPH_ENOMEM;
+            use = true;
+        } else if (p->strategy == OPH_STRATEGY_AUTO && dom && fits) {
+            // AUTO: where PROBE would not apply, or this collection was found to be a BRUTE one
+            const bool probe_ok =
+                res->mode != OPH_RES_DENSE &&
+                (method == OPH_METHOD_FULL ||
+                 (method == OPH_METHOD_GOPH && (plan.l0 == nlev || plan.thr[plan.l0 - 1].rej >= 0)) ||
+                 (method == OPH_METHOD_HOPH && (nlev == 1 || plan.thr[0].rej >= 0)));
+            int cached = -1;
+            {
+                std::lock_guard<std::mutex> g(g_auto_mu);
+                auto it = g_auto.find(AutoKey{(uintptr_t)Sv->d_values, n_s, nb, method});
+                if (it != g_auto.end()) cached = it->second;
+            }
+            use = !probe_ok || cached == 1;
+        }
+        if (use) return run_bitmap(method, Qv, Sv, set_id_base, nb, nw, nlev, kp, plan, p, res, d_ws, fixed, stream);
+    }
     uint64_t chunk = ceil_div(n_q, 32) * 32;
     uint64_t cap = 0;
     const bool levels = (method == OPH_METHOD_GOPH || method == OPH_METHOD_HOPH) && (plan.l0 < nlev || ea);
@@ -977,6 +1106,18 @@ oph_status oph_workspace_size(uint32_t method, uint64_t n_q, uint64_t n_sets, ui
     size_t b = ws_fixed_bytes(n_q, n_sets, n_bins);
     if (method == OPH_METHOD_GOPH || method == OPH_METHOD_HOPH) b += surv_region_bytes(std::max<uint64_t>(cap, 32 * n_sets));
     *bytes = b;
+    return OPH_OK;
+}
+
+oph_status oph_workspace_size_for(uint32_t method, const oph_sketches *q, const oph_sketches *s,
+                                  const oph_params *p, uint64_t cap, size_t *bytes) {
+    if (!q || !s || !p || !bytes) return OPH_EINVAL;
+    oph_status st = oph_workspace_size(method, q->n_sets, s->n_sets, q->n_bins, cap, bytes);
+    if (st != OPH_OK) return st;
+    if (method != OPH_METHOD_MINWISE && p->variant == OPH_VARIANT_PAPER && bitmap_sizes_ok(q->vocab_size, q->n_bins) &&
+        (p->strategy == OPH_STRATEGY_AUTO || p->strategy == OPH_STRATEGY_BITMAP))
+        *bytes = std::max(*bytes, ws_fixed_bytes(q->n_sets, s->n_sets, q->n_bins) +
+                                      bitmap_region_bytes(q->vocab_size, q->n_bins));
     return OPH_OK;
 }
 

@@ -13,6 +13,8 @@
 //   K4 level_kernel     one GOPH/HOPH level over the compacted survivors;
 //                       the last level applies the final verdict            a7-a8
 //   K6 run_select       threshold / top-k result lists (CUB radix sort)     a10
+//   K7 bit_scan_kernel  BITMAP: value-indexed bitmap join, bit-sliced counts
+//                       (bitjoin.cuh): full OPH / GOPH / HOPH 1:1         a6-a8
 //   -- jaccard_kernel   exact Jaccard of hit pairs (quality check)
 //   -- sh_* kernels     text shingling (ingestion before K1)
 //
@@ -2262,5 +2264,7 @@ cudaError_t run_shingle(const ShingleArgs &a, void *ws, size_t ws_bytes, cudaStr
     sh_output<<<gt, 256, 0, st>>>(a, w.k0, w.n_unique);
     return cudaGetLastError();
 }
+
+#include "bitjoin.cuh"
 
 }  // namespace ophgpu

@@ -18,10 +18,13 @@ def gpu_build(offsets, ids, V, seed, k=None, kprime=None, hier=None, identity=Fa
     return sets, so, sh
 
 
-def gpu_dense(method, q, s, *, layout=None, t_num, t_den, eps=1e-4, joint=False, survivor_capacity=0):
-    """Dense per-pair records [n_q, n_s] from the GPU."""
+def gpu_dense(method, q, s, *, layout=None, t_num, t_den, eps=1e-4, joint=False, survivor_capacity=0,
+              strategy=og.OPH_STRATEGY_AUTO):
+    """Dense per-pair records [n_q, n_s] from the GPU (AUTO: the BITMAP join where it
+    applies -- |V| <= 2^23, not MinWise -- else the BRUTE scan)."""
     res = og.Results(q.n_sets * s.n_sets, dense=True)
-    prm = og.params(t_num, t_den, eps, joint, variant=og.OPH_VARIANT_EMPTY_AWARE if method == "goph_e" else 0)
+    prm = og.params(t_num, t_den, eps, joint, strategy,
+                    variant=og.OPH_VARIANT_EMPTY_AWARE if method == "goph_e" else 0)
     if method == "full":
         og.compare_full(q, s, layout, prm, res)
     elif method in ("goph", "goph_e"):
@@ -75,7 +78,8 @@ def gpu_threshold_hits(method, q, s, *, layout=None, t_num, t_den, eps=1e-4, joi
 
 
 def oracle_records(method, Q, S, *, t_num, t_den, eps=1e-4, joint=False, k=None, kprime=None, L=None, a=1, b=1,
-                   qflags=None, sflags=None):
+                   qflags=None, sflags=None, strategy=None):
+    """The oracle's dense records (`strategy` is the GPU's and ignored here)."""
     if method == "full":
         return oracle.compare_full(Q, S, t_num=t_num, t_den=t_den, joint=joint, groups=k // kprime)
     if method in ("goph", "goph_e"):

@@ -86,31 +86,37 @@ def test_tiny_sketches_bit_exact(tiny_run):
     assert (r["mw"].flags.cpu().numpy()[: len(fl)] == fl).all()
 
 
+@pytest.mark.parametrize("strategy", [og.OPH_STRATEGY_BRUTE, og.OPH_STRATEGY_BITMAP])
 @pytest.mark.parametrize("joint", [False, True])
 @pytest.mark.parametrize("method", ["full", "goph", "hoph", "minwise"])
-def test_tiny_dense_records(tiny_run, method, joint):
+def test_tiny_dense_records(tiny_run, method, joint, strategy):
     r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
-    if method == "minwise" and joint:
-        pytest.skip("MinWise has no empty bins")
-    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"], joint=joint)
+    if method == "minwise" and (joint or strategy == og.OPH_STRATEGY_BITMAP):
+        pytest.skip("MinWise has no empty bins / no BITMAP join")
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"], joint=joint, strategy=strategy)
     if method in ("full", "goph"):
         lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
         g = gpu_dense(method, r["qo"], r["so"], layout=lay, **kw)
+        kw.pop("strategy")
         want = oracle_records(method, o["QF"], o["F"], k=p["k"], kprime=p["kprime"], **kw)
     elif method == "hoph":
         g = gpu_dense(method, r["qh"], r["sh"], layout=r["hier"], **kw)
+        kw.pop("strategy")
         want = oracle_records(method, o["QH"], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw)
     else:
         g = gpu_dense(method, r["qmw"], r["mw"], **kw)
+        kw.pop("strategy")
         want = oracle_records(method, o["QMW"][0], o["MW"][0], qflags=o["QMW"][1], sflags=o["MW"][1], **kw)
-    assert_records_equal(g, want, f"tiny {method} joint={joint}")
+    assert_records_equal(g, want, f"tiny {method} joint={joint} strategy={strategy}")
 
 
-@pytest.mark.parametrize("strategy", [og.OPH_STRATEGY_BRUTE, og.OPH_STRATEGY_PROBE])
+@pytest.mark.parametrize("strategy", [og.OPH_STRATEGY_BRUTE, og.OPH_STRATEGY_PROBE, og.OPH_STRATEGY_BITMAP])
 @pytest.mark.parametrize("method", ["full", "goph", "hoph", "minwise"])
 def test_tiny_threshold_lists(tiny_run, method, strategy):
-    """Threshold hit lists (sorted by (query, set_id)) == oracle's, with set_id_base, for both scan strategies."""
+    """Threshold hit lists (sorted by (query, set_id)) == oracle's, with set_id_base, for every scan strategy."""
     r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    if method == "minwise" and strategy == og.OPH_STRATEGY_BITMAP:
+        pytest.skip("no BITMAP join for MinWise")
     kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
     base = 1000
     if method in ("full", "goph"):
@@ -139,7 +145,7 @@ def test_tiny_query_blocks(tiny_run, method, nq):
     scan (4 / 8 / 16 / 32 queries, the 4- and 8-query blocks at 8 / 7 CTAs per SM)
     and its partial last block; 33 adds a second 32-query block of one query."""
     r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
-    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"], strategy=og.OPH_STRATEGY_BRUTE)
     if method in ("full", "goph"):
         lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
         g = gpu_dense(method, subview(r["qo"], nq), r["so"], layout=lay, **kw)
@@ -285,21 +291,24 @@ def test_ragged_and_edges(V, k, kp, hkp, seed):
     assert (so.numpy() == F).all() and (qo.numpy() == QF).all()
     assert (so.empty_numpy() == masks_from_values(F)).all()
     lay = og.flat_layout(V, k, kp)
+    strategies = (og.OPH_STRATEGY_AUTO, og.OPH_STRATEGY_BRUTE)  # AUTO: BITMAP where |V| <= 2^23
     for joint in (False, True):
-        kw = dict(t_num=7, t_den=10, eps=1e-4, joint=joint)
-        assert_records_equal(gpu_dense("full", qo, so, layout=lay, **kw),
-                             oracle_records("full", QF, F, k=k, kprime=kp, **kw), f"full {V}")
-        assert_records_equal(gpu_dense("goph", qo, so, layout=lay, **kw),
-                             oracle_records("goph", QF, F, k=k, kprime=kp, **kw), f"goph {V}")
+        for st in strategies:
+            kw = dict(t_num=7, t_den=10, eps=1e-4, joint=joint, strategy=st)
+            assert_records_equal(gpu_dense("full", qo, so, layout=lay, **kw),
+                                 oracle_records("full", QF, F, k=k, kprime=kp, **kw), f"full {V} {st}")
+            assert_records_equal(gpu_dense("goph", qo, so, layout=lay, **kw),
+                                 oracle_records("goph", QF, F, k=k, kprime=kp, **kw), f"goph {V} {st}")
     if hier is not None:
         glay = oracle.hoph_layout(V, 1, 1, hkp)
         H = oracle.hoph_sketch(offs, ids, V, glay, hkp, seed)
         QH = oracle.hoph_sketch(qoffs, qids, V, glay, hkp, seed)
         assert (sh.numpy() == H).all() and (sh.empty_numpy() == masks_from_values(H)).all()
         for joint in (False, True):
-            kw = dict(t_num=7, t_den=10, eps=1e-4, joint=joint)
-            assert_records_equal(gpu_dense("hoph", qh, sh, layout=hier, **kw),
-                                 oracle_records("hoph", QH, H, kprime=hkp, L=len(glay), **kw), f"hoph {V}")
+            for st in strategies:
+                kw = dict(t_num=7, t_den=10, eps=1e-4, joint=joint, strategy=st)
+                assert_records_equal(gpu_dense("hoph", qh, sh, layout=hier, **kw),
+                                     oracle_records("hoph", QH, H, kprime=hkp, L=len(glay), **kw), f"hoph {V} {st}")
     sets_t = og.SetCollection.from_numpy(offs, ids)
     q_t = og.SetCollection.from_numpy(qoffs, qids)
     mk = min(k, 64)
@@ -313,9 +322,10 @@ def test_ragged_and_edges(V, k, kp, hkp, seed):
 
 
 @pytest.mark.parametrize("tn,td,eps", [(1, 1, 1e-4), (1, 20, 1e-4), (7, 10, 0.5), (7, 10, 1e-300), (4, 5, 1e-2)])
-def test_threshold_and_epsilon_extremes(tiny_run, tn, td, eps):
+@pytest.mark.parametrize("strategy", [og.OPH_STRATEGY_BRUTE, og.OPH_STRATEGY_BITMAP])
+def test_threshold_and_epsilon_extremes(tiny_run, tn, td, eps, strategy):
     r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
-    kw = dict(t_num=tn, t_den=td, eps=eps)
+    kw = dict(t_num=tn, t_den=td, eps=eps, strategy=strategy)
     lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
     q = subview(r["qo"], 40)
     assert_records_equal(gpu_dense("goph", q, r["so"], layout=lay, **kw),
@@ -593,12 +603,14 @@ def test_probe_filter_widths(wide_run, method, nq):
 
 
 # ----------------------------------------------------------------------------- termination-level histograms
-@pytest.mark.parametrize("strategy", [og.OPH_STRATEGY_BRUTE, og.OPH_STRATEGY_PROBE])
+@pytest.mark.parametrize("strategy", [og.OPH_STRATEGY_BRUTE, og.OPH_STRATEGY_PROBE, og.OPH_STRATEGY_BITMAP])
 @pytest.mark.parametrize("method", ["full", "goph", "hoph", "minwise"])
 def test_tiny_stop_histogram(tiny_run, method, strategy):
     """d_stop_hist == the histogram of the oracle's per-pair `groups` (groups compared when
-    decided: Alg. 1 / Alg. 2 early termination), summing to Q x N, for both scan strategies."""
+    decided: Alg. 1 / Alg. 2 early termination), summing to Q x N, for every scan strategy."""
     r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    if method == "minwise" and strategy == og.OPH_STRATEGY_BITMAP:
+        pytest.skip("no BITMAP join for MinWise")
     kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
     res = og.Results(1 << 20, stop_hist=True)
     prm = og.params(p["t_num"], p["t_den"], p["eps"], False, strategy)
@@ -655,16 +667,17 @@ def test_exact_jaccard_pairs_vs_oracle():
 
 
 # ----------------------------------------------------------------------------- parameter sweeps
+@pytest.mark.parametrize("strategy", [og.OPH_STRATEGY_BRUTE, og.OPH_STRATEGY_BITMAP])
 @pytest.mark.parametrize("kprime", [8, 16, 32])
 @pytest.mark.parametrize("t_num,t_den", [(1, 2), (3, 5), (4, 5), (9, 10)])
 @pytest.mark.parametrize("eps", [1e-3, 1e-5])
-def test_tiny_parameter_sweep(tiny_run, kprime, t_num, t_den, eps):
+def test_tiny_parameter_sweep(tiny_run, kprime, t_num, t_den, eps, strategy):
     """The paper's sweeps (GOPH group count n = k/k', T in [0.5, 0.9], eps in {1e-3, 1e-5}):
-    GOPH and HOPH dense records bit-exact with the oracle (tiny, k = 64)."""
+    GOPH and HOPH dense records bit-exact with the oracle (tiny, k = 64), BRUTE and BITMAP."""
     r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
     w = r["w"]
     V = w.vocab_size
-    kw = dict(t_num=t_num, t_den=t_den, eps=eps)
+    kw = dict(t_num=t_num, t_den=t_den, eps=eps, strategy=strategy)
     lay = og.flat_layout(V, p["k"], kprime)
     assert_records_equal(gpu_dense("goph", r["qo"], r["so"], layout=lay, **kw),
                          oracle_records("goph", o["QF"], o["F"], k=p["k"], kprime=kprime, **kw),
@@ -780,3 +793,100 @@ def test_survivor_lists_many_late_pairs(monkeypatch):
     sel = want[got["query"].astype(np.int64), got["set_id"].astype(np.int64)]
     for f in ("n_mb", "n_excl", "groups", "verdict", "flags"):
         assert (got[f].astype(np.int64) == sel[f].astype(np.int64)).all(), f
+
+
+# ----------------------------------------------------------------------------- BITMAP join (K7)
+@pytest.fixture(scope="module")
+def image_small():
+    """An image-like collection (Zipf words over 2^20, k = 512, k' = 32, HOPH L = 15) with
+    1,100 queries: two BITMAP query blocks, the second one ragged (76 queries)."""
+    from workloads import gen
+    w = gen.image_like(n_sets=20_000, n_queries=1100)
+    p = w.params
+    V, seed = w.vocab_size, p["perm_seed"]
+    hier = og.oph_hier_layout_make(V, 1, 1, p["hoph_kprime"])
+    _, so, sh = gpu_build(w.offsets, w.ids, V, seed, k=p["k"], kprime=p["kprime"], hier=hier)
+    _, qo, qh = gpu_build(w.q_offsets, w.q_ids, V, seed, k=p["k"], kprime=p["kprime"], hier=hier)
+    glay = oracle.hoph_layout(V, 1, 1, p["hoph_kprime"])
+    orc = dict(F=oracle.oph_sketch(w.offsets, w.ids, V, p["k"], seed),
+               QF=oracle.oph_sketch(w.q_offsets, w.q_ids, V, p["k"], seed),
+               H=oracle.hoph_sketch(w.offsets, w.ids, V, glay, p["hoph_kprime"], seed),
+               QH=oracle.hoph_sketch(w.q_offsets, w.q_ids, V, glay, p["hoph_kprime"], seed), L=len(glay))
+    return dict(w=w, p=p, hier=hier, so=so, sh=sh, qo=qo, qh=qh, orc=orc)
+
+
+@pytest.mark.parametrize("joint", [False, True])
+@pytest.mark.parametrize("method", ["full", "goph", "hoph"])
+def test_bitmap_image_like_dense(image_small, method, joint):
+    """BITMAP dense records of all 1,100 queries x the first 2,000 sets == the oracle's."""
+    r, o, p = image_small, image_small["orc"], image_small["p"]
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"], joint=joint, strategy=og.OPH_STRATEGY_BITMAP)
+    n = 2000
+    if method == "hoph":
+        g = gpu_dense(method, r["qh"], subview(r["sh"], n), layout=r["hier"], **kw)
+        want = oracle_records(method, o["QH"], o["H"][:n], kprime=p["hoph_kprime"], L=o["L"], **kw)
+    else:
+        lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+        g = gpu_dense(method, r["qo"], subview(r["so"], n), layout=lay, **kw)
+        want = oracle_records(method, o["QF"], o["F"][:n], k=p["k"], kprime=p["kprime"], **kw)
+    assert_records_equal(g, want, f"bitmap image-like {method} joint={joint}")
+
+
+@pytest.mark.parametrize("method", ["full", "goph", "hoph"])
+def test_bitmap_image_like_lists_and_histogram(image_small, method):
+    """BITMAP threshold lists (every record field) and termination histogram over all
+    20,000 sets x 1,100 queries == the oracle's; equal to the BRUTE strategy's list."""
+    r, o, p = image_small, image_small["orc"], image_small["p"]
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    if method == "hoph":
+        q, s, lay = r["qh"], r["sh"], r["hier"]
+        want = oracle_records(method, o["QH"], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw)
+    else:
+        q, s, lay = r["qo"], r["so"], og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+        want = oracle_records(method, o["QF"], o["F"], k=p["k"], kprime=p["kprime"], **kw)
+    res = og.Results(1 << 22, stop_hist=True)
+    prm = og.params(p["t_num"], p["t_den"], p["eps"], strategy=og.OPH_STRATEGY_BITMAP)
+    fn = {"full": og.compare_full, "goph": og.compare_goph, "hoph": og.compare_hoph}[method]
+    fn(q, s, lay, prm, res)
+    hist = res.hist().astype(np.int64)
+    assert (hist == np.bincount(want["groups"].ravel(), minlength=len(hist))).all()
+    n = res.n()
+    out = og.Results(max(n, 1))
+    og.topk_or_threshold_results(res, n, og.OPH_SELECT_THRESHOLD, out)
+    got = out.numpy(n)
+    assert list(zip(got["query"].tolist(), got["set_id"].tolist())) == oracle.threshold_list(want)
+    assert n > 0
+    sel = want[got["query"].astype(np.int64), got["set_id"].astype(np.int64)]
+    for f in ("n_mb", "n_excl", "groups", "verdict", "flags"):
+        assert (got[f].astype(np.int64) == sel[f].astype(np.int64)).all(), f
+    assert np.abs(got["estimate"][sel["flags"] == 0] - sel["estimate"][sel["flags"] == 0]).max(initial=0) <= 1e-6
+    brute = gpu_threshold_hits(method, q, s, layout=lay, strategy=og.OPH_STRATEGY_BRUTE, capacity=1 << 22, **kw)
+    assert brute.tobytes() == got.tobytes()
+
+
+def test_bitmap_domain_errors(tiny_run):
+    """An explicit BITMAP request outside its domain fails (MinWise; |V| > 2^23); a
+    workspace of only oph_workspace_size bytes is too small (OPH_ENOMEM) while AUTO
+    then keeps the other strategies."""
+    r, p = tiny_run, tiny_run["p"]
+    prm = og.params(p["t_num"], p["t_den"], p["eps"], strategy=og.OPH_STRATEGY_BITMAP)
+    with pytest.raises(og.OphError) as e:
+        og.compare_minwise(r["qmw"], r["mw"], prm, og.Results(1 << 16))
+    assert e.value.status == og.OPH_EINVAL
+    lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+    class FixedWs(og.Workspace):  # a caller-owned workspace that does not grow
+        def get(self, nbytes):
+            return self.buf
+
+    small = FixedWs()
+    og.Workspace.get(small, og.oph_workspace_size(og.OPH_METHOD_FULL, r["qo"].n_sets, r["so"].n_sets, p["k"]))
+    with pytest.raises(og.OphError) as e:
+        og.compare_full(r["qo"], r["so"], lay, prm, og.Results(1 << 16), ws=small)
+    assert e.value.status == og.OPH_ENOMEM
+    og.compare_full(r["qo"], r["so"], lay, og.params(p["t_num"], p["t_den"], p["eps"]), og.Results(1 << 16), ws=small)
+    V = 1 << 32
+    offs, ids = make_csr([[1, 2, 3], [5, 6]])
+    _, so, _ = gpu_build(offs, ids, V, 1, k=64, kprime=16)
+    with pytest.raises(og.OphError) as e:
+        og.compare_full(so, so, og.flat_layout(V, 64, 16), prm, og.Results(16))
+    assert e.value.status == og.OPH_EINVAL
