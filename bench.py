@@ -327,6 +327,9 @@ def run_ours(args):
     hier = og.oph_hier_layout_make(V, p["a"], p["b"], hkp)
     L = hier.L
     prm = og.params(p["t_num"], p["t_den"], p["eps"], strategy=strategy)
+    # MinWise has no BITMAP join (its values span the universe per permutation): its register scan
+    prm_mw = og.params(p["t_num"], p["t_den"], p["eps"],
+                       strategy=og.OPH_STRATEGY_BRUTE if strategy == og.OPH_STRATEGY_BITMAP else strategy)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
 
@@ -406,7 +409,7 @@ def run_ours(args):
         if world > 1:
             odist.broadcast_tensors([qmw.values, qmw.flags])
         mark(ev, 2)
-        og.compare_minwise(qmw, mw, prm, res[3], set_id_base=base, ws=ws[3])
+        og.compare_minwise(qmw, mw, prm_mw, res[3], set_id_base=base, ws=ws[3])
         mark(ev, 3)
         n = int(counts[3:].cpu()[0])
         assert n <= cap, f"hit buffer overflow {n}"
@@ -726,7 +729,7 @@ def run_ours(args):
         "config": {"workload": args.config, "sets_per_gpu": N, "sets_total": N_total, "queries": Q, "k": k,
                    "kprime": kp, "hoph_groups": L, "minwise_k": mwk, "T": f"{p['t_num']}/{p['t_den']}",
                    "epsilon": p["eps"], "parallelism": f"set-sharded x{world} ({args.dist_backend})",
-                   "scan_strategy": ["auto", "brute", "probe"][strategy], "l2": flush},
+                   "scan_strategy": ["auto", "brute", "probe", "bitmap"][strategy], "l2": flush},
         "value_definition": "3 * queries * sets_total / step time; a step = OPH+HOPH sketches of the collection "
                             "and the queries, full OPH + GOPH + HOPH threshold scoring of every pair, hit lists "
                             "gathered and sorted (MinWise: baseline_minwise)",
