@@ -691,7 +691,7 @@ def run_ours(args):
         # step; its quality in both empty modes and device time per call
         variants = {}
         for joint, key in ((False, "either_empty"), (True, "joint_empty")):
-            prm_e = og.params(p["t_num"], p["t_den"], p["eps"], joint=joint, strategy=strategy,
+            prm_e = og.params(p["t_num"], p["t_den"], p["eps"], joint=joint, strategy=prm_mw.strategy,
                               variant=og.OPH_VARIANT_EMPTY_AWARE)
             er = og.Results(cap, stop_hist=True)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -201,7 +201,7 @@ __device__ void bit_hoph_final(const BitArgs &a, uint32_t qg, uint64_t s, uint32
 // levels of k' bins with thresholds on M_c).  MODE 1: HOPH 1:1, per-group counts
 // folded into T_l = 2 T_(l-1) + M_l, thresholds on T_l, the HOPH estimator at L.
 template <int MODE>
-__global__ void __launch_bounds__(32 * kBitWarps, 3) bit_scan_kernel(const __grid_constant__ BitArgs a) {
+__global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_kernel(const __grid_constant__ BitArgs a) {
     __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
     for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
         uint32_t st, wd;
@@ -232,38 +232,60 @@ __global__ void __launch_bounds__(32 * kBitWarps, 3) bit_scan_kernel(const __gri
         for (int i = 0; i < (MODE == 1 ? (int)kBitTS : 1); i++) T[i] = 0u;
         uint32_t alive = qvalid;
 
-        // row of (bin b, this set): the set's value of bin b, looked up in idx (lanes 0-15
-        // hold bins b0 + lane); rows are then broadcast by shuffle
-        auto lookup = [&](uint32_t b0, uint32_t nbat) -> uint32_t {
-            uint32_t r = 0;
-            if (lane < nbat) {
-                const uint32_t b = b0 + lane;
-                const uint32_t v = __ldg(Fs + (uint64_t)b * a.ld);
-                if (v < s_width[b]) r = __ldg(a.idx + s_start[b] + v);
-            }
-            return r;
+        // The bins are scanned in batches of <= 16 (a level's bins split into bpl batches; a
+        // batch never straddles a level).  Per batch: lanes 0-15 load the set's value of bins
+        // b0 + lane (v) and look up its row (r); rows are then broadcast by shuffle and every
+        // lane loads its word (x).  Software pipeline, one batch per stage and iteration:
+        // x of batch g+1, r of g+2 and v of g+3 are in flight while batch g is counted.
+        const uint32_t bpl = (bins_per_level + 15u) / 16u;
+        const uint32_t nbt = nlev_scan * bpl;
+        auto range = [&](uint32_t g, uint32_t &b0, uint32_t &b1) {
+            const uint32_t lv = g / bpl, jj = g - lv * bpl;
+            const uint32_t lb0 = lv * bins_per_level;
+            b0 = lb0 + 16u * jj;
+            b1 = min(min(lb0 + bins_per_level, a.nscan), b0 + 16u);
         };
-        for (uint32_t l = 1; l <= nlev_scan; l++) {
-            if (!__any_sync(0xFFFFFFFFu, alive != 0u)) break;  // every pair of this set is decided
-            const uint32_t lb0 = (l - 1) * bins_per_level;
-            const uint32_t lb1 = min(lb0 + bins_per_level, a.nscan);
-            if (MODE == 1) {
+        auto vload = [&](uint32_t g) -> uint32_t {
+            uint32_t b0, b1;
+            range(g, b0, b1);
+            const uint32_t b = b0 + lane;
+            return (lane < 16u && b < b1) ? __ldg(Fs + (uint64_t)b * a.ld) : kEmpty;
+        };
+        auto ilook = [&](uint32_t g, uint32_t v) -> uint32_t {
+            uint32_t b0, b1;
+            range(g, b0, b1);
+            const uint32_t b = b0 + lane;
+            return (lane < 16u && b < b1 && v < s_width[b]) ? __ldg(a.idx + s_start[b] + v) : 0u;
+        };
+        auto rload = [&](uint32_t r, uint32_t (&x)[16]) {
+#pragma unroll
+            for (int u = 0; u < 16; u++) {
+                const uint32_t ru = __shfl_sync(0xFFFFFFFFu, r, u);
+                x[u] = __ldg(rows_lane + (uint64_t)ru * 32);  // ru = 0 (no row, or past the batch): zero row
+            }
+        };
+        uint32_t x[16], r1 = 0u, v3 = kEmpty;
+        {
+            const uint32_t v1 = vload(0), v2 = nbt > 1 ? vload(1) : kEmpty;
+            const uint32_t r0 = ilook(0, v1);
+            if (nbt > 2) v3 = vload(2);
+            if (nbt > 1) r1 = ilook(1, v2);
+            rload(r0, x);
+        }
+        for (uint32_t g = 0; g < nbt; g++) {
+            uint32_t xn[16];
+            if (g + 1 < nbt) rload(r1, xn);
+            if (g + 2 < nbt) r1 = ilook(g + 2, v3);
+            if (g + 3 < nbt) v3 = vload(g + 3);
+            const uint32_t l = g / bpl + 1, jj = g - (l - 1) * bpl;
+            if (MODE == 1 && jj == 0) {
 #pragma unroll
                 for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;  // M_l: this group's count
             }
-            uint32_t rn = lookup(lb0, min(16u, lb1 - lb0));
-            for (uint32_t b0 = lb0; b0 < lb1; b0 += 16) {
-                const uint32_t nbat = min(16u, lb1 - b0);
-                const uint32_t rc = rn;
-                uint32_t x[16];
+            csa16(c, x);
 #pragma unroll
-                for (int u = 0; u < 16; u++) {
-                    const uint32_t r = __shfl_sync(0xFFFFFFFFu, rc, u);
-                    x[u] = __ldg(rows_lane + (uint64_t)r * 32);  // r = 0 (no row, or past nbat): zero row
-                }
-                if (b0 + 16 < lb1) rn = lookup(b0 + 16, min(16u, lb1 - b0 - 16));
-                csa16(c, x);
-            }
+            for (int u = 0; u < 16; u++) x[u] = xn[u];
+            if (jj + 1 < bpl) continue;
             // ---- decisions at the end of level l
             const bool last = l == (MODE == 1 ? a.nlev : nlev_scan);
             uint32_t acc = 0u, dec = 0u;
@@ -303,7 +325,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, 3) bit_scan_kernel(const __gri
                     uint32_t nmb = 0, ex = 0;
                     if (has) {
                         if (MODE == 1) {
-                            for (uint32_t g = 0; g < l; g++) nmb += bit_group_matches(a, qg, s, g);
+                            for (uint32_t gg = 0; gg < l; gg++) nmb += bit_group_matches(a, qg, s, gg);
                         } else {
                             nmb = sliced_get<kBitCS>(c, j);
                         }
@@ -313,7 +335,10 @@ __global__ void __launch_bounds__(32 * kBitWarps, 3) bit_scan_kernel(const __gri
                 }
                 alive &= ~dec;
             }
-            if (!last) continue;
+            if (!last) {
+                if (!__any_sync(0xFFFFFFFFu, alive != 0u)) break;  // every pair of this set is decided
+                continue;
+            }
             // ---- the final verdict of every pair still alive
             hist_add(a.out.hist, MODE == 1 ? a.nlev : a.level_final, __popc(alive));
             if (MODE == 1) {

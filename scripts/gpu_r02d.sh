@@ -1,0 +1,6 @@
+# r02d: pipelined BITMAP scan: parity subset, image-like bench, ncu of the three bitmap scans
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests/test_gpu_parity.py -q -x --timeout 600 -k "bitmap or tiny_dense or tiny_threshold or stop_hist or ragged or sweep or extremes" > gpurun_out/pytest_d.log 2>&1; echo pytest=$?
+timeout 1200 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_image_d.log 2>&1; echo bench=$?
+ARGS="--steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-launch-count --no-quality --no-minwise"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:bit_scan_kernel -c 9 -o gpurun_out/bitscan_d python bench.py $ARGS > gpurun_out/ncu_d.log 2>&1; echo ncu=$?

@@ -29,7 +29,7 @@ for row in rows[2:]:
     try:
         v = [int(row[i] or 0) for i in idx]
         x = int(row[ex] or 0)
-    except ValueError:
+    except (ValueError, IndexError):
         continue
     for c, y in zip(cols, v):
         tot[c] += y
