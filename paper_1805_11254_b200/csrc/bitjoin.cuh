@@ -232,52 +232,44 @@ __global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_ke
         for (int i = 0; i < (MODE == 1 ? (int)kBitTS : 1); i++) T[i] = 0u;
         uint32_t alive = qvalid;
 
-        // The bins are scanned in batches of <= 16 (a level's bins split into bpl batches; a
-        // batch never straddles a level).  Per batch: lanes 0-15 load the set's value of bins
-        // b0 + lane (v) and look up its row (r); rows are then broadcast by shuffle and every
-        // lane loads its word (x).  Software pipeline, one batch per stage and iteration:
-        // x of batch g+1, r of g+2 and v of g+3 are in flight while batch g is counted.
-        const uint32_t bpl = (bins_per_level + 15u) / 16u;
-        const uint32_t nbt = nlev_scan * bpl;
-        auto range = [&](uint32_t g, uint32_t &b0, uint32_t &b1) {
-            const uint32_t lv = g / bpl, jj = g - lv * bpl;
-            const uint32_t lb0 = lv * bins_per_level;
-            b0 = lb0 + 16u * jj;
-            b1 = min(min(lb0 + bins_per_level, a.nscan), b0 + 16u);
-        };
+        // The bins are scanned in batches of 16 (GOPH / HOPH levels are whole batches: k' is
+        // a multiple of 16; full OPH's last batch may be partial).  Per batch: lanes 0-15
+        // load the set's value of bins b0 + lane (v) and look up its row (r); rows are then
+        // broadcast by shuffle and every lane loads its word (x).  Software pipeline, one
+        // batch per stage and iteration: x of batch g+1, r of g+2 and v of g+3 are in flight
+        // while batch g is counted.
+        const uint32_t nbt = (a.nscan + 15u) / 16u;
+        const uint32_t bpl = bins_per_level / 16u;  // batches per level (full OPH: unused)
         auto vload = [&](uint32_t g) -> uint32_t {
-            uint32_t b0, b1;
-            range(g, b0, b1);
-            const uint32_t b = b0 + lane;
-            return (lane < 16u && b < b1) ? __ldg(Fs + (uint64_t)b * a.ld) : kEmpty;
+            const uint32_t b = 16u * g + lane;
+            return (lane < 16u && b < a.nscan) ? __ldg(Fs + (uint64_t)b * a.ld) : kEmpty;
         };
         auto ilook = [&](uint32_t g, uint32_t v) -> uint32_t {
-            uint32_t b0, b1;
-            range(g, b0, b1);
-            const uint32_t b = b0 + lane;
-            return (lane < 16u && b < b1 && v < s_width[b]) ? __ldg(a.idx + s_start[b] + v) : 0u;
+            const uint32_t b = 16u * g + lane;
+            return (lane < 16u && b < a.nscan && v < s_width[b]) ? __ldg(a.idx + s_start[b] + v) : 0u;
         };
         auto rload = [&](uint32_t r, uint32_t (&x)[16]) {
 #pragma unroll
             for (int u = 0; u < 16; u++) {
                 const uint32_t ru = __shfl_sync(0xFFFFFFFFu, r, u);
-                x[u] = __ldg(rows_lane + (uint64_t)ru * 32);  // ru = 0 (no row, or past the batch): zero row
+                x[u] = __ldg(rows_lane + (uint64_t)ru * 32);  // ru = 0 (no row, or past the scan): zero row
             }
         };
         uint32_t x[16], r1 = 0u, v3 = kEmpty;
         {
-            const uint32_t v1 = vload(0), v2 = nbt > 1 ? vload(1) : kEmpty;
+            const uint32_t v1 = vload(0), v2 = vload(1);
             const uint32_t r0 = ilook(0, v1);
-            if (nbt > 2) v3 = vload(2);
-            if (nbt > 1) r1 = ilook(1, v2);
+            v3 = vload(2);
+            r1 = ilook(1, v2);
             rload(r0, x);
         }
+        uint32_t l = 1, jj = 0;  // level of batch g, batch index inside the level
+#pragma unroll 2
         for (uint32_t g = 0; g < nbt; g++) {
             uint32_t xn[16];
-            if (g + 1 < nbt) rload(r1, xn);
-            if (g + 2 < nbt) r1 = ilook(g + 2, v3);
-            if (g + 3 < nbt) v3 = vload(g + 3);
-            const uint32_t l = g / bpl + 1, jj = g - (l - 1) * bpl;
+            rload(r1, xn);               // past the scan: r1 = 0, the zero row
+            r1 = ilook(g + 2, v3);
+            v3 = vload(g + 3);
             if (MODE == 1 && jj == 0) {
 #pragma unroll
                 for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;  // M_l: this group's count
@@ -285,7 +277,11 @@ __global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_ke
             csa16(c, x);
 #pragma unroll
             for (int u = 0; u < 16; u++) x[u] = xn[u];
-            if (jj + 1 < bpl) continue;
+            const bool level_end = bins_per_level == a.nscan ? g + 1 == nbt : jj + 1 == bpl;
+            if (!level_end) {
+                jj++;
+                continue;
+            }
             // ---- decisions at the end of level l
             const bool last = l == (MODE == 1 ? a.nlev : nlev_scan);
             uint32_t acc = 0u, dec = 0u;
@@ -337,6 +333,8 @@ __global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_ke
             }
             if (!last) {
                 if (!__any_sync(0xFFFFFFFFu, alive != 0u)) break;  // every pair of this set is decided
+                l++;
+                jj = 0;
                 continue;
             }
             // ---- the final verdict of every pair still alive

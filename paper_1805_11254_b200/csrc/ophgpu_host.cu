@@ -551,7 +551,9 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     // BITMAP (bitjoin.cuh): full OPH, GOPH (Algorithm 1) and HOPH with power-of-two weights
     // (the 1:1 split: T_l = S_l / 2^(L-1-l) in <= 24 bit slices), |V| <= 2^23, <= 1023 bins
     {
+        // (GOPH / HOPH levels must be whole batches of 16 bins: k' % 16 == 0)
         const bool dom = !mw && !ea && bitmap_sizes_ok(Qv->vocab_size, nb) &&
+                         (method == OPH_METHOD_FULL || kp % 16 == 0) &&
                          (method != OPH_METHOD_HOPH || (a == 1 && b == 1 && nlev >= 2 && nlev <= 20 && plan.lam));
         const bool fits = ws_bytes >= fixed + bitmap_region_bytes(Qv->vocab_size, nb);
         bool use = false;

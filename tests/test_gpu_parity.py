@@ -675,6 +675,8 @@ def test_tiny_parameter_sweep(tiny_run, kprime, t_num, t_den, eps, strategy):
     """The paper's sweeps (GOPH group count n = k/k', T in [0.5, 0.9], eps in {1e-3, 1e-5}):
     GOPH and HOPH dense records bit-exact with the oracle (tiny, k = 64), BRUTE and BITMAP."""
     r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    if strategy == og.OPH_STRATEGY_BITMAP and kprime % 16:
+        pytest.skip("BITMAP levels are whole batches of 16 bins")
     w = r["w"]
     V = w.vocab_size
     kw = dict(t_num=t_num, t_den=t_den, eps=eps, strategy=strategy)
