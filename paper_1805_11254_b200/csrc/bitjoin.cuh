@@ -201,7 +201,7 @@ __device__ void bit_hoph_final(const BitArgs &a, uint32_t qg, uint64_t s, uint32
 // levels of k' bins with thresholds on M_c).  MODE 1: HOPH 1:1, per-group counts
 // folded into T_l = 2 T_(l-1) + M_l, thresholds on T_l, the HOPH estimator at L.
 template <int MODE>
-__global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_kernel(const __grid_constant__ BitArgs a) {
+__global__ void __launch_bounds__(32 * kBitWarps, 2) bit_scan_kernel(const __grid_constant__ BitArgs a) {
     __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
     for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
         uint32_t st, wd;
@@ -264,9 +264,10 @@ __global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_ke
             rload(r0, x);
         }
         uint32_t l = 1, jj = 0;  // level of batch g, batch index inside the level
-#pragma unroll 2
-        for (uint32_t g = 0; g < nbt; g++) {
-            uint32_t xn[16];
+        // one batch: count xc (batch g) while xn (g + 1), r1 (g + 2), v3 (g + 3) load; the two
+        // row buffers alternate (a copy between them would wait for the loads in flight)
+        // returns true when the set is done
+        auto step = [&](uint32_t g, uint32_t (&xc)[16], uint32_t (&xn)[16]) -> bool {
             rload(r1, xn);               // past the scan: r1 = 0, the zero row
             r1 = ilook(g + 2, v3);
             v3 = vload(g + 3);
@@ -274,13 +275,11 @@ __global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_ke
 #pragma unroll
                 for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;  // M_l: this group's count
             }
-            csa16(c, x);
-#pragma unroll
-            for (int u = 0; u < 16; u++) x[u] = xn[u];
+            csa16(c, xc);
             const bool level_end = bins_per_level == a.nscan ? g + 1 == nbt : jj + 1 == bpl;
             if (!level_end) {
                 jj++;
-                continue;
+                return false;
             }
             // ---- decisions at the end of level l
             const bool last = l == (MODE == 1 ? a.nlev : nlev_scan);
@@ -332,10 +331,10 @@ __global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_ke
                 alive &= ~dec;
             }
             if (!last) {
-                if (!__any_sync(0xFFFFFFFFu, alive != 0u)) break;  // every pair of this set is decided
+                if (!__any_sync(0xFFFFFFFFu, alive != 0u)) return true;  // every pair of this set is decided
                 l++;
                 jj = 0;
-                continue;
+                return false;
             }
             // ---- the final verdict of every pair still alive
             hist_add(a.out.hist, MODE == 1 ? a.nlev : a.level_final, __popc(alive));
@@ -381,6 +380,12 @@ __global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_ke
                 }
             }
             alive = 0u;
+            return true;
+        };
+        uint32_t xb[16];
+        for (uint32_t g = 0; g < nbt; g += 2) {
+            if (step(g, x, xb)) break;
+            if (g + 1 < nbt && step(g + 1, xb, x)) break;
         }
     }
 }
@@ -396,9 +401,9 @@ cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     bit_claim_kernel<<<g, 256, 0, st>>>(a);
     bit_fill_kernel<<<g, 256, 0, st>>>(a);
     bit_maxeq_kernel<<<1, 1024, 0, st>>>(a);
-    // the scan: 8 consecutive sets per CTA tile, grid-stride; 3 CTAs per SM
+    // the scan: 8 consecutive sets per CTA tile, grid-stride; 2 CTAs per SM (the double-buffered pipeline needs ~124 registers)
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
-    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * 3 * 8);
+    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * 2 * 8);
     if (a.mode_hoph) bit_scan_kernel<1><<<grid, 32 * kBitWarps, 0, st>>>(a);
     else bit_scan_kernel<0><<<grid, 32 * kBitWarps, 0, st>>>(a);
     return cudaGetLastError();
