@@ -200,17 +200,33 @@ __device__ void bit_hoph_final(const BitArgs &a, uint32_t qg, uint64_t s, uint32
 // MODE 0: a count over the scanned bins (FULL: one level, the final verdict; GOPH:
 // levels of k' bins with thresholds on M_c).  MODE 1: HOPH 1:1, per-group counts
 // folded into T_l = 2 T_(l-1) + M_l, thresholds on T_l, the HOPH estimator at L.
+// the set's values of every scanned bin, gathered from the bin-major matrix into this
+// warp's shared-memory buffer with cp.async (4-B copies, L1-cached: the CTA's 8 warps
+// read the same 32-B sectors); issued one set ahead, so the gathers' latency (one DRAM
+// page per bin row) is hidden behind a whole set's scan
+__device__ __forceinline__ void bit_prefetch_values(const BitArgs &a, uint64_t s, uint32_t *dst, uint32_t lane) {
+    const uint32_t *src = a.F + s;
+    for (uint32_t b = lane; b < a.nscan; b += 32) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst + b)),
+                     "l"(src + (uint64_t)b * a.ld)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(32 * kBitWarps, 2) bit_scan_kernel(const __grid_constant__ BitArgs a) {
+__global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_kernel(const __grid_constant__ BitArgs a) {
     __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
+    extern __shared__ __align__(16) uint32_t s_vals[];  // [kBitWarps][2][nsv]
     for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
         uint32_t st, wd;
         bit_bin_range(a, b, st, wd);
         s_start[b] = st;
         s_width[b] = wd;
     }
-    __syncthreads();
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t nsv = (a.nscan + 31u) & ~31u;
+    uint32_t *sv = s_vals + (size_t)warp * 2 * nsv;
     // this lane's word of the block: queries qb0 + 32 lane + j
     const uint32_t qw0 = 32u * lane;
     const uint32_t qvalid = qw0 >= a.nqb ? 0u : (a.nqb - qw0 >= 32u ? 0xFFFFFFFFu : ((1u << (a.nqb - qw0)) - 1u));
@@ -219,11 +235,24 @@ __global__ void __launch_bounds__(32 * kBitWarps, 2) bit_scan_kernel(const __gri
     const uint32_t nlev_scan = MODE == 1 ? a.nlev : (a.method == kGoph ? a.nlev : 1u);
     const uint32_t bins_per_level = MODE == 1 || a.method == kGoph ? a.kp : a.nscan;
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
+    {
+        const uint64_t s0 = a.s_begin + (uint64_t)blockIdx.x * kBitWarps + warp;
+        if ((uint64_t)blockIdx.x < ntiles && s0 < a.n_sets) bit_prefetch_values(a, s0, sv, lane);
+    }
+    __syncthreads();
+    uint32_t buf = 0;
 
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint64_t s = a.s_begin + tile * kBitWarps + warp;
-        if (s >= a.n_sets) continue;  // warp-uniform
-        const uint32_t *Fs = a.F + s;
+        if (s >= a.n_sets) continue;  // warp-uniform (and nothing prefetched for it)
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        const uint32_t *v_cur = sv + buf * nsv;
+        {   // the next set of this warp
+            const uint64_t sn = s + (uint64_t)gridDim.x * kBitWarps;
+            if (sn < a.n_sets) bit_prefetch_values(a, sn, sv + (buf ^ 1u) * nsv, lane);
+        }
+        buf ^= 1u;
         uint32_t c[kBitCS];
 #pragma unroll
         for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;
@@ -234,19 +263,20 @@ __global__ void __launch_bounds__(32 * kBitWarps, 2) bit_scan_kernel(const __gri
 
         // The bins are scanned in batches of 16 (GOPH / HOPH levels are whole batches: k' is
         // a multiple of 16; full OPH's last batch may be partial).  Per batch: lanes 0-15
-        // load the set's value of bins b0 + lane (v) and look up its row (r); rows are then
-        // broadcast by shuffle and every lane loads its word (x).  Software pipeline, one
-        // batch per stage and iteration: x of batch g+1, r of g+2 and v of g+3 are in flight
-        // while batch g is counted.
+        // take the set's value of bins b0 + lane (shared memory) and look up its row (r);
+        // rows are then broadcast by shuffle and every lane loads its word (x).  Software
+        // pipeline: the row words of batch g+1 and the row indices of g+2 and g+3 are in
+        // flight while batch g is counted.
         const uint32_t nbt = (a.nscan + 15u) / 16u;
         const uint32_t bpl = bins_per_level / 16u;  // batches per level (full OPH: unused)
-        auto vload = [&](uint32_t g) -> uint32_t {
+        auto ilook = [&](uint32_t g) -> uint32_t {
             const uint32_t b = 16u * g + lane;
-            return (lane < 16u && b < a.nscan) ? __ldg(Fs + (uint64_t)b * a.ld) : kEmpty;
-        };
-        auto ilook = [&](uint32_t g, uint32_t v) -> uint32_t {
-            const uint32_t b = 16u * g + lane;
-            return (lane < 16u && b < a.nscan && v < s_width[b]) ? __ldg(a.idx + s_start[b] + v) : 0u;
+            uint32_t r = 0u;
+            if (lane < 16u && b < a.nscan) {
+                const uint32_t v = v_cur[b];
+                if (v < s_width[b]) r = __ldg(a.idx + s_start[b] + v);
+            }
+            return r;
         };
         auto rload = [&](uint32_t r, uint32_t (&x)[16]) {
 #pragma unroll
@@ -255,12 +285,11 @@ __global__ void __launch_bounds__(32 * kBitWarps, 2) bit_scan_kernel(const __gri
                 x[u] = __ldg(rows_lane + (uint64_t)ru * 32);  // ru = 0 (no row, or past the scan): zero row
             }
         };
-        uint32_t x[16], r1 = 0u, v3 = kEmpty;
+        uint32_t x[16], rA, rB;
         {
-            const uint32_t v1 = vload(0), v2 = vload(1);
-            const uint32_t r0 = ilook(0, v1);
-            v3 = vload(2);
-            r1 = ilook(1, v2);
+            const uint32_t r0 = ilook(0);
+            rA = ilook(1);
+            rB = ilook(2);
             rload(r0, x);
         }
         uint32_t l = 1, jj = 0;  // level of batch g, batch index inside the level
@@ -268,9 +297,9 @@ __global__ void __launch_bounds__(32 * kBitWarps, 2) bit_scan_kernel(const __gri
         // row buffers alternate (a copy between them would wait for the loads in flight)
         // returns true when the set is done
         auto step = [&](uint32_t g, uint32_t (&xc)[16], uint32_t (&xn)[16]) -> bool {
-            rload(r1, xn);               // past the scan: r1 = 0, the zero row
-            r1 = ilook(g + 2, v3);
-            v3 = vload(g + 3);
+            rload(rA, xn);               // past the scan: rA = 0, the zero row
+            rA = rB;
+            rB = ilook(g + 3);
             if (MODE == 1 && jj == 0) {
 #pragma unroll
                 for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;  // M_l: this group's count
@@ -401,10 +430,13 @@ cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     bit_claim_kernel<<<g, 256, 0, st>>>(a);
     bit_fill_kernel<<<g, 256, 0, st>>>(a);
     bit_maxeq_kernel<<<1, 1024, 0, st>>>(a);
-    // the scan: 8 consecutive sets per CTA tile, grid-stride; 2 CTAs per SM (the double-buffered pipeline needs ~124 registers)
+    // the scan: 8 consecutive sets per CTA tile, grid-stride; 3 CTAs per SM (HOPH: 2, its T slices need 128 registers)
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
-    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * 2 * 8);
-    if (a.mode_hoph) bit_scan_kernel<1><<<grid, 32 * kBitWarps, 0, st>>>(a);
-    else bit_scan_kernel<0><<<grid, 32 * kBitWarps, 0, st>>>(a);
+    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * (a.mode_hoph ? 2 : 3) * 8);
+    const size_t smem = (size_t)kBitWarps * 2 * ((a.nscan + 31u) & ~31u) * 4;
+    auto kern = a.mode_hoph ? bit_scan_kernel<1> : bit_scan_kernel<0>;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+        return e;
+    kern<<<grid, 32 * kBitWarps, smem, st>>>(a);
     return cudaGetLastError();
 }
