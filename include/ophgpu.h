@@ -171,7 +171,8 @@ enum { OPH_VARIANT_PAPER = 0, OPH_VARIANT_EMPTY_AWARE = 1 };
  *          to the bit-sliced states level by level (no survivor lists).
  *          Applies to compare_full, compare_goph (Algorithm 1) and compare_hoph
  *          with the 1:1 split (L <= 20) when |V| <= 2^23, at most 1023
- *          bins are compared and (GOPH / HOPH) k' is a multiple of 16; needs the workspace of oph_workspace_size_for.
+ *          bins are compared, (GOPH / HOPH) k' is a multiple of 16 and the
+ *          collection's row stride ld is a multiple of 8; needs the workspace of oph_workspace_size_for.
  *          AUTO uses it wherever it would otherwise scan BRUTE (and the
  *          workspace is large enough); an explicit BITMAP request outside its
  *          domain fails with OPH_EINVAL (OPH_ENOMEM: workspace too small). */

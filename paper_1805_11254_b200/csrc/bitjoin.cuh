@@ -200,24 +200,25 @@ __device__ void bit_hoph_final(const BitArgs &a, uint32_t qg, uint64_t s, uint32
 // MODE 0: a count over the scanned bins (FULL: one level, the final verdict; GOPH:
 // levels of k' bins with thresholds on M_c).  MODE 1: HOPH 1:1, per-group counts
 // folded into T_l = 2 T_(l-1) + M_l, thresholds on T_l, the HOPH estimator at L.
-// the set's values of every scanned bin, gathered from the bin-major matrix into this
-// warp's shared-memory buffer with cp.async (4-B copies, L1-cached: the CTA's 8 warps
-// read the same 32-B sectors); issued one set ahead, so the gathers' latency (one DRAM
-// page per bin row) is hidden behind a whole set's scan
-__device__ __forceinline__ void bit_prefetch_values(const BitArgs &a, uint64_t s, uint32_t *dst, uint32_t lane) {
-    const uint32_t *src = a.F + s;
-    for (uint32_t b = lane; b < a.nscan; b += 32) {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst + b)),
-                     "l"(src + (uint64_t)b * a.ld)
-                     : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
+// The values of a CTA tile (8 consecutive sets) in the first npre bins: per bin row one
+// 32-B bulk copy (TMA engine) of the 8 sets into vbuf[buffer][bin][8], completion on an
+// mbarrier.  Issued by the 32 lanes of the last warp to finish the tile two tiles back
+// (a double buffer; no CTA-wide barrier), so the copies' latency is hidden behind a
+// whole tile's scan and the gathers cost no L1 requests.
+__device__ __forceinline__ void bit_tile_load(const BitArgs &a, uint64_t tile, uint32_t *dst, uint64_t *bar,
+                                              uint32_t lane) {
+    const uint64_t s0 = a.s_begin + tile * kBitWarps;
+    if (lane == 0) mbar_expect_tx(bar, a.npre * 32u);
+    __syncwarp();
+    for (uint32_t b = lane; b < a.npre; b += 32) bulk_g2s(dst + 8 * b, a.F + (uint64_t)b * a.ld + s0, 32u, bar);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_kernel(const __grid_constant__ BitArgs a) {
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __grid_constant__ BitArgs a) {
     __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
-    extern __shared__ __align__(16) uint32_t s_vals[];  // [kBitWarps][2][nsv]
+    __shared__ uint64_t s_full[2];
+    __shared__ uint32_t s_done[2];
+    extern __shared__ __align__(128) uint32_t s_vals[];  // [2][npre][8]
     for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
         uint32_t st, wd;
         bit_bin_range(a, b, st, wd);
@@ -225,8 +226,6 @@ __global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_ke
         s_width[b] = wd;
     }
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t nsv = (a.nscan + 31u) & ~31u;
-    uint32_t *sv = s_vals + (size_t)warp * 2 * nsv;
     // this lane's word of the block: queries qb0 + 32 lane + j
     const uint32_t qw0 = 32u * lane;
     const uint32_t qvalid = qw0 >= a.nqb ? 0u : (a.nqb - qw0 >= 32u ? 0xFFFFFFFFu : ((1u << (a.nqb - qw0)) - 1u));
@@ -234,25 +233,50 @@ __global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_ke
     const uint32_t *rows_lane = a.rows + lane;
     const uint32_t nlev_scan = MODE == 1 ? a.nlev : (a.method == kGoph ? a.nlev : 1u);
     const uint32_t bins_per_level = MODE == 1 || a.method == kGoph ? a.kp : a.nscan;
+    // (a.n_sets - s_begin and ld are multiples of 8 sets / 32 B: the tiles' 32-B copies are
+    // aligned and in bounds; sets past n_sets are never scored)
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
-    {
-        const uint64_t s0 = a.s_begin + (uint64_t)blockIdx.x * kBitWarps + warp;
-        if ((uint64_t)blockIdx.x < ntiles && s0 < a.n_sets) bit_prefetch_values(a, s0, sv, lane);
+    const uint32_t vstride = a.npre * 8u;  // words per buffer
+    if (threadIdx.x == 0) {
+        mbar_init(&s_full[0], 1);
+        mbar_init(&s_full[1], 1);
+        s_done[0] = s_done[1] = 0u;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    uint32_t buf = 0;
-
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t s = a.s_begin + tile * kBitWarps + warp;
-        if (s >= a.n_sets) continue;  // warp-uniform (and nothing prefetched for it)
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncwarp();
-        const uint32_t *v_cur = sv + buf * nsv;
-        {   // the next set of this warp
-            const uint64_t sn = s + (uint64_t)gridDim.x * kBitWarps;
-            if (sn < a.n_sets) bit_prefetch_values(a, sn, sv + (buf ^ 1u) * nsv, lane);
+    if (warp == 0) {
+        for (uint32_t i = 0; i < 2; i++) {
+            const uint64_t t = blockIdx.x + (uint64_t)i * gridDim.x;
+            if (t < ntiles) bit_tile_load(a, t, s_vals + i * vstride, &s_full[i], lane);
         }
-        buf ^= 1u;
+    }
+
+    uint32_t it = 0;  // this CTA's tile counter
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+        const uint32_t bi = it & 1u;
+        const uint64_t s = a.s_begin + tile * kBitWarps + warp;
+        const uint32_t *v_cur = s_vals + bi * vstride + warp;  // value of bin b: v_cur[8 b]
+        mbar_wait(&s_full[bi], (it >> 1) & 1u);
+        // the tile is processed; the last warp done with this buffer refills it with tile + 2
+        auto release = [&]() {
+            __syncwarp();
+            uint32_t last = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                last = atomicAdd(&s_done[bi], 1u) == kBitWarps - 1;
+                if (last) s_done[bi] = 0u;
+            }
+            last = __shfl_sync(0xFFFFFFFFu, last, 0);
+            const uint64_t tn = tile + 2ull * gridDim.x;
+            if (last && tn < ntiles) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                bit_tile_load(a, tn, s_vals + bi * vstride, &s_full[bi], lane);
+            }
+        };
+        if (s >= a.n_sets) {  // warp-uniform: a tail tile's missing set
+            release();
+            continue;
+        }
         uint32_t c[kBitCS];
 #pragma unroll
         for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;
@@ -273,7 +297,8 @@ __global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_ke
             const uint32_t b = 16u * g + lane;
             uint32_t r = 0u;
             if (lane < 16u && b < a.nscan) {
-                const uint32_t v = v_cur[b];
+                // bins past the staged prefix (GOPH / HOPH levels most sets never reach): direct
+                const uint32_t v = b < a.npre ? v_cur[8 * b] : __ldg(a.F + (uint64_t)b * a.ld + s);
                 if (v < s_width[b]) r = __ldg(a.idx + s_start[b] + v);
             }
             return r;
@@ -416,6 +441,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MODE == 1 ? 2 : 3) bit_scan_ke
             if (step(g, x, xb)) break;
             if (g + 1 < nbt && step(g + 1, xb, x)) break;
         }
+        release();
     }
 }
 
@@ -432,9 +458,12 @@ cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     bit_maxeq_kernel<<<1, 1024, 0, st>>>(a);
     // the scan: 8 consecutive sets per CTA tile, grid-stride; 3 CTAs per SM (HOPH: 2, its T slices need 128 registers)
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
-    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * (a.mode_hoph ? 2 : 3) * 8);
-    const size_t smem = (size_t)kBitWarps * 2 * ((a.nscan + 31u) & ~31u) * 4;
-    auto kern = a.mode_hoph ? bit_scan_kernel<1> : bit_scan_kernel<0>;
+    // (OPHGPU_BIT_CTAS=2: the full-OPH / GOPH scan at 2 CTAs per SM without register limit, A/B)
+    static const bool two = getenv("OPHGPU_BIT_CTAS") && atoi(getenv("OPHGPU_BIT_CTAS")) == 2;
+    const int ctas = a.mode_hoph || two ? 2 : 3;
+    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * ctas * 8);
+    const size_t smem = (size_t)2 * a.npre * kBitWarps * 4;
+    auto kern = a.mode_hoph ? bit_scan_kernel<1, 2> : (two ? bit_scan_kernel<0, 2> : bit_scan_kernel<0, 3>);
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return e;
     kern<<<grid, 32 * kBitWarps, smem, st>>>(a);

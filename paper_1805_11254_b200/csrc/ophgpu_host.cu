@@ -467,6 +467,10 @@ oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketche
     ba.nb = nb;
     ba.nw = nw;
     ba.nscan = nb;
+    // bins staged per CTA tile: all (full OPH); the levels most pairs reach (GOPH: up to the
+    // first decidable level + 1; HOPH: groups 1-2); the rest is read directly when reached
+    ba.npre = method == OPH_METHOD_FULL ? nb
+                                        : std::min<uint32_t>(nb, kp * (method == OPH_METHOD_GOPH ? plan.l0 + 1 : 2));
     ba.kp = kp;
     ba.nbins_total = nb;
     ba.method = method;
@@ -552,7 +556,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     // (the 1:1 split: T_l = S_l / 2^(L-1-l) in <= 24 bit slices), |V| <= 2^23, <= 1023 bins
     {
         // (GOPH / HOPH levels must be whole batches of 16 bins: k' % 16 == 0)
-        const bool dom = !mw && !ea && bitmap_sizes_ok(Qv->vocab_size, nb) &&
+        const bool dom = !mw && !ea && bitmap_sizes_ok(Qv->vocab_size, nb) && Sv->ld % 8 == 0 &&
                          (method == OPH_METHOD_FULL || kp % 16 == 0) &&
                          (method != OPH_METHOD_HOPH || (a == 1 && b == 1 && nlev >= 2 && nlev <= 20 && plan.lam));
         const bool fits = ws_bytes >= fixed + bitmap_region_bytes(Qv->vocab_size, nb);

@@ -21,6 +21,8 @@
 // All decisions are exact integer arithmetic against thresholds the host
 // planner compiled from the paper's rules (R23); no floating
 // point decides anything.  Layouts: DESIGN.md "Data layout in HBM".
+#include <cstdlib>
+
 #include <cub/cub.cuh>
 
 #include "internal.h"
