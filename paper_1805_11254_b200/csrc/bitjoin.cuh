@@ -200,17 +200,22 @@ __device__ void bit_hoph_final(const BitArgs &a, uint32_t qg, uint64_t s, uint32
 // MODE 0: a count over the scanned bins (FULL: one level, the final verdict; GOPH:
 // levels of k' bins with thresholds on M_c).  MODE 1: HOPH 1:1, per-group counts
 // folded into T_l = 2 T_(l-1) + M_l, thresholds on T_l, the HOPH estimator at L.
-// The values of a CTA tile (8 consecutive sets) in the first npre bins: per bin row one
-// 32-B bulk copy (TMA engine) of the 8 sets into vbuf[buffer][bin][8], completion on an
-// mbarrier.  Issued by the 32 lanes of the last warp to finish the tile two tiles back
-// (a double buffer; no CTA-wide barrier), so the copies' latency is hidden behind a
-// whole tile's scan and the gathers cost no L1 requests.
+// The values of a CTA tile (8 consecutive sets) in the first npre bins: per bin row the
+// tile's 32-B segment is copied with two 16-B cp.async (L1-bypassing) into
+// vbuf[buffer][bin][8]; each issuing lane then arrives on the buffer's mbarrier when its
+// copies have landed (cp.async.mbarrier.arrive.noinc; 32 arrivals per fill).  Issued by
+// the 32 lanes of the last warp to finish the tile two tiles back (a double buffer; no
+// CTA-wide barrier): one gather request per 16 B of the tile instead of one per set
+// value per warp, and the latency hidden behind a whole tile's scan.
 __device__ __forceinline__ void bit_tile_load(const BitArgs &a, uint64_t tile, uint32_t *dst, uint64_t *bar,
                                               uint32_t lane) {
-    const uint64_t s0 = a.s_begin + tile * kBitWarps;
-    if (lane == 0) mbar_expect_tx(bar, a.npre * 32u);
-    __syncwarp();
-    for (uint32_t b = lane; b < a.npre; b += 32) bulk_g2s(dst + 8 * b, a.F + (uint64_t)b * a.ld + s0, 32u, bar);
+    const uint64_t s0 = a.s_begin + tile * kBitWarps + 4u * (lane & 1u);
+    for (uint32_t b = lane >> 1; b < a.npre; b += 16) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + 8 * b + 4 * (lane & 1u))),
+                     "l"(a.F + (uint64_t)b * a.ld + s0)
+                     : "memory");
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
 template <int MODE, int MINB>
@@ -238,8 +243,8 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
     const uint32_t vstride = a.npre * 8u;  // words per buffer
     if (threadIdx.x == 0) {
-        mbar_init(&s_full[0], 1);
-        mbar_init(&s_full[1], 1);
+        mbar_init(&s_full[0], 32);  // the 32 lanes of the filling warp
+        mbar_init(&s_full[1], 32);
         s_done[0] = s_done[1] = 0u;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -268,10 +273,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
             }
             last = __shfl_sync(0xFFFFFFFFu, last, 0);
             const uint64_t tn = tile + 2ull * gridDim.x;
-            if (last && tn < ntiles) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                bit_tile_load(a, tn, s_vals + bi * vstride, &s_full[bi], lane);
-            }
+            if (last && tn < ntiles) bit_tile_load(a, tn, s_vals + bi * vstride, &s_full[bi], lane);
         };
         if (s >= a.n_sets) {  // warp-uniform: a tail tile's missing set
             release();
