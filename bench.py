@@ -604,7 +604,21 @@ def run_ours(args):
                   "compare_hoph": N * (4 * hkp + 4)}
     models = {}
 
+    # BITMAP join (K7): per (set, bin, block of 1024 queries) one 4-B entry of the value -> row
+    # table and one 128-B row of query bits, gathered from the L2-resident block tables; peak =
+    # the measured random 128-B row-gather rate from a 16-MB table (scripts/ubench.cu)
+    l2_peak = (ub or {}).get("gather_128B_rows_GBps", {}).get(str(16 << 20))
+    l2_src = ("measured: scripts/ubench.cu random 128-B row gathers, 16-MB table (profiles/ubench_r02.json)"
+              if l2_peak else "none measured")
+    qblocks = -(-Q // 1024)
+
     def model_for(kernel: str, phase: str):
+        if kernel.startswith("bit_scan_kernel"):
+            m = phase.split("_")[1]
+            bins = (bins_compared.get(m, Q * N * k) / Q) if m != "full" else N * k  # (set, bin) pairs scanned
+            gathered = bins * qblocks * (128 + 4)
+            return ("l2", gathered, (l2_peak or float("nan")) * 1e9, "GB/s", 1e9,
+                    "bytes: one 128-B query-bit row + one 4-B table entry per (set, bin compared, 1024-query block)")
         if kernel.startswith("build_kernel"):
             return ("hbm", build_bytes, hbm, "GB/s", 1e9, "bytes: CSR in + OPH/HOPH sketches and masks out")
         if kernel.startswith("join_kernel"):
@@ -638,7 +652,9 @@ def run_ours(args):
                     "unit": unit, "frac": ach / peak, "traffic": tr, "launches_per_step": launches_dom,
                     "work_per_step": work, "work": what, "kernel_ms": t_kernel * 1e3,
                     "kernel_share_of_call": share,
-                    "peak_source": (peak_src if bound == "hbm" else issue_src),
+                    "peak_source": {"hbm": peak_src, "l2": l2_src}.get(bound, issue_src),
+                    "bin_compares_per_s": (Q * N * k if dom_phase == "compare_full" else
+                                           bins_compared.get(dom_phase.split("_")[1], 0)) / t_kernel,
                     "step_share": t_kernel * 1e3 / ms}
     per_phase = {}
     for ph, byt in list(scan_bytes.items()) + [("build_oph_hoph", build_bytes)]:

@@ -84,21 +84,22 @@ __global__ void __launch_bounds__(256) imad(uint32_t iters, uint32_t k, uint32_t
     if (s == 0x9E3779B9u) *sink = s;
 }
 
-// each warp reads `per_warp` random rows of 128 B (lane = word), U rows in flight
+// each warp reads `per_warp` random rows of 128 B (lane = word), U rows in flight; the row
+// sequence is a multiplicative walk (one IMAD per row) so the loads, not the index math,
+// bound the rate
 template <int U>
 __global__ void __launch_bounds__(256) gather(const uint32_t *tab, uint32_t nrows_mask, uint32_t per_warp,
                                               uint32_t *sink) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t h = wid * 0x9E3779B1u + 12345u, acc = 0;
+    const uint32_t *tl = tab + lane;
     for (uint32_t i = 0; i < per_warp; i += U) {
         uint32_t r[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            h ^= h << 13;
-            h ^= h >> 17;
-            h ^= h << 5;
-            r[u] = __ldg(tab + (uint64_t)(h & nrows_mask) * 32 + lane);
+            h = h * 0x2545F491u + 0x9E3779B9u;
+            r[u] = __ldg(tl + (uint64_t)((h >> 7) & nrows_mask) * 32);
         }
 #pragma unroll
         for (int u = 0; u < U; u++) acc ^= r[u];
@@ -171,7 +172,7 @@ int main() {
         const uint64_t sizes[] = {64ull << 10, 1ull << 20, 16ull << 20, 64ull << 20, 256ull << 20};
         for (int i = 0; i < 5; i++) {
             const uint32_t nrows = (uint32_t)(sizes[i] / 128);
-            float ms = time_ms([&] { gather<8><<<grid, 256>>>(tab, nrows - 1, per_warp, sink); }, 5);
+            float ms = time_ms([&] { gather<16><<<grid, 256>>>(tab, nrows - 1, per_warp, sink); }, 5);
             const double bytes = (double)grid * 8 * per_warp * 128;
             printf("%s\"%llu\": %.1f", i ? ", " : "", (unsigned long long)sizes[i], bytes / (ms / 1e3) / 1e9);
         }
