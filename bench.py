@@ -53,7 +53,7 @@ UNIT = "comparisons/s"
 CONFIG_NAMES = ["image-like", "text-like", "scale", "sweep-0.2", "sweep-0.5", "sweep-0.9", "tiny"]
 
 # bounded CPU samples of each workload for the oracle legs (about 5-10 s of CPU work each)
-CPU_SAMPLE = {"image-like": (100_000, 64), "text-like": (100_000, 64), "scale": (100_000, 64),
+CPU_SAMPLE = {"image-like": (300_000, 64), "text-like": (100_000, 64), "scale": (100_000, 64),
               "sweep-0.2": (100_000, 64), "sweep-0.5": (100_000, 64), "sweep-0.9": (100_000, 64),
               "tiny": (2000, 100)}
 
@@ -373,28 +373,45 @@ def run_ours(args):
         og.topk_or_threshold_results(src, n, og.OPH_SELECT_THRESHOLD, outs[idx], ws=ws[4])
         return n
 
+    nvtx = torch.cuda.nvtx
+
     def step(ev=None, sets=sets, qsets=qsets):
-        """One OPH-family pass (rows a1-a3, a5-a8, a10); ev[i] marks phase boundaries."""
+        """One OPH-family pass (rows a1-a3, a5-a8, a10); ev[i] marks phase boundaries; NVTX
+        ranges name the phases (ncu --nvtx --nvtx-include "oph_step/")."""
+        nvtx.range_push("oph_step")
         mark(ev, 0)
         counts[:3].zero_()
         hists[:3].zero_()
+        nvtx.range_push("build_oph_hoph")
         og.oph_build_sketches(sets, V, seed, flat=flat, hier=hier, out_oph=so, out_hoph=sh)
+        nvtx.range_pop()
         mark(ev, 1)
+        nvtx.range_push("query_sketches")
         if rank == 0:
             og.oph_build_sketches(qsets, V, seed, flat=flat, hier=hier, out_oph=qo, out_hoph=qh)
         if world > 1:
             odist.broadcast_tensors([qo.values, qo.empty, qh.values, qh.empty])
+        nvtx.range_pop()
         mark(ev, 2)
+        nvtx.range_push("compare_full")
         og.compare_full(qo, so, flat, prm, res[0], set_id_base=base, ws=ws[0])
+        nvtx.range_pop()
         mark(ev, 3)
+        nvtx.range_push("compare_goph")
         og.compare_goph(qo, so, flat, prm, res[1], set_id_base=base, ws=ws[1], survivor_capacity=surv_cap)
+        nvtx.range_pop()
         mark(ev, 4)
+        nvtx.range_push("compare_hoph")
         og.compare_hoph(qh, sh, hier, prm, res[2], set_id_base=base, ws=ws[2], survivor_capacity=surv_cap)
+        nvtx.range_pop()
         mark(ev, 5)
+        nvtx.range_push("select")
         n4 = [int(x) for x in counts[:3].cpu()]  # one device->host read of the three hit counts
         assert max(n4) <= cap, f"hit buffer overflow {n4}"
         total = [select(i, n4) for i in range(3)]
+        nvtx.range_pop()
         mark(ev, 6)
+        nvtx.range_pop()
         return total
 
     def step_mw(ev=None, sets=sets, qsets=qsets):
