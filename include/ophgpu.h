@@ -16,15 +16,30 @@
  *    stream).  Every call only ENQUEUES work on that stream and returns; the
  *    caller synchronises.  Returned statuses cover argument checking and
  *    launch errors (OPH_ECUDA); device-side result overflow is reported
- *    through the result counters (see oph_results).
+ *    through the result counters (see oph_results).  The exceptions, each one
+ *    host synchronisation of `stream` inside the call:
+ *      (1) compare_goph / compare_hoph with the PROBE strategy (or AUTO
+ *          choosing it) when the survivor capacity is smaller than
+ *          32 x n_sets x the query count: the call first scores every query
+ *          at once and reads the survivor count back; only if the list
+ *          overflowed does it redo the queries in capacity-sized chunks
+ *          (a larger survivor_capacity avoids it);
+ *      (2) the first AUTO call on a collection (keyed by its value pointer,
+ *          size, bins and method) reads the PROBE sample's overflow count to
+ *          choose between PROBE and a register scan; later calls reuse the
+ *          decision without synchronising (OPH_STRATEGY_PROBE / BRUTE /
+ *          BITMAP never sample);
+ *      (3) oph_validate_sets, and the builds when OPHGPU_VALIDATE is set.
  *  - Sketch matrices are BIN-MAJOR uint32: element (bin b, set s) lives at
  *    d_values[b * ld + s], with a row stride ld >= n_sets that is a multiple
  *    of 4 (oph_sketch_ld() gives the canonical one).  An empty bin holds
  *    OPH_EMPTY.  Empty masks are bin-major too: bit (b % 32) of word
  *    d_empty[(b / 32) * ld + s] is set iff bin b of set s is empty.
  *  - Sets are CSR on the device: ids of set s are d_ids[d_offsets[s] ..
- *    d_offsets[s+1]), strictly increasing and < vocab_size (not
- *    validated on the device).
+ *    d_offsets[s+1]), strictly increasing and < vocab_size.  The
+ *    hot path does not check this; oph_validate_sets does (a debug aid), and
+ *    with the environment variable OPHGPU_VALIDATE set the two builds run it
+ *    first and return OPH_EINVAL on a violation.
  *  - Errors: OPH_EINVAL for bad arguments; OPH_EINCOMPAT when query and
  *    collection sketches differ in permutation seed, universe or layout
  *    (S:62); OPH_EAMBIGUOUS when a binomial tail lies within 1e-9
@@ -232,6 +247,13 @@ uint64_t oph_sketch_ld(uint64_t n_sets);
  * vocab_size > 2^32, a or b is 0, or more than 64 groups result. */
 oph_status oph_hier_layout_make(uint64_t vocab_size, uint32_t a, uint32_t b, uint32_t kprime,
                                 oph_hier_layout *out);
+
+/* Input contract check (debug aid): offsets non-decreasing with
+ * offsets[0] = 0 is NOT required, only offsets[s] <= offsets[s+1]; ids of every
+ * set strictly increasing and < vocab_size.  One validation kernel, then a
+ * host synchronisation of `stream`.  OPH_OK, OPH_EINVAL (violation or bad
+ * arguments), OPH_ECUDA. */
+oph_status oph_validate_sets(const oph_sets *sets, uint64_t vocab_size, void *stream);
 
 /* ---------------------------------------------------------------- build (rows a1-a3) */
 

@@ -91,7 +91,7 @@ _lib = None
 EXPORTS = ["oph_status_string", "oph_sketch_ld", "oph_hier_layout_make", "oph_build_sketches",
            "minwise_build_sketches", "oph_workspace_size", "oph_workspace_size_for", "compare_full", "compare_goph", "compare_hoph",
            "compare_minwise", "oph_select_workspace_size", "topk_or_threshold_results", "oph_plan_thresholds",
-           "exact_jaccard_pairs", "shingle_workspace_size", "shingle_text"]
+           "exact_jaccard_pairs", "shingle_workspace_size", "shingle_text", "oph_validate_sets"]
 
 
 def lib():
@@ -264,6 +264,14 @@ def _oph_build_sketches_impl(sets: SetCollection, vocab_size: int, seed: int, fl
         ctypes.byref(hier) if hier is not None else None, _ptr(sh.values) if sh else None,
         _ptr(sh.empty) if sh else None, c_u64(ld), _stream(stream)), "oph_build_sketches")
     return so, sh
+
+
+def oph_validate_sets(sets: SetCollection, vocab_size: int, stream=None):
+    """The CSR input contract check (debug aid; synchronises): raises OphError(OPH_EINVAL)
+    on a violation (ids not strictly increasing, an id >= vocab_size, offsets decreasing)."""
+    with _on(stream):
+        _check(lib().oph_validate_sets(ctypes.byref(sets.c()), c_u64(vocab_size), _stream(stream)),
+               "oph_validate_sets")
 
 
 def _minwise_build_sketches_impl(sets: SetCollection, vocab_size: int, seed: int, k: int, stream=None,

@@ -276,6 +276,9 @@ cudaError_t launch_level_e(const LevelArgs &a, cudaStream_t st);  // empty-aware
 cudaError_t launch_levels_scan(const LevelArgs &a, cudaStream_t st);
 cudaError_t launch_jaccard(const JaccardArgs &a, cudaStream_t st);
 cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st);
+// CSR contract check: *bad (device) |= 1 on a violation
+cudaError_t launch_validate(const uint64_t *offsets, const uint32_t *ids, uint64_t n_sets, uint64_t V, uint32_t *bad,
+                            cudaStream_t st);
 size_t shingle_temp_bytes(uint64_t n_bytes, uint64_t n_docs);
 cudaError_t run_shingle(const ShingleArgs &a, void *ws, size_t ws_bytes, cudaStream_t st);
 size_t select_temp_bytes(uint64_t n);

@@ -1025,6 +1025,28 @@ oph_status oph_hier_layout_make(uint64_t V, uint32_t a, uint32_t b, uint32_t kp,
     return OPH_OK;
 }
 
+oph_status oph_validate_sets(const oph_sets *sets, uint64_t V, void *stream) {
+    oph_status st;
+    if ((st = check_sets(sets))) return st;
+    if (V == 0 || V > (1ull << 32)) return OPH_EINVAL;
+    if (sets->n_sets == 0) return OPH_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t *bad = nullptr, h = 0;
+    if (cudaMallocAsync((void **)&bad, 4, s) != cudaSuccess) return OPH_ECUDA;
+    cudaError_t e = cudaMemsetAsync(bad, 0, 4, s);
+    if (e == cudaSuccess) e = launch_validate(sets->d_offsets, sets->d_ids, sets->n_sets, V, bad, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(bad, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return OPH_ECUDA;
+    return h ? OPH_EINVAL : OPH_OK;
+}
+
+static bool validate_env() {
+    static const bool on = getenv("OPHGPU_VALIDATE") != nullptr;
+    return on;
+}
+
 oph_status oph_build_sketches(const oph_sets *sets, const oph_perm *perm, const oph_flat_layout *flat, uint32_t *d_oph,
                               uint32_t *d_oph_empty, const oph_hier_layout *hier, uint32_t *d_hoph,
                               uint32_t *d_hoph_empty, uint64_t ld, void *stream) {
@@ -1083,6 +1105,7 @@ oph_status oph_build_sketches(const oph_sets *sets, const oph_perm *perm, const 
         per_set += ((uint64_t)hier->L * hier->kprime + 31) / 32 * 32 + 1;
     }
     if (per_set * 4 + 16 > 200 * 1024) return OPH_EINVAL;
+    if (validate_env() && (st = oph_validate_sets(sets, V, stream)) != OPH_OK) return st;
     return cuda_status(launch_build(a, (cudaStream_t)stream));
 }
 
@@ -1092,6 +1115,7 @@ oph_status minwise_build_sketches(const oph_sets *sets, uint64_t V, uint64_t see
     if ((st = check_sets(sets))) return st;
     if (V == 0 || V > (1ull << 32) || k == 0 || k > 65535 || !d_mw || !d_set_flags || ld < sets->n_sets || ld % 4)
         return OPH_EINVAL;
+    if (validate_env() && (st = oph_validate_sets(sets, V, stream)) != OPH_OK) return st;
     MinwiseArgs a{};
     a.offsets = sets->d_offsets;
     a.ids = sets->d_ids;

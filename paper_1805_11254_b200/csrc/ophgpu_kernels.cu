@@ -2267,6 +2267,35 @@ cudaError_t run_shingle(const ShingleArgs &a, void *ws, size_t ws_bytes, cudaStr
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// CSR contract check (debug aid, oph_validate_sets): warp per set, lanes compare
+// neighbouring ids; any violation sets *bad.
+// ---------------------------------------------------------------------------
+__global__ void validate_kernel(const uint64_t *offsets, const uint32_t *ids, uint64_t n_sets, uint64_t V,
+                                uint32_t *bad) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t s = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); s < n_sets; s += nwarps) {
+        const uint64_t lo = offsets[s], hi = offsets[s + 1];
+        bool err = hi < lo;
+        if (!err)
+            for (uint64_t e = lo + lane; e < hi; e += 32) {
+                const uint32_t x = ids[e];
+                err |= (uint64_t)x >= V;
+                if (e + 1 < hi) err |= ids[e + 1] <= x;
+            }
+        if (__any_sync(0xFFFFFFFFu, err) && lane == 0) atomicOr(bad, 1u);
+    }
+}
+
+cudaError_t launch_validate(const uint64_t *offsets, const uint32_t *ids, uint64_t n_sets, uint64_t V, uint32_t *bad,
+                            cudaStream_t st) {
+    if (n_sets == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<uint64_t>((n_sets + 7) / 8, 148ull * 16);
+    validate_kernel<<<grid, 256, 0, st>>>(offsets, ids, n_sets, V, bad);
+    return cudaGetLastError();
+}
+
 #include "bitjoin.cuh"
 
 }  // namespace ophgpu

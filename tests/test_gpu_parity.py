@@ -892,3 +892,30 @@ def test_bitmap_domain_errors(tiny_run):
     with pytest.raises(og.OphError) as e:
         og.compare_full(so, so, og.flat_layout(V, 64, 16), prm, og.Results(16))
     assert e.value.status == og.OPH_EINVAL
+
+
+def test_validate_sets(monkeypatch):
+    """oph_validate_sets (the CSR contract): valid collections pass; a repeated id,
+    a decreasing pair and an id >= |V| are each reported (OPH_EINVAL); with OPHGPU_VALIDATE
+    set the builds refuse such input."""
+    V = 1000
+    good_o, good_i = make_csr([[1, 2, 3], [], [999], [5, 7]])
+    og.oph_validate_sets(og.SetCollection.from_numpy(good_o, good_i), V)
+    bad = [np.array([1, 2, 2, 5], np.uint32), np.array([1, 3, 2, 5], np.uint32), np.array([1, 2, 3, 1000], np.uint32)]
+    offs = np.array([0, 4], dtype=np.uint64)
+    for ids in bad:
+        with pytest.raises(og.OphError) as e:
+            og.oph_validate_sets(og.SetCollection.from_numpy(offs, ids), V)
+        assert e.value.status == og.OPH_EINVAL
+    monkeypatch.setenv("OPHGPU_VALIDATE", "1")
+    # (the environment variable is read once per process: a fresh interpreter)
+    import subprocess
+    import sys
+    code = ("import numpy as np, paper_1805_11254_b200 as og; "
+            "s = og.SetCollection.from_numpy(np.array([0, 3], np.uint64), np.array([4, 4, 9], np.uint32)); "
+            "fl = og.flat_layout(1000, 8, 8)\n"
+            "try:\n    og.oph_build_sketches(s, 1000, 1, flat=fl)\n    print('built')\n"
+            "except og.OphError as e:\n    print('refused', e.status)\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    assert r.stdout.strip() == f"refused {og.OPH_EINVAL}", r.stdout + r.stderr
