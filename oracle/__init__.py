@@ -177,7 +177,7 @@ def compare_goph(Q, S, *, n, kprime, t_num, t_den, eps, joint=False, trace=False
     return (out, tr) if trace else out
 
 
-def compare_hoph(Q, S, *, L, kprime, a, b, t_num, t_den, eps, joint=False, trace=False):
+def compare_hoph(Q, S, *, L, kprime, a, b, t_num, t_den, eps, joint=False, trace=False, empty_aware=False):
     Q = np.ascontiguousarray(Q, dtype=np.uint32)
     S = np.ascontiguousarray(S, dtype=np.uint32)
     assert Q.shape[1] == S.shape[1] == L * kprime and L <= 64
@@ -188,7 +188,7 @@ def compare_hoph(Q, S, *, L, kprime, a, b, t_num, t_den, eps, joint=False, trace
     tr = np.zeros((Q.shape[0], S.shape[0], L, 2), dtype=np.int64) if trace else None
     lib().orc_compare_hoph(_p(Q), _u64(Q.shape[0]), _p(S), _u64(S.shape[0]), _u32(L), _u32(kprime),
                            _u32(a), _u32(b), ctypes.c_int(int(joint)), _u32(t_num), _u32(t_den),
-                           _p(lo), _p(up), _p(out), _p(tr))
+                           _p(lo), _p(up), _p(out), _p(tr), ctypes.c_int(int(empty_aware)))
     return (out, tr) if trace else out
 
 

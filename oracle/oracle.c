@@ -549,6 +549,85 @@ static void pair_hoph(const uint32_t *q, const uint32_t *s, uint32_t L, uint32_t
 }
 
 /* ------------------------------------------------------------------------ */
+/* O10e empty-aware HOPH (readings EH1-EH5).
+ *     Algorithm 2's mass balance (R19) with each group's trials taken to be
+ *     its non-excluded bins d_j = k' - excl_j (known from the empty masks
+ *     before any value is compared, EH1).  The groups with d_j > 0 form K; the
+ *     final verdict is the HOPH estimator sum_K c_j m_j/d_j / C_K >= T
+ *     (R21, R22; C_K = sum_K c_j).  After l groups the achieved mass is
+ *     A_l = sum_{j<=l, j in K} c_j m_j / d_j and the usable weight still to
+ *     compare is W_l = sum_{j>l, j in K} c_j, so the remaining groups must
+ *     reach P_r = (T C_K - A_l) / W_l, and Alg. 2's four tests run unchanged
+ *     on x = P_r k' (EH2, EH3).  With no excluded bin d_j = k', C_K = D,
+ *     A_l = S_l / k' and x is Alg. 2's (T D k' - S_l) / W_l exactly.  W_l = 0
+ *     before group L (every remaining group excluded) completes the comparison:
+ *     the final record, groups = l (EH4).  Exact: x = num / den with both
+ *     scaled by t_den lcm{d_j : j <= l, j in K}.                             */
+/* ------------------------------------------------------------------------ */
+static i128 i128_lcm(i128 a, i128 b) { return a / i128_gcd(a, b) * b; }
+
+static void pair_hoph_e(const uint32_t *q, const uint32_t *s, uint32_t L, uint32_t kp, uint32_t a, uint32_t b,
+                        int joint, uint32_t t_num, uint32_t t_den, const uint8_t *lower_le,
+                        const uint8_t *upper_le, orc_rec *r, int64_t *trace)
+{
+    i128 c[64], D;
+    hoph_weights(a, b, L, c, &D);
+    memset(r, 0, sizeof(*r));
+    uint32_t M[64], ex[64];
+    i128 C_K = 0;                         /* EH1: usable weight of the pair */
+    for (uint32_t j = 0; j < L; j++) {
+        M[j] = ex[j] = 0;
+        for (uint32_t t = j * kp; t < (j + 1) * kp; t++) {
+            M[j] += bin_matched(q[t], s[t]);
+            ex[j] += bin_excluded(q[t], s[t], joint);
+        }
+        if (ex[j] < kp) C_K += c[j];
+    }
+    i128 W = C_K;                         /* usable weight not yet compared */
+    i128 lam = 1;                         /* lcm of the compared usable d_j */
+    uint32_t nmb = 0, nex = 0;
+    for (uint32_t l = 1; l <= L; l++) {
+        const uint32_t d = kp - ex[l - 1];
+        nmb += M[l - 1];
+        nex += ex[l - 1];
+        if (d > 0) {
+            W -= c[l - 1];
+            lam = i128_lcm(lam, (i128)d);
+        }
+        r->groups = l;
+        r->n_mb = nmb;
+        r->n_excl = nex;
+        if (l == L || W == 0) { /* EH4 / EH5: the HOPH estimator over all groups */
+            uint32_t nmb_all = 0, nex_all = 0;
+            for (uint32_t j = 0; j < L; j++) { nmb_all += M[j]; nex_all += ex[j]; }
+            r->n_mb = nmb_all;
+            r->n_excl = nex_all;
+            hoph_final(M, ex, L, kp, c, t_num, t_den, r);
+            return;
+        }
+        /* A_l lam = sum_{j<=l, d_j>0} c_j m_j (lam / d_j) */
+        i128 A = 0;
+        for (uint32_t j = 0; j < l; j++)
+            if (ex[j] < kp) A += c[j] * M[j] * (lam / (kp - ex[j]));
+        i128 num = (i128)kp * ((i128)t_num * C_K * lam - (i128)t_den * A);
+        i128 den = (i128)t_den * lam * W;
+        if (trace) { trace[2 * (l - 1)] = (int64_t)num; trace[2 * (l - 1) + 1] = (int64_t)den; }
+        r->estimate = -1.0;
+        r->flags = ORC_EARLY;
+        if (num <= 0) { r->verdict = 1; return; }
+        if (num > (i128)kp * den) { r->verdict = 0; return; }
+        if (num * t_den < (i128)kp * t_num * den) {
+            int64_t m = (int64_t)(num / den);
+            if (lower_le[m]) { r->verdict = 1; return; }
+        } else {
+            int64_t m = (int64_t)((num + den - 1) / den);
+            if (upper_le[m]) { r->verdict = 0; return; }
+        }
+        r->flags = 0;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* MinWise comparison: fraction of equal fingerprints.          */
 /* ------------------------------------------------------------------------ */
 static void pair_minwise(const uint32_t *q, const uint32_t *s, uint8_t qf, uint8_t sf, uint32_t k,
@@ -597,15 +676,17 @@ void orc_compare_goph(const uint32_t *Q, uint64_t n_q, const uint32_t *S, uint64
 
 void orc_compare_hoph(const uint32_t *Q, uint64_t n_q, const uint32_t *S, uint64_t n_s, uint32_t L,
                       uint32_t kp, uint32_t a, uint32_t b, int joint, uint32_t t_num, uint32_t t_den,
-                      const uint8_t *lower_le, const uint8_t *upper_le, orc_rec *out, int64_t *trace)
+                      const uint8_t *lower_le, const uint8_t *upper_le, orc_rec *out, int64_t *trace,
+                      int empty_aware)
 {
     uint64_t k = (uint64_t)L * kp;
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t qi = 0; qi < (int64_t)n_q; qi++)
         for (uint64_t si = 0; si < n_s; si++) {
             uint64_t pi = (uint64_t)qi * n_s + si;
-            pair_hoph(Q + (uint64_t)qi * k, S + si * k, L, kp, a, b, joint, t_num, t_den, lower_le,
-                      upper_le, &out[pi], trace ? trace + 2 * L * pi : NULL);
+            (empty_aware ? pair_hoph_e : pair_hoph)(Q + (uint64_t)qi * k, S + si * k, L, kp, a, b, joint, t_num,
+                                                    t_den, lower_le, upper_le, &out[pi],
+                                                    trace ? trace + 2 * L * pi : NULL);
         }
 }
 

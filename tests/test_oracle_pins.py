@@ -411,6 +411,98 @@ def test_hoph_example2(golden):
     assert float(binomial.upper_tail(80, 100, 3, 5)) == pytest.approx(g["upper_80"], rel=1e-5)
 
 
+def test_hoph_e_example2(golden):
+    """The empty-aware HOPH rule (EH1-EH5) has no excluded bin in Example 2 and
+    reproduces it: x = 80 as a rational, NotSimilar after group 1."""
+    g = golden("example2.json")
+    lay = oracle.hoph_layout(g["vocab_size"], g["a"], g["b"], g["kprime"])
+    L, kp = len(lay), g["kprime"]
+    q = np.zeros((1, L * kp), dtype=np.uint32)
+    s = np.ones((1, L * kp), dtype=np.uint32)
+    s[0, :g["first_group_matches"]] = 0
+    r, tr = oracle.compare_hoph(q, s, L=L, kprime=kp, a=1, b=1, t_num=g["t_num"], t_den=g["t_den"],
+                                eps=g["eps"], trace=True, empty_aware=True)
+    num, den = tr[0, 0, 0]
+    assert Fraction(int(num), int(den)) == g["x"]
+    assert (r[0, 0]["groups"], r[0, 0]["verdict"]) == (g["groups_compared"], 0)
+
+
+def _hoph_pair_groups(M, ex, kp):
+    """A HOPH sketch pair whose group j has M[j] matched bins and ex[j] bins empty on
+    both sides (excluded in either mode), the rest unequal and non-empty."""
+    L = len(M)
+    q = np.zeros(L * kp, dtype=np.uint32)
+    s = np.ones(L * kp, dtype=np.uint32)
+    for j in range(L):
+        s[j * kp: j * kp + M[j]] = 0
+        q[j * kp + kp - ex[j]: (j + 1) * kp] = E
+        s[j * kp + kp - ex[j]: (j + 1) * kp] = E
+    return q, s
+
+
+def test_hoph_e_excluded_group_hand_example():
+    """EH2-EH3 by hand: k' = 4, L = 3 (1:1: c = [2, 1, 1], D = 4), T = 1/2, group 2 fully
+    excluded, so C_K = 3 and after group 1 the usable weight left is W_1 = c_3 = 1.
+      m_1 = 3 of 4: A_1 = 2 * 3/4 = 3/2, x = k' (T C_K - A_1) / W_1 = 4 (3/2 - 3/2) = 0
+                    -> Similar at group 1;  Alg. 2: S_1 = 6, x = (T D k' - S_1) / W_1' =
+                    (8 - 6) / 2 = 1, P(X <= 1) = 5/16 > eps -> it continues.
+      m_1 = 0:      x = 4 * 3/2 / 1 = 6 > k' -> NotSimilar at group 1;  Alg. 2: x = 8 / 2 = 4,
+                    P(X >= 4) = 1/16 > eps -> it continues."""
+    kp = 4
+    for m1, verdict, x in [(3, 1, Fraction(0)), (0, 0, Fraction(6))]:
+        q, s = _hoph_pair_groups([m1, 0, 0], [0, kp, 0], kp)
+        kw = dict(L=3, kprime=kp, a=1, b=1, t_num=1, t_den=2, eps=1e-3, trace=True)
+        r, tr = oracle.compare_hoph(q[None], s[None], empty_aware=True, **kw)
+        num, den = tr[0, 0, 0]
+        assert Fraction(int(num), int(den)) == x
+        assert (r[0, 0]["groups"], r[0, 0]["verdict"], r[0, 0]["flags"]) == (1, verdict, oracle.EARLY)
+        p = oracle.compare_hoph(q[None], s[None], **kw)[0][0, 0]
+        assert p["groups"] > 1
+
+
+def test_hoph_e_reduces_to_alg2_without_empties():
+    """No excluded bin: the variant's records equal Algorithm 2's (R19) on random per-group
+    match counts (1:1 and 1:2 layouts, three parameter sets, both empty modes)."""
+    rng = np.random.default_rng(66)
+    for kp, L, a, b, tn, td, eps in [(16, 6, 1, 1, 7, 10, 1e-4), (32, 8, 1, 1, 4, 5, 1e-3), (10, 5, 1, 2, 1, 2, 1e-2)]:
+        Q, S = [], []
+        for _ in range(200):
+            q, s = _hoph_pair_groups(rng.binomial(kp, rng.uniform(0, 1), size=L).tolist(), [0] * L, kp)
+            Q.append(q); S.append(s)
+        Q, S = np.array(Q), np.array(S)
+        for joint in (False, True):
+            kw = dict(L=L, kprime=kp, a=a, b=b, t_num=tn, t_den=td, eps=eps, joint=joint)
+            assert np.array_equal(oracle.compare_hoph(Q, S, **kw), oracle.compare_hoph(Q, S, empty_aware=True, **kw))
+
+
+def test_hoph_e_final_records_are_the_estimator():
+    """EH4 / EH5: a pair the variant does not stop early carries the HOPH estimator's record
+    over all groups (R21, R22); a pair with no matched bin is never Similar."""
+    rng = np.random.default_rng(67)
+    kp, L = 8, 5
+    Q, S = [], []
+    for _ in range(400):
+        ex = [int(x) if rng.random() < 0.6 else kp for x in rng.integers(0, kp, size=L)]
+        M = [int(rng.integers(0, kp - e + 1)) for e in ex]
+        q, s = _hoph_pair_groups(M, ex, kp)
+        Q.append(q); S.append(s)
+    Q, S = np.array(Q), np.array(S)
+    for joint in (False, True):
+        r = oracle.compare_hoph(Q, S, L=L, kprime=kp, a=1, b=1, t_num=3, t_den=5, eps=1e-3, joint=joint,
+                                empty_aware=True)
+        d = np.arange(len(Q))
+        rr = r[d, d]
+        done = (rr["flags"] & oracle.EARLY) == 0
+        assert done.sum() > 50 and (~done).sum() > 50
+        for i in np.nonzero(done)[0]:
+            h = oracle.hoph_estimate(Q[i], S[i], L=L, kprime=kp, a=1, b=1, t_num=3, t_den=5, joint=joint)
+            assert (rr["verdict"][i], rr["flags"][i], rr["n_mb"][i], rr["n_excl"][i]) == \
+                (h["verdict"], h["flags"], h["n_mb"], h["n_excl"])
+            assert rr["estimate"][i] == h["estimate"]
+        nomatch = np.array([((Q[i] == S[i]) & (Q[i] != E)).sum() == 0 for i in range(len(Q))])
+        assert nomatch.any() and (rr["verdict"][nomatch] == 0).all()
+
+
 def test_hoph_mass_balance_cross_check():
     """Algorithm 2 with the mass balance P_r = (T - sum_{j<=l} w_j M_j/k') /
     sum_{j>l} w_j (R19) re-evaluated with Fractions on random match counts."""
@@ -614,6 +706,69 @@ def test_hoph_drop_renormalise_unbiased_sparse():
     assert dropped >= 0.99 * len(ests)
     assert abs(ests.mean() - float(Jt)) < 3 * se
     assert abs(mutant.mean() - float(Jt)) > 3 * (mutant.std(ddof=1) / np.sqrt(len(mutant)))
+
+
+# --------------------------------------------------------------------- Lemmas 1-3
+def test_lemma1_lemma2_spec_examples():
+    """S:426-439: r = 1/2, l = 2, N_mb = [1, 2] -> (1/4 + 2/8) 3 = 3/2; N_eb = [2, 0] ->
+    (2/4) 3 = 3/2; all zeros -> 0."""
+    from oracle import lemmas
+    assert lemmas.hoph_aggregate([1, 2], Fraction(1, 2), 2) == Fraction(3, 2)
+    assert lemmas.hoph_aggregate([2, 0], Fraction(1, 2), 2) == Fraction(3, 2)
+    assert lemmas.hoph_aggregate([0, 0, 0], Fraction(1, 3), 3) == 0
+
+
+def test_lemma1_equals_its_proof_first_line():
+    """Lemma 1/2's closed form equals the proof's probability form times k_h = (l+1) k'
+    (k_j = k'/r^j), exactly, on random counts for r in {1/2, 1/3, 2/3}: a wrong
+    exponent (r^(2l) for r^(2l-1)) or factor ((l) for (l+1)) fails."""
+    from oracle import lemmas
+    rng = np.random.default_rng(91)
+    for r in (Fraction(1, 2), Fraction(1, 3), Fraction(2, 3)):
+        for l in (1, 2, 3, 5, 9):
+            for _ in range(20):
+                kp = int(rng.integers(1, 64))
+                N = [int(x) for x in rng.integers(0, 2 * kp, size=l)]
+                assert lemmas.hoph_aggregate(N, r, l) == \
+                    lemmas.hoph_aggregate_probability(N, r, l, kp) * (l + 1) * kp
+
+
+def test_lemma3_golden_and_terms():
+    """Lemma 3 on the P:482 worked example, D1 vs D2 (groups [[1,1],[(x),0],[0,1]] vs
+    [[1,2],[(x),0],[0,0]], k' = 2, r = 1/2): terms N_mb = [1, 1 + 1], N_eb = [0, 1 + 0] ->
+    1/2 * 1/2 + 1/2 * 2/3 = 7/12 (S:467's 0.583 under R31); the last two groups' counts are
+    summed (P:592)."""
+    from oracle import lemmas
+    assert lemmas.lemma_terms([1, 1, 1]) == [1, 2]
+    assert lemmas.lemma_terms([0, 1, 0]) == [0, 1]
+    assert lemmas.hoph_lemma3_estimate([1, 2], [0, 1], Fraction(1, 2), 2, 2) == Fraction(7, 12)
+    assert lemmas.hoph_lemma3_estimate([1, 2], [2, 0], Fraction(1, 2), 2, 2) is None
+
+
+def test_lemma3_unbiased_joint_empty():
+    """Lemma 3 ("the unbiased estimator"): under JointEmpty each term N_mb/(k - N_eb)
+    is unbiased for J given the union's placement and the weights sum to 1 at r = 1/2, so
+    over 3000 permutations the mean is J within 3 s.e. (1:1 HOPH over 2^12, k' = 16, a
+    2048-element union: no term loses all its bins)."""
+    from oracle import lemmas
+    rng = np.random.default_rng(92)
+    V, kp = 1 << 12, 16
+    lay = oracle.hoph_layout(V, 1, 1, kp)
+    L = len(lay)
+    A, B, Jt = _pair_with_union(2048, 0.5, V, rng)
+    offs, ids = make_csr([A, B])
+    ests = []
+    for seed in range(3000):
+        H = oracle.hoph_sketch(offs, ids, V, lay, kp, seed)
+        g0, g1 = H[0].reshape(L, kp), H[1].reshape(L, kp)
+        m = ((g0 == g1) & (g0 != E)).sum(1).tolist()
+        e = ((g0 == E) & (g1 == E)).sum(1).tolist()
+        est = lemmas.hoph_lemma3_estimate(lemmas.lemma_terms(m), lemmas.lemma_terms(e), Fraction(1, 2), L - 1, kp)
+        assert est is not None
+        ests.append(float(est))
+    ests = np.array(ests)
+    se = ests.std(ddof=1) / np.sqrt(len(ests))
+    assert abs(ests.mean() - float(Jt)) < 3 * se
 
 
 # --------------------------------------------------------------------- MinWise
