@@ -139,7 +139,7 @@ typedef struct {
     uint32_t variant;    /* OPH_VARIANT_*: the filter rule (compare_goph only; 0 elsewhere) */
 } oph_params;
 
-/* Filter rule of compare_goph.
+/* Filter rule of compare_goph / compare_hoph.
  *   PAPER       : Algorithm 1 as read in DESIGN.md R10-R16: the
  *                 binomial trials of a group are its k' bins.
  *   EMPTY_AWARE : the empty-aware variant (DESIGN.md
@@ -153,7 +153,18 @@ typedef struct {
  *                 bin is never Similar under it (E5), so threshold results
  *                 without a termination histogram take the PROBE join (AUTO /
  *                 PROBE) and decide only the listed pairs; dense records, a
- *                 histogram or BRUTE run one register scan over all groups. */
+ *                 histogram or BRUTE run one register scan over all groups.
+ *                 compare_hoph (EH1-EH5): Algorithm 2's mass balance
+ *                 with group j's trials its usable bins d_j = k' - excl_j; the
+ *                 groups with d_j > 0 (weight C_K) decide: after l groups
+ *                 x = k' (T C_K - A_l) / W_l with A_l = sum_{j<=l} c_j m_j / d_j
+ *                 and W_l the usable weight left, Algorithm 2's tests on x,
+ *                 exact in 128-bit integers; W_l = 0 or the last group: the
+ *                 HOPH estimator.  Identical to PAPER when no bin is excluded.
+ *                 Threshold results without a histogram take the PROBE join
+ *                 (pairs with a matched bin); otherwise every pair is walked.
+ *                 EINVAL when k'^2 t_num t_den D lcm(1..k') >= 2^124.
+ *   Full OPH and MinWise refuse EMPTY_AWARE (OPH_EINVAL). */
 enum { OPH_VARIANT_PAPER = 0, OPH_VARIANT_EMPTY_AWARE = 1 };
 
 /* Collection-scan strategies; every strategy returns

@@ -202,6 +202,8 @@ struct LevelArgs {
     const uint32_t *QE;     // query empty masks, bin-major [nw][ldq]
     uint32_t ma1;           // #{m : P(X <= m) <= eps}, X ~ Bin(k', T) (0: never Similar by the tail)
     uint32_t mr1;           // min{m : P(X >= m) <= eps} - 1
+    // empty-aware HOPH over every pair of queries [q_col0, q_col0 + nq) x the sets (no list)
+    uint32_t implicit;
 };
 
 // BITMAP strategy (bitjoin.cuh): one block of <= 1024 queries against the collection

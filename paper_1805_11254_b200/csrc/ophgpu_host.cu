@@ -529,7 +529,7 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     if (p->strategy > OPH_STRATEGY_BITMAP || p->variant > OPH_VARIANT_EMPTY_AWARE) return OPH_EINVAL;
     // the empty-aware GOPH rule (E1-E4) runs as one register scan of every group
     const bool ea = p->variant == OPH_VARIANT_EMPTY_AWARE;
-    if (ea && method != OPH_METHOD_GOPH) return OPH_EINVAL;
+    if (ea && method != OPH_METHOD_GOPH && method != OPH_METHOD_HOPH) return OPH_EINVAL;
     if (Qv->seed != Sv->seed || Qv->vocab_size != Sv->vocab_size || Qv->n_bins != Sv->n_bins) return OPH_EINCOMPAT;
     const uint32_t nb = Qv->n_bins;
     const uint32_t nw = (uint32_t)ceil_div(nb, 32);
@@ -547,7 +547,14 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         plan = make_plan(method, nlev, kp, a, b, p->t_num, p->t_den, p->epsilon);
         if (plan.st != OPH_OK) return plan.st;
         if (method == OPH_METHOD_HOPH && nlev > 1 && plan.lam == 0) return OPH_EINVAL;
-        if (ea && (uint64_t)nlev * kp > 512) return OPH_EINVAL;
+        if (ea && method == OPH_METHOD_GOPH && (uint64_t)nlev * kp > 512) return OPH_EINVAL;
+        if (ea && method == OPH_METHOD_HOPH) {
+            // the empty-aware HOPH rule's exact 128-bit states: k'^2 t_num t_den D lcm(1..k') < 2^124
+            u128 D = 0;
+            for (uint32_t j = 0; j < nlev; j++) D += plan.c[j];
+            const long double mag = (long double)kp * kp * p->t_num * p->t_den * (long double)D * (long double)plan.lam;
+            if (plan.lam == 0 || nlev < 2 || mag >= 1.0e37L) return OPH_EINVAL;
+        }
     }
 
     const size_t fixed = ws_fixed_bytes(n_q, n_s, nb);
@@ -610,7 +617,11 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
     // parity test of that path)
     const bool no_multi = getenv("OPHGPU_NO_MULTI_LEVEL_SCAN") != nullptr;
     const bool multi =
-        levels && (uint64_t)nlev * kp <= 512 && (((state_max << msh) < (u128)UINT32_MAX && !no_multi) || ea);
+        levels && (uint64_t)nlev * kp <= 512 &&
+        (((state_max << msh) < (u128)UINT32_MAX && !no_multi && !ea) || (ea && method == OPH_METHOD_GOPH));
+    // the empty-aware HOPH rule without a join list (dense records, histograms, BRUTE): one
+    // per-pair walk over every (query, set) pair
+    const bool he_all = ea && method == OPH_METHOD_HOPH && !ea_probe;
     // the multi-level scan of a BRUTE or dense call produces no survivor lists: all
     // queries in one chunk (survivor-sized chunks cut its grid into small launches)
     const bool no_lists = multi && !ea_probe && (strategy == OPH_STRATEGY_BRUTE || res->mode == OPH_RES_DENSE);
@@ -898,6 +909,13 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         if (levels || probe)
             if ((e = cudaMemsetAsync(w.counters, 0, (kMaxGroups + 3) * 8, stream)) != cudaSuccess) return e;
         if (!probe) {
+            if (he_all) {
+                LevelArgs lm = la;
+                lm.q_col0 = (uint32_t)q0;
+                lm.nq = (uint32_t)nq;
+                lm.implicit = 1;
+                return launch_level_e(lm, stream);
+            }
             if (!multi) return launch_scan(s, 32, stream);
             LevelArgs lm = la;
             lm.q_col0 = (uint32_t)q0;

@@ -1958,8 +1958,105 @@ __global__ void __launch_bounds__(256) level_e_kernel(const __grid_constant__ Le
     }
 }
 
+// The empty-aware HOPH rule (EH1-EH5, oracle pair_hoph_e): per pair, the groups' usable
+// bins d_j and the usable weight C_K come from the masks first; then group by group the
+// achieved mass A_l = sum_{j<=l, d_j>0} c_j m_j / d_j and the usable weight left W_l give
+// x = k' (T C_K - A_l) / W_l, tested with Alg. 2's rules in exact 128-bit integers scaled
+// by t_den lcm{d_j compared}; W_l = 0 or the last group: the HOPH estimator.  Pairs come
+// from the join's list (those with a matched bin; no other pair can be Similar) or, with
+// `implicit`, every (query, set) pair.
+__device__ __forceinline__ i128_t i128_gcd_d(i128_t x, i128_t y) {
+    while (y != 0) {
+        const i128_t t = x % y;
+        x = y;
+        y = t;
+    }
+    return x;
+}
+
+__global__ void __launch_bounds__(256) level_he_kernel(const __grid_constant__ LevelArgs a) {
+    const unsigned long long n = a.implicit ? (unsigned long long)a.nq * a.n_sets : *a.count_in;
+    const i128_t kp = a.kp, tn = a.t_num, td = a.t_den;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long base = blockIdx.x * (unsigned long long)blockDim.x + (threadIdx.x & ~31u); base < n;
+         base += stride) {
+        const unsigned long long i = base + (threadIdx.x & 31u);
+        bool alive = i < n;
+        uint32_t q = 0, s = 0;
+        uint64_t usable = 0;  // bit j: group j has a usable bin
+        i128_t CK = 0;
+        if (alive) {
+            if (a.implicit) {
+                q = a.q_col0 + (uint32_t)(i / a.n_sets);
+                s = (uint32_t)(i % a.n_sets);
+            } else {
+                q = a.in.q[i];
+                s = a.in.s[i];
+            }
+            for (uint32_t g = 0; g < a.nlev; g++)
+                if (group_excl(a, q, s, g) < a.kp) {
+                    usable |= 1ull << g;
+                    CK += (i128_t)a.c[g];
+                }
+        }
+        i128_t W = CK, lam = 1, A = 0;  // A = A_l lam
+        uint32_t nmb = 0, nex = 0;
+        for (uint32_t l = 1; l <= a.nlev; l++) {
+            if (!__any_sync(0xFFFFFFFFu, alive)) break;
+            bool dec = false, acc = false;
+            uint32_t flags = OPH_FLAG_EARLY, n_mb = 0, n_ex = 0;
+            float est = -1.0f;
+            if (alive) {
+                const uint32_t m = group_matches(a, q, s, l - 1);
+                const uint32_t e = group_excl(a, q, s, l - 1);
+                nmb += m;
+                nex += e;
+                if ((usable >> (l - 1)) & 1ull) {
+                    const i128_t d = (i128_t)(a.kp - e);
+                    W -= (i128_t)a.c[l - 1];
+                    const i128_t nl = lam / i128_gcd_d(lam, d) * d;  // lcm
+                    A = A * (nl / lam) + (i128_t)a.c[l - 1] * m * (nl / d);
+                    lam = nl;
+                }
+                n_mb = nmb;
+                n_ex = nex;
+                if (l == a.nlev || W == 0) {  // EH4 / EH5: the HOPH estimator over all groups
+                    dec = true;
+                    u128_t num = 0, csum = 0;
+                    n_mb = n_ex = 0;
+                    for (uint32_t g = 0; g < a.nlev; g++) {
+                        const uint32_t mg = group_matches(a, q, s, g);
+                        const uint32_t eg = group_excl(a, q, s, g);
+                        n_mb += mg;
+                        n_ex += eg;
+                        const uint32_t dg = a.kp - eg;
+                        if (dg == 0) continue;
+                        num += a.c[g] * mg * (a.lam / dg);
+                        csum += a.c[g];
+                    }
+                    flags = 0;
+                    if (csum == 0) {
+                        flags = OPH_FLAG_UNDEFINED;
+                    } else {
+                        acc = num * a.t_den >= (u128_t)a.t_num * a.lam * csum;
+                        est = (float)((double)num / ((double)a.lam * (double)csum));
+                    }
+                } else {
+                    const i128_t num = kp * (tn * CK * lam - td * A), den = td * lam * W;
+                    acc = num <= 0 || (num * td < kp * tn * den && num < (i128_t)a.ma1 * den);
+                    dec = acc || num > kp * den || (num * td >= kp * tn * den && num > (i128_t)a.mr1 * den);
+                }
+            }
+            emit(a.res, dec, q, s, n_mb, n_ex, l, acc, flags, est);
+            hist_add(a.res.hist, l, dec ? 1u : 0u);
+            alive = alive && !dec;
+        }
+    }
+}
+
 cudaError_t launch_level_e(const LevelArgs &a, cudaStream_t st) {
-    level_e_kernel<<<148 * 2, 256, 0, st>>>(a);
+    if (a.method == kHoph) level_he_kernel<<<148 * 4, 256, 0, st>>>(a);
+    else level_e_kernel<<<148 * 2, 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 

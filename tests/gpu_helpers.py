@@ -24,12 +24,12 @@ def gpu_dense(method, q, s, *, layout=None, t_num, t_den, eps=1e-4, joint=False,
     applies -- |V| <= 2^23, not MinWise -- else the BRUTE scan)."""
     res = og.Results(q.n_sets * s.n_sets, dense=True)
     prm = og.params(t_num, t_den, eps, joint, strategy,
-                    variant=og.OPH_VARIANT_EMPTY_AWARE if method == "goph_e" else 0)
+                    variant=og.OPH_VARIANT_EMPTY_AWARE if method in ("goph_e", "hoph_e") else 0)
     if method == "full":
         og.compare_full(q, s, layout, prm, res)
     elif method in ("goph", "goph_e"):
         og.compare_goph(q, s, layout, prm, res, survivor_capacity=survivor_capacity)
-    elif method == "hoph":
+    elif method in ("hoph", "hoph_e"):
         og.compare_hoph(q, s, layout, prm, res, survivor_capacity=survivor_capacity)
     elif method == "minwise":
         og.compare_minwise(q, s, prm, res)
@@ -59,12 +59,12 @@ def gpu_threshold_hits(method, q, s, *, layout=None, t_num, t_den, eps=1e-4, joi
     """Sorted threshold hit list from the GPU (compare + topk_or_threshold_results)."""
     res = og.Results(capacity)
     prm = og.params(t_num, t_den, eps, joint, strategy,
-                    variant=og.OPH_VARIANT_EMPTY_AWARE if method == "goph_e" else 0)
+                    variant=og.OPH_VARIANT_EMPTY_AWARE if method in ("goph_e", "hoph_e") else 0)
     if method == "full":
         og.compare_full(q, s, layout, prm, res, set_id_base=set_id_base)
     elif method in ("goph", "goph_e"):
         og.compare_goph(q, s, layout, prm, res, set_id_base=set_id_base, survivor_capacity=survivor_capacity)
-    elif method == "hoph":
+    elif method in ("hoph", "hoph_e"):
         og.compare_hoph(q, s, layout, prm, res, set_id_base=set_id_base, survivor_capacity=survivor_capacity)
     elif method == "minwise":
         og.compare_minwise(q, s, prm, res, set_id_base=set_id_base)
@@ -85,8 +85,9 @@ def oracle_records(method, Q, S, *, t_num, t_den, eps=1e-4, joint=False, k=None,
     if method in ("goph", "goph_e"):
         return oracle.compare_goph(Q, S, n=k // kprime, kprime=kprime, t_num=t_num, t_den=t_den, eps=eps, joint=joint,
                                    empty_aware=method == "goph_e")
-    if method == "hoph":
-        return oracle.compare_hoph(Q, S, L=L, kprime=kprime, a=a, b=b, t_num=t_num, t_den=t_den, eps=eps, joint=joint)
+    if method in ("hoph", "hoph_e"):
+        return oracle.compare_hoph(Q, S, L=L, kprime=kprime, a=a, b=b, t_num=t_num, t_den=t_den, eps=eps, joint=joint,
+                                   empty_aware=method == "hoph_e")
     if method == "minwise":
         return oracle.compare_minwise(Q, qflags, S, sflags, t_num=t_num, t_den=t_den)
     raise ValueError(method)

@@ -216,7 +216,7 @@ def test_goph_empty_aware_ragged(V, k, kp, seed):
 
 
 def test_goph_empty_aware_invalid(tiny_run):
-    """The variant is a GOPH rule: other methods refuse it, and so does a GOPH
+    """The variant is a GOPH / HOPH rule: full OPH (and MinWise) refuse it, and so does a GOPH
     layout with n k' > 512 (the register scan holds every group)."""
     r, p = tiny_run, tiny_run["p"]
     prm = og.params(p["t_num"], p["t_den"], p["eps"], variant=og.OPH_VARIANT_EMPTY_AWARE)
@@ -224,7 +224,7 @@ def test_goph_empty_aware_invalid(tiny_run):
     with pytest.raises(RuntimeError):
         og.compare_full(r["qo"], r["so"], lay, prm, og.Results(1 << 16))
     with pytest.raises(RuntimeError):
-        og.compare_hoph(r["qh"], r["sh"], r["hier"], prm, og.Results(1 << 16))
+        og.compare_minwise(r["qmw"], r["mw"], prm, og.Results(1 << 16))
     w = text_like(seed=3, n_sets=300, n_queries=10)
     big = og.flat_layout(w.vocab_size, 1024, 32)
     _, so, _ = gpu_build(w.offsets, w.ids, w.vocab_size, 1, k=1024, kprime=32)
@@ -919,3 +919,49 @@ def test_validate_sets(monkeypatch):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
                        cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
     assert r.stdout.strip() == f"refused {og.OPH_EINVAL}", r.stdout + r.stderr
+
+
+# ----------------------------------------------------------------------------- empty-aware HOPH (EH1-EH5)
+@pytest.mark.parametrize("joint", [False, True])
+def test_tiny_hoph_empty_aware(tiny_run, joint):
+    """The empty-aware HOPH rule (OPH_VARIANT_EMPTY_AWARE on compare_hoph): dense records (every
+    pair walked), termination histogram, and threshold lists through the join (pairs with a
+    matched bin) and through the all-pairs walk (BRUTE) == the oracle's (O10e)."""
+    r, o, p = tiny_run, tiny_run["orc"], tiny_run["p"]
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"], joint=joint)
+    want = oracle_records("hoph_e", o["QH"], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw)
+    g = gpu_dense("hoph_e", r["qh"], r["sh"], layout=r["hier"], **kw)
+    assert_records_equal(g, want, f"tiny hoph_e joint={joint}")
+    res = og.Results(1 << 20, stop_hist=True)
+    og.compare_hoph(r["qh"], r["sh"], r["hier"], og.params(p["t_num"], p["t_den"], p["eps"], joint,
+                                                           variant=og.OPH_VARIANT_EMPTY_AWARE), res)
+    assert (res.hist().astype(np.int64) == np.bincount(want["groups"].ravel(), minlength=og.OPH_STOP_HIST_LEN)).all()
+    for st in (og.OPH_STRATEGY_AUTO, og.OPH_STRATEGY_PROBE, og.OPH_STRATEGY_BRUTE):
+        hits = gpu_threshold_hits("hoph_e", r["qh"], r["sh"], layout=r["hier"], strategy=st, **kw)
+        assert [(int(h["query"]), int(h["set_id"])) for h in hits] == oracle.threshold_list(want), st
+    # the variant differs from Algorithm 2 on these sparse sketches (it is not a no-op)
+    paper = oracle_records("hoph", o["QH"], o["H"], kprime=p["hoph_kprime"], L=o["L"], **kw)
+    assert (paper["groups"] != want["groups"]).any()
+
+
+@pytest.mark.parametrize("V,hkp,seed", [(1000003, 8, 3), (4097, 32, 4), (1 << 20, 32, 5), (1 << 32, 32, 7)])
+def test_hoph_empty_aware_ragged(V, hkp, seed):
+    """Empty-aware HOPH dense records on ragged collections (empty sets / queries, non-power-of-
+    two universes, 2^32), both empty modes."""
+    rng = np.random.default_rng(seed + 100)
+    sets = [rng.choice(V, size=int(s), replace=False) if s else [] for s in rng.integers(0, 60, size=300)]
+    qsets = [sets[i] if i % 3 == 0 else rng.choice(V, size=int(rng.integers(0, 60)), replace=False)
+             for i in range(37)]
+    qsets[1] = []
+    offs, ids = make_csr(sets)
+    qoffs, qids = make_csr(qsets)
+    hier = og.oph_hier_layout_make(V, 1, 1, hkp)
+    _, _, sh = gpu_build(offs, ids, V, seed, hier=hier)
+    _, _, qh = gpu_build(qoffs, qids, V, seed, hier=hier)
+    glay = oracle.hoph_layout(V, 1, 1, hkp)
+    H = oracle.hoph_sketch(offs, ids, V, glay, hkp, seed)
+    QH = oracle.hoph_sketch(qoffs, qids, V, glay, hkp, seed)
+    for joint in (False, True):
+        kw = dict(t_num=7, t_den=10, eps=1e-4, joint=joint)
+        assert_records_equal(gpu_dense("hoph_e", qh, sh, layout=hier, **kw),
+                             oracle_records("hoph_e", QH, H, kprime=hkp, L=len(glay), **kw), f"hoph_e {V}")
