@@ -341,23 +341,32 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
             const bool last = l == (MODE == 1 ? a.nlev : nlev_scan);
             uint32_t acc = 0u, dec = 0u;
             if (MODE == 1) {
-                // T_l = 2 T_(l-1) + M_l (bit-sliced shift, then ripple add of the 6-bit M_l)
+                if (l == 1) {
+                    // T_1 = M_1: the group count's 6 slices (most pairs decide here)
 #pragma unroll
-                for (int i = (int)kBitTS - 1; i >= 1; i--) T[i] = T[i - 1];
-                T[0] = 0u;
-                uint32_t carry = 0u;
+                    for (int i = 0; i < 6; i++) T[i] = c[i];
+                } else {
+                    // T_l = 2 T_(l-1) + M_l (bit-sliced shift, then ripple add of the 6-bit M_l)
 #pragma unroll
-                for (int i = 0; i < (int)kBitTS; i++) {
-                    const uint32_t m = i < 6 ? c[i] : 0u;  // M_l <= 32: slices 1 .. 32
-                    const uint32_t t = T[i];
-                    T[i] = t ^ m ^ carry;
-                    carry = (t & m) | ((t ^ m) & carry);
+                    for (int i = (int)kBitTS - 1; i >= 1; i--) T[i] = T[i - 1];
+                    T[0] = 0u;
+                    uint32_t carry = 0u;
+#pragma unroll
+                    for (int i = 0; i < (int)kBitTS; i++) {
+                        const uint32_t m = i < 6 ? c[i] : 0u;  // M_l <= 32: slices 1 .. 32
+                        const uint32_t t = T[i];
+                        T[i] = t ^ m ^ carry;
+                        carry = (t & m) | ((t ^ m) & carry);
+                    }
                 }
             }
             if (!last && a.thr_on[l - 1]) {
                 const uint32_t A = a.acc_cnt[l - 1];
                 const int32_t R = a.rej_cnt[l - 1];
-                if (MODE == 1) {
+                if (MODE == 1 && l == 1) {  // T_1 < 2^6
+                    acc = sliced_ge<6>(T, A);
+                    dec = acc | (R >= 0 ? ~sliced_ge<6>(T, (uint32_t)R + 1u) : 0u);
+                } else if (MODE == 1) {
                     acc = sliced_ge<kBitTS>(T, A);
                     dec = acc | (R >= 0 ? ~sliced_ge<kBitTS>(T, (uint32_t)R + 1u) : 0u);
                 } else {

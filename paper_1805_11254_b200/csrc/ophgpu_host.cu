@@ -468,9 +468,9 @@ oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketche
     ba.nw = nw;
     ba.nscan = nb;
     // bins staged per CTA tile: all (full OPH); the levels most pairs reach (GOPH: up to the
-    // first decidable level + 1; HOPH: groups 1-2); the rest is read directly when reached
+    // first decidable level + 1; HOPH: group 1); the rest is read directly when reached
     ba.npre = method == OPH_METHOD_FULL ? nb
-                                        : std::min<uint32_t>(nb, kp * (method == OPH_METHOD_GOPH ? plan.l0 + 1 : 2));
+                                        : std::min<uint32_t>(nb, kp * (method == OPH_METHOD_GOPH ? plan.l0 + 1 : 1));
     ba.kp = kp;
     ba.nbins_total = nb;
     ba.method = method;
