@@ -27,6 +27,7 @@ constexpr uint32_t kBitMaxBins = 1023;  // bins scanned: counts fit 10 bit slice
 constexpr uint32_t kBitCS = 10;       // count slices: ones, twos, fours, eights, hi[6]
 constexpr uint32_t kBitTS = 24;       // HOPH T_l slices (L <= 20)
 constexpr int kBitWarps = 8;          // warps per CTA = consecutive sets per CTA tile
+constexpr uint32_t kBitMaxStages = 8; // staged CTA tiles in flight (ring of value buffers)
 
 // bin b -> (first position, width) of its value range
 __device__ __forceinline__ void bit_bin_range(const BitArgs &a, uint32_t b, uint32_t &start, uint32_t &width) {
@@ -204,7 +205,7 @@ __device__ void bit_hoph_final(const BitArgs &a, uint32_t qg, uint64_t s, uint32
 // tile's 32-B segment is copied with two 16-B cp.async (L1-bypassing) into
 // vbuf[buffer][bin][8]; each issuing lane then arrives on the buffer's mbarrier when its
 // copies have landed (cp.async.mbarrier.arrive.noinc; 32 arrivals per fill).  Issued by
-// the 32 lanes of the last warp to finish the tile two tiles back (a double buffer; no
+// the 32 lanes of the last warp to finish the tile nstage tiles back (a ring of buffers; no
 // CTA-wide barrier): one gather request per 16 B of the tile instead of one per set
 // value per warp, and the latency hidden behind a whole tile's scan.
 __device__ __forceinline__ void bit_tile_load(const BitArgs &a, uint64_t tile, uint32_t *dst, uint64_t *bar,
@@ -221,8 +222,8 @@ __device__ __forceinline__ void bit_tile_load(const BitArgs &a, uint64_t tile, u
 template <int MODE, int MINB>
 __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __grid_constant__ BitArgs a) {
     __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
-    __shared__ uint64_t s_full[2];
-    __shared__ uint32_t s_done[2];
+    __shared__ uint64_t s_full[kBitMaxStages];
+    __shared__ uint32_t s_done[kBitMaxStages];
     extern __shared__ __align__(128) uint32_t s_vals[];  // [2][npre][8]
     for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
         uint32_t st, wd;
@@ -243,14 +244,15 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
     const uint32_t vstride = a.npre * 8u;  // words per buffer
     if (threadIdx.x == 0) {
-        mbar_init(&s_full[0], 32);  // the 32 lanes of the filling warp
-        mbar_init(&s_full[1], 32);
-        s_done[0] = s_done[1] = 0u;
+        for (uint32_t i = 0; i < a.nstage; i++) {
+            mbar_init(&s_full[i], 32);  // the 32 lanes of the filling warp
+            s_done[i] = 0u;
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (warp == 0) {
-        for (uint32_t i = 0; i < 2; i++) {
+        for (uint32_t i = 0; i < a.nstage; i++) {
             const uint64_t t = blockIdx.x + (uint64_t)i * gridDim.x;
             if (t < ntiles) bit_tile_load(a, t, s_vals + i * vstride, &s_full[i], lane);
         }
@@ -258,11 +260,11 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
 
     uint32_t it = 0;  // this CTA's tile counter
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
-        const uint32_t bi = it & 1u;
+        const uint32_t bi = it % a.nstage;
         const uint64_t s = a.s_begin + tile * kBitWarps + warp;
         const uint32_t *v_cur = s_vals + bi * vstride + warp;  // value of bin b: v_cur[8 b]
-        mbar_wait(&s_full[bi], (it >> 1) & 1u);
-        // the tile is processed; the last warp done with this buffer refills it with tile + 2
+        mbar_wait(&s_full[bi], (it / a.nstage) & 1u);
+        // the tile is processed; the last warp done with this buffer refills it with tile + nstage
         auto release = [&]() {
             __syncwarp();
             uint32_t last = 0;
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
                 if (last) s_done[bi] = 0u;
             }
             last = __shfl_sync(0xFFFFFFFFu, last, 0);
-            const uint64_t tn = tile + 2ull * gridDim.x;
+            const uint64_t tn = tile + (uint64_t)a.nstage * gridDim.x;
             if (last && tn < ntiles) bit_tile_load(a, tn, s_vals + bi * vstride, &s_full[bi], lane);
         };
         if (s >= a.n_sets) {  // warp-uniform: a tail tile's missing set
@@ -473,7 +475,7 @@ cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     static const bool two = getenv("OPHGPU_BIT_CTAS") && atoi(getenv("OPHGPU_BIT_CTAS")) == 2;
     const int ctas = a.mode_hoph || two ? 2 : 3;
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * ctas * 8);
-    const size_t smem = (size_t)2 * a.npre * kBitWarps * 4;
+    const size_t smem = (size_t)a.nstage * a.npre * kBitWarps * 4;
     auto kern = a.mode_hoph ? bit_scan_kernel<1, 2> : (two ? bit_scan_kernel<0, 2> : bit_scan_kernel<0, 3>);
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return e;

@@ -216,6 +216,7 @@ struct BitArgs {
     const uint32_t *QEM;    // query masks, query-major [n_q][nw]
     uint32_t nb, nw, nscan, kp, nlev, nbins_total;
     uint32_t npre;          // bins [0, npre) are staged per CTA tile (the rest read directly)
+    uint32_t nstage;        // CTA tiles staged ahead (ring of value buffers, 2 .. 8)
     uint32_t qb0, nqb;      // this block: query columns [qb0, qb0 + nqb), nqb <= 1024
     uint32_t method, mode_hoph, joint, t_num, t_den, level_final;
     // value ranges of the bins: bin b = range b / bins_per_range, floor rule inside it

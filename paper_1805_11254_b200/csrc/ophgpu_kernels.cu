@@ -33,6 +33,8 @@
 
 namespace ophgpu {
 
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
 // ---------------------------------------------------------------------------
 // psi: keyed 4-round bijection of [0, 2^w), cycle-walked into [0, |V|)
 // (DESIGN.md section 4).  W32: w == 32, the mask is a no-op.
@@ -254,9 +256,24 @@ __global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ Buil
     constexpr int kU = FAST ? 8 : 4;  // ids in flight per thread
     uint32_t j = 0;
     if (FAST) {
+        // the keys and layout constants in registers (not re-read from the parameter bank per
+        // element), shared rows as 32-bit shared addresses, and the bin minima as
+        // fire-and-forget shared reductions (red.shared.min: no load, compare and branch per
+        // element; an EMPTY slot is the identity of min)
+        uint32_t kap[4], mu[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            kap[r] = a.psi.kappa[r];
+            mu[r] = a.psi.mu[r];
+        }
+        const uint32_t mask = a.psi.mask, pshift = a.psi.shift, hmul = a.psi.hmul, hsh = a.psi.hsh;
+        const uint32_t fsh = a.flat.shift, fmask = (1u << a.flat.shift) - 1u;
+        const uint32_t vsh = 32u - a.log2V, Lm1 = a.L - 1u, lkp = a.log2kp, kpw = a.kp;
+        const uint32_t osh = 32u - a.log2V + a.log2kp, bsh = 32u - a.log2kp;
         const uint32_t n = (uint32_t)(e1 - e0);
         const uint32_t *ids = a.ids + e0;
-        uint32_t *so_j = so, *sh_j = sh;
+        const uint32_t so_base = smem_addr(so), sh_base = smem_addr(sh);
+        uint32_t so_j = so_base, sh_j = sh_base;
         for (uint32_t e = threadIdx.x; e < n; e += kU * blockDim.x) {
             uint32_t id[kU];
 #pragma unroll
@@ -267,10 +284,21 @@ __global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ Buil
                 if (eu >= n) break;
                 if (loffs[j + 1] <= eu) {  // the set owning element eu (empty sets are skipped)
                     do j++; while (loffs[j + 1] <= eu);
-                    so_j = so + j * kst;
-                    sh_j = sh + j * hst;
+                    so_j = so_base + 4u * j * kst;
+                    sh_j = sh_base + 4u * j * hst;
                 }
-                build_one_fast<W32>(a, so_j, sh_j, id[u]);
+                const uint32_t p = psi_pass<W32>(kap, mu, mask, pshift, hmul, hsh, id[u]);
+                const uint32_t fo = p & fmask;
+                asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(so_j + 4u * (p >> fsh)), "r"(fo));
+                // HOPH 1:1 on 2^log2V: group g = leading ones of the left-aligned p (capped at L-1),
+                // then drop them and the 0 after them (not for the last group): bin and offset
+                const uint32_t t = p << vsh;
+                const uint32_t g = min((uint32_t)__clz(~t), Lm1);
+                const uint32_t sc = g + (g < Lm1 ? 1u : 0u);
+                const uint32_t y = t << sc;
+                const uint32_t hb = y >> bsh;
+                const uint32_t ho = __funnelshift_rc(y << lkp, 0u, osh + sc);
+                asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(sh_j + 4u * (g * kpw + hb)), "r"(ho));
             }
         }
     } else
@@ -871,7 +899,6 @@ __global__ void table_kernel(const __grid_constant__ TableArgs a) {
 }
 
 // ---- mbarrier / bulk-copy (TMA engine) primitives
-__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
 }
