@@ -258,203 +258,249 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
         }
     }
 
-    uint32_t it = 0;  // this CTA's tile counter
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
-        const uint32_t bi = it % a.nstage;
-        const uint64_t s = a.s_begin + tile * kBitWarps + warp;
-        const uint32_t *v_cur = s_vals + bi * vstride + warp;  // value of bin b: v_cur[8 b]
-        mbar_wait(&s_full[bi], (it / a.nstage) & 1u);
-        // the tile is processed; the last warp done with this buffer refills it with tile + nstage
-        auto release = [&]() {
+    const uint32_t nbt = (a.nscan + 15u) / 16u;       // batches of 16 bins of a whole set
+    const uint32_t nbs = (a.npre + 15u) / 16u;        // ... of its staged prefix
+    const uint32_t bpl = bins_per_level / 16u;        // batches per level (GOPH / HOPH)
+    // this CTA's tiles: blockIdx.x + i gridDim.x, i < n_it; every warp walks all of them
+    const uint64_t n_it = (uint64_t)blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint64_t nitems = n_it * nbs;
+    auto set_of = [&](uint64_t ti) -> uint64_t {
+        return a.s_begin + ((uint64_t)blockIdx.x + ti * gridDim.x) * kBitWarps + warp;
+    };
+
+    // ---- stage A: the row indices of the next item (tile ti, staged batch bj): lanes 0-15 take
+    // the set's values of bins 16 bj + lane from the staged tile and look them up in idx.  After
+    // its last batch the tile's buffer is released; the last warp to release refills it with
+    // the tile nstage iterations later.
+    uint64_t tiA = 0;
+    uint32_t bjA = 0, slotA = 0, phaseA = 0;
+    auto stageA = [&]() -> uint32_t {
+        uint32_t r = 0u;
+        if (tiA >= n_it) return r;
+        if (bjA == 0) mbar_wait(&s_full[slotA], phaseA);
+        const uint32_t b = 16u * bjA + lane;
+        if (lane < 16u && b < a.npre) {
+            const uint32_t v = s_vals[slotA * vstride + 8u * b + warp];
+            if (v < s_width[b]) r = __ldg(a.idx + s_start[b] + v);
+        }
+        if (++bjA == nbs) {
             __syncwarp();
             uint32_t last = 0;
             if (lane == 0) {
                 __threadfence_block();
-                last = atomicAdd(&s_done[bi], 1u) == kBitWarps - 1;
-                if (last) s_done[bi] = 0u;
+                last = atomicAdd(&s_done[slotA], 1u) == kBitWarps - 1;
+                if (last) s_done[slotA] = 0u;
             }
             last = __shfl_sync(0xFFFFFFFFu, last, 0);
-            const uint64_t tn = tile + (uint64_t)a.nstage * gridDim.x;
-            if (last && tn < ntiles) bit_tile_load(a, tn, s_vals + bi * vstride, &s_full[bi], lane);
-        };
-        if (s >= a.n_sets) {  // warp-uniform: a tail tile's missing set
-            release();
-            continue;
+            const uint64_t tn = (uint64_t)blockIdx.x + (tiA + a.nstage) * gridDim.x;
+            if (last && tn < ntiles) bit_tile_load(a, tn, s_vals + slotA * vstride, &s_full[slotA], lane);
+            bjA = 0;
+            tiA++;
+            if (++slotA == a.nstage) {
+                slotA = 0;
+                phaseA ^= 1u;
+            }
         }
-        uint32_t c[kBitCS];
+        return r;
+    };
+    auto rload = [&](uint32_t r, uint32_t (&x)[16]) {
 #pragma unroll
-        for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;
-        uint32_t T[MODE == 1 ? kBitTS : 1];
-#pragma unroll
-        for (int i = 0; i < (MODE == 1 ? (int)kBitTS : 1); i++) T[i] = 0u;
-        uint32_t alive = qvalid;
+        for (int u = 0; u < 16; u++) {
+            const uint32_t ru = __shfl_sync(0xFFFFFFFFu, r, u);
+            x[u] = __ldg(rows_lane + (uint64_t)ru * 32);  // ru = 0 (no row, or past the scan): zero row
+        }
+    };
 
-        // The bins are scanned in batches of 16 (GOPH / HOPH levels are whole batches: k' is
-        // a multiple of 16; full OPH's last batch may be partial).  Per batch: lanes 0-15
-        // take the set's value of bins b0 + lane (shared memory) and look up its row (r);
-        // rows are then broadcast by shuffle and every lane loads its word (x).  Software
-        // pipeline: the row words of batch g+1 and the row indices of g+2 and g+3 are in
-        // flight while batch g is counted.
-        const uint32_t nbt = (a.nscan + 15u) / 16u;
-        const uint32_t bpl = bins_per_level / 16u;  // batches per level (full OPH: unused)
-        auto ilook = [&](uint32_t g) -> uint32_t {
-            const uint32_t b = 16u * g + lane;
+    // ---- stage C state: the set being counted
+    uint64_t tiC = 0, s = 0;
+    uint32_t bjC = 0, l = 1, jj = 0;
+    bool done = true;
+    uint32_t c[kBitCS];
+    uint32_t T[MODE == 1 ? kBitTS : 1];
+    uint32_t alive = 0u;
+
+    // decisions at the end of level l; returns true when the set is done
+    auto level_end = [&]() -> bool {
+        const bool last = l == (MODE == 1 ? a.nlev : nlev_scan);
+        uint32_t acc = 0u, dec = 0u;
+        if (MODE == 1) {
+            if (l == 1) {
+                // T_1 = M_1: the group count's 6 slices (most pairs decide here)
+#pragma unroll
+                for (int i = 0; i < 6; i++) T[i] = c[i];
+            } else {
+                // T_l = 2 T_(l-1) + M_l (bit-sliced shift, then ripple add of the 6-bit M_l)
+#pragma unroll
+                for (int i = (int)kBitTS - 1; i >= 1; i--) T[i] = T[i - 1];
+                T[0] = 0u;
+                uint32_t carry = 0u;
+#pragma unroll
+                for (int i = 0; i < (int)kBitTS; i++) {
+                    const uint32_t m = i < 6 ? c[i] : 0u;  // M_l <= 32: slices 1 .. 32
+                    const uint32_t t = T[i];
+                    T[i] = t ^ m ^ carry;
+                    carry = (t & m) | ((t ^ m) & carry);
+                }
+            }
+        }
+        if (!last && a.thr_on[l - 1]) {
+            const uint32_t A = a.acc_cnt[l - 1];
+            const int32_t R = a.rej_cnt[l - 1];
+            if (MODE == 1 && l == 1) {  // T_1 < 2^6
+                acc = sliced_ge<6>(T, A);
+                dec = acc | (R >= 0 ? ~sliced_ge<6>(T, (uint32_t)R + 1u) : 0u);
+            } else if (MODE == 1) {
+                acc = sliced_ge<kBitTS>(T, A);
+                dec = acc | (R >= 0 ? ~sliced_ge<kBitTS>(T, (uint32_t)R + 1u) : 0u);
+            } else {
+                acc = sliced_ge<kBitCS>(c, A);
+                dec = acc | (R >= 0 ? ~sliced_ge<kBitCS>(c, (uint32_t)R + 1u) : 0u);
+            }
+            acc &= alive;
+            dec &= alive;
+            hist_add(a.out.hist, l, __popc(dec));
+            uint32_t want = a.out.dense ? dec : acc;
+            while (__any_sync(0xFFFFFFFFu, want != 0u)) {
+                const bool has = want != 0u;
+                const uint32_t j = has ? __ffs(want) - 1 : 0u;
+                want &= want - 1u;
+                const uint32_t qg = a.qb0 + qw0 + j;
+                uint32_t nmb = 0, ex = 0;
+                if (has) {
+                    if (MODE == 1) {
+                        for (uint32_t gg = 0; gg < l; gg++) nmb += bit_group_matches(a, qg, s, gg);
+                    } else {
+                        nmb = sliced_get<kBitCS>(c, j);
+                    }
+                    ex = bit_excl(a, qg, s, 0, l * a.kp);
+                }
+                emit(a.out, has, qg, s, nmb, ex, l, (acc >> j) & 1u, OPH_FLAG_EARLY, -1.0f);
+            }
+            alive &= ~dec;
+        }
+        if (!last) return !__any_sync(0xFFFFFFFFu, alive != 0u);  // every pair of this set decided?
+        // ---- the final verdict of every pair still alive
+        hist_add(a.out.hist, MODE == 1 ? a.nlev : a.level_final, __popc(alive));
+        if (MODE == 1) {
+            uint32_t want = alive;
+            while (__any_sync(0xFFFFFFFFu, want != 0u)) {
+                const bool has = want != 0u;
+                const uint32_t j = has ? __ffs(want) - 1 : 0u;
+                want &= want - 1u;
+                const uint32_t qg = a.qb0 + qw0 + j;
+                uint32_t nmb = 0, ex = 0, verdict = 0, flags = 0;
+                float est = -1.0f;
+                if (has) bit_hoph_final(a, qg, s, nmb, ex, verdict, flags, est);
+                emit(a.out, has, qg, s, nmb, ex, a.nlev, verdict, flags, est);
+            }
+        } else {
+            // full-OPH verdict (Eq. 6): den = k - N_excl >= k - (max_q |Eq| + |Es|) (EitherEmpty)
+            // or k - min(max_q |Eq|, |Es|) (JointEmpty), so a pair can only be Similar if
+            // N_mb >= ceil(t_num den_min / t_den): the candidates, verified exactly
+            const uint32_t es_w = lane < a.nw ? __ldg(a.E + (uint64_t)lane * a.ld + s) : 0u;
+            const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, a.nbins_total));
+            const uint32_t k = a.nbins_total;
+            uint32_t den_min = a.joint ? k - min(max_eq, es) : k - min(k, max_eq + es);
+            const uint32_t theta =
+                a.out.dense ? 0u : (uint32_t)(((uint64_t)a.t_num * den_min + a.t_den - 1) / a.t_den);
+            uint32_t want = sliced_ge<kBitCS>(c, theta) & alive;
+            while (__any_sync(0xFFFFFFFFu, want != 0u)) {
+                const bool has = want != 0u;
+                const uint32_t j = has ? __ffs(want) - 1 : 0u;
+                want &= want - 1u;
+                const uint32_t qg = a.qb0 + qw0 + j;
+                uint32_t ex = 0;
+                for (uint32_t w = 0; w < a.nw; w++) {
+                    const uint32_t sw = __shfl_sync(0xFFFFFFFFu, es_w, w);
+                    if (has) ex += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + w), sw, a.joint, w, k);
+                }
+                const uint32_t nmb = sliced_get<kBitCS>(c, j);
+                const uint32_t den = k - ex;
+                const bool undef = den == 0;
+                const uint32_t verdict = !undef && (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
+                emit(a.out, has, qg, s, nmb, ex, a.level_final, verdict, undef ? OPH_FLAG_UNDEFINED : 0u,
+                     undef ? -1.0f : (float)nmb / (float)den);
+            }
+        }
+        alive = 0u;
+        return true;
+    };
+    // one counted batch of the current set (MODE 1 resets the group count at a level start)
+    auto count_batch = [&](const uint32_t (&xc)[16]) {
+        if (MODE == 1 && jj == 0) {
+#pragma unroll
+            for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;  // M_l: this group's count
+        }
+        csa16(c, xc);
+        const bool lend = bins_per_level == a.nscan ? false : jj + 1 == bpl;
+        if (!lend) {
+            jj++;
+            return;
+        }
+        if (level_end()) {
+            done = true;
+            return;
+        }
+        l++;
+        jj = 0;
+    };
+    // past the staged prefix (GOPH / HOPH levels most sets never reach): the rest of the set,
+    // batch by batch with direct loads of its values, no pipeline
+    auto finish_set = [&]() {
+        for (uint32_t g = nbs; g < nbt && !done; g++) {
             uint32_t r = 0u;
+            const uint32_t b = 16u * g + lane;
             if (lane < 16u && b < a.nscan) {
-                // bins past the staged prefix (GOPH / HOPH levels most sets never reach): direct
-                const uint32_t v = b < a.npre ? v_cur[8 * b] : __ldg(a.F + (uint64_t)b * a.ld + s);
+                const uint32_t v = __ldg(a.F + (uint64_t)b * a.ld + s);
                 if (v < s_width[b]) r = __ldg(a.idx + s_start[b] + v);
             }
-            return r;
-        };
-        auto rload = [&](uint32_t r, uint32_t (&x)[16]) {
+            uint32_t xs[16];
+            rload(r, xs);
+            count_batch(xs);
+        }
+    };
+    // ---- stage C: count item (tiC, bjC)
+    auto stageC = [&](const uint32_t (&xc)[16]) {
+        if (bjC == 0) {  // a new set
+            s = set_of(tiC);
+            done = s >= a.n_sets;
+            alive = done ? 0u : qvalid;
+            l = 1;
+            jj = 0;
 #pragma unroll
-            for (int u = 0; u < 16; u++) {
-                const uint32_t ru = __shfl_sync(0xFFFFFFFFu, r, u);
-                x[u] = __ldg(rows_lane + (uint64_t)ru * 32);  // ru = 0 (no row, or past the scan): zero row
-            }
-        };
-        uint32_t x[16], rA, rB;
+            for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;
+#pragma unroll
+            for (int i = 0; i < (MODE == 1 ? (int)kBitTS : 1); i++) T[i] = 0u;
+        }
+        if (!done) count_batch(xc);
+        if (++bjC == nbs) {  // the staged prefix is counted
+            if (!done && nbs == nbt && bins_per_level == a.nscan) done = level_end();  // full OPH
+            if (!done) finish_set();
+            bjC = 0;
+            tiC++;
+        }
+    };
+
+    // ---- the pipeline over this warp's items: rows of item g+1 and the row indices of items
+    // g+2, g+3 are in flight while item g is counted; the two row buffers alternate
+    if (nitems) {
+        uint32_t x[16], xb[16], rA, rB;
         {
-            const uint32_t r0 = ilook(0);
-            rA = ilook(1);
-            rB = ilook(2);
+            const uint32_t r0 = stageA();
+            rA = stageA();
+            rB = stageA();
             rload(r0, x);
         }
-        uint32_t l = 1, jj = 0;  // level of batch g, batch index inside the level
-        // one batch: count xc (batch g) while xn (g + 1), r1 (g + 2), v3 (g + 3) load; the two
-        // row buffers alternate (a copy between them would wait for the loads in flight)
-        // returns true when the set is done
-        auto step = [&](uint32_t g, uint32_t (&xc)[16], uint32_t (&xn)[16]) -> bool {
-            rload(rA, xn);               // past the scan: rA = 0, the zero row
+        auto step = [&](uint64_t g, uint32_t (&xc)[16], uint32_t (&xn)[16]) {
+            if (g + 1 < nitems) rload(rA, xn);
             rA = rB;
-            rB = ilook(g + 3);
-            if (MODE == 1 && jj == 0) {
-#pragma unroll
-                for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;  // M_l: this group's count
-            }
-            csa16(c, xc);
-            const bool level_end = bins_per_level == a.nscan ? g + 1 == nbt : jj + 1 == bpl;
-            if (!level_end) {
-                jj++;
-                return false;
-            }
-            // ---- decisions at the end of level l
-            const bool last = l == (MODE == 1 ? a.nlev : nlev_scan);
-            uint32_t acc = 0u, dec = 0u;
-            if (MODE == 1) {
-                if (l == 1) {
-                    // T_1 = M_1: the group count's 6 slices (most pairs decide here)
-#pragma unroll
-                    for (int i = 0; i < 6; i++) T[i] = c[i];
-                } else {
-                    // T_l = 2 T_(l-1) + M_l (bit-sliced shift, then ripple add of the 6-bit M_l)
-#pragma unroll
-                    for (int i = (int)kBitTS - 1; i >= 1; i--) T[i] = T[i - 1];
-                    T[0] = 0u;
-                    uint32_t carry = 0u;
-#pragma unroll
-                    for (int i = 0; i < (int)kBitTS; i++) {
-                        const uint32_t m = i < 6 ? c[i] : 0u;  // M_l <= 32: slices 1 .. 32
-                        const uint32_t t = T[i];
-                        T[i] = t ^ m ^ carry;
-                        carry = (t & m) | ((t ^ m) & carry);
-                    }
-                }
-            }
-            if (!last && a.thr_on[l - 1]) {
-                const uint32_t A = a.acc_cnt[l - 1];
-                const int32_t R = a.rej_cnt[l - 1];
-                if (MODE == 1 && l == 1) {  // T_1 < 2^6
-                    acc = sliced_ge<6>(T, A);
-                    dec = acc | (R >= 0 ? ~sliced_ge<6>(T, (uint32_t)R + 1u) : 0u);
-                } else if (MODE == 1) {
-                    acc = sliced_ge<kBitTS>(T, A);
-                    dec = acc | (R >= 0 ? ~sliced_ge<kBitTS>(T, (uint32_t)R + 1u) : 0u);
-                } else {
-                    acc = sliced_ge<kBitCS>(c, A);
-                    dec = acc | (R >= 0 ? ~sliced_ge<kBitCS>(c, (uint32_t)R + 1u) : 0u);
-                }
-                acc &= alive;
-                dec &= alive;
-                hist_add(a.out.hist, l, __popc(dec));
-                uint32_t want = a.out.dense ? dec : acc;
-                while (__any_sync(0xFFFFFFFFu, want != 0u)) {
-                    const bool has = want != 0u;
-                    const uint32_t j = has ? __ffs(want) - 1 : 0u;
-                    want &= want - 1u;
-                    const uint32_t qg = a.qb0 + qw0 + j;
-                    uint32_t nmb = 0, ex = 0;
-                    if (has) {
-                        if (MODE == 1) {
-                            for (uint32_t gg = 0; gg < l; gg++) nmb += bit_group_matches(a, qg, s, gg);
-                        } else {
-                            nmb = sliced_get<kBitCS>(c, j);
-                        }
-                        ex = bit_excl(a, qg, s, 0, l * a.kp);
-                    }
-                    emit(a.out, has, qg, s, nmb, ex, l, (acc >> j) & 1u, OPH_FLAG_EARLY, -1.0f);
-                }
-                alive &= ~dec;
-            }
-            if (!last) {
-                if (!__any_sync(0xFFFFFFFFu, alive != 0u)) return true;  // every pair of this set is decided
-                l++;
-                jj = 0;
-                return false;
-            }
-            // ---- the final verdict of every pair still alive
-            hist_add(a.out.hist, MODE == 1 ? a.nlev : a.level_final, __popc(alive));
-            if (MODE == 1) {
-                uint32_t want = alive;
-                while (__any_sync(0xFFFFFFFFu, want != 0u)) {
-                    const bool has = want != 0u;
-                    const uint32_t j = has ? __ffs(want) - 1 : 0u;
-                    want &= want - 1u;
-                    const uint32_t qg = a.qb0 + qw0 + j;
-                    uint32_t nmb = 0, ex = 0, verdict = 0, flags = 0;
-                    float est = -1.0f;
-                    if (has) bit_hoph_final(a, qg, s, nmb, ex, verdict, flags, est);
-                    emit(a.out, has, qg, s, nmb, ex, a.nlev, verdict, flags, est);
-                }
-            } else {
-                // full-OPH verdict (Eq. 6): den = k - N_excl >= k - (max_q |Eq| + |Es|) (EitherEmpty)
-                // or k - min(max_q |Eq|, |Es|) (JointEmpty), so a pair can only be Similar if
-                // N_mb >= ceil(t_num den_min / t_den): the candidates, verified exactly
-                const uint32_t es_w = lane < a.nw ? __ldg(a.E + (uint64_t)lane * a.ld + s) : 0u;
-                const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, a.nbins_total));
-                const uint32_t k = a.nbins_total;
-                uint32_t den_min = a.joint ? k - min(max_eq, es) : k - min(k, max_eq + es);
-                const uint32_t theta =
-                    a.out.dense ? 0u : (uint32_t)(((uint64_t)a.t_num * den_min + a.t_den - 1) / a.t_den);
-                uint32_t want = sliced_ge<kBitCS>(c, theta) & alive;
-                while (__any_sync(0xFFFFFFFFu, want != 0u)) {
-                    const bool has = want != 0u;
-                    const uint32_t j = has ? __ffs(want) - 1 : 0u;
-                    want &= want - 1u;
-                    const uint32_t qg = a.qb0 + qw0 + j;
-                    uint32_t ex = 0;
-                    for (uint32_t w = 0; w < a.nw; w++) {
-                        const uint32_t sw = __shfl_sync(0xFFFFFFFFu, es_w, w);
-                        if (has) ex += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + w), sw, a.joint, w, k);
-                    }
-                    const uint32_t nmb = sliced_get<kBitCS>(c, j);
-                    const uint32_t den = k - ex;
-                    const bool undef = den == 0;
-                    const uint32_t verdict = !undef && (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
-                    emit(a.out, has, qg, s, nmb, ex, a.level_final, verdict, undef ? OPH_FLAG_UNDEFINED : 0u,
-                         undef ? -1.0f : (float)nmb / (float)den);
-                }
-            }
-            alive = 0u;
-            return true;
+            rB = stageA();
+            stageC(xc);
         };
-        uint32_t xb[16];
-        for (uint32_t g = 0; g < nbt; g += 2) {
-            if (step(g, x, xb)) break;
-            if (g + 1 < nbt && step(g + 1, xb, x)) break;
+        for (uint64_t g = 0; g < nitems; g += 2) {
+            step(g, x, xb);
+            if (g + 1 < nitems) step(g + 1, xb, x);
         }
-        release();
     }
 }
 
