@@ -219,8 +219,253 @@ __device__ __forceinline__ void bit_tile_load(const BitArgs &a, uint64_t tile, u
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
+// Per-set software pipeline (full OPH, GOPH).
 template <int MODE, int MINB>
 __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __grid_constant__ BitArgs a) {
+    __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
+    __shared__ uint64_t s_full[kBitMaxStages];
+    __shared__ uint32_t s_done[kBitMaxStages];
+    extern __shared__ __align__(128) uint32_t s_vals[];  // [2][npre][8]
+    for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
+        uint32_t st, wd;
+        bit_bin_range(a, b, st, wd);
+        s_start[b] = st;
+        s_width[b] = wd;
+    }
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    // this lane's word of the block: queries qb0 + 32 lane + j
+    const uint32_t qw0 = 32u * lane;
+    const uint32_t qvalid = qw0 >= a.nqb ? 0u : (a.nqb - qw0 >= 32u ? 0xFFFFFFFFu : ((1u << (a.nqb - qw0)) - 1u));
+    const uint32_t max_eq = a.max_eq[lane];
+    const uint32_t *rows_lane = a.rows + lane;
+    const uint32_t nlev_scan = MODE == 1 ? a.nlev : (a.method == kGoph ? a.nlev : 1u);
+    const uint32_t bins_per_level = MODE == 1 || a.method == kGoph ? a.kp : a.nscan;
+    // (a.n_sets - s_begin and ld are multiples of 8 sets / 32 B: the tiles' 32-B copies are
+    // aligned and in bounds; sets past n_sets are never scored)
+    const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
+    const uint32_t vstride = a.npre * 8u;  // words per buffer
+    if (threadIdx.x == 0) {
+        for (uint32_t i = 0; i < a.nstage; i++) {
+            mbar_init(&s_full[i], 32);  // the 32 lanes of the filling warp
+            s_done[i] = 0u;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) {
+        for (uint32_t i = 0; i < a.nstage; i++) {
+            const uint64_t t = blockIdx.x + (uint64_t)i * gridDim.x;
+            if (t < ntiles) bit_tile_load(a, t, s_vals + i * vstride, &s_full[i], lane);
+        }
+    }
+
+    uint32_t it = 0;  // this CTA's tile counter
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+        const uint32_t bi = it % a.nstage;
+        const uint64_t s = a.s_begin + tile * kBitWarps + warp;
+        const uint32_t *v_cur = s_vals + bi * vstride + warp;  // value of bin b: v_cur[8 b]
+        mbar_wait(&s_full[bi], (it / a.nstage) & 1u);
+        // the tile is processed; the last warp done with this buffer refills it with tile + nstage
+        auto release = [&]() {
+            __syncwarp();
+            uint32_t last = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                last = atomicAdd(&s_done[bi], 1u) == kBitWarps - 1;
+                if (last) s_done[bi] = 0u;
+            }
+            last = __shfl_sync(0xFFFFFFFFu, last, 0);
+            const uint64_t tn = tile + (uint64_t)a.nstage * gridDim.x;
+            if (last && tn < ntiles) bit_tile_load(a, tn, s_vals + bi * vstride, &s_full[bi], lane);
+        };
+        if (s >= a.n_sets) {  // warp-uniform: a tail tile's missing set
+            release();
+            continue;
+        }
+        uint32_t c[kBitCS];
+#pragma unroll
+        for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;
+        uint32_t T[MODE == 1 ? kBitTS : 1];
+#pragma unroll
+        for (int i = 0; i < (MODE == 1 ? (int)kBitTS : 1); i++) T[i] = 0u;
+        uint32_t alive = qvalid;
+
+        // The bins are scanned in batches of 16 (GOPH / HOPH levels are whole batches: k' is
+        // a multiple of 16; full OPH's last batch may be partial).  Per batch: lanes 0-15
+        // take the set's value of bins b0 + lane (shared memory) and look up its row (r);
+        // rows are then broadcast by shuffle and every lane loads its word (x).  Software
+        // pipeline: the row words of batch g+1 and the row indices of g+2 and g+3 are in
+        // flight while batch g is counted.
+        const uint32_t nbt = (a.nscan + 15u) / 16u;
+        const uint32_t bpl = bins_per_level / 16u;  // batches per level (full OPH: unused)
+        auto ilook = [&](uint32_t g) -> uint32_t {
+            const uint32_t b = 16u * g + lane;
+            uint32_t r = 0u;
+            if (lane < 16u && b < a.nscan) {
+                // bins past the staged prefix (GOPH / HOPH levels most sets never reach): direct
+                const uint32_t v = b < a.npre ? v_cur[8 * b] : __ldg(a.F + (uint64_t)b * a.ld + s);
+                if (v < s_width[b]) r = __ldg(a.idx + s_start[b] + v);
+            }
+            return r;
+        };
+        auto rload = [&](uint32_t r, uint32_t (&x)[16]) {
+#pragma unroll
+            for (int u = 0; u < 16; u++) {
+                const uint32_t ru = __shfl_sync(0xFFFFFFFFu, r, u);
+                x[u] = __ldg(rows_lane + (uint64_t)ru * 32);  // ru = 0 (no row, or past the scan): zero row
+            }
+        };
+        uint32_t x[16], rA, rB;
+        {
+            const uint32_t r0 = ilook(0);
+            rA = ilook(1);
+            rB = ilook(2);
+            rload(r0, x);
+        }
+        uint32_t l = 1, jj = 0;  // level of batch g, batch index inside the level
+        // one batch: count xc (batch g) while xn (g + 1), r1 (g + 2), v3 (g + 3) load; the two
+        // row buffers alternate (a copy between them would wait for the loads in flight)
+        // returns true when the set is done
+        auto step = [&](uint32_t g, uint32_t (&xc)[16], uint32_t (&xn)[16]) -> bool {
+            rload(rA, xn);               // past the scan: rA = 0, the zero row
+            rA = rB;
+            rB = ilook(g + 3);
+            if (MODE == 1 && jj == 0) {
+#pragma unroll
+                for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;  // M_l: this group's count
+            }
+            csa16(c, xc);
+            const bool level_end = bins_per_level == a.nscan ? g + 1 == nbt : jj + 1 == bpl;
+            if (!level_end) {
+                jj++;
+                return false;
+            }
+            // ---- decisions at the end of level l
+            const bool last = l == (MODE == 1 ? a.nlev : nlev_scan);
+            uint32_t acc = 0u, dec = 0u;
+            if (MODE == 1) {
+                if (l == 1) {
+                    // T_1 = M_1: the group count's 6 slices (most pairs decide here)
+#pragma unroll
+                    for (int i = 0; i < 6; i++) T[i] = c[i];
+                } else {
+                    // T_l = 2 T_(l-1) + M_l (bit-sliced shift, then ripple add of the 6-bit M_l)
+#pragma unroll
+                    for (int i = (int)kBitTS - 1; i >= 1; i--) T[i] = T[i - 1];
+                    T[0] = 0u;
+                    uint32_t carry = 0u;
+#pragma unroll
+                    for (int i = 0; i < (int)kBitTS; i++) {
+                        const uint32_t m = i < 6 ? c[i] : 0u;  // M_l <= 32: slices 1 .. 32
+                        const uint32_t t = T[i];
+                        T[i] = t ^ m ^ carry;
+                        carry = (t & m) | ((t ^ m) & carry);
+                    }
+                }
+            }
+            if (!last && a.thr_on[l - 1]) {
+                const uint32_t A = a.acc_cnt[l - 1];
+                const int32_t R = a.rej_cnt[l - 1];
+                if (MODE == 1 && l == 1) {  // T_1 < 2^6
+                    acc = sliced_ge<6>(T, A);
+                    dec = acc | (R >= 0 ? ~sliced_ge<6>(T, (uint32_t)R + 1u) : 0u);
+                } else if (MODE == 1) {
+                    acc = sliced_ge<kBitTS>(T, A);
+                    dec = acc | (R >= 0 ? ~sliced_ge<kBitTS>(T, (uint32_t)R + 1u) : 0u);
+                } else {
+                    acc = sliced_ge<kBitCS>(c, A);
+                    dec = acc | (R >= 0 ? ~sliced_ge<kBitCS>(c, (uint32_t)R + 1u) : 0u);
+                }
+                acc &= alive;
+                dec &= alive;
+                hist_add(a.out.hist, l, __popc(dec));
+                uint32_t want = a.out.dense ? dec : acc;
+                while (__any_sync(0xFFFFFFFFu, want != 0u)) {
+                    const bool has = want != 0u;
+                    const uint32_t j = has ? __ffs(want) - 1 : 0u;
+                    want &= want - 1u;
+                    const uint32_t qg = a.qb0 + qw0 + j;
+                    uint32_t nmb = 0, ex = 0;
+                    if (has) {
+                        if (MODE == 1) {
+                            for (uint32_t gg = 0; gg < l; gg++) nmb += bit_group_matches(a, qg, s, gg);
+                        } else {
+                            nmb = sliced_get<kBitCS>(c, j);
+                        }
+                        ex = bit_excl(a, qg, s, 0, l * a.kp);
+                    }
+                    emit(a.out, has, qg, s, nmb, ex, l, (acc >> j) & 1u, OPH_FLAG_EARLY, -1.0f);
+                }
+                alive &= ~dec;
+            }
+            if (!last) {
+                if (!__any_sync(0xFFFFFFFFu, alive != 0u)) return true;  // every pair of this set is decided
+                l++;
+                jj = 0;
+                return false;
+            }
+            // ---- the final verdict of every pair still alive
+            hist_add(a.out.hist, MODE == 1 ? a.nlev : a.level_final, __popc(alive));
+            if (MODE == 1) {
+                uint32_t want = alive;
+                while (__any_sync(0xFFFFFFFFu, want != 0u)) {
+                    const bool has = want != 0u;
+                    const uint32_t j = has ? __ffs(want) - 1 : 0u;
+                    want &= want - 1u;
+                    const uint32_t qg = a.qb0 + qw0 + j;
+                    uint32_t nmb = 0, ex = 0, verdict = 0, flags = 0;
+                    float est = -1.0f;
+                    if (has) bit_hoph_final(a, qg, s, nmb, ex, verdict, flags, est);
+                    emit(a.out, has, qg, s, nmb, ex, a.nlev, verdict, flags, est);
+                }
+            } else {
+                // full-OPH verdict (Eq. 6): den = k - N_excl >= k - (max_q |Eq| + |Es|) (EitherEmpty)
+                // or k - min(max_q |Eq|, |Es|) (JointEmpty), so a pair can only be Similar if
+                // N_mb >= ceil(t_num den_min / t_den): the candidates, verified exactly
+                const uint32_t es_w = lane < a.nw ? __ldg(a.E + (uint64_t)lane * a.ld + s) : 0u;
+                const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, a.nbins_total));
+                const uint32_t k = a.nbins_total;
+                uint32_t den_min = a.joint ? k - min(max_eq, es) : k - min(k, max_eq + es);
+                const uint32_t theta =
+                    a.out.dense ? 0u : (uint32_t)(((uint64_t)a.t_num * den_min + a.t_den - 1) / a.t_den);
+                uint32_t want = sliced_ge<kBitCS>(c, theta) & alive;
+                while (__any_sync(0xFFFFFFFFu, want != 0u)) {
+                    const bool has = want != 0u;
+                    const uint32_t j = has ? __ffs(want) - 1 : 0u;
+                    want &= want - 1u;
+                    const uint32_t qg = a.qb0 + qw0 + j;
+                    uint32_t ex = 0;
+                    for (uint32_t w = 0; w < a.nw; w++) {
+                        const uint32_t sw = __shfl_sync(0xFFFFFFFFu, es_w, w);
+                        if (has) ex += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + w), sw, a.joint, w, k);
+                    }
+                    const uint32_t nmb = sliced_get<kBitCS>(c, j);
+                    const uint32_t den = k - ex;
+                    const bool undef = den == 0;
+                    const uint32_t verdict = !undef && (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
+                    emit(a.out, has, qg, s, nmb, ex, a.level_final, verdict, undef ? OPH_FLAG_UNDEFINED : 0u,
+                         undef ? -1.0f : (float)nmb / (float)den);
+                }
+            }
+            alive = 0u;
+            return true;
+        };
+        uint32_t xb[16];
+        for (uint32_t g = 0; g < nbt; g += 2) {
+            if (step(g, x, xb)) break;
+            if (g + 1 < nbt && step(g + 1, xb, x)) break;
+        }
+        release();
+    }
+}
+
+// The same scan with one software pipeline across the warp's sets (items = the staged
+// batches of its sets, the staged tile buffers released by the lookup stage): pays when
+// a set's staged prefix is short (HOPH: one group of 2 batches), where the per-set
+// pipeline fill of bit_scan_kernel dominated (image-like HOPH 8.2 -> 5.4 ms); for full OPH
+// (32 batches per set) its bookkeeping cost more than the fills (38.2 -> 45.6 ms).
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_x_kernel(const __grid_constant__ BitArgs a) {
     __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
     __shared__ uint64_t s_full[kBitMaxStages];
     __shared__ uint32_t s_done[kBitMaxStages];
@@ -522,7 +767,7 @@ cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     const int ctas = a.mode_hoph || two ? 2 : 3;
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * ctas * 8);
     const size_t smem = (size_t)a.nstage * a.npre * kBitWarps * 4;
-    auto kern = a.mode_hoph ? bit_scan_kernel<1, 2> : (two ? bit_scan_kernel<0, 2> : bit_scan_kernel<0, 3>);
+    auto kern = a.mode_hoph ? bit_scan_x_kernel<1, 2> : (two ? bit_scan_kernel<0, 2> : bit_scan_kernel<0, 3>);
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return e;
     kern<<<grid, 32 * kBitWarps, smem, st>>>(a);
