@@ -53,9 +53,8 @@ __global__ void bit_claim_kernel(const __grid_constant__ BitArgs a) {
         uint32_t *slot = a.idx + st + v;
         if (atomicCAS(slot, 0u, 0xFFFFFFFFu) == 0u) {
             const uint32_t r = atomicAdd(a.nrows, 1u) + 1u;  // row 0 stays the zero row
-            uint4 *row = reinterpret_cast<uint4 *>(a.rows + (uint64_t)r * 32);
-#pragma unroll
-            for (int w = 0; w < 8; w++) row[w] = make_uint4(0, 0, 0, 0);
+            uint4 *row = reinterpret_cast<uint4 *>(a.rows + (uint64_t)r * 32 * a.qw);
+            for (uint32_t w = 0; w < 8 * a.qw; w++) row[w] = make_uint4(0, 0, 0, 0);
             atomicExch(slot, r);
         }
     }
@@ -70,14 +69,14 @@ __global__ void bit_fill_kernel(const __grid_constant__ BitArgs a) {
         bit_bin_range(a, b, st, wd);
         if (v >= wd) continue;
         const uint32_t r = a.idx[st + v];
-        atomicOr(a.rows + (uint64_t)r * 32 + (q >> 5), 1u << (q & 31u));
+        atomicOr(a.rows + (uint64_t)r * 32 * a.qw + (q >> 5), 1u << (q & 31u));
     }
 }
 
 // max over each word's 32 queries of the query's empty bins (the filter bound of the
 // final verdict, see bit_final)
 __global__ void bit_maxeq_kernel(const __grid_constant__ BitArgs a) {
-    const uint32_t q = threadIdx.x;  // one CTA of 1024 threads
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;  // qw CTAs of 1024 threads
     uint32_t e = 0;
     if (q < a.nqb) {
         const uint32_t qg = a.qb0 + q;
@@ -459,6 +458,203 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
     }
 }
 
+// Full OPH / GOPH with QW query words per lane (QW = 2: blocks of 2,048 queries, rows of
+// 256 B read as one 8-B load per lane): per (set, bin) one table lookup and one shuffle /
+// address for 2,048 queries instead of 1,024 -- the lookups were a third of the L1
+// requests and the shuffles / addresses a third of the issued instructions.
+template <int QW, int MINB>
+__global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_q_kernel(const __grid_constant__ BitArgs a) {
+    __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
+    __shared__ uint64_t s_full[kBitMaxStages];
+    __shared__ uint32_t s_done[kBitMaxStages];
+    extern __shared__ __align__(128) uint32_t s_vals[];  // [nstage][npre][8]
+    for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
+        uint32_t st, wd;
+        bit_bin_range(a, b, st, wd);
+        s_start[b] = st;
+        s_width[b] = wd;
+    }
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    // this lane's words of the block: word w holds queries qb0 + 32 (QW lane + w) + j
+    uint32_t qw0[QW], qvalid[QW], max_eq[QW];
+#pragma unroll
+    for (int w = 0; w < QW; w++) {
+        qw0[w] = 32u * (QW * lane + w);
+        qvalid[w] = qw0[w] >= a.nqb ? 0u : (a.nqb - qw0[w] >= 32u ? 0xFFFFFFFFu : ((1u << (a.nqb - qw0[w])) - 1u));
+        max_eq[w] = a.max_eq[QW * lane + w];
+    }
+    const uint32_t *rows_lane = a.rows + QW * lane;
+    const uint32_t nlev_scan = a.method == kGoph ? a.nlev : 1u;
+    const uint32_t bins_per_level = a.method == kGoph ? a.kp : a.nscan;
+    const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
+    const uint32_t vstride = a.npre * 8u;  // words per buffer
+    if (threadIdx.x == 0) {
+        for (uint32_t i = 0; i < a.nstage; i++) {
+            mbar_init(&s_full[i], 32);  // the 32 lanes of the filling warp
+            s_done[i] = 0u;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) {
+        for (uint32_t i = 0; i < a.nstage; i++) {
+            const uint64_t t = blockIdx.x + (uint64_t)i * gridDim.x;
+            if (t < ntiles) bit_tile_load(a, t, s_vals + i * vstride, &s_full[i], lane);
+        }
+    }
+
+    uint32_t it = 0;  // this CTA's tile counter
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+        const uint32_t bi = it % a.nstage;
+        const uint64_t s = a.s_begin + tile * kBitWarps + warp;
+        const uint32_t *v_cur = s_vals + bi * vstride + warp;  // value of bin b: v_cur[8 b]
+        mbar_wait(&s_full[bi], (it / a.nstage) & 1u);
+        auto release = [&]() {
+            __syncwarp();
+            uint32_t last = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                last = atomicAdd(&s_done[bi], 1u) == kBitWarps - 1;
+                if (last) s_done[bi] = 0u;
+            }
+            last = __shfl_sync(0xFFFFFFFFu, last, 0);
+            const uint64_t tn = tile + (uint64_t)a.nstage * gridDim.x;
+            if (last && tn < ntiles) bit_tile_load(a, tn, s_vals + bi * vstride, &s_full[bi], lane);
+        };
+        if (s >= a.n_sets) {  // warp-uniform: a tail tile's missing set
+            release();
+            continue;
+        }
+        uint32_t c[QW][kBitCS];
+        uint32_t alive[QW];
+#pragma unroll
+        for (int w = 0; w < QW; w++) {
+            alive[w] = qvalid[w];
+#pragma unroll
+            for (int i = 0; i < (int)kBitCS; i++) c[w][i] = 0u;
+        }
+        const uint32_t nbt = (a.nscan + 15u) / 16u;
+        const uint32_t bpl = bins_per_level / 16u;
+        auto ilook = [&](uint32_t g) -> uint32_t {
+            const uint32_t b = 16u * g + lane;
+            uint32_t r = 0u;
+            if (lane < 16u && b < a.nscan) {
+                const uint32_t v = b < a.npre ? v_cur[8 * b] : __ldg(a.F + (uint64_t)b * a.ld + s);
+                if (v < s_width[b]) r = __ldg(a.idx + s_start[b] + v);
+            }
+            return r;
+        };
+        auto rload = [&](uint32_t r, uint32_t (&x)[QW][16]) {
+#pragma unroll
+            for (int u = 0; u < 16; u++) {
+                const uint32_t ru = __shfl_sync(0xFFFFFFFFu, r, u);
+                if (QW == 2) {
+                    const uint2 y = __ldg(reinterpret_cast<const uint2 *>(rows_lane + (uint64_t)ru * 64));
+                    x[0][u] = y.x;
+                    x[QW - 1][u] = y.y;
+                } else {
+                    x[0][u] = __ldg(rows_lane + (uint64_t)ru * 32);
+                }
+            }
+        };
+        uint32_t x[QW][16], xb[QW][16], rA, rB;
+        {
+            const uint32_t r0 = ilook(0);
+            rA = ilook(1);
+            rB = ilook(2);
+            rload(r0, x);
+        }
+        uint32_t l = 1, jj = 0;
+        auto step = [&](uint32_t g, uint32_t (&xc)[QW][16], uint32_t (&xn)[QW][16]) -> bool {
+            rload(rA, xn);
+            rA = rB;
+            rB = ilook(g + 3);
+#pragma unroll
+            for (int w = 0; w < QW; w++) csa16(c[w], xc[w]);
+            const bool level_end = bins_per_level == a.nscan ? g + 1 == nbt : jj + 1 == bpl;
+            if (!level_end) {
+                jj++;
+                return false;
+            }
+            const bool last = l == nlev_scan;
+            if (!last && a.thr_on[l - 1]) {
+                const uint32_t A = a.acc_cnt[l - 1];
+                const int32_t R = a.rej_cnt[l - 1];
+#pragma unroll
+                for (int w = 0; w < QW; w++) {
+                    uint32_t acc = sliced_ge<kBitCS>(c[w], A);
+                    uint32_t dec = acc | (R >= 0 ? ~sliced_ge<kBitCS>(c[w], (uint32_t)R + 1u) : 0u);
+                    acc &= alive[w];
+                    dec &= alive[w];
+                    hist_add(a.out.hist, l, __popc(dec));
+                    uint32_t want = a.out.dense ? dec : acc;
+                    while (__any_sync(0xFFFFFFFFu, want != 0u)) {
+                        const bool has = want != 0u;
+                        const uint32_t j = has ? __ffs(want) - 1 : 0u;
+                        want &= want - 1u;
+                        const uint32_t qg = a.qb0 + qw0[w] + j;
+                        uint32_t nmb = 0, ex = 0;
+                        if (has) {
+                            nmb = sliced_get<kBitCS>(c[w], j);
+                            ex = bit_excl(a, qg, s, 0, l * a.kp);
+                        }
+                        emit(a.out, has, qg, s, nmb, ex, l, (acc >> j) & 1u, OPH_FLAG_EARLY, -1.0f);
+                    }
+                    alive[w] &= ~dec;
+                }
+            }
+            if (!last) {
+                uint32_t any = 0u;
+#pragma unroll
+                for (int w = 0; w < QW; w++) any |= alive[w];
+                if (!__any_sync(0xFFFFFFFFu, any != 0u)) return true;  // every pair of this set is decided
+                l++;
+                jj = 0;
+                return false;
+            }
+            // ---- the full-OPH verdict of every pair still alive (Eq. 6): den = k - N_excl >=
+            // k - (max_q |Eq| + |Es|) (EitherEmpty) or k - min(max_q |Eq|, |Es|) (JointEmpty), so
+            // a pair can only be Similar if N_mb >= ceil(t_num den_min / t_den): the candidates,
+            // verified exactly
+            const uint32_t es_w = lane < a.nw ? __ldg(a.E + (uint64_t)lane * a.ld + s) : 0u;
+            const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, a.nbins_total));
+            const uint32_t k = a.nbins_total;
+#pragma unroll
+            for (int w = 0; w < QW; w++) {
+                hist_add(a.out.hist, a.level_final, __popc(alive[w]));
+                const uint32_t den_min = a.joint ? k - min(max_eq[w], es) : k - min(k, max_eq[w] + es);
+                const uint32_t theta =
+                    a.out.dense ? 0u : (uint32_t)(((uint64_t)a.t_num * den_min + a.t_den - 1) / a.t_den);
+                uint32_t want = sliced_ge<kBitCS>(c[w], theta) & alive[w];
+                while (__any_sync(0xFFFFFFFFu, want != 0u)) {
+                    const bool has = want != 0u;
+                    const uint32_t j = has ? __ffs(want) - 1 : 0u;
+                    want &= want - 1u;
+                    const uint32_t qg = a.qb0 + qw0[w] + j;
+                    uint32_t ex = 0;
+                    for (uint32_t ww = 0; ww < a.nw; ww++) {
+                        const uint32_t sw = __shfl_sync(0xFFFFFFFFu, es_w, ww);
+                        if (has) ex += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + ww), sw, a.joint, ww, k);
+                    }
+                    const uint32_t nmb = sliced_get<kBitCS>(c[w], j);
+                    const uint32_t den = k - ex;
+                    const bool undef = den == 0;
+                    const uint32_t verdict = !undef && (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
+                    emit(a.out, has, qg, s, nmb, ex, a.level_final, verdict, undef ? OPH_FLAG_UNDEFINED : 0u,
+                         undef ? -1.0f : (float)nmb / (float)den);
+                }
+                alive[w] = 0u;
+            }
+            return true;
+        };
+        for (uint32_t g = 0; g < nbt; g += 2) {
+            if (step(g, x, xb)) break;
+            if (g + 1 < nbt && step(g + 1, xb, x)) break;
+        }
+        release();
+    }
+}
+
 // The same scan with one software pipeline across the warp's sets (items = the staged
 // batches of its sets, the staged tile buffers released by the lookup stage): pays when
 // a set's staged prefix is short (HOPH: one group of 2 batches), where the per-set
@@ -759,15 +955,17 @@ cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     const unsigned g = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
     bit_claim_kernel<<<g, 256, 0, st>>>(a);
     bit_fill_kernel<<<g, 256, 0, st>>>(a);
-    bit_maxeq_kernel<<<1, 1024, 0, st>>>(a);
+    bit_maxeq_kernel<<<a.qw, 1024, 0, st>>>(a);
     // the scan: 8 consecutive sets per CTA tile, grid-stride; 3 CTAs per SM (HOPH: 2, its T slices need 128 registers)
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
     // (OPHGPU_BIT_CTAS=2: the full-OPH / GOPH scan at 2 CTAs per SM without register limit, A/B)
     static const bool two = getenv("OPHGPU_BIT_CTAS") && atoi(getenv("OPHGPU_BIT_CTAS")) == 2;
-    const int ctas = a.mode_hoph || two ? 2 : 3;
+    const int ctas = a.mode_hoph || two || a.qw == 2 ? 2 : 3;
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * ctas * 8);
     const size_t smem = (size_t)a.nstage * a.npre * kBitWarps * 4;
-    auto kern = a.mode_hoph ? bit_scan_x_kernel<1, 2> : (two ? bit_scan_kernel<0, 2> : bit_scan_kernel<0, 3>);
+    auto kern = a.mode_hoph ? bit_scan_x_kernel<1, 2>
+                            : (a.qw == 2 ? bit_scan_q_kernel<2, 2>
+                                         : (two ? bit_scan_kernel<0, 2> : bit_scan_kernel<0, 3>));
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return e;
     kern<<<grid, 32 * kBitWarps, smem, st>>>(a);

@@ -217,7 +217,8 @@ struct BitArgs {
     uint32_t nb, nw, nscan, kp, nlev, nbins_total;
     uint32_t npre;          // bins [0, npre) are staged per CTA tile (the rest read directly)
     uint32_t nstage;        // CTA tiles staged ahead (ring of value buffers, 2 .. 8)
-    uint32_t qb0, nqb;      // this block: query columns [qb0, qb0 + nqb), nqb <= 1024
+    uint32_t qb0, nqb;      // this block: query columns [qb0, qb0 + nqb), nqb <= 1024 qw
+    uint32_t qw;            // 32-query words per lane: rows of 1024 qw bits (1, or 2 for full OPH / GOPH)
     uint32_t method, mode_hoph, joint, t_num, t_den, level_final;
     // value ranges of the bins: bin b = range b / bins_per_range, floor rule inside it
     uint32_t bins_per_range;
@@ -231,7 +232,7 @@ struct BitArgs {
     uint64_t vpos;                  // |V|
     uint32_t *rows;                 // [1 + rows][32] query bitmasks
     uint32_t *nrows;                // rows claimed
-    uint32_t *max_eq;               // [32] per query word: max empty bins of its queries
+    uint32_t *max_eq;               // [32 qw] per query word: max empty bins of its queries
     OutArgs out;
 };
 

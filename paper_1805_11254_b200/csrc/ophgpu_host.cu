@@ -407,8 +407,9 @@ size_t surv_region_bytes(uint64_t cap) { return 2 * (align256(cap * 4) * 3 + ali
 constexpr uint64_t kBitMaxV = 1ull << 23;
 constexpr uint32_t kBitMaxNb = 1023;
 bool bitmap_sizes_ok(uint64_t V, uint32_t nb) { return V <= kBitMaxV && nb <= kBitMaxNb; }
+// (rows of up to 2,048 query bits: blocks of 2,048 queries for full OPH / GOPH)
 size_t bitmap_region_bytes(uint64_t V, uint32_t nb) {
-    return align256(V * 4) + align256((1 + (uint64_t)nb * 1024) * 128) + align256(4) + align256(32 * 4);
+    return align256(V * 4) + align256((1 + (uint64_t)nb * 2048) * 256) + align256(4) + align256(64 * 4);
 }
 
 // largest survivor capacity that fits in ws_bytes
@@ -434,7 +435,7 @@ oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketche
     char *bp = (char *)d_ws + fixed;
     BitArgs ba{};
     ba.idx = (uint32_t *)bp; bp += align256(V * 4);
-    ba.rows = (uint32_t *)bp; bp += align256((1 + (uint64_t)nb * 1024) * 128);
+    ba.rows = (uint32_t *)bp; bp += align256((1 + (uint64_t)nb * 2048) * 256);
     ba.nrows = (uint32_t *)bp; bp += align256(4);
     ba.max_eq = (uint32_t *)bp;
     ba.vpos = V;
@@ -512,9 +513,14 @@ oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketche
         ba.rej_cnt[l - 1] = T.rej < 0 ? -1 : (int32_t)std::min<i128>(T.rej / (i128)div, (i128)INT32_MAX);
         ba.thr_on[l - 1] = ba.acc_cnt[l - 1] != UINT32_MAX || ba.rej_cnt[l - 1] >= 0;
     }
-    for (uint64_t q0 = 0; q0 < n_q; q0 += 1024) {
+    // blocks of 2,048 queries (two words per lane) for full OPH / GOPH, 1,024 for HOPH (its
+    // kernel carries the T_l slices); OPHGPU_BIT_QW=1 forces 1,024 (A/B)
+    static const bool qw1 = getenv("OPHGPU_BIT_QW") && atoi(getenv("OPHGPU_BIT_QW")) == 1;
+    ba.qw = (method == OPH_METHOD_HOPH || qw1) ? 1 : 2;
+    const uint64_t qb = 1024ull * ba.qw;
+    for (uint64_t q0 = 0; q0 < n_q; q0 += qb) {
         ba.qb0 = (uint32_t)q0;
-        ba.nqb = (uint32_t)std::min<uint64_t>(1024, n_q - q0);
+        ba.nqb = (uint32_t)std::min<uint64_t>(qb, n_q - q0);
         if (launch_bit_block(ba, stream) != cudaSuccess) return OPH_ECUDA;
     }
     return OPH_OK;

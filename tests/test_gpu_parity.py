@@ -801,9 +801,10 @@ def test_survivor_lists_many_late_pairs(monkeypatch):
 @pytest.fixture(scope="module")
 def image_small():
     """An image-like collection (Zipf words over 2^20, k = 512, k' = 32, HOPH L = 15) with
-    1,100 queries: two BITMAP query blocks, the second one ragged (76 queries)."""
+    2,100 queries: two BITMAP query blocks of 2,048 (full OPH, GOPH) or three of 1,024 (HOPH),
+    the last one ragged."""
     from workloads import gen
-    w = gen.image_like(n_sets=20_000, n_queries=1100)
+    w = gen.image_like(n_sets=20_000, n_queries=2100)
     p = w.params
     V, seed = w.vocab_size, p["perm_seed"]
     hier = og.oph_hier_layout_make(V, 1, 1, p["hoph_kprime"])
@@ -820,7 +821,7 @@ def image_small():
 @pytest.mark.parametrize("joint", [False, True])
 @pytest.mark.parametrize("method", ["full", "goph", "hoph"])
 def test_bitmap_image_like_dense(image_small, method, joint):
-    """BITMAP dense records of all 1,100 queries x the first 2,000 sets == the oracle's."""
+    """BITMAP dense records of all 2,100 queries x the first 2,000 sets == the oracle."""
     r, o, p = image_small, image_small["orc"], image_small["p"]
     kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"], joint=joint, strategy=og.OPH_STRATEGY_BITMAP)
     n = 2000
