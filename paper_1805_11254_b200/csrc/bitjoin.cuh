@@ -950,7 +950,7 @@ cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     // the value -> row table of this block: clear, claim rows, set the bits
     if ((e = cudaMemsetAsync(a.idx, 0, (size_t)a.vpos * 4, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(a.nrows, 0, 4, st)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(a.rows, 0, 128, st)) != cudaSuccess) return e;  // the zero row
+    if ((e = cudaMemsetAsync(a.rows, 0, 128 * a.qw, st)) != cudaSuccess) return e;  // the zero row
     const uint64_t n = (uint64_t)a.nscan * a.nqb;
     const unsigned g = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
     bit_claim_kernel<<<g, 256, 0, st>>>(a);

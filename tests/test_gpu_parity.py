@@ -850,7 +850,12 @@ def test_bitmap_image_like_lists_and_histogram(image_small, method):
     res = og.Results(1 << 22, stop_hist=True)
     prm = og.params(p["t_num"], p["t_den"], p["eps"], strategy=og.OPH_STRATEGY_BITMAP)
     fn = {"full": og.compare_full, "goph": og.compare_goph, "hoph": og.compare_hoph}[method]
-    fn(q, s, lay, prm, res)
+    # a workspace full of garbage: nothing may rely on it being zero (r02: the zero row of the
+    # 2,048-query rows was only half cleared)
+    ws = og.Workspace()
+    meth = {"full": og.OPH_METHOD_FULL, "goph": og.OPH_METHOD_GOPH, "hoph": og.OPH_METHOD_HOPH}[method]
+    ws.get(og.oph_workspace_size_for(meth, q, s, prm, 0)).fill_(0xFF)
+    fn(q, s, lay, prm, res, ws=ws)
     hist = res.hist().astype(np.int64)
     assert (hist == np.bincount(want["groups"].ravel(), minlength=len(hist))).all()
     n = res.n()
