@@ -620,22 +620,30 @@ def run_ours(args):
                   "compare_goph": N * (4 * g_l0 * kp + 4 * ((g_l0 * kp + 31) // 32)),
                   "compare_hoph": N * (4 * hkp + 4)}
     models = {}
+    l2_src = "none measured"
 
     # BITMAP join (K7): per (set, bin, block of 1024 queries) one 4-B entry of the value -> row
     # table and one 128-B row of query bits, gathered from the L2-resident block tables; peak =
     # the measured random 128-B row-gather rate from a 16-MB table (scripts/ubench.cu)
-    l2_peak = (ub or {}).get("gather_128B_rows_GBps", {}).get(str(16 << 20))
-    l2_src = ("measured: scripts/ubench.cu random 128-B row gathers, 16-MB table (profiles/ubench_r02.json)"
-              if l2_peak else "none measured")
-    qblocks = -(-Q // 1024)
+    def l2_peak_for(row_bytes):
+        key = "gather_128B_rows_GBps" if row_bytes == 128 else "gather_256B_rows_GBps"
+        return (ub or {}).get(key, {}).get(str(16 << 20))
 
     def model_for(kernel: str, phase: str):
-        if kernel.startswith("bit_scan_kernel"):
+        if kernel.startswith("bit_scan"):
+            # full OPH / GOPH: blocks of 2,048 queries (256-B rows, bit_scan_q_kernel); HOPH 1,024
+            qwords = 2 if kernel.startswith("bit_scan_q_kernel") else 1
+            row = 128 * qwords
             m = phase.split("_")[1]
             bins = (bins_compared.get(m, Q * N * k) / Q) if m != "full" else N * k  # (set, bin) pairs scanned
-            gathered = bins * qblocks * (128 + 4)
-            return ("l2", gathered, (l2_peak or float("nan")) * 1e9, "GB/s", 1e9,
-                    "bytes: one 128-B query-bit row + one 4-B table entry per (set, bin compared, 1024-query block)")
+            gathered = bins * -(-Q // (1024 * qwords)) * (row + 4)
+            peak = l2_peak_for(row)
+            nonlocal l2_src
+            l2_src = (f"measured: scripts/ubench.cu random {row}-B row gathers, 16-MB table "
+                      "(profiles/ubench_r02.json)" if peak else "none measured")
+            return ("l2", gathered, (peak or float("nan")) * 1e9, "GB/s", 1e9,
+                    f"bytes: one {row}-B query-bit row + one 4-B table entry per (set, bin compared, "
+                    f"{1024 * qwords}-query block)")
         if kernel.startswith("build_kernel"):
             return ("hbm", build_bytes, hbm, "GB/s", 1e9, "bytes: CSR in + OPH/HOPH sketches and masks out")
         if kernel.startswith("join_kernel"):

@@ -107,6 +107,27 @@ __global__ void __launch_bounds__(256) gather(const uint32_t *tab, uint32_t nrow
     if (acc == 0x9E3779B9u) *sink = acc;
 }
 
+// the same with 256-B rows, one 8-B load per lane (the BITMAP scan's 2,048-query rows)
+template <int U>
+__global__ void __launch_bounds__(256) gather2(const uint2 *tab, uint32_t nrows_mask, uint32_t per_warp,
+                                               uint32_t *sink) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t h = wid * 0x9E3779B1u + 12345u, acc = 0;
+    const uint2 *tl = tab + lane;
+    for (uint32_t i = 0; i < per_warp; i += U) {
+        uint2 r[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            h = h * 0x2545F491u + 0x9E3779B9u;
+            r[u] = __ldg(tl + (uint64_t)((h >> 7) & nrows_mask) * 32);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) acc ^= r[u].x ^ r[u].y;
+    }
+    if (acc == 0x9E3779B9u) *sink = acc;
+}
+
 __global__ void stream(const uint4 *F, uint64_t n, uint32_t *sink) {
     uint32_t acc = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -174,6 +195,13 @@ int main() {
             const uint32_t nrows = (uint32_t)(sizes[i] / 128);
             float ms = time_ms([&] { gather<16><<<grid, 256>>>(tab, nrows - 1, per_warp, sink); }, 5);
             const double bytes = (double)grid * 8 * per_warp * 128;
+            printf("%s\"%llu\": %.1f", i ? ", " : "", (unsigned long long)sizes[i], bytes / (ms / 1e3) / 1e9);
+        }
+        printf("}, \"gather_256B_rows_GBps\": {");
+        for (int i = 0; i < 5; i++) {
+            const uint32_t nrows = (uint32_t)(sizes[i] / 256);
+            float ms = time_ms([&] { gather2<16><<<grid, 256>>>((const uint2 *)tab, nrows - 1, per_warp, sink); }, 5);
+            const double bytes = (double)grid * 8 * per_warp * 256;
             printf("%s\"%llu\": %.1f", i ? ", " : "", (unsigned long long)sizes[i], bytes / (ms / 1e3) / 1e9);
         }
         printf("}");
