@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
 // 256 B read as one 8-B load per lane): per (set, bin) one table lookup and one shuffle /
 // address for 2,048 queries instead of 1,024 -- the lookups were a third of the L1
 // requests and the shuffles / addresses a third of the issued instructions.
-template <int QW, int MINB>
+template <int QW, int MINB, bool ALLSTAGED>
 __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_q_kernel(const __grid_constant__ BitArgs a) {
     __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
     __shared__ uint64_t s_full[kBitMaxStages];
@@ -535,8 +535,16 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_q_kernel(const 
         }
         const uint32_t nbt = (a.nscan + 15u) / 16u;
         const uint32_t bpl = bins_per_level / 16u;
+        // (ALLSTAGED: every scanned bin is staged -- full OPH -- so no direct-load path; the
+        // lookup is branch-free: lanes past the batch read a staged slot they do not use)
         auto ilook = [&](uint32_t g) -> uint32_t {
             const uint32_t b = 16u * g + lane;
+            if (ALLSTAGED) {
+                const uint32_t bc = min(b, a.nscan - 1u);
+                const uint32_t v = v_cur[8 * bc];
+                const bool ok = lane < 16u && b < a.nscan && v < s_width[bc];
+                return ok ? __ldg(a.idx + s_start[bc] + v) : 0u;
+            }
             uint32_t r = 0u;
             if (lane < 16u && b < a.nscan) {
                 const uint32_t v = b < a.npre ? v_cur[8 * b] : __ldg(a.F + (uint64_t)b * a.ld + s);
@@ -960,11 +968,15 @@ cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
     // (OPHGPU_BIT_CTAS=2: the full-OPH / GOPH scan at 2 CTAs per SM without register limit, A/B)
     static const bool two = getenv("OPHGPU_BIT_CTAS") && atoi(getenv("OPHGPU_BIT_CTAS")) == 2;
-    const int ctas = a.mode_hoph || two || a.qw == 2 ? 2 : 3;
+    // (OPHGPU_BIT_CTAS=3: the 2,048-query scan at 3 CTAs per SM, 85 registers, A/B)
+    static const bool three = getenv("OPHGPU_BIT_CTAS") && atoi(getenv("OPHGPU_BIT_CTAS")) == 3;
+    const int ctas = a.mode_hoph || two || (a.qw == 2 && !three) ? 2 : 3;
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * ctas * 8);
     const size_t smem = (size_t)a.nstage * a.npre * kBitWarps * 4;
     auto kern = a.mode_hoph ? bit_scan_x_kernel<1, 2>
-                            : (a.qw == 2 ? bit_scan_q_kernel<2, 2>
+                            : (a.qw == 2 ? (a.npre == a.nscan ? (three ? bit_scan_q_kernel<2, 3, true>
+                                                                       : bit_scan_q_kernel<2, 2, true>)
+                                                              : bit_scan_q_kernel<2, 2, false>)
                                          : (two ? bit_scan_kernel<0, 2> : bit_scan_kernel<0, 3>));
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return e;

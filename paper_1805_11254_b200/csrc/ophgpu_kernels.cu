@@ -223,7 +223,7 @@ __device__ __forceinline__ void write_sketch(const uint32_t *src, uint32_t strid
 }
 
 template <bool W32, int SB, bool FAST>
-__global__ void __launch_bounds__(256) build_kernel(const __grid_constant__ BuildArgs a) {
+__global__ void __launch_bounds__(512) build_kernel(const __grid_constant__ BuildArgs a) {
     extern __shared__ __align__(16) uint32_t smem_u32[];
     // group table in shared memory: lanes index it divergently, which would
     // serialise on the constant cache if read from the kernel parameters
@@ -1795,7 +1795,7 @@ cudaError_t launch_jaccard(const JaccardArgs &a, cudaStream_t st) {
 // launchers
 // ---------------------------------------------------------------------------
 template <int SB>
-static cudaError_t launch_build_sb(const BuildArgs &a, size_t smem, cudaStream_t st) {
+static cudaError_t launch_build_sb(const BuildArgs &a, size_t smem, cudaStream_t st, uint32_t threads) {
     const uint64_t grid = (a.n_sets + SB - 1) / SB;
     const bool fast = a.do_flat && a.flat.pow2 && a.flat.start == 0 && a.psi.pow2 && !a.psi.identity && a.do_hier &&
                       a.hier_pow2_halves && a.L <= 32 && a.log2kp >= 1;
@@ -1804,7 +1804,7 @@ static cudaError_t launch_build_sb(const BuildArgs &a, size_t smem, cudaStream_t
                      : (w32 ? build_kernel<true, SB, false> : build_kernel<false, SB, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)grid, 256, smem, st>>>(a);
+    kern<<<(unsigned)grid, threads, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -1814,14 +1814,20 @@ cudaError_t launch_build(const BuildArgs &a, cudaStream_t st) {
                              (a.do_hier ? (a.L * a.kp + 31) / 32 * 32 + 1 : 0);
     // 8 sets per CTA: 36 KB of shared memory at text-like sizes -> 6 CTAs (48 warps) per SM,
     // and a bin row of the tile is one full 32-B sector; fewer for very large sketches
-    uint32_t SB = 8;
+    // (OPHGPU_BUILD_SB / OPHGPU_BUILD_THREADS override the tile for A/B sweeps)
+    uint32_t SB = 8, threads = 256;
+    if (const char *e = getenv("OPHGPU_BUILD_SB")) SB = (uint32_t)atoi(e);
+    if (const char *e = getenv("OPHGPU_BUILD_THREADS")) threads = (uint32_t)atoi(e);
+    if (SB != 1 && SB != 2 && SB != 4 && SB != 8 && SB != 16) SB = 8;
+    if (threads != 128 && threads != 256 && threads != 512) threads = 256;
     while (SB > 1 && (size_t)SB * per_set * 4 + 16 > 200 * 1024) SB >>= 1;
     const size_t smem = ((size_t)SB * per_set * 4 + 15) / 16 * 16;
     switch (SB) {
-        case 8: return launch_build_sb<8>(a, smem, st);
-        case 4: return launch_build_sb<4>(a, smem, st);
-        case 2: return launch_build_sb<2>(a, smem, st);
-        default: return launch_build_sb<1>(a, smem, st);
+        case 16: return launch_build_sb<16>(a, smem, st, threads);
+        case 8: return launch_build_sb<8>(a, smem, st, threads);
+        case 4: return launch_build_sb<4>(a, smem, st, threads);
+        case 2: return launch_build_sb<2>(a, smem, st, threads);
+        default: return launch_build_sb<1>(a, smem, st, threads);
     }
 }
 
