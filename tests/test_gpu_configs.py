@@ -98,7 +98,9 @@ def test_image_like_full_size():
     from workloads.gen_gpu import image_like
     w = image_like()
     assert w.n_sets == 1_000_000 and w.n_queries == 4096
-    check_config(w, sample=[0, 1, 2, 1000, 2047, 4095], strategy=og.OPH_STRATEGY_BRUTE)
+    # the bench's strategy (BITMAP, blocks of 2,048 queries for full OPH / GOPH); samples on
+    # both sides of every block boundary
+    check_config(w, sample=[0, 1, 2, 1000, 2047, 2048, 3071, 4095], strategy=og.OPH_STRATEGY_BITMAP)
 
 
 def test_scale_shard_full_size():
@@ -140,8 +142,42 @@ def test_probe_survivor_overflow_redo(method):
     assert [(int(h["query"]), int(h["set_id"])) for h in hits] == oracle.threshold_list(want)
 
 
-@pytest.mark.parametrize("jmax,n_sets", [(0.9, 2_000_000), (0.5, 200_000), (0.2, 200_000)])
-def test_sweep(jmax, n_sets):
+@pytest.mark.parametrize("jmax", [0.9, 0.5, 0.2])
+def test_sweep(jmax):
+    """configs[4] at its full size (2 x 10^6 sets per Jmax), the bench's BITMAP strategy."""
     from workloads.gen_gpu import sweep
-    w = sweep(jmax, n_sets=n_sets)
-    check_config(w, sample=[0, 3, 17, 31], strategy=og.OPH_STRATEGY_AUTO, dense_q=2, hit_queries=32)
+    w = sweep(jmax, n_sets=2_000_000)
+    check_config(w, sample=[0, 3, 17, 31], strategy=og.OPH_STRATEGY_BITMAP, dense_q=2, hit_queries=32)
+
+
+@pytest.mark.parametrize("shard", [1, 2, 3, 4, 5, 6, 7])
+def test_scale_other_shards(shard):
+    """configs[3]'s other seven per-GPU shards: every sketch == the oracle's, and the hit lists
+    of two sampled queries over all 1.25 x 10^6 sets (AUTO: the PROBE join) == the oracle's."""
+    from workloads.gen_gpu import scale_shard
+    w = scale_shard(shard=shard)
+    p = w.params
+    V, seed = w.vocab_size, p["perm_seed"]
+    hier = og.oph_hier_layout_make(V, p["a"], p["b"], p["hoph_kprime"])
+    flat = og.flat_layout(V, p["k"], p["kprime"])
+    so, sh = og.oph_build_sketches(og.SetCollection.from_numpy(w.offsets, w.ids), V, seed, flat=flat, hier=hier)
+    qo, qh = og.oph_build_sketches(og.SetCollection.from_numpy(w.q_offsets, w.q_ids), V, seed, flat=flat,
+                                   hier=hier)
+    glay = oracle.hoph_layout(V, p["a"], p["b"], p["hoph_kprime"])
+    F = oracle.oph_sketch(w.offsets, w.ids, V, p["k"], seed)
+    _check_sketches_chunked(so, F)
+    H = oracle.hoph_sketch(w.offsets, w.ids, V, glay, p["hoph_kprime"], seed)
+    _check_sketches_chunked(sh, H)
+    sample = [shard * 1000 + 3, 16383 - shard]
+    QF = oracle.oph_sketch(w.q_offsets, w.q_ids, V, p["k"], seed)
+    QH = oracle.hoph_sketch(w.q_offsets, w.q_ids, V, glay, p["hoph_kprime"], seed)
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    for m in ("full", "goph", "hoph"):
+        if m == "hoph":
+            hits = gpu_threshold_hits(m, qh, sh, layout=hier, strategy=og.OPH_STRATEGY_AUTO, capacity=1 << 24, **kw)
+            want = oracle_records(m, QH[sample], H, kprime=p["hoph_kprime"], L=len(glay), **kw)
+        else:
+            hits = gpu_threshold_hits(m, qo, so, layout=flat, strategy=og.OPH_STRATEGY_AUTO, capacity=1 << 24, **kw)
+            want = oracle_records(m, QF[sample], F, k=p["k"], kprime=p["kprime"], **kw)
+        got = [(int(h["query"]), int(h["set_id"])) for h in hits if int(h["query"]) in set(sample)]
+        assert got == [(sample[q], s) for q, s in oracle.threshold_list(want)], (shard, m)

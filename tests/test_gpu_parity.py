@@ -498,6 +498,41 @@ def test_text_sketches_full_collection(text_run):
     r["F"], r["H"] = F, H
 
 
+@pytest.mark.parametrize("method", ["full", "goph", "hoph"])
+def test_text_all_queries_hit_lists(text_run, method):
+    """configs[1] as the bench runs it (AUTO: the PROBE join): the hit lists of ALL 1,000
+    queries x 200,000 sets, every record field, == the oracle's (evaluated in query chunks)."""
+    r = text_run
+    w, p = r["w"], r["p"]
+    if "F" not in r:
+        r["F"] = oracle.oph_sketch(w.offsets, w.ids, w.vocab_size, p["k"], p["perm_seed"])
+        r["H"] = oracle.hoph_sketch(w.offsets, w.ids, w.vocab_size, r["glay"], p["hoph_kprime"], p["perm_seed"])
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    if method == "hoph":
+        Q = oracle.hoph_sketch(w.q_offsets, w.q_ids, w.vocab_size, r["glay"], p["hoph_kprime"], p["perm_seed"])
+        hits = gpu_threshold_hits(method, r["qh"], r["sh"], layout=r["hier"], strategy=og.OPH_STRATEGY_AUTO, **kw)
+    else:
+        Q = oracle.oph_sketch(w.q_offsets, w.q_ids, w.vocab_size, p["k"], p["perm_seed"])
+        lay = og.flat_layout(w.vocab_size, p["k"], p["kprime"])
+        hits = gpu_threshold_hits(method, r["qo"], r["so"], layout=lay, strategy=og.OPH_STRATEGY_AUTO, **kw)
+    want = []
+    rec = {}
+    for q0 in range(0, Q.shape[0], 50):
+        if method == "hoph":
+            o = oracle_records(method, Q[q0:q0 + 50], r["H"], kprime=p["hoph_kprime"], L=len(r["glay"]), **kw)
+        else:
+            o = oracle_records(method, Q[q0:q0 + 50], r["F"], k=p["k"], kprime=p["kprime"], **kw)
+        for q, s in oracle.threshold_list(o):
+            want.append((q0 + q, s))
+            rec[(q0 + q, s)] = o[q, s]
+    got = [(int(h["query"]), int(h["set_id"])) for h in hits]
+    assert got == want
+    assert len(want) > 500
+    for h in hits:
+        o = rec[(int(h["query"]), int(h["set_id"]))]
+        assert (h["n_mb"], h["n_excl"], h["groups"], h["flags"]) == (o["n_mb"], o["n_excl"], o["groups"], o["flags"])
+
+
 @pytest.mark.parametrize("strategy", [og.OPH_STRATEGY_AUTO, og.OPH_STRATEGY_BRUTE])
 @pytest.mark.parametrize("method", ["full", "goph", "hoph", "goph_e"])
 def test_text_full_size_sampled_queries(text_run, method, strategy):
