@@ -931,10 +931,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  : "memory");
 }
 
-// 20 warps with two tiles in flight each (the next tile's rows load while this one is
-// probed; 102 registers): r01's single-buffered 28 warps left the row loads' latency exposed
-// (long-scoreboard stalls on the tile values, 0.42 of the copy peak)
-constexpr int kJoinWarps = 16;
+constexpr int kJoinWarps = 28;
 constexpr int kJoinThreads = 32 * kJoinWarps;
 // candidate queue per warp (4-B entries).  Small on purpose: the verification re-reads
 // each candidate's value, which is still in L2 only if the flush follows within a few
@@ -1204,22 +1201,10 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
             join_push(a, s_lo, cm, sl, j * SBN + rb * kJoinRPT, lists, ovf, myq, qn);
         };
         mbar_wait(&tfull[tb], (j >> 1) & 1u);  // the slab's filters
-        {
-            // two tiles in flight: the next tile (from the slab's counter) loads while this one
-            // is probed; the buffers alternate (no register copies of loads in flight)
-            uint32_t va[kJoinVals], vb[kJoinVals];
-            uint32_t t = next_tile();
-            if (t < ntile) load_tile(t, va);
-            while (t < ntile) {
-                const uint32_t t2 = next_tile();
-                if (t2 < ntile) load_tile(t2, vb);
-                probe_tile(t, va);
-                if (t2 >= ntile) break;
-                const uint32_t t3 = next_tile();
-                if (t3 < ntile) load_tile(t3, va);
-                probe_tile(t2, vb);
-                t = t3;
-            }
+        for (uint32_t t = next_tile(); t < ntile; t = next_tile()) {
+            uint32_t v[kJoinVals];
+            load_tile(t, v);
+            probe_tile(t, v);
         }
         // the last warp done with slab j recycles its filter buffer for slab j + 2
         __syncwarp();
