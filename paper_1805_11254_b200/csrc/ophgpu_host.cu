@@ -950,8 +950,10 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
         // one (input and output must never alias: the grid-stride walk of the input runs
         // concurrently with other warps' appends).
         uint32_t cur = surv_l % 2;  // the scan appended its survivors to list[surv_l % 2]
+        // k' <= 32: one launch of the warp-per-pair walk decides every remaining level
+        const bool walk = kp <= 32;
         for (uint32_t l = plan.l0 + 1, first = 1; l <= nlev; first = 0) {
-            const uint32_t l_last = first ? std::min(nlev, l + kLevelsPerLaunch - 1) : nlev;
+            const uint32_t l_last = (first && !walk) ? std::min(nlev, l + kLevelsPerLaunch - 1) : nlev;
             la.level = l;
             la.level_last = l_last;
             la.in = w.list[cur];

@@ -2093,9 +2093,124 @@ cudaError_t launch_level_e(const LevelArgs &a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// The survivor levels, one warp per surviving pair (k' <= 32: lane = bin of a group):
+// the values of up to 8 further groups (query side contiguous in QM, set side one gather per
+// lane and group) are loaded at once and the levels then decided from registers, so a pair
+// costs one memory latency per 8 levels instead of one per level (r01's level_kernel walked
+// its 32 pairs level by level in two launches with a compaction between).  Same decisions
+// and records as level_kernel.
+__device__ __forceinline__ void emit_one(const OutArgs &o, uint32_t q, uint32_t s, uint32_t n_mb, uint32_t n_excl,
+                                         uint32_t groups, uint32_t verdict, uint32_t flags, float est) {
+    if (o.dense) {
+        write_hit(o.hits + (uint64_t)q * o.n_sets + s, q, o.set_id_base + s, n_mb, n_excl, groups, verdict, flags, est);
+    } else if (verdict) {
+        const unsigned long long idx = atomicAdd(o.count, 1ull);
+        if (idx < o.cap) write_hit(o.hits + idx, q, o.set_id_base + s, n_mb, n_excl, groups, verdict, flags, est);
+    }
+}
+
+// excluded bins of a pair among bins [0, nbins), lane-parallel over the mask words
+__device__ __forceinline__ uint32_t excl_warp(const LevelArgs &a, uint32_t q, uint32_t s, uint32_t nbins, uint32_t lane) {
+    uint32_t ex = 0;
+    for (uint32_t w = lane; w * 32 < nbins; w += 32)
+        ex += popc_masked(__ldg(a.QEM + (uint64_t)q * a.nw + w), __ldg(a.E + (uint64_t)w * a.ld + s), a.joint, w, nbins);
+    return __reduce_add_sync(0xFFFFFFFFu, ex);
+}
+
+__global__ void __launch_bounds__(256) level_walk_kernel(const __grid_constant__ LevelArgs a) {
+    constexpr uint32_t kAhead = 8;  // groups loaded at once
+    const unsigned long long n = *a.count_in;
+    const uint32_t lane = threadIdx.x & 31u;
+    const unsigned long long nwarps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+    const bool in_grp = lane < a.kp;
+    for (unsigned long long i = blockIdx.x * (unsigned long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
+         i += nwarps) {
+        const uint32_t q = a.in.q[i], s = a.in.s[i];
+        u128_t st = a.in.state[i];
+        uint32_t nmb = a.in.nmb[i];
+        const uint32_t *qp = a.QM + (uint64_t)q * a.nb + lane;
+        const uint32_t *fp = a.F + (uint64_t)lane * a.ld + s;
+        bool done = false;
+        for (uint32_t l0 = a.level; l0 <= a.nlev && !done; l0 += kAhead) {
+            uint32_t qv[kAhead], sv[kAhead];
+#pragma unroll
+            for (uint32_t u = 0; u < kAhead; u++) {
+                const uint32_t g = l0 - 1 + u;
+                const bool ok = in_grp && g < a.nlev;
+                qv[u] = ok ? __ldg(qp + (uint64_t)g * a.kp) : 0u;
+                sv[u] = ok ? __ldg(fp + (uint64_t)g * a.kp * a.ld) : 1u;  // never equal when masked
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < kAhead; u++) {
+                const uint32_t l = l0 + u;
+                if (done || l > a.nlev) break;
+                const uint32_t M = __popc(__ballot_sync(0xFFFFFFFFu, qv[u] == sv[u]));
+                nmb += M;
+                st += a.c[l - 1] * M;
+                if (l == a.nlev) {  // the last group: final verdict
+                    uint32_t verdict = 0, flags = 0, ex_tot = 0, nmb_out = nmb;
+                    float est = -1.0f;
+                    if (a.method == kGoph) {
+                        ex_tot = excl_warp(a, q, s, a.nb, lane);
+                        const uint32_t den = a.nb - ex_tot;
+                        if (den == 0) {
+                            flags = OPH_FLAG_UNDEFINED;
+                        } else {
+                            verdict = (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
+                            est = (float)nmb / (float)den;
+                        }
+                    } else {
+                        // HOPH estimator over every group (R21, R22), exact over lam = lcm(1..k')
+                        u128_t num = 0, csum = 0;
+                        nmb_out = 0;
+                        for (uint32_t g = 0; g < a.nlev; g++) {
+                            const uint32_t qg = in_grp ? __ldg(qp + (uint64_t)g * a.kp) : 0u;
+                            const uint32_t sg = in_grp ? __ldg(fp + (uint64_t)g * a.kp * a.ld) : 1u;
+                            const uint32_t m = __popc(__ballot_sync(0xFFFFFFFFu, qg == sg));
+                            const uint32_t ex = group_excl(a, q, s, g);
+                            nmb_out += m;
+                            ex_tot += ex;
+                            const uint32_t d = a.kp - ex;
+                            if (d == 0) continue;
+                            num += a.c[g] * m * (a.lam / d);
+                            csum += a.c[g];
+                        }
+                        if (csum == 0) {
+                            flags = OPH_FLAG_UNDEFINED;
+                        } else {
+                            verdict = num * a.t_den >= (u128_t)a.t_num * a.lam * csum;
+                            est = (float)((double)num / ((double)a.lam * (double)csum));
+                        }
+                    }
+                    if (lane == 0) {
+                        emit_one(a.res, q, s, nmb_out, ex_tot, a.nlev, verdict, flags, est);
+                        if (a.res.hist) atomicAdd(a.res.hist + a.nlev, 1ull);
+                    }
+                    done = true;
+                    break;
+                }
+                const bool acc = st >= a.acc[l - 1];
+                const bool rej = !acc && (i128_t)st <= a.rej[l - 1];
+                if (acc || rej) {
+                    if (a.res.dense || acc) {
+                        const uint32_t ex = excl_warp(a, q, s, l * a.kp, lane);
+                        if (lane == 0) emit_one(a.res, q, s, nmb, ex, l, acc ? 1u : 0u, OPH_FLAG_EARLY, -1.0f);
+                    }
+                    if (lane == 0 && a.res.hist) atomicAdd(a.res.hist + l, 1ull);
+                    done = true;
+                }
+            }
+        }
+    }
+}
+
 cudaError_t launch_level(const LevelArgs &a, cudaStream_t st) {
     // grid-stride over a device-side count: one CTA per SM covers sparse
     // survivor lists cheaply and still fills the chip for dense ones
+    if (a.kp <= 32 && a.level_last == a.nlev) {
+        level_walk_kernel<<<148 * 8, 256, 0, st>>>(a);
+        return cudaGetLastError();
+    }
     level_kernel<<<148 * 2, 256, 0, st>>>(a);
     return cudaGetLastError();
 }
