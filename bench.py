@@ -169,7 +169,7 @@ def make_workload(config: str, rank: int, world: int, scaling: str):
         return gen_gpu.image_like(shard=rank), og.OPH_STRATEGY_BITMAP, 1 << 23, 1 << 28
     if config.startswith("sweep-"):
         # 256 of the 1,024 hub perturbations per step: at Jmax = 0.9 a quarter of all pairs are hits
-        return (gen_gpu.sweep(float(config.split("-")[1]), shard=rank, n_queries=256), og.OPH_STRATEGY_BITMAP,
+        return (gen_gpu.sweep(float(config.split("-")[1]), shard=rank, n_queries=256), og.OPH_STRATEGY_AUTO,
                 1 << 28, 1 << 28)
     if config == "tiny":
         return tiny(), og.OPH_STRATEGY_AUTO, 1 << 20, 1 << 24

@@ -199,8 +199,8 @@ enum { OPH_VARIANT_PAPER = 0, OPH_VARIANT_EMPTY_AWARE = 1 };
  *          with the 1:1 split (L <= 20) when |V| <= 2^23, at most 1023
  *          bins are compared, (GOPH / HOPH) k' is a multiple of 16 and the
  *          collection's row stride ld is a multiple of 8; needs the workspace of oph_workspace_size_for.
- *          AUTO uses it wherever it would otherwise scan BRUTE (and the
- *          workspace is large enough); an explicit BITMAP request outside its
+ *          AUTO uses it, for batches of >= 1024 queries, wherever it would
+ *          otherwise scan BRUTE (and the workspace is large enough); an explicit BITMAP request outside its
  *          domain fails with OPH_EINVAL (OPH_ENOMEM: workspace too small). */
 enum { OPH_STRATEGY_AUTO = 0, OPH_STRATEGY_BRUTE = 1, OPH_STRATEGY_PROBE = 2, OPH_STRATEGY_BITMAP = 3 };
 
