@@ -291,12 +291,15 @@ def test_ragged_and_edges(V, k, kp, hkp, seed):
     assert (so.numpy() == F).all() and (qo.numpy() == QF).all()
     assert (so.empty_numpy() == masks_from_values(F)).all()
     lay = og.flat_layout(V, k, kp)
-    strategies = (og.OPH_STRATEGY_AUTO, og.OPH_STRATEGY_BRUTE)  # AUTO: BITMAP where |V| <= 2^23
+    def strategies(kp_levels):  # BRUTE always; BITMAP where its domain allows (|V| <= 2^23, k' % 16)
+        return (og.OPH_STRATEGY_BRUTE,) + ((og.OPH_STRATEGY_BITMAP,) if V <= (1 << 23) and kp_levels else ())
     for joint in (False, True):
-        for st in strategies:
+        for st in strategies(True):
             kw = dict(t_num=7, t_den=10, eps=1e-4, joint=joint, strategy=st)
             assert_records_equal(gpu_dense("full", qo, so, layout=lay, **kw),
                                  oracle_records("full", QF, F, k=k, kprime=kp, **kw), f"full {V} {st}")
+        for st in strategies(kp % 16 == 0):
+            kw = dict(t_num=7, t_den=10, eps=1e-4, joint=joint, strategy=st)
             assert_records_equal(gpu_dense("goph", qo, so, layout=lay, **kw),
                                  oracle_records("goph", QF, F, k=k, kprime=kp, **kw), f"goph {V} {st}")
     if hier is not None:
@@ -304,8 +307,9 @@ def test_ragged_and_edges(V, k, kp, hkp, seed):
         H = oracle.hoph_sketch(offs, ids, V, glay, hkp, seed)
         QH = oracle.hoph_sketch(qoffs, qids, V, glay, hkp, seed)
         assert (sh.numpy() == H).all() and (sh.empty_numpy() == masks_from_values(H)).all()
+        hier_l = len(oracle.hoph_layout(V, 1, 1, hkp))
         for joint in (False, True):
-            for st in strategies:
+            for st in strategies(hkp % 16 == 0 and 2 <= hier_l <= 20):
                 kw = dict(t_num=7, t_den=10, eps=1e-4, joint=joint, strategy=st)
                 assert_records_equal(gpu_dense("hoph", qh, sh, layout=hier, **kw),
                                      oracle_records("hoph", QH, H, kprime=hkp, L=len(glay), **kw), f"hoph {V} {st}")
