@@ -194,9 +194,11 @@ enum { OPH_VARIANT_PAPER = 0, OPH_VARIANT_EMPTY_AWARE = 1 };
  *          per (set, bin) a warp looks the set's value up and adds the mask to
  *          bit-sliced per-query counters (carry-save adders), so 32 equality
  *          tests cost ~3 lane-instructions; GOPH / HOPH thresholds are applied
- *          to the bit-sliced states level by level (no survivor lists).
+ *          to the bit-sliced states level by level (no survivor lists; HOPH:
+ *          group 1 bit-sliced, the pairs it leaves undecided walked one by
+ *          one over the later groups).
  *          Applies to compare_full, compare_goph (Algorithm 1) and compare_hoph
- *          with the 1:1 split (L <= 20) when |V| <= 2^23, at most 1023
+ *          with the 1:1 split when |V| <= 2^23, at most 1023
  *          bins are compared, (GOPH / HOPH) k' is a multiple of 16 and the
  *          collection's row stride ld is a multiple of 8; needs the workspace of oph_workspace_size_for.
  *          AUTO uses it, for batches of >= 1024 queries, wherever it would

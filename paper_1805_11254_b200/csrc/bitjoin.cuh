@@ -25,7 +25,6 @@
 constexpr uint32_t kBitQB = 1024;     // queries per block: 32 lanes x 32 bits
 constexpr uint32_t kBitMaxBins = 1023;  // bins scanned: counts fit 10 bit slices
 constexpr uint32_t kBitCS = 10;       // count slices: ones, twos, fours, eights, hi[6]
-constexpr uint32_t kBitTS = 24;       // HOPH T_l slices (L <= 20)
 constexpr int kBitWarps = 8;          // warps per CTA = consecutive sets per CTA tile
 constexpr uint32_t kBitMaxStages = 8; // staged CTA tiles in flight (ring of value buffers)
 
@@ -145,17 +144,6 @@ __device__ __forceinline__ uint32_t sliced_get(const uint32_t *c, uint32_t j) {
     return v;
 }
 
-// matched bins of group g for query qg vs set s (query-major prepared values QM, as
-// level_kernel's group_matches)
-__device__ __forceinline__ uint32_t bit_group_matches(const BitArgs &a, uint32_t qg, uint64_t s, uint32_t g) {
-    const uint32_t *qp = a.QM + (uint64_t)qg * a.nb + (uint64_t)g * a.kp;
-    const uint32_t *fp = a.F + (uint64_t)g * a.kp * a.ld + s;
-    uint32_t m = 0;
-#pragma unroll 8
-    for (uint32_t i = 0; i < a.kp; i++) m += (__ldg(fp + (uint64_t)i * a.ld) == __ldg(qp + i));
-    return m;
-}
-
 // excluded bins of a pair among bins [b0, b1) (query-major masks QEM, set masks E)
 __device__ __forceinline__ uint32_t bit_excl(const BitArgs &a, uint32_t qg, uint64_t s, uint32_t b0, uint32_t b1) {
     uint32_t ex = 0;
@@ -170,36 +158,8 @@ __device__ __forceinline__ uint32_t bit_excl(const BitArgs &a, uint32_t qg, uint
     return ex;
 }
 
-// HOPH final estimator of one pair (R21, R22), exact over lam = lcm(1..k'), as in
-// levels_kernel: groups with no usable bin dropped, weights renormalised
-__device__ void bit_hoph_final(const BitArgs &a, uint32_t qg, uint64_t s, uint32_t &nmb, uint32_t &ex_tot,
-                               uint32_t &verdict, uint32_t &flags, float &est) {
-    u128_t num = 0, csum = 0;
-    nmb = ex_tot = 0;
-    for (uint32_t g = 0; g < a.nlev; g++) {
-        const uint32_t m = bit_group_matches(a, qg, s, g);
-        const uint32_t ex = bit_excl(a, qg, s, g * a.kp, (g + 1) * a.kp);
-        nmb += m;
-        ex_tot += ex;
-        const uint32_t d = a.kp - ex;
-        if (d == 0) continue;
-        num += a.c[g] * m * (a.lam / d);
-        csum += a.c[g];
-    }
-    verdict = 0;
-    est = -1.0f;
-    flags = 0;
-    if (csum == 0) {
-        flags = OPH_FLAG_UNDEFINED;
-    } else {
-        verdict = num * a.t_den >= (u128_t)a.t_num * a.lam * csum;
-        est = (float)((double)num / ((double)a.lam * (double)csum));
-    }
-}
-
-// MODE 0: a count over the scanned bins (FULL: one level, the final verdict; GOPH:
-// levels of k' bins with thresholds on M_c).  MODE 1: HOPH 1:1, per-group counts
-// folded into T_l = 2 T_(l-1) + M_l, thresholds on T_l, the HOPH estimator at L.
+// A count over the scanned bins (FULL: one level, the final verdict; GOPH: levels of k'
+// bins with thresholds on M_c).
 // The values of a CTA tile (8 consecutive sets) in the first npre bins: per bin row the
 // tile's 32-B segment is copied with two 16-B cp.async (L1-bypassing) into
 // vbuf[buffer][bin][8]; each issuing lane then arrives on the buffer's mbarrier when its
@@ -218,8 +178,8 @@ __device__ __forceinline__ void bit_tile_load(const BitArgs &a, uint64_t tile, u
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
-// Per-set software pipeline (full OPH, GOPH).
-template <int MODE, int MINB>
+// Per-set software pipeline (full OPH, GOPH), blocks of 1,024 queries.
+template <int MINB>
 __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __grid_constant__ BitArgs a) {
     __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
     __shared__ uint64_t s_full[kBitMaxStages];
@@ -237,8 +197,8 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
     const uint32_t qvalid = qw0 >= a.nqb ? 0u : (a.nqb - qw0 >= 32u ? 0xFFFFFFFFu : ((1u << (a.nqb - qw0)) - 1u));
     const uint32_t max_eq = a.max_eq[lane];
     const uint32_t *rows_lane = a.rows + lane;
-    const uint32_t nlev_scan = MODE == 1 ? a.nlev : (a.method == kGoph ? a.nlev : 1u);
-    const uint32_t bins_per_level = MODE == 1 || a.method == kGoph ? a.kp : a.nscan;
+    const uint32_t nlev_scan = a.method == kGoph ? a.nlev : 1u;
+    const uint32_t bins_per_level = a.method == kGoph ? a.kp : a.nscan;
     // (a.n_sets - s_begin and ld are multiples of 8 sets / 32 B: the tiles' 32-B copies are
     // aligned and in bounds; sets past n_sets are never scored)
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
@@ -284,12 +244,9 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
         uint32_t c[kBitCS];
 #pragma unroll
         for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;
-        uint32_t T[MODE == 1 ? kBitTS : 1];
-#pragma unroll
-        for (int i = 0; i < (MODE == 1 ? (int)kBitTS : 1); i++) T[i] = 0u;
         uint32_t alive = qvalid;
 
-        // The bins are scanned in batches of 16 (GOPH / HOPH levels are whole batches: k' is
+        // The bins are scanned in batches of 16 (GOPH levels are whole batches: k' is
         // a multiple of 16; full OPH's last batch may be partial).  Per batch: lanes 0-15
         // take the set's value of bins b0 + lane (shared memory) and look up its row (r);
         // rows are then broadcast by shuffle and every lane loads its word (x).  Software
@@ -301,7 +258,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
             const uint32_t b = 16u * g + lane;
             uint32_t r = 0u;
             if (lane < 16u && b < a.nscan) {
-                // bins past the staged prefix (GOPH / HOPH levels most sets never reach): direct
+                // bins past the staged prefix (GOPH levels most sets never reach): direct
                 const uint32_t v = b < a.npre ? v_cur[8 * b] : __ldg(a.F + (uint64_t)b * a.ld + s);
                 if (v < s_width[b]) r = __ldg(a.idx + s_start[b] + v);
             }
@@ -329,10 +286,6 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
             rload(rA, xn);               // past the scan: rA = 0, the zero row
             rA = rB;
             rB = ilook(g + 3);
-            if (MODE == 1 && jj == 0) {
-#pragma unroll
-                for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;  // M_l: this group's count
-            }
             csa16(c, xc);
             const bool level_end = bins_per_level == a.nscan ? g + 1 == nbt : jj + 1 == bpl;
             if (!level_end) {
@@ -340,41 +293,13 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
                 return false;
             }
             // ---- decisions at the end of level l
-            const bool last = l == (MODE == 1 ? a.nlev : nlev_scan);
+            const bool last = l == nlev_scan;
             uint32_t acc = 0u, dec = 0u;
-            if (MODE == 1) {
-                if (l == 1) {
-                    // T_1 = M_1: the group count's 6 slices (most pairs decide here)
-#pragma unroll
-                    for (int i = 0; i < 6; i++) T[i] = c[i];
-                } else {
-                    // T_l = 2 T_(l-1) + M_l (bit-sliced shift, then ripple add of the 6-bit M_l)
-#pragma unroll
-                    for (int i = (int)kBitTS - 1; i >= 1; i--) T[i] = T[i - 1];
-                    T[0] = 0u;
-                    uint32_t carry = 0u;
-#pragma unroll
-                    for (int i = 0; i < (int)kBitTS; i++) {
-                        const uint32_t m = i < 6 ? c[i] : 0u;  // M_l <= 32: slices 1 .. 32
-                        const uint32_t t = T[i];
-                        T[i] = t ^ m ^ carry;
-                        carry = (t & m) | ((t ^ m) & carry);
-                    }
-                }
-            }
             if (!last && a.thr_on[l - 1]) {
                 const uint32_t A = a.acc_cnt[l - 1];
                 const int32_t R = a.rej_cnt[l - 1];
-                if (MODE == 1 && l == 1) {  // T_1 < 2^6
-                    acc = sliced_ge<6>(T, A);
-                    dec = acc | (R >= 0 ? ~sliced_ge<6>(T, (uint32_t)R + 1u) : 0u);
-                } else if (MODE == 1) {
-                    acc = sliced_ge<kBitTS>(T, A);
-                    dec = acc | (R >= 0 ? ~sliced_ge<kBitTS>(T, (uint32_t)R + 1u) : 0u);
-                } else {
-                    acc = sliced_ge<kBitCS>(c, A);
-                    dec = acc | (R >= 0 ? ~sliced_ge<kBitCS>(c, (uint32_t)R + 1u) : 0u);
-                }
+                acc = sliced_ge<kBitCS>(c, A);
+                dec = acc | (R >= 0 ? ~sliced_ge<kBitCS>(c, (uint32_t)R + 1u) : 0u);
                 acc &= alive;
                 dec &= alive;
                 hist_add(a.out.hist, l, __popc(dec));
@@ -386,11 +311,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
                     const uint32_t qg = a.qb0 + qw0 + j;
                     uint32_t nmb = 0, ex = 0;
                     if (has) {
-                        if (MODE == 1) {
-                            for (uint32_t gg = 0; gg < l; gg++) nmb += bit_group_matches(a, qg, s, gg);
-                        } else {
-                            nmb = sliced_get<kBitCS>(c, j);
-                        }
+                        nmb = sliced_get<kBitCS>(c, j);
                         ex = bit_excl(a, qg, s, 0, l * a.kp);
                     }
                     emit(a.out, has, qg, s, nmb, ex, l, (acc >> j) & 1u, OPH_FLAG_EARLY, -1.0f);
@@ -404,20 +325,8 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
                 return false;
             }
             // ---- the final verdict of every pair still alive
-            hist_add(a.out.hist, MODE == 1 ? a.nlev : a.level_final, __popc(alive));
-            if (MODE == 1) {
-                uint32_t want = alive;
-                while (__any_sync(0xFFFFFFFFu, want != 0u)) {
-                    const bool has = want != 0u;
-                    const uint32_t j = has ? __ffs(want) - 1 : 0u;
-                    want &= want - 1u;
-                    const uint32_t qg = a.qb0 + qw0 + j;
-                    uint32_t nmb = 0, ex = 0, verdict = 0, flags = 0;
-                    float est = -1.0f;
-                    if (has) bit_hoph_final(a, qg, s, nmb, ex, verdict, flags, est);
-                    emit(a.out, has, qg, s, nmb, ex, a.nlev, verdict, flags, est);
-                }
-            } else {
+            hist_add(a.out.hist, a.level_final, __popc(alive));
+            {
                 // full-OPH verdict (Eq. 6): den = k - N_excl >= k - (max_q |Eq| + |Es|) (EitherEmpty)
                 // or k - min(max_q |Eq|, |Es|) (JointEmpty), so a pair can only be Similar if
                 // N_mb >= ceil(t_num den_min / t_den): the candidates, verified exactly
@@ -663,33 +572,87 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_q_kernel(const 
     }
 }
 
-// The same scan with one software pipeline across the warp's sets (items = the staged
-// batches of its sets, the staged tile buffers released by the lookup stage): pays when
-// a set's staged prefix is short (HOPH: one group of 2 batches), where the per-set
-// pipeline fill of bit_scan_kernel dominated (image-like HOPH 8.2 -> 5.4 ms); for full OPH
-// (32 batches per set) its bookkeeping cost more than the fills (38.2 -> 45.6 ms).
-template <int MODE, int MINB>
+// HOPH (1:1): group 1 by the bitmap join in blocks of 2,048 queries (two words per lane) with
+// one software pipeline across the warp's sets (items = the two batches of group 1 of its
+// sets; the staged tile buffers are released by the lookup stage) -- a set's bitmap work is
+// only 2 batches, so a per-set pipeline fill would dominate; then, for the few pairs group 1
+// leaves undecided, the later groups one pair at a time by the whole warp (lane = bin:
+// ballot counts, exact 128-bit state S_l = sum c_j M_j against the planner's thresholds, the
+// HOPH estimator after group L), as level_walk_kernel.
+__device__ __forceinline__ void bit_walk_pair(const BitArgs &a, uint32_t qg, uint64_t s, uint32_t m1, uint32_t lane) {
+    const bool in_grp = lane < a.kp;
+    const uint32_t *qp = a.QM + (uint64_t)qg * a.nb + lane;
+    const uint32_t *fp = a.F + (uint64_t)lane * a.ld + s;
+    u128_t st = a.c[0] * m1;
+    uint32_t nmb = m1;
+    for (uint32_t l = 2; l <= a.nlev; l++) {
+        const uint32_t g = l - 1;
+        const uint32_t qv = in_grp ? __ldg(qp + (uint64_t)g * a.kp) : 0u;
+        const uint32_t sv = in_grp ? __ldg(fp + (uint64_t)g * a.kp * a.ld) : 1u;
+        const uint32_t M = __popc(__ballot_sync(0xFFFFFFFFu, qv == sv));
+        nmb += M;
+        st += a.c[g] * M;
+        if (l == a.nlev) {
+            uint32_t nmb_out = 0, ex_tot = 0, verdict = 0, flags = 0;
+            float est = -1.0f;
+            u128_t num = 0, csum = 0;
+            for (uint32_t gg = 0; gg < a.nlev; gg++) {
+                const uint32_t q2 = in_grp ? __ldg(qp + (uint64_t)gg * a.kp) : 0u;
+                const uint32_t s2 = in_grp ? __ldg(fp + (uint64_t)gg * a.kp * a.ld) : 1u;
+                const uint32_t m = __popc(__ballot_sync(0xFFFFFFFFu, q2 == s2));
+                const uint32_t ex = bit_excl(a, qg, s, gg * a.kp, (gg + 1) * a.kp);
+                nmb_out += m;
+                ex_tot += ex;
+                const uint32_t d = a.kp - ex;
+                if (d == 0) continue;
+                num += a.c[gg] * m * (a.lam / d);
+                csum += a.c[gg];
+            }
+            if (csum == 0) {
+                flags = OPH_FLAG_UNDEFINED;
+            } else {
+                verdict = num * a.t_den >= (u128_t)a.t_num * a.lam * csum;
+                est = (float)((double)num / ((double)a.lam * (double)csum));
+            }
+            if (lane == 0) {
+                emit_one(a.out, qg, (uint32_t)s, nmb_out, ex_tot, a.nlev, verdict, flags, est);
+                if (a.out.hist) atomicAdd(a.out.hist + a.nlev, 1ull);
+            }
+            return;
+        }
+        const bool acc = st >= a.acc128[l - 1];
+        const bool rej = !acc && (i128_t)st <= a.rej128[l - 1];
+        if (acc || rej) {
+            if (a.out.dense || acc) {
+                const uint32_t ex = bit_excl(a, qg, s, 0, l * a.kp);
+                if (lane == 0) emit_one(a.out, qg, (uint32_t)s, nmb, ex, l, acc ? 1u : 0u, OPH_FLAG_EARLY, -1.0f);
+            }
+            if (lane == 0 && a.out.hist) atomicAdd(a.out.hist + l, 1ull);
+            return;
+        }
+    }
+}
+
+template <int QW, int MINB>
 __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_x_kernel(const __grid_constant__ BitArgs a) {
     __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
     __shared__ uint64_t s_full[kBitMaxStages];
     __shared__ uint32_t s_done[kBitMaxStages];
-    extern __shared__ __align__(128) uint32_t s_vals[];  // [2][npre][8]
-    for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
+    extern __shared__ __align__(128) uint32_t s_vals[];  // [nstage][npre][8]
+    for (uint32_t b = threadIdx.x; b < a.npre; b += blockDim.x) {
         uint32_t st, wd;
         bit_bin_range(a, b, st, wd);
         s_start[b] = st;
         s_width[b] = wd;
     }
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    // this lane's word of the block: queries qb0 + 32 lane + j
-    const uint32_t qw0 = 32u * lane;
-    const uint32_t qvalid = qw0 >= a.nqb ? 0u : (a.nqb - qw0 >= 32u ? 0xFFFFFFFFu : ((1u << (a.nqb - qw0)) - 1u));
-    const uint32_t max_eq = a.max_eq[lane];
-    const uint32_t *rows_lane = a.rows + lane;
-    const uint32_t nlev_scan = MODE == 1 ? a.nlev : (a.method == kGoph ? a.nlev : 1u);
-    const uint32_t bins_per_level = MODE == 1 || a.method == kGoph ? a.kp : a.nscan;
-    // (a.n_sets - s_begin and ld are multiples of 8 sets / 32 B: the tiles' 32-B copies are
-    // aligned and in bounds; sets past n_sets are never scored)
+    uint32_t qw0[QW], qvalid[QW];
+#pragma unroll
+    for (int w = 0; w < QW; w++) {
+        qw0[w] = 32u * (QW * lane + w);
+        qvalid[w] = qw0[w] >= a.nqb ? 0u : (a.nqb - qw0[w] >= 32u ? 0xFFFFFFFFu : ((1u << (a.nqb - qw0[w])) - 1u));
+    }
+    const uint32_t *rows_lane = a.rows + QW * lane;
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
     const uint32_t vstride = a.npre * 8u;  // words per buffer
     if (threadIdx.x == 0) {
@@ -706,21 +669,11 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_x_kernel(const 
             if (t < ntiles) bit_tile_load(a, t, s_vals + i * vstride, &s_full[i], lane);
         }
     }
-
-    const uint32_t nbt = (a.nscan + 15u) / 16u;       // batches of 16 bins of a whole set
-    const uint32_t nbs = (a.npre + 15u) / 16u;        // ... of its staged prefix
-    const uint32_t bpl = bins_per_level / 16u;        // batches per level (GOPH / HOPH)
-    // this CTA's tiles: blockIdx.x + i gridDim.x, i < n_it; every warp walks all of them
+    const uint32_t nbs = (a.npre + 15u) / 16u;  // batches of group 1 (the staged prefix)
     const uint64_t n_it = (uint64_t)blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const uint64_t nitems = n_it * nbs;
-    auto set_of = [&](uint64_t ti) -> uint64_t {
-        return a.s_begin + ((uint64_t)blockIdx.x + ti * gridDim.x) * kBitWarps + warp;
-    };
 
-    // ---- stage A: the row indices of the next item (tile ti, staged batch bj): lanes 0-15 take
-    // the set's values of bins 16 bj + lane from the staged tile and look them up in idx.  After
-    // its last batch the tile's buffer is released; the last warp to release refills it with
-    // the tile nstage iterations later.
+    // ---- stage A: row indices of the next item; releases a tile after its last batch
     uint64_t tiA = 0;
     uint32_t bjA = 0, slotA = 0, phaseA = 0;
     auto stageA = [&]() -> uint32_t {
@@ -728,10 +681,9 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_x_kernel(const 
         if (tiA >= n_it) return r;
         if (bjA == 0) mbar_wait(&s_full[slotA], phaseA);
         const uint32_t b = 16u * bjA + lane;
-        if (lane < 16u && b < a.npre) {
-            const uint32_t v = s_vals[slotA * vstride + 8u * b + warp];
-            if (v < s_width[b]) r = __ldg(a.idx + s_start[b] + v);
-        }
+        const uint32_t bc = min(b, a.npre - 1u);
+        const uint32_t v = s_vals[slotA * vstride + 8u * bc + warp];
+        if (lane < 16u && b < a.npre && v < s_width[bc]) r = __ldg(a.idx + s_start[bc] + v);
         if (++bjA == nbs) {
             __syncwarp();
             uint32_t last = 0;
@@ -752,195 +704,81 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_x_kernel(const 
         }
         return r;
     };
-    auto rload = [&](uint32_t r, uint32_t (&x)[16]) {
+    auto rload = [&](uint32_t r, uint32_t (&x)[QW][16]) {
 #pragma unroll
         for (int u = 0; u < 16; u++) {
             const uint32_t ru = __shfl_sync(0xFFFFFFFFu, r, u);
-            x[u] = __ldg(rows_lane + (uint64_t)ru * 32);  // ru = 0 (no row, or past the scan): zero row
+            if (QW == 2) {
+                const uint2 y = __ldg(reinterpret_cast<const uint2 *>(rows_lane + (uint64_t)ru * 64));
+                x[0][u] = y.x;
+                x[QW - 1][u] = y.y;
+            } else {
+                x[0][u] = __ldg(rows_lane + (uint64_t)ru * 32);
+            }
         }
     };
 
-    // ---- stage C state: the set being counted
-    uint64_t tiC = 0, s = 0;
-    uint32_t bjC = 0, l = 1, jj = 0;
-    bool done = true;
-    uint32_t c[kBitCS];
-    uint32_t T[MODE == 1 ? kBitTS : 1];
-    uint32_t alive = 0u;
-
-    // decisions at the end of level l; returns true when the set is done
-    auto level_end = [&]() -> bool {
-        const bool last = l == (MODE == 1 ? a.nlev : nlev_scan);
-        uint32_t acc = 0u, dec = 0u;
-        if (MODE == 1) {
-            if (l == 1) {
-                // T_1 = M_1: the group count's 6 slices (most pairs decide here)
+    // ---- stage C: count item (tiC, bjC); after group 1, decide and walk the undecided pairs
+    uint64_t tiC = 0;
+    uint32_t bjC = 0;
+    uint32_t c[QW][kBitCS];
+    auto stageC = [&](const uint32_t (&xc)[QW][16]) {
+        if (bjC == 0) {
 #pragma unroll
-                for (int i = 0; i < 6; i++) T[i] = c[i];
-            } else {
-                // T_l = 2 T_(l-1) + M_l (bit-sliced shift, then ripple add of the 6-bit M_l)
+            for (int w = 0; w < QW; w++)
 #pragma unroll
-                for (int i = (int)kBitTS - 1; i >= 1; i--) T[i] = T[i - 1];
-                T[0] = 0u;
-                uint32_t carry = 0u;
-#pragma unroll
-                for (int i = 0; i < (int)kBitTS; i++) {
-                    const uint32_t m = i < 6 ? c[i] : 0u;  // M_l <= 32: slices 1 .. 32
-                    const uint32_t t = T[i];
-                    T[i] = t ^ m ^ carry;
-                    carry = (t & m) | ((t ^ m) & carry);
-                }
-            }
+                for (int i = 0; i < (int)kBitCS; i++) c[w][i] = 0u;
         }
-        if (!last && a.thr_on[l - 1]) {
-            const uint32_t A = a.acc_cnt[l - 1];
-            const int32_t R = a.rej_cnt[l - 1];
-            if (MODE == 1 && l == 1) {  // T_1 < 2^6
-                acc = sliced_ge<6>(T, A);
-                dec = acc | (R >= 0 ? ~sliced_ge<6>(T, (uint32_t)R + 1u) : 0u);
-            } else if (MODE == 1) {
-                acc = sliced_ge<kBitTS>(T, A);
-                dec = acc | (R >= 0 ? ~sliced_ge<kBitTS>(T, (uint32_t)R + 1u) : 0u);
-            } else {
-                acc = sliced_ge<kBitCS>(c, A);
-                dec = acc | (R >= 0 ? ~sliced_ge<kBitCS>(c, (uint32_t)R + 1u) : 0u);
-            }
-            acc &= alive;
-            dec &= alive;
-            hist_add(a.out.hist, l, __popc(dec));
+#pragma unroll
+        for (int w = 0; w < QW; w++) csa16(c[w], xc[w]);
+        if (++bjC < nbs) return;
+        bjC = 0;
+        const uint64_t s = a.s_begin + ((uint64_t)blockIdx.x + tiC * gridDim.x) * kBitWarps + warp;
+        tiC++;
+        if (s >= a.n_sets) return;  // warp-uniform: a tail tile's missing set
+        // ---- group 1 decided on T_1 = M_1 (6 slices; S_1 = c_1 M_1)
+        const uint32_t A = a.acc_cnt[0];
+        const int32_t R = a.rej_cnt[0];
+#pragma unroll
+        for (int w = 0; w < QW; w++) {
+            uint32_t acc = sliced_ge<6>(c[w], A) & qvalid[w];
+            uint32_t dec = (acc | (R >= 0 ? ~sliced_ge<6>(c[w], (uint32_t)R + 1u) : 0u)) & qvalid[w];
+            hist_add(a.out.hist, 1, __popc(dec));
             uint32_t want = a.out.dense ? dec : acc;
             while (__any_sync(0xFFFFFFFFu, want != 0u)) {
                 const bool has = want != 0u;
                 const uint32_t j = has ? __ffs(want) - 1 : 0u;
                 want &= want - 1u;
-                const uint32_t qg = a.qb0 + qw0 + j;
+                const uint32_t qg = a.qb0 + qw0[w] + j;
                 uint32_t nmb = 0, ex = 0;
                 if (has) {
-                    if (MODE == 1) {
-                        for (uint32_t gg = 0; gg < l; gg++) nmb += bit_group_matches(a, qg, s, gg);
-                    } else {
-                        nmb = sliced_get<kBitCS>(c, j);
-                    }
-                    ex = bit_excl(a, qg, s, 0, l * a.kp);
+                    nmb = sliced_get<6>(c[w], j);
+                    ex = bit_excl(a, qg, s, 0, a.kp);
                 }
-                emit(a.out, has, qg, s, nmb, ex, l, (acc >> j) & 1u, OPH_FLAG_EARLY, -1.0f);
+                emit(a.out, has, qg, s, nmb, ex, 1, (acc >> j) & 1u, OPH_FLAG_EARLY, -1.0f);
             }
-            alive &= ~dec;
-        }
-        if (!last) return !__any_sync(0xFFFFFFFFu, alive != 0u);  // every pair of this set decided?
-        // ---- the final verdict of every pair still alive
-        hist_add(a.out.hist, MODE == 1 ? a.nlev : a.level_final, __popc(alive));
-        if (MODE == 1) {
-            uint32_t want = alive;
-            while (__any_sync(0xFFFFFFFFu, want != 0u)) {
-                const bool has = want != 0u;
-                const uint32_t j = has ? __ffs(want) - 1 : 0u;
-                want &= want - 1u;
-                const uint32_t qg = a.qb0 + qw0 + j;
-                uint32_t nmb = 0, ex = 0, verdict = 0, flags = 0;
-                float est = -1.0f;
-                if (has) bit_hoph_final(a, qg, s, nmb, ex, verdict, flags, est);
-                emit(a.out, has, qg, s, nmb, ex, a.nlev, verdict, flags, est);
+            // the undecided pairs: the later groups pair by pair, the whole warp per pair
+            uint32_t alive = qvalid[w] & ~dec;
+            while (__any_sync(0xFFFFFFFFu, alive != 0u)) {
+                const uint32_t src = __ffs(__ballot_sync(0xFFFFFFFFu, alive != 0u)) - 1;
+                const uint32_t mine = alive != 0u ? __ffs(alive) - 1 : 0u;
+                const uint32_t j = __shfl_sync(0xFFFFFFFFu, mine, src);
+                const uint32_t m1 = __shfl_sync(0xFFFFFFFFu, sliced_get<6>(c[w], mine), src);
+                if (lane == src) alive &= alive - 1u;
+                bit_walk_pair(a, a.qb0 + 32u * (QW * src + w) + j, s, m1, lane);
             }
-        } else {
-            // full-OPH verdict (Eq. 6): den = k - N_excl >= k - (max_q |Eq| + |Es|) (EitherEmpty)
-            // or k - min(max_q |Eq|, |Es|) (JointEmpty), so a pair can only be Similar if
-            // N_mb >= ceil(t_num den_min / t_den): the candidates, verified exactly
-            const uint32_t es_w = lane < a.nw ? __ldg(a.E + (uint64_t)lane * a.ld + s) : 0u;
-            const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, a.nbins_total));
-            const uint32_t k = a.nbins_total;
-            uint32_t den_min = a.joint ? k - min(max_eq, es) : k - min(k, max_eq + es);
-            const uint32_t theta =
-                a.out.dense ? 0u : (uint32_t)(((uint64_t)a.t_num * den_min + a.t_den - 1) / a.t_den);
-            uint32_t want = sliced_ge<kBitCS>(c, theta) & alive;
-            while (__any_sync(0xFFFFFFFFu, want != 0u)) {
-                const bool has = want != 0u;
-                const uint32_t j = has ? __ffs(want) - 1 : 0u;
-                want &= want - 1u;
-                const uint32_t qg = a.qb0 + qw0 + j;
-                uint32_t ex = 0;
-                for (uint32_t w = 0; w < a.nw; w++) {
-                    const uint32_t sw = __shfl_sync(0xFFFFFFFFu, es_w, w);
-                    if (has) ex += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + w), sw, a.joint, w, k);
-                }
-                const uint32_t nmb = sliced_get<kBitCS>(c, j);
-                const uint32_t den = k - ex;
-                const bool undef = den == 0;
-                const uint32_t verdict = !undef && (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
-                emit(a.out, has, qg, s, nmb, ex, a.level_final, verdict, undef ? OPH_FLAG_UNDEFINED : 0u,
-                     undef ? -1.0f : (float)nmb / (float)den);
-            }
-        }
-        alive = 0u;
-        return true;
-    };
-    // one counted batch of the current set (MODE 1 resets the group count at a level start)
-    auto count_batch = [&](const uint32_t (&xc)[16]) {
-        if (MODE == 1 && jj == 0) {
-#pragma unroll
-            for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;  // M_l: this group's count
-        }
-        csa16(c, xc);
-        const bool lend = bins_per_level == a.nscan ? false : jj + 1 == bpl;
-        if (!lend) {
-            jj++;
-            return;
-        }
-        if (level_end()) {
-            done = true;
-            return;
-        }
-        l++;
-        jj = 0;
-    };
-    // past the staged prefix (GOPH / HOPH levels most sets never reach): the rest of the set,
-    // batch by batch with direct loads of its values, no pipeline
-    auto finish_set = [&]() {
-        for (uint32_t g = nbs; g < nbt && !done; g++) {
-            uint32_t r = 0u;
-            const uint32_t b = 16u * g + lane;
-            if (lane < 16u && b < a.nscan) {
-                const uint32_t v = __ldg(a.F + (uint64_t)b * a.ld + s);
-                if (v < s_width[b]) r = __ldg(a.idx + s_start[b] + v);
-            }
-            uint32_t xs[16];
-            rload(r, xs);
-            count_batch(xs);
-        }
-    };
-    // ---- stage C: count item (tiC, bjC)
-    auto stageC = [&](const uint32_t (&xc)[16]) {
-        if (bjC == 0) {  // a new set
-            s = set_of(tiC);
-            done = s >= a.n_sets;
-            alive = done ? 0u : qvalid;
-            l = 1;
-            jj = 0;
-#pragma unroll
-            for (int i = 0; i < (int)kBitCS; i++) c[i] = 0u;
-#pragma unroll
-            for (int i = 0; i < (MODE == 1 ? (int)kBitTS : 1); i++) T[i] = 0u;
-        }
-        if (!done) count_batch(xc);
-        if (++bjC == nbs) {  // the staged prefix is counted
-            if (!done && nbs == nbt && bins_per_level == a.nscan) done = level_end();  // full OPH
-            if (!done) finish_set();
-            bjC = 0;
-            tiC++;
         }
     };
 
-    // ---- the pipeline over this warp's items: rows of item g+1 and the row indices of items
-    // g+2, g+3 are in flight while item g is counted; the two row buffers alternate
     if (nitems) {
-        uint32_t x[16], xb[16], rA, rB;
+        uint32_t x[QW][16], xb[QW][16], rA, rB;
         {
             const uint32_t r0 = stageA();
             rA = stageA();
             rB = stageA();
             rload(r0, x);
         }
-        auto step = [&](uint64_t g, uint32_t (&xc)[16], uint32_t (&xn)[16]) {
+        auto step = [&](uint64_t g, uint32_t (&xc)[QW][16], uint32_t (&xn)[QW][16]) {
             if (g + 1 < nitems) rload(rA, xn);
             rA = rB;
             rB = stageA();
@@ -964,7 +802,8 @@ cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     bit_claim_kernel<<<g, 256, 0, st>>>(a);
     bit_fill_kernel<<<g, 256, 0, st>>>(a);
     bit_maxeq_kernel<<<a.qw, 1024, 0, st>>>(a);
-    // the scan: 8 consecutive sets per CTA tile, grid-stride; 3 CTAs per SM (HOPH: 2, its T slices need 128 registers)
+    // the scan: 8 consecutive sets per CTA tile, grid-stride; 3 CTAs per SM at 1,024-query
+    // rows, 2 at 2,048 (two words of counters per lane)
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
     // (OPHGPU_BIT_CTAS=2: the full-OPH / GOPH scan at 2 CTAs per SM without register limit, A/B)
     static const bool two = getenv("OPHGPU_BIT_CTAS") && atoi(getenv("OPHGPU_BIT_CTAS")) == 2;
@@ -973,11 +812,11 @@ cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     const int ctas = a.mode_hoph || two || (a.qw == 2 && !three) ? 2 : 3;
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * ctas * 8);
     const size_t smem = (size_t)a.nstage * a.npre * kBitWarps * 4;
-    auto kern = a.mode_hoph ? bit_scan_x_kernel<1, 2>
+    auto kern = a.mode_hoph ? bit_scan_x_kernel<2, 2>
                             : (a.qw == 2 ? (a.npre == a.nscan ? (three ? bit_scan_q_kernel<2, 3, true>
                                                                        : bit_scan_q_kernel<2, 2, true>)
                                                               : bit_scan_q_kernel<2, 2, false>)
-                                         : (two ? bit_scan_kernel<0, 2> : bit_scan_kernel<0, 3>));
+                                         : (two ? bit_scan_kernel<2> : bit_scan_kernel<3>));
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return e;
     kern<<<grid, 32 * kBitWarps, smem, st>>>(a);

@@ -226,6 +226,8 @@ struct BitArgs {
     uint32_t thr_on[kMaxGroups];    // level l (index l-1) has a threshold
     uint32_t acc_cnt[kMaxGroups];   // Similar iff state >= acc_cnt (GOPH: M_c; HOPH: T_l)
     int32_t rej_cnt[kMaxGroups];    // NotSimilar iff state <= rej_cnt (-1: never)
+    u128_t acc128[kMaxGroups];      // HOPH: the planner's thresholds on S_l (the per-pair walk)
+    i128_t rej128[kMaxGroups];
     u128_t c[kMaxGroups];           // HOPH weights (final estimator)
     u128_t lam;                     // lcm(1..kp)
     uint32_t *idx;                  // [vpos] position -> row (0: the zero row)

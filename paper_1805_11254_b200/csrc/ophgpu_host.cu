@@ -424,9 +424,9 @@ uint64_t cap_from_ws(size_t ws_bytes, size_t fixed) {
 }
 
 // ---------------------------------------------------------------- the BITMAP driver
-// Query prep, then per block of 1024 queries: the value -> row table (bit_claim / bit_fill)
-// and one scan of the collection deciding every level (bit_scan_kernel).  No host
-// synchronisation, no survivor lists.
+// Query prep, then per block of 2,048 (or 1,024) queries: the value -> row table (bit_claim /
+// bit_fill) and one scan of the collection deciding every level (bit_scan_q_kernel /
+// bit_scan_kernel; HOPH: bit_scan_x_kernel).  No host synchronisation, no survivor lists.
 oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketches *Sv, uint32_t set_id_base,
                       uint32_t nb, uint32_t nw, uint32_t nlev, uint32_t kp, const Plan &plan, const oph_params *p,
                       oph_results *res, void *d_ws, size_t fixed, cudaStream_t stream) {
@@ -467,11 +467,12 @@ oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketche
     ba.QEM = w.QEM;
     ba.nb = nb;
     ba.nw = nw;
-    ba.nscan = nb;
-    // bins staged per CTA tile: all for full OPH and GOPH (GOPH staging only up to level l0 + 1
-    // measured 13.5 vs 12.9 ms on image-like: the branch-free all-staged lookup wins); HOPH:
-    // group 1 (the rest is read directly when reached)
-    ba.npre = method == OPH_METHOD_HOPH ? std::min<uint32_t>(nb, kp) : nb;
+    // bins in the value -> row table: all for full OPH and GOPH, group 1 for HOPH (its later
+    // groups are compared pair by pair from QM)
+    ba.nscan = method == OPH_METHOD_HOPH ? std::min<uint32_t>(nb, kp) : nb;
+    // bins staged per CTA tile: all (GOPH staging only up to level l0 + 1 measured 13.5 vs
+    // 12.9 ms on image-like: the branch-free all-staged lookup wins)
+    ba.npre = ba.nscan;
     // short staged tiles (HOPH: one group) need more of them in flight: ~32 KB of staged values
     ba.nstage = std::max<uint32_t>(2, std::min<uint32_t>(8, 32768 / (ba.npre * 32)));
     ba.kp = kp;
@@ -502,8 +503,9 @@ oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketche
         ba.bins_per_range = nb;
         ba.ranges[0] = make_range(0, V, nb);
     }
-    // level thresholds on the bit-sliced states: GOPH M_c as compiled; HOPH S_l = 2^(L-1-l) T_l,
-    // so S_l >= A <=> T_l >= ceil(A / 2^(L-1-l)) and S_l <= R <=> T_l <= floor(R / 2^(L-1-l))
+    // level thresholds on the bit-sliced states: GOPH M_c as compiled; HOPH group 1:
+    // S_1 = c_1 M_1 = 2^(L-2) M_1, so S_1 >= A <=> M_1 >= ceil(A / 2^(L-2)) and S_1 <= R <=>
+    // M_1 <= floor(R / 2^(L-2)); acc128 / rej128: the exact thresholds of the per-pair walk
     for (uint32_t l = 1; method != OPH_METHOD_FULL && l < nlev; l++) {
         const LevelThr &T = plan.thr[l - 1];
         const uint32_t sh = method == OPH_METHOD_HOPH ? nlev - 1 - l : 0;
@@ -512,11 +514,13 @@ oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketche
         ba.acc_cnt[l - 1] = A >= (u128)UINT32_MAX ? UINT32_MAX : (uint32_t)A;
         ba.rej_cnt[l - 1] = T.rej < 0 ? -1 : (int32_t)std::min<i128>(T.rej / (i128)div, (i128)INT32_MAX);
         ba.thr_on[l - 1] = ba.acc_cnt[l - 1] != UINT32_MAX || ba.rej_cnt[l - 1] >= 0;
+        ba.acc128[l - 1] = T.acc;
+        ba.rej128[l - 1] = T.rej;
     }
-    // blocks of 2,048 queries (two words per lane) for full OPH / GOPH, 1,024 for HOPH (its
-    // kernel carries the T_l slices); OPHGPU_BIT_QW=1 forces 1,024 (A/B)
+    // blocks of 2,048 queries (two words per lane); OPHGPU_BIT_QW=1 forces 1,024 for full OPH /
+    // GOPH (A/B)
     static const bool qw1 = getenv("OPHGPU_BIT_QW") && atoi(getenv("OPHGPU_BIT_QW")) == 1;
-    ba.qw = (method == OPH_METHOD_HOPH || qw1) ? 1 : 2;
+    ba.qw = qw1 && method != OPH_METHOD_HOPH ? 1 : 2;
     const uint64_t qb = 1024ull * ba.qw;
     for (uint64_t q0 = 0; q0 < n_q; q0 += qb) {
         ba.qb0 = (uint32_t)q0;
@@ -567,13 +571,14 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
 
     const size_t fixed = ws_fixed_bytes(n_q, n_s, nb);
 
-    // BITMAP (bitjoin.cuh): full OPH, GOPH (Algorithm 1) and HOPH with power-of-two weights
-    // (the 1:1 split: T_l = S_l / 2^(L-1-l) in <= 24 bit slices), |V| <= 2^23, <= 1023 bins
+    // BITMAP (bitjoin.cuh): full OPH, GOPH (Algorithm 1) and HOPH with the 1:1 split (group 1
+    // bit-sliced, S_1 = c_1 M_1; the later groups per pair on exact 128-bit S_l), |V| <= 2^23,
+    // <= 1023 bins
     {
         // (GOPH / HOPH levels must be whole batches of 16 bins: k' % 16 == 0)
         const bool dom = !mw && !ea && bitmap_sizes_ok(Qv->vocab_size, nb) && Sv->ld % 8 == 0 &&
                          (method == OPH_METHOD_FULL || kp % 16 == 0) &&
-                         (method != OPH_METHOD_HOPH || (a == 1 && b == 1 && nlev >= 2 && nlev <= 20 && plan.lam));
+                         (method != OPH_METHOD_HOPH || (a == 1 && b == 1 && nlev >= 2 && plan.lam));
         const bool fits = ws_bytes >= fixed + bitmap_region_bytes(Qv->vocab_size, nb);
         bool use = false;
         if (p->strategy == OPH_STRATEGY_BITMAP) {

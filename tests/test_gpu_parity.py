@@ -840,8 +840,8 @@ def test_survivor_lists_many_late_pairs(monkeypatch):
 @pytest.fixture(scope="module")
 def image_small():
     """An image-like collection (Zipf words over 2^20, k = 512, k' = 32, HOPH L = 15) with
-    2,100 queries: two BITMAP query blocks of 2,048 (full OPH, GOPH) or three of 1,024 (HOPH),
-    the last one ragged."""
+    2,100 queries: two BITMAP query blocks of 2,048, the last one ragged (HOPH: group 1
+    bit-sliced, the undecided pairs walked per pair over both query words of a lane)."""
     from workloads import gen
     w = gen.image_like(n_sets=20_000, n_queries=2100)
     p = w.params
