@@ -622,17 +622,17 @@ def run_ours(args):
     models = {}
     l2_src = "none measured"
 
-    # BITMAP join (K7): per (set, bin, block of 1024 queries) one 4-B entry of the value -> row
-    # table and one 128-B row of query bits, gathered from the L2-resident block tables; peak =
-    # the measured random 128-B row-gather rate from a 16-MB table (scripts/ubench.cu)
+    # BITMAP join (K7): per (set, bin, block of 2,048 queries) one 4-B entry of the value -> row
+    # table and one 256-B row of query bits, gathered from the L2-resident block tables; peak =
+    # the measured random 256-B row-gather rate from a 16-MB table (scripts/ubench.cu)
     def l2_peak_for(row_bytes):
         key = "gather_128B_rows_GBps" if row_bytes == 128 else "gather_256B_rows_GBps"
         return (ub or {}).get(key, {}).get(str(16 << 20))
 
     def model_for(kernel: str, phase: str):
-        if kernel.startswith("bit_scan"):
-            # full OPH / GOPH: blocks of 2,048 queries (256-B rows, bit_scan_q_kernel); HOPH 1,024
-            qwords = 2 if kernel.startswith("bit_scan_q_kernel") else 1
+        if kernel.startswith("bit_scan") or kernel.startswith("bit_full"):
+            # blocks of 2,048 queries (256-B rows; bit_scan_kernel, the OPHGPU_BIT_QW=1 A/B: 1,024)
+            qwords = 1 if kernel.startswith("bit_scan_kernel") else 2
             row = 128 * qwords
             m = phase.split("_")[1]
             bins = (bins_compared.get(m, Q * N * k) / Q) if m != "full" else N * k  # (set, bin) pairs scanned

@@ -791,6 +791,190 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_x_kernel(const 
     }
 }
 
+// Full OPH (Eq. 6) with 2,048-query rows and one software pipeline across the warp's sets
+// (items = the k/16 batches of each set, k % 16 == 0), four stages per item:
+//   A  look the set's 16 values up (value -> row index), 3 items ahead
+//   B  park the 16 row indices in the warp's shared ring, 2 items ahead (the lookups have
+//      landed by then: no stall on them)
+//   C  read the ring back (4 broadcast 16-B loads instead of 16 shuffles) and issue the 16
+//      row loads (one 8-B load per lane), 1 item ahead
+//   D  count (csa16 on both words); at a set's last batch, the verdicts
+// The termination histogram (every pair at level_final) is counted in shared memory and
+// added once per CTA (no per-set global atomics); a set's empty-bin mask word is fetched at
+// its first batch and used at its last.
+template <int MINB>
+__global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_full_kernel(const __grid_constant__ BitArgs a) {
+    __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
+    __shared__ uint64_t s_full[kBitMaxStages];
+    __shared__ uint32_t s_done[kBitMaxStages];
+    __shared__ __align__(16) uint32_t s_ring[kBitWarps][4][16];
+    __shared__ unsigned long long s_hist;
+    extern __shared__ __align__(128) uint32_t s_vals[];  // [nstage][npre][8]
+    for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
+        uint32_t st, wd;
+        bit_bin_range(a, b, st, wd);
+        s_start[b] = st;
+        s_width[b] = wd;
+    }
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t qw0[2], qvalid[2], max_eq[2];
+#pragma unroll
+    for (int w = 0; w < 2; w++) {
+        qw0[w] = 32u * (2 * lane + w);
+        qvalid[w] = qw0[w] >= a.nqb ? 0u : (a.nqb - qw0[w] >= 32u ? 0xFFFFFFFFu : ((1u << (a.nqb - qw0[w])) - 1u));
+        max_eq[w] = a.max_eq[2 * lane + w];
+    }
+    const uint2 *rows_lane = reinterpret_cast<const uint2 *>(a.rows) + lane;
+    const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
+    const uint32_t vstride = a.npre * 8u;
+    if (threadIdx.x == 0) {
+        for (uint32_t i = 0; i < a.nstage; i++) {
+            mbar_init(&s_full[i], 32);
+            s_done[i] = 0u;
+        }
+        s_hist = 0ull;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) {
+        for (uint32_t i = 0; i < a.nstage; i++) {
+            const uint64_t t = blockIdx.x + (uint64_t)i * gridDim.x;
+            if (t < ntiles) bit_tile_load(a, t, s_vals + i * vstride, &s_full[i], lane);
+        }
+    }
+    const uint32_t nbs = a.nscan / 16u;
+    // (per-CTA tile and item counts fit 32 bits: ntiles / grid tiles of k / 16 items)
+    const uint32_t n_it = (uint64_t)blockIdx.x < ntiles ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
+    const uint32_t nitems = n_it * nbs;
+    uint32_t *ring = &s_ring[warp][0][0];
+
+    // ---- stage A: the row index of this lane's bin (lanes 16-31 repeat lanes 0-15's lookups:
+    // same addresses, no extra traffic, no divergence); releases a tile after its last batch
+    uint32_t tiA = 0, bjA = 0, slotA = 0, phaseA = 0;
+    auto stageA = [&]() -> uint32_t {
+        if (tiA >= n_it) return 0u;
+        if (bjA == 0) mbar_wait(&s_full[slotA], phaseA);
+        const uint32_t b = 16u * bjA + (lane & 15u);
+        const uint32_t v = s_vals[slotA * vstride + 8u * b + warp];
+        const uint32_t r = v < s_width[b] ? __ldg(a.idx + s_start[b] + v) : 0u;
+        if (++bjA == nbs) {
+            __syncwarp();
+            uint32_t last = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                last = atomicAdd(&s_done[slotA], 1u) == kBitWarps - 1;
+                if (last) s_done[slotA] = 0u;
+            }
+            last = __shfl_sync(0xFFFFFFFFu, last, 0);
+            const uint64_t tn = (uint64_t)blockIdx.x + (tiA + a.nstage) * gridDim.x;
+            if (last && tn < ntiles) bit_tile_load(a, tn, s_vals + slotA * vstride, &s_full[slotA], lane);
+            bjA = 0;
+            tiA++;
+            if (++slotA == a.nstage) {
+                slotA = 0;
+                phaseA ^= 1u;
+            }
+        }
+        return r;
+    };
+    // ---- stage C: the 16 rows of a parked item
+    auto stageC = [&](uint32_t slot, uint32_t (&x)[2][16]) {
+        const uint4 *rp = reinterpret_cast<const uint4 *>(ring + 16u * slot);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint4 o = rp[j];
+            const uint32_t r4[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint2 y = __ldg(rows_lane + (uint64_t)r4[u] * 32u);
+                x[0][4 * j + u] = y.x;
+                x[1][4 * j + u] = y.y;
+            }
+        }
+    };
+    // ---- stage D: count; at a set's last batch the verdicts (as bit_scan_q_kernel's full path)
+    uint32_t tiD = 0, bjD = 0, es_w = 0, n_final = 0;
+    uint32_t c[2][kBitCS];
+#pragma unroll
+    for (int w = 0; w < 2; w++)
+#pragma unroll
+        for (int i = 0; i < (int)kBitCS; i++) c[w][i] = 0u;
+    auto stageD = [&](const uint32_t (&xc)[2][16]) {
+        const uint64_t s = a.s_begin + ((uint64_t)blockIdx.x + tiD * gridDim.x) * kBitWarps + warp;
+        if (bjD == 0 && s < a.n_sets) es_w = lane < a.nw ? __ldg(a.E + (uint64_t)lane * a.ld + s) : 0u;
+#pragma unroll
+        for (int w = 0; w < 2; w++) csa16(c[w], xc[w]);
+        if (++bjD < nbs) return;
+        bjD = 0;
+        tiD++;
+        if (s < a.n_sets) {  // warp-uniform: a tail tile's missing set is counted, never scored
+            const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, a.nbins_total));
+            const uint32_t k = a.nbins_total;
+#pragma unroll
+            for (int w = 0; w < 2; w++) {
+                n_final += __popc(qvalid[w]);
+                const uint32_t den_min = a.joint ? k - min(max_eq[w], es) : k - min(k, max_eq[w] + es);
+                const uint32_t theta =
+                    a.out.dense ? 0u : (uint32_t)(((uint64_t)a.t_num * den_min + a.t_den - 1) / a.t_den);
+                uint32_t want = sliced_ge<kBitCS>(c[w], theta) & qvalid[w];
+                while (__any_sync(0xFFFFFFFFu, want != 0u)) {
+                    const bool has = want != 0u;
+                    const uint32_t j = has ? __ffs(want) - 1 : 0u;
+                    want &= want - 1u;
+                    const uint32_t qg = a.qb0 + qw0[w] + j;
+                    uint32_t ex = 0;
+                    for (uint32_t ww = 0; ww < a.nw; ww++) {
+                        const uint32_t sw = __shfl_sync(0xFFFFFFFFu, es_w, ww);
+                        if (has) ex += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + ww), sw, a.joint, ww, k);
+                    }
+                    const uint32_t nmb = sliced_get<kBitCS>(c[w], j);
+                    const uint32_t den = k - ex;
+                    const bool undef = den == 0;
+                    const uint32_t verdict = !undef && (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
+                    emit(a.out, has, qg, s, nmb, ex, a.level_final, verdict, undef ? OPH_FLAG_UNDEFINED : 0u,
+                         undef ? -1.0f : (float)nmb / (float)den);
+                }
+            }
+        }
+#pragma unroll
+        for (int w = 0; w < 2; w++)
+#pragma unroll
+            for (int i = 0; i < (int)kBitCS; i++) c[w][i] = 0u;
+    };
+
+    if (nitems) {
+        uint32_t x[2][16], xb[2][16], pend;
+        {
+            const uint32_t r0 = stageA(), r1 = stageA();
+            pend = stageA();
+            if (lane < 16u) {
+                ring[lane] = r0;
+                ring[16u + lane] = r1;
+            }
+            __syncwarp();
+            stageC(0, x);
+        }
+        // item g: rows of g + 1 issued, lookup of g + 2 parked, lookup of g + 3 issued, g counted
+        auto step = [&](uint32_t g, uint32_t (&xc)[2][16], uint32_t (&xn)[2][16]) {
+            if (g + 1 < nitems) stageC((g + 1) & 3u, xn);
+            if (lane < 16u) ring[16u * ((g + 2) & 3u) + lane] = pend;
+            pend = stageA();
+            __syncwarp();
+            stageD(xc);
+        };
+        for (uint32_t g = 0; g < nitems; g += 2) {
+            step(g, x, xb);
+            if (g + 1 < nitems) step(g + 1, xb, x);
+        }
+    }
+    if (a.out.hist) {
+        const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, n_final);
+        if (lane == 0 && tot) atomicAdd(&s_hist, (unsigned long long)tot);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_hist) atomicAdd(a.out.hist + a.level_final, s_hist);
+    }
+}
+
 cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     cudaError_t e;
     // the value -> row table of this block: clear, claim rows, set the bits
@@ -811,8 +995,12 @@ cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     static const bool three = getenv("OPHGPU_BIT_CTAS") && atoi(getenv("OPHGPU_BIT_CTAS")) == 3;
     const int ctas = a.mode_hoph || two || (a.qw == 2 && !three) ? 2 : 3;
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * ctas * 8);
+    // (OPHGPU_BIT_FULL=0: full OPH through bit_scan_q_kernel, A/B)
+    static const bool no_full = getenv("OPHGPU_BIT_FULL") && atoi(getenv("OPHGPU_BIT_FULL")) == 0;
+    const bool full = a.method == kFull && a.qw == 2 && a.nscan % 16 == 0 && a.npre == a.nscan && !no_full;
     const size_t smem = (size_t)a.nstage * a.npre * kBitWarps * 4;
     auto kern = a.mode_hoph ? bit_scan_x_kernel<2, 2>
+                : full      ? bit_full_kernel<2>
                             : (a.qw == 2 ? (a.npre == a.nscan ? (three ? bit_scan_q_kernel<2, 3, true>
                                                                        : bit_scan_q_kernel<2, 2, true>)
                                                               : bit_scan_q_kernel<2, 2, false>)
