@@ -792,19 +792,20 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_x_kernel(const 
 }
 
 // Full OPH (Eq. 6) with 2,048-query rows and one software pipeline across the warp's sets
-// (items = the k/16 batches of each set, k % 16 == 0), four stages per item:
-//   A  look the set's 16 values up (value -> row index), 3 items ahead
-//   B  park the 16 row indices in the warp's shared ring, 2 items ahead (the lookups have
+// (k/16 batches per set, k % 64 == 0), four stages per batch:
+//   A  look the set's 16 values up (value -> row index), 3 batches ahead
+//   B  park the 16 row indices in the warp's shared ring, 2 batches ahead (the lookups have
 //      landed by then: no stall on them)
 //   C  read the ring back (4 broadcast 16-B loads instead of 16 shuffles) and issue the 16
-//      row loads (one 8-B load per lane), 1 item ahead
-//   D  count (csa16 on both words); at a set's last batch, the verdicts
-// The termination histogram (every pair at level_final) is counted in shared memory and
-// added once per CTA (no per-set global atomics); a set's empty-bin mask word is fetched at
-// its first batch and used at its last.
+//      row loads (one 8-B load per lane), 1 batch ahead
+//   D  count (csa16 on both words); after a set's last batch, the verdicts
+// The batch loop is straight-line: the lookahead crosses into the next set only in the last
+// three batches of a set (written out after the loop), so no per-batch bookkeeping.  The
+// termination histogram (every pair at level_final) is counted in shared memory and added
+// once per CTA; a set's empty-bin mask word is fetched at its first batch.
 template <int MINB>
 __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_full_kernel(const __grid_constant__ BitArgs a) {
-    __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
+    __shared__ uint2 s_sw[kBitMaxBins + 1];  // per bin: (first position, width)
     __shared__ uint64_t s_full[kBitMaxStages];
     __shared__ uint32_t s_done[kBitMaxStages];
     __shared__ __align__(16) uint32_t s_ring[kBitWarps][4][16];
@@ -813,8 +814,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_full_kernel(const __
     for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
         uint32_t st, wd;
         bit_bin_range(a, b, st, wd);
-        s_start[b] = st;
-        s_width[b] = wd;
+        s_sw[b] = make_uint2(st, wd);
     }
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     uint32_t qw0[2], qvalid[2], max_eq[2];
@@ -843,43 +843,23 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_full_kernel(const __
         }
     }
     const uint32_t nbs = a.nscan / 16u;
-    // (per-CTA tile and item counts fit 32 bits: ntiles / grid tiles of k / 16 items)
+    // (per-CTA tile counts fit 32 bits)
     const uint32_t n_it = (uint64_t)blockIdx.x < ntiles ? (uint32_t)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0u;
-    const uint32_t nitems = n_it * nbs;
     uint32_t *ring = &s_ring[warp][0][0];
+    const uint32_t bl = lane & 15u;
+    const uint32_t *vals_lane = s_vals + 8u * bl + warp;  // + slot * vstride + 128 j: bin 16 j + bl
+    const uint2 *sw_lane = s_sw + bl;                     // + 16 j
 
-    // ---- stage A: the row index of this lane's bin (lanes 16-31 repeat lanes 0-15's lookups:
-    // same addresses, no extra traffic, no divergence); releases a tile after its last batch
-    uint32_t tiA = 0, bjA = 0, slotA = 0, phaseA = 0;
-    auto stageA = [&]() -> uint32_t {
-        if (tiA >= n_it) return 0u;
-        if (bjA == 0) mbar_wait(&s_full[slotA], phaseA);
-        const uint32_t b = 16u * bjA + (lane & 15u);
-        const uint32_t v = s_vals[slotA * vstride + 8u * b + warp];
-        const uint32_t r = v < s_width[b] ? __ldg(a.idx + s_start[b] + v) : 0u;
-        if (++bjA == nbs) {
-            __syncwarp();
-            uint32_t last = 0;
-            if (lane == 0) {
-                __threadfence_block();
-                last = atomicAdd(&s_done[slotA], 1u) == kBitWarps - 1;
-                if (last) s_done[slotA] = 0u;
-            }
-            last = __shfl_sync(0xFFFFFFFFu, last, 0);
-            const uint64_t tn = (uint64_t)blockIdx.x + (tiA + a.nstage) * gridDim.x;
-            if (last && tn < ntiles) bit_tile_load(a, tn, s_vals + slotA * vstride, &s_full[slotA], lane);
-            bjA = 0;
-            tiA++;
-            if (++slotA == a.nstage) {
-                slotA = 0;
-                phaseA ^= 1u;
-            }
-        }
-        return r;
+    // A: the row index of this lane's bin of batch j of the set staged in `slot` (lanes 16-31
+    // repeat lanes 0-15: same addresses, no extra traffic)
+    auto look = [&](uint32_t slot, uint32_t j) -> uint32_t {
+        const uint32_t v = vals_lane[slot * vstride + 128u * j];
+        const uint2 sw = sw_lane[16u * j];
+        return v < sw.y ? __ldg(a.idx + sw.x + v) : 0u;
     };
-    // ---- stage C: the 16 rows of a parked item
-    auto stageC = [&](uint32_t slot, uint32_t (&x)[2][16]) {
-        const uint4 *rp = reinterpret_cast<const uint4 *>(ring + 16u * slot);
+    // C: the 16 rows of the batch parked in ring slot q
+    auto rows = [&](uint32_t q, uint32_t (&x)[2][16]) {
+        const uint4 *rp = reinterpret_cast<const uint4 *>(ring + 16u * q);
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             const uint4 o = rp[j];
@@ -892,21 +872,70 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_full_kernel(const __
             }
         }
     };
-    // ---- stage D: count; at a set's last batch the verdicts (as bit_scan_q_kernel's full path)
-    uint32_t tiD = 0, bjD = 0, es_w = 0, n_final = 0;
     uint32_t c[2][kBitCS];
 #pragma unroll
     for (int w = 0; w < 2; w++)
 #pragma unroll
         for (int i = 0; i < (int)kBitCS; i++) c[w][i] = 0u;
-    auto stageD = [&](const uint32_t (&xc)[2][16]) {
-        const uint64_t s = a.s_begin + ((uint64_t)blockIdx.x + tiD * gridDim.x) * kBitWarps + warp;
-        if (bjD == 0 && s < a.n_sets) es_w = lane < a.nw ? __ldg(a.E + (uint64_t)lane * a.ld + s) : 0u;
+    uint32_t pend = 0u, n_final = 0u;
+    // one batch j (ring slots j & 3, nbs % 4 == 0): rows of j + 1 issued, the lookup of j + 2
+    // parked, `nl` (the lookup of j + 3) becomes pending, batch j counted
+    auto step = [&](uint32_t j, uint32_t (&xc)[2][16], uint32_t (&xn)[2][16], uint32_t nl) {
+        rows((j + 1) & 3u, xn);
+        if (lane < 16u) ring[16u * ((j + 2) & 3u) + lane] = pend;
+        pend = nl;
+        __syncwarp();
 #pragma unroll
         for (int w = 0; w < 2; w++) csa16(c[w], xc[w]);
-        if (++bjD < nbs) return;
-        bjD = 0;
-        tiD++;
+    };
+
+    uint32_t x[2][16], xb[2][16];
+    uint32_t slot = 0, phase = 0;
+    if (n_it) {
+        mbar_wait(&s_full[0], 0);
+        const uint32_t r0 = look(0, 0), r1 = look(0, 1);
+        pend = look(0, 2);
+        if (lane < 16u) {
+            ring[lane] = r0;
+            ring[16u + lane] = r1;
+        }
+        __syncwarp();
+        rows(0, x);
+    }
+    for (uint32_t it = 0; it < n_it; it++) {
+        const uint64_t tile = blockIdx.x + (uint64_t)it * gridDim.x;
+        const uint64_t s = a.s_begin + tile * kBitWarps + warp;
+        uint32_t es_w = 0;
+        if (s < a.n_sets) es_w = lane < a.nw ? __ldg(a.E + (uint64_t)lane * a.ld + s) : 0u;
+        uint32_t j = 0;
+        for (; j + 4 < nbs; j += 2) {
+            step(j, x, xb, look(slot, j + 3));
+            step(j + 1, xb, x, look(slot, j + 4));
+        }
+        // j = nbs - 4: the set's last lookup, then its tile is released and the next one awaited
+        step(j, x, xb, look(slot, j + 3));
+        {
+            __syncwarp();
+            uint32_t last = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                last = atomicAdd(&s_done[slot], 1u) == kBitWarps - 1;
+                if (last) s_done[slot] = 0u;
+            }
+            last = __shfl_sync(0xFFFFFFFFu, last, 0);
+            const uint64_t tn = tile + (uint64_t)a.nstage * gridDim.x;
+            if (last && tn < ntiles) bit_tile_load(a, tn, s_vals + slot * vstride, &s_full[slot], lane);
+        }
+        const bool more = it + 1 < n_it;
+        if (++slot == a.nstage) {
+            slot = 0;
+            phase ^= 1u;
+        }
+        if (more) mbar_wait(&s_full[slot], phase);
+        step(j + 1, xb, x, more ? look(slot, 0) : 0u);
+        step(j + 2, x, xb, more ? look(slot, 1) : 0u);
+        step(j + 3, xb, x, more ? look(slot, 2) : 0u);
+        // (nbs even: the next set's batch 0 is in x again)
         if (s < a.n_sets) {  // warp-uniform: a tail tile's missing set is counted, never scored
             const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, a.nbins_total));
             const uint32_t k = a.nbins_total;
@@ -919,15 +948,15 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_full_kernel(const __
                 uint32_t want = sliced_ge<kBitCS>(c[w], theta) & qvalid[w];
                 while (__any_sync(0xFFFFFFFFu, want != 0u)) {
                     const bool has = want != 0u;
-                    const uint32_t j = has ? __ffs(want) - 1 : 0u;
+                    const uint32_t jj = has ? __ffs(want) - 1 : 0u;
                     want &= want - 1u;
-                    const uint32_t qg = a.qb0 + qw0[w] + j;
+                    const uint32_t qg = a.qb0 + qw0[w] + jj;
                     uint32_t ex = 0;
                     for (uint32_t ww = 0; ww < a.nw; ww++) {
                         const uint32_t sw = __shfl_sync(0xFFFFFFFFu, es_w, ww);
                         if (has) ex += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + ww), sw, a.joint, ww, k);
                     }
-                    const uint32_t nmb = sliced_get<kBitCS>(c[w], j);
+                    const uint32_t nmb = sliced_get<kBitCS>(c[w], jj);
                     const uint32_t den = k - ex;
                     const bool undef = den == 0;
                     const uint32_t verdict = !undef && (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
@@ -940,32 +969,6 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_full_kernel(const __
         for (int w = 0; w < 2; w++)
 #pragma unroll
             for (int i = 0; i < (int)kBitCS; i++) c[w][i] = 0u;
-    };
-
-    if (nitems) {
-        uint32_t x[2][16], xb[2][16], pend;
-        {
-            const uint32_t r0 = stageA(), r1 = stageA();
-            pend = stageA();
-            if (lane < 16u) {
-                ring[lane] = r0;
-                ring[16u + lane] = r1;
-            }
-            __syncwarp();
-            stageC(0, x);
-        }
-        // item g: rows of g + 1 issued, lookup of g + 2 parked, lookup of g + 3 issued, g counted
-        auto step = [&](uint32_t g, uint32_t (&xc)[2][16], uint32_t (&xn)[2][16]) {
-            if (g + 1 < nitems) stageC((g + 1) & 3u, xn);
-            if (lane < 16u) ring[16u * ((g + 2) & 3u) + lane] = pend;
-            pend = stageA();
-            __syncwarp();
-            stageD(xc);
-        };
-        for (uint32_t g = 0; g < nitems; g += 2) {
-            step(g, x, xb);
-            if (g + 1 < nitems) step(g + 1, xb, x);
-        }
     }
     if (a.out.hist) {
         const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, n_final);
@@ -997,7 +1000,7 @@ cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * ctas * 8);
     // (OPHGPU_BIT_FULL=0: full OPH through bit_scan_q_kernel, A/B)
     static const bool no_full = getenv("OPHGPU_BIT_FULL") && atoi(getenv("OPHGPU_BIT_FULL")) == 0;
-    const bool full = a.method == kFull && a.qw == 2 && a.nscan % 16 == 0 && a.npre == a.nscan && !no_full;
+    const bool full = a.method == kFull && a.qw == 2 && a.nscan % 64 == 0 && a.npre == a.nscan && !no_full;
     const size_t smem = (size_t)a.nstage * a.npre * kBitWarps * 4;
     auto kern = a.mode_hoph ? bit_scan_x_kernel<2, 2>
                 : full      ? bit_full_kernel<2>
