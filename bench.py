@@ -630,7 +630,7 @@ def run_ours(args):
         return (ub or {}).get(key, {}).get(str(16 << 20))
 
     def model_for(kernel: str, phase: str):
-        if kernel.startswith("bit_scan") or kernel.startswith("bit_full"):
+        if kernel.startswith("bit_scan") or kernel.startswith("bit_pipe"):
             # blocks of 2,048 queries (256-B rows; bit_scan_kernel, the OPHGPU_BIT_QW=1 A/B: 1,024)
             qwords = 1 if kernel.startswith("bit_scan_kernel") else 2
             row = 128 * qwords

@@ -791,25 +791,79 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_x_kernel(const 
     }
 }
 
-// Full OPH (Eq. 6) with 2,048-query rows and one software pipeline across the warp's sets
-// (k/16 batches per set, k % 64 == 0), four stages per batch:
+// GOPH's pairs left after the bitmap part (levels 1 .. level_b): the later levels one pair at
+// a time by the whole warp (lane = bin of the level; ballot counts), Algorithm 1's thresholds
+// on the running count, the full-OPH verdict (Eq. 6) after level L -- as level_walk_kernel.
+__device__ __forceinline__ uint32_t bit_excl_warp(const BitArgs &a, uint32_t qg, uint64_t s, uint32_t nbins,
+                                                  uint32_t lane) {
+    uint32_t ex = 0;
+    for (uint32_t w = lane; w * 32 < nbins; w += 32)
+        ex += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + w), __ldg(a.E + (uint64_t)w * a.ld + s), a.joint, w,
+                          nbins);
+    return __reduce_add_sync(0xFFFFFFFFu, ex);
+}
+
+__device__ void bit_walk_goph(const BitArgs &a, uint32_t qg, uint64_t s, uint32_t nmb, uint32_t lane,
+                              unsigned long long *hist) {
+    const uint32_t *qrow = a.QM + (uint64_t)qg * a.nb;
+    for (uint32_t l = a.level_b + 1; l <= a.nlev; l++) {
+        uint32_t M = 0;
+        for (uint32_t b0 = (l - 1) * a.kp; b0 < l * a.kp; b0 += 32) {
+            const uint32_t b = b0 + lane;
+            const bool in = b < l * a.kp;
+            const uint32_t qv = in ? __ldg(qrow + b) : 0u;
+            const uint32_t sv = in ? __ldg(a.F + (uint64_t)b * a.ld + s) : 1u;  // never equal when masked
+            M += __popc(__ballot_sync(0xFFFFFFFFu, qv == sv));
+        }
+        nmb += M;
+        if (l == a.nlev) {
+            const uint32_t ex = bit_excl_warp(a, qg, s, a.nbins_total, lane);
+            const uint32_t den = a.nbins_total - ex;
+            const bool undef = den == 0;
+            const uint32_t verdict = !undef && (uint64_t)nmb * a.t_den >= (uint64_t)a.t_num * den;
+            if (lane == 0) {
+                emit_one(a.out, qg, (uint32_t)s, nmb, ex, a.nlev, verdict, undef ? OPH_FLAG_UNDEFINED : 0u,
+                         undef ? -1.0f : (float)nmb / (float)den);
+                if (hist) atomicAdd(hist + a.nlev, 1ull);
+            }
+            return;
+        }
+        if (!a.thr_on[l - 1]) continue;
+        const bool acc = nmb >= a.acc_cnt[l - 1];
+        const bool rej = !acc && a.rej_cnt[l - 1] >= 0 && nmb <= (uint32_t)a.rej_cnt[l - 1];
+        if (acc || rej) {
+            if (a.out.dense || acc) {
+                const uint32_t ex = bit_excl_warp(a, qg, s, l * a.kp, lane);
+                if (lane == 0) emit_one(a.out, qg, (uint32_t)s, nmb, ex, l, acc ? 1u : 0u, OPH_FLAG_EARLY, -1.0f);
+            }
+            if (lane == 0 && hist) atomicAdd(hist + l, 1ull);
+            return;
+        }
+    }
+}
+
+// Full OPH (Eq. 6), and GOPH (Algorithm 1) over its first level_b levels, with 2,048-query
+// rows and one software pipeline across the warp's sets (nscan / 16 batches per set, an even
+// number >= 4), four stages per batch:
 //   A  look the set's 16 values up (value -> row index), 3 batches ahead
 //   B  park the 16 row indices in the warp's shared ring, 2 batches ahead (the lookups have
 //      landed by then: no stall on them)
 //   C  read the ring back (4 broadcast 16-B loads instead of 16 shuffles) and issue the 16
 //      row loads (one 8-B load per lane), 1 batch ahead
-//   D  count (csa16 on both words); after a set's last batch, the verdicts
+//   D  count (csa16 on both words); GOPH: at each level end Algorithm 1's thresholds on the
+//      bit-sliced counts; after a set's last batch the final verdicts (full OPH; GOPH when
+//      level_b = L) or the per-pair walk of the pairs still undecided (GOPH, level_b < L)
 // The batch loop is straight-line: the lookahead crosses into the next set only in the last
 // three batches of a set (written out after the loop), so no per-batch bookkeeping.  The
-// termination histogram (every pair at level_final) is counted in shared memory and added
-// once per CTA; a set's empty-bin mask word is fetched at its first batch.
-template <int MINB>
-__global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_full_kernel(const __grid_constant__ BitArgs a) {
+// termination histogram is counted in shared memory and added once per CTA; a set's
+// empty-bin mask word is fetched at its first batch.
+template <int MINB, bool GOPH>
+__global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_pipe_kernel(const __grid_constant__ BitArgs a) {
     __shared__ uint2 s_sw[kBitMaxBins + 1];  // per bin: (first position, width)
     __shared__ uint64_t s_full[kBitMaxStages];
     __shared__ uint32_t s_done[kBitMaxStages];
     __shared__ __align__(16) uint32_t s_ring[kBitWarps][4][16];
-    __shared__ unsigned long long s_hist;
+    __shared__ unsigned long long s_hist[kMaxGroups + 1];
     extern __shared__ __align__(128) uint32_t s_vals[];  // [nstage][npre][8]
     for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
         uint32_t st, wd;
@@ -827,12 +881,12 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_full_kernel(const __
     const uint2 *rows_lane = reinterpret_cast<const uint2 *>(a.rows) + lane;
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
     const uint32_t vstride = a.npre * 8u;
+    if (threadIdx.x <= kMaxGroups) s_hist[threadIdx.x] = 0ull;
     if (threadIdx.x == 0) {
         for (uint32_t i = 0; i < a.nstage; i++) {
             mbar_init(&s_full[i], 32);
             s_done[i] = 0u;
         }
-        s_hist = 0ull;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -878,15 +932,53 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_full_kernel(const __
 #pragma unroll
         for (int i = 0; i < (int)kBitCS; i++) c[w][i] = 0u;
     uint32_t pend = 0u, n_final = 0u;
-    // one batch j (ring slots j & 3, nbs % 4 == 0): rows of j + 1 issued, the lookup of j + 2
-    // parked, `nl` (the lookup of j + 3) becomes pending, batch j counted
+    uint32_t alive[2] = {qvalid[0], qvalid[1]};
+    uint32_t lev = 1, lend = a.kp / 16u;  // GOPH: the level being counted, the batch it ends at
+    uint32_t gb = 0;                      // batches of the warp's earlier sets (ring slots)
+    uint64_t s_cur = 0;
+    // GOPH: Algorithm 1's decisions at the end of level l < L (as bit_scan_q_kernel)
+    auto decide = [&](uint32_t l) {
+        const uint32_t A = a.acc_cnt[l - 1];
+        const int32_t R = a.rej_cnt[l - 1];
+#pragma unroll
+        for (int w = 0; w < 2; w++) {
+            const uint32_t acc = sliced_ge<kBitCS>(c[w], A) & alive[w];
+            const uint32_t dec = (acc | (R >= 0 ? ~sliced_ge<kBitCS>(c[w], (uint32_t)R + 1u) : 0u)) & alive[w];
+            const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, __popc(dec));
+            if (lane == 0 && tot) atomicAdd(&s_hist[l], (unsigned long long)tot);
+            uint32_t want = a.out.dense ? dec : acc;
+            while (__any_sync(0xFFFFFFFFu, want != 0u)) {
+                const bool has = want != 0u;
+                const uint32_t jj = has ? __ffs(want) - 1 : 0u;
+                want &= want - 1u;
+                const uint32_t qg = a.qb0 + qw0[w] + jj;
+                uint32_t nmb = 0, ex = 0;
+                if (has) {
+                    nmb = sliced_get<kBitCS>(c[w], jj);
+                    ex = bit_excl(a, qg, s_cur, 0, l * a.kp);
+                }
+                emit(a.out, has, qg, s_cur, nmb, ex, l, (acc >> jj) & 1u, OPH_FLAG_EARLY, -1.0f);
+            }
+            alive[w] &= ~dec;
+        }
+    };
+    // one batch j: rows of j + 1 issued, the lookup of j + 2 parked, `nl` (the lookup of j + 3)
+    // becomes pending, batch j counted
     auto step = [&](uint32_t j, uint32_t (&xc)[2][16], uint32_t (&xn)[2][16], uint32_t nl) {
-        rows((j + 1) & 3u, xn);
-        if (lane < 16u) ring[16u * ((j + 2) & 3u) + lane] = pend;
+        // (full OPH: nbs % 4 == 0, the ring slots restart with every set)
+        const uint32_t g = GOPH ? gb + j : j;
+        rows((g + 1) & 3u, xn);
+        if (lane < 16u) ring[16u * ((g + 2) & 3u) + lane] = pend;
         pend = nl;
         __syncwarp();
 #pragma unroll
         for (int w = 0; w < 2; w++) csa16(c[w], xc[w]);
+        if constexpr (GOPH) {
+            if (j + 1 != lend) return;  // warp-uniform
+            if (lev < a.nlev && a.thr_on[lev - 1] && s_cur < a.n_sets) decide(lev);
+            lev++;
+            lend += a.kp / 16u;
+        }
     };
 
     uint32_t x[2][16], xb[2][16];
@@ -905,6 +997,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_full_kernel(const __
     for (uint32_t it = 0; it < n_it; it++) {
         const uint64_t tile = blockIdx.x + (uint64_t)it * gridDim.x;
         const uint64_t s = a.s_begin + tile * kBitWarps + warp;
+        if constexpr (GOPH) s_cur = s;
         uint32_t es_w = 0;
         if (s < a.n_sets) es_w = lane < a.nw ? __ldg(a.E + (uint64_t)lane * a.ld + s) : 0u;
         uint32_t j = 0;
@@ -936,16 +1029,31 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_full_kernel(const __
         step(j + 2, x, xb, more ? look(slot, 1) : 0u);
         step(j + 3, xb, x, more ? look(slot, 2) : 0u);
         // (nbs even: the next set's batch 0 is in x again)
-        if (s < a.n_sets) {  // warp-uniform: a tail tile's missing set is counted, never scored
+        if (GOPH && a.level_b < a.nlev && s < a.n_sets) {
+            // the pairs still undecided after level_b: walked one by one over the later levels
+#pragma unroll
+            for (int w = 0; w < 2; w++) {
+                uint32_t al = alive[w];
+                while (__any_sync(0xFFFFFFFFu, al != 0u)) {
+                    const uint32_t src = __ffs(__ballot_sync(0xFFFFFFFFu, al != 0u)) - 1;
+                    const uint32_t mine = al != 0u ? __ffs(al) - 1 : 0u;
+                    const uint32_t jj = __shfl_sync(0xFFFFFFFFu, mine, src);
+                    const uint32_t m = __shfl_sync(0xFFFFFFFFu, sliced_get<kBitCS>(c[w], mine), src);
+                    if (lane == src) al &= al - 1u;
+                    bit_walk_goph(a, a.qb0 + 32u * (2 * src + w) + jj, s, m, lane, a.out.hist ? s_hist : nullptr);
+                }
+            }
+        } else if (s < a.n_sets) {  // warp-uniform: a tail tile's missing set is counted, never scored
             const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, a.nbins_total));
             const uint32_t k = a.nbins_total;
 #pragma unroll
             for (int w = 0; w < 2; w++) {
-                n_final += __popc(qvalid[w]);
+                const uint32_t al = GOPH ? alive[w] : qvalid[w];
+                n_final += __popc(al);
                 const uint32_t den_min = a.joint ? k - min(max_eq[w], es) : k - min(k, max_eq[w] + es);
                 const uint32_t theta =
                     a.out.dense ? 0u : (uint32_t)(((uint64_t)a.t_num * den_min + a.t_den - 1) / a.t_den);
-                uint32_t want = sliced_ge<kBitCS>(c[w], theta) & qvalid[w];
+                uint32_t want = sliced_ge<kBitCS>(c[w], theta) & al;
                 while (__any_sync(0xFFFFFFFFu, want != 0u)) {
                     const bool has = want != 0u;
                     const uint32_t jj = has ? __ffs(want) - 1 : 0u;
@@ -966,15 +1074,22 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_full_kernel(const __
             }
         }
 #pragma unroll
-        for (int w = 0; w < 2; w++)
+        for (int w = 0; w < 2; w++) {
+            if (GOPH) alive[w] = qvalid[w];
 #pragma unroll
             for (int i = 0; i < (int)kBitCS; i++) c[w][i] = 0u;
+        }
+        if constexpr (GOPH) {
+            lev = 1;
+            lend = a.kp / 16u;
+            gb += nbs;
+        }
     }
     if (a.out.hist) {
         const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, n_final);
-        if (lane == 0 && tot) atomicAdd(&s_hist, (unsigned long long)tot);
+        if (lane == 0 && tot) atomicAdd(&s_hist[a.level_final], (unsigned long long)tot);
         __syncthreads();
-        if (threadIdx.x == 0 && s_hist) atomicAdd(a.out.hist + a.level_final, s_hist);
+        if (threadIdx.x <= kMaxGroups && s_hist[threadIdx.x]) atomicAdd(a.out.hist + threadIdx.x, s_hist[threadIdx.x]);
     }
 }
 
@@ -998,12 +1113,9 @@ cudaError_t launch_bit_block(const BitArgs &a, cudaStream_t st) {
     static const bool three = getenv("OPHGPU_BIT_CTAS") && atoi(getenv("OPHGPU_BIT_CTAS")) == 3;
     const int ctas = a.mode_hoph || two || (a.qw == 2 && !three) ? 2 : 3;
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, 148ull * ctas * 8);
-    // (OPHGPU_BIT_FULL=0: full OPH through bit_scan_q_kernel, A/B)
-    static const bool no_full = getenv("OPHGPU_BIT_FULL") && atoi(getenv("OPHGPU_BIT_FULL")) == 0;
-    const bool full = a.method == kFull && a.qw == 2 && a.nscan % 64 == 0 && a.npre == a.nscan && !no_full;
     const size_t smem = (size_t)a.nstage * a.npre * kBitWarps * 4;
     auto kern = a.mode_hoph ? bit_scan_x_kernel<2, 2>
-                : full      ? bit_full_kernel<2>
+                : a.pipe    ? (a.method == kGoph ? bit_pipe_kernel<2, true> : bit_pipe_kernel<2, false>)
                             : (a.qw == 2 ? (a.npre == a.nscan ? (three ? bit_scan_q_kernel<2, 3, true>
                                                                        : bit_scan_q_kernel<2, 2, true>)
                                                               : bit_scan_q_kernel<2, 2, false>)

@@ -218,6 +218,8 @@ struct BitArgs {
     uint32_t npre;          // bins [0, npre) are staged per CTA tile (the rest read directly)
     uint32_t nstage;        // CTA tiles staged ahead (ring of value buffers, 2 .. 8)
     uint32_t qb0, nqb;      // this block: query columns [qb0, qb0 + nqb), nqb <= 1024 qw
+    uint32_t pipe;          // 1: bit_pipe_kernel (full OPH; GOPH over levels 1 .. level_b, then walks)
+    uint32_t level_b;       // GOPH levels decided by the bitmap in bit_pipe_kernel (the rest walked)
     uint32_t qw;            // 32-query words per lane: rows of 1024 qw bits (1, or 2 for full OPH / GOPH)
     uint32_t method, mode_hoph, joint, t_num, t_den, level_final;
     // value ranges of the bins: bin b = range b / bins_per_range, floor rule inside it

@@ -521,6 +521,31 @@ oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketche
     // GOPH (A/B)
     static const bool qw1 = getenv("OPHGPU_BIT_QW") && atoi(getenv("OPHGPU_BIT_QW")) == 1;
     ba.qw = qw1 && method != OPH_METHOD_HOPH ? 1 : 2;
+    // bit_pipe_kernel (2,048-query rows; nscan / 16 batches per set, even, >= 4): full OPH, and
+    // GOPH over levels 1 .. level_b = l0 + 1 (the first level with a decision, and one more:
+    // on image-like l0 decides 2/3 of the pairs and l0 + 1 nearly all the rest), the few
+    // pairs left walked one by one; the bitmap table and the staged tiles then cover only
+    // those levels.  OPHGPU_BIT_PIPE=0 / OPHGPU_GOPH_LB=n: A/B (read per call: tests set them)
+    ba.pipe = 0;
+    ba.level_b = ba.nlev;
+    const char *pipe_env = getenv("OPHGPU_BIT_PIPE");
+    if (ba.qw == 2 && method != OPH_METHOD_HOPH && !(pipe_env && atoi(pipe_env) == 0)) {
+        auto ok = [](uint32_t bins) { return bins % 32 == 0 && bins >= 64; };
+        if (method == OPH_METHOD_FULL) {
+            ba.pipe = nb % 64 == 0;  // (ring slots restart with every set: batches % 4 == 0)
+        } else {
+            const char *lb_env = getenv("OPHGPU_GOPH_LB");
+            uint32_t Lb = lb_env ? (uint32_t)atoi(lb_env) : plan.l0 + 1;
+            Lb = std::max<uint32_t>(1u, std::min<uint32_t>(Lb, nlev));
+            while (Lb < nlev && !ok(Lb * kp)) Lb++;
+            if (ok(Lb * kp)) {
+                ba.pipe = 1;
+                ba.level_b = Lb;
+                ba.nscan = ba.npre = Lb * kp;
+                ba.nstage = std::max<uint32_t>(2, std::min<uint32_t>(8, 32768 / (ba.npre * 32)));
+            }
+        }
+    }
     const uint64_t qb = 1024ull * ba.qw;
     for (uint64_t q0 = 0; q0 < n_q; q0 += qb) {
         ba.qb0 = (uint32_t)q0;

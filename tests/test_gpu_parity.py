@@ -911,6 +911,37 @@ def test_bitmap_image_like_lists_and_histogram(image_small, method):
     assert brute.tobytes() == got.tobytes()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("lb,pipe", [("1", "1"), ("2", "1"), ("4", "1"), ("16", "1"), ("6", "0")])
+def test_bitmap_goph_level_split(image_small, monkeypatch, lb, pipe):
+    """GOPH through bit_pipe_kernel with the bitmap part forced to levels 1..lb (OPHGPU_GOPH_LB;
+    lb = 1 and 2 are raised to the kernel's minimum of 64 bins) and every pair still undecided
+    walked one by one over the later levels: dense records and threshold lists (with the
+    termination histogram) == the oracle; pipe = 0 is the per-set bit_scan_q_kernel."""
+    monkeypatch.setenv("OPHGPU_GOPH_LB", lb)
+    monkeypatch.setenv("OPHGPU_BIT_PIPE", pipe)
+    r, o, p = image_small, image_small["orc"], image_small["p"]
+    lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+    for joint in (False, True):
+        kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"], joint=joint, strategy=og.OPH_STRATEGY_BITMAP)
+        n = 1000
+        g = gpu_dense("goph", r["qo"], subview(r["so"], n), layout=lay, **kw)
+        want = oracle_records("goph", o["QF"], o["F"][:n], k=p["k"], kprime=p["kprime"], **kw)
+        assert_records_equal(g, want, f"goph lb={lb} joint={joint}")
+    kw = dict(t_num=p["t_num"], t_den=p["t_den"], eps=p["eps"])
+    want = oracle_records("goph", o["QF"], o["F"], k=p["k"], kprime=p["kprime"], **kw)
+    res = og.Results(1 << 22, stop_hist=True)
+    og.compare_goph(r["qo"], r["so"], lay, og.params(p["t_num"], p["t_den"], p["eps"],
+                                                     strategy=og.OPH_STRATEGY_BITMAP), res)
+    hist = res.hist().astype(np.int64)
+    assert (hist == np.bincount(want["groups"].ravel(), minlength=len(hist))).all()
+    n = res.n()
+    out = og.Results(max(n, 1))
+    og.topk_or_threshold_results(res, n, og.OPH_SELECT_THRESHOLD, out)
+    got = out.numpy(n)
+    assert list(zip(got["query"].tolist(), got["set_id"].tolist())) == oracle.threshold_list(want)
+
+
 def test_bitmap_domain_errors(tiny_run):
     """An explicit BITMAP request outside its domain fails (MinWise; |V| > 2^23); a
     workspace of only oph_workspace_size bytes is too small (OPH_ENOMEM) while AUTO
