@@ -46,6 +46,7 @@ struct BuildArgs {
     uint32_t log2V, log2kp;
     RangeBins grp[kMaxGroups];
     uint32_t *hoph, *hoph_empty;
+    uint32_t hder;  // FAST layout: leading HOPH groups derived from the OPH minima (set by launch_build)
 };
 
 struct MinwiseArgs {

@@ -323,6 +323,190 @@ __global__ void __launch_bounds__(512) build_kernel(const __grid_constant__ Buil
     if (a.do_hier) write_sketch<SB>(sh, hst, nbh, nloc, a.hoph, a.hoph_empty, a.ld, s0);
 }
 
+// K1 (FAST layout, r02): a warp per SPW consecutive sets of the CTA's SB.
+//  * The warp streams its sets' contiguous id range (the owning set is a compare
+//    against SPW - 1 register boundaries, no per-element shared lookup) with the next
+//    batch of ids in flight while the current one is hashed.
+//  * HOPH groups 0 .. hder-1 are unions of whole OPH bins: with |V| = 2^m, group g
+//    (g < L - 1) bins are 2^(m - g - 1 - log2 k') wide and start at multiples of their
+//    width, an OPH bin is 2^(m - log2 k) wide, so for g <= log2 k - log2 k' - 1 every
+//    HOPH bin of group g is M_g = 2^(log2 k - log2 k' - 1 - g) consecutive OPH bins.
+//    Its minimum offset is that of its first non-empty OPH bin, t 2^fsh + off_t
+//    (positions increase with t), exactly the min over its elements (P:143-160 for
+//    both layouts: the same psi, min per bin).  So only elements of groups >= hder
+//    (the last 2^-hder of the universe) update the HOPH tile: one shared reduction per
+//    element instead of two (the kernel is bound by the shared-memory pipe).  The
+//    derived bins are written from the OPH tile: a lane reads 4 consecutive OPH bins
+//    (one 16-B load; rows are 16-B aligned), takes their min in registers and, for
+//    M_g > 4, across M_g / 4 lanes by shuffles.
+//  * Each warp initialises and finishes its own sets' rows (no CTA barrier until
+//    the bin-major write-out of the SB sets).
+// Row strides = 4 mod 32 words (16-B aligned rows; the write-out reads one set's
+// consecutive bins per instruction, conflict-free for any stride).
+__host__ __device__ inline uint32_t build_warp_stride(uint32_t nbins) { return (nbins + 31u) / 32u * 32u + 4u; }
+
+// count of leading zeros on the ALU / FMA pipes (FLO is a variable-latency op whose
+// results queue behind the tile's shared-memory reductions: 36 % short-scoreboard stalls
+// in the build, r02z6).  For x < 2^23, 2^23 + x is exact as a float and its exponent field
+// is 150 + msb(x); x = u >> 9 when that is non-zero (msb(u) = msb(x) + 9), else u itself:
+// clz(u) = 31 - msb(u) = 158 - add - exponent field.  u = 0 gives 158 (>= 32: callers cap).
+__device__ __forceinline__ uint32_t clz_alu(uint32_t u) {
+    const uint32_t hi = u >> 9;
+    const uint32_t x = hi ? hi : u;
+    const uint32_t add = hi ? 9u : 0u;
+    const float f = __fsub_rn(__uint_as_float(0x4B000000u | x), 8388608.0f);
+    return 158u - add - (__float_as_uint(f) >> 23);
+}
+
+__device__ __forceinline__ uint32_t derive_cand(uint32_t v, uint32_t t, uint32_t fsh) {
+    return v == kEmpty ? kEmpty : ((t << fsh) | v);
+}
+
+template <bool W32, int SB, int SPW>
+__global__ void __launch_bounds__(32 * SB / SPW) build_warp_kernel(const __grid_constant__ BuildArgs a) {
+    extern __shared__ __align__(16) uint32_t smem_u32[];
+    const uint32_t kst = build_warp_stride(a.k);
+    const uint32_t nbh = a.L * a.kp;
+    const uint32_t hst = build_warp_stride(nbh);
+    uint32_t *so = smem_u32;               // [SB][kst]
+    uint32_t *sh = so + (size_t)SB * kst;  // [SB][hst]
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+
+    const uint64_t s0 = (uint64_t)blockIdx.x * SB;
+    const uint32_t nloc = (uint32_t)min((uint64_t)SB, a.n_sets - s0);
+    const uint32_t j0 = warp * SPW;  // this warp's first local set
+    // offsets of the warp's sets (lane t holds offsets[s0 + j0 + t], t <= SPW)
+    uint64_t offl = 0;
+    if (lane <= (uint32_t)SPW && j0 + lane <= nloc) offl = __ldg(a.offsets + s0 + j0 + lane);
+    const uint32_t nmine = j0 < nloc ? min((uint32_t)SPW, nloc - j0) : 0u;
+    const uint64_t E0 = __shfl_sync(0xFFFFFFFFu, offl, 0);
+    const uint64_t E1 = __shfl_sync(0xFFFFFFFFu, offl, nmine);
+    const uint32_t n = nmine ? (uint32_t)(E1 - E0) : 0u;
+    uint32_t bnd[SPW];  // local element index where set j0 + t starts (none: past every element)
+#pragma unroll
+    for (int t = 0; t < SPW; t++) {
+        const uint64_t o = __shfl_sync(0xFFFFFFFFu, offl, t);
+        bnd[t] = (uint32_t)t <= nmine ? (uint32_t)(o - E0) : 0xFFFFFFFFu;
+    }
+
+    // the first batch of ids is in flight while the rows are initialised
+    constexpr int kU = 8;
+    const uint32_t *ids = a.ids + E0;
+    uint32_t idn[kU];
+#pragma unroll
+    for (int u = 0; u < kU; u++) idn[u] = lane + 32u * u < n ? __ldg(ids + lane + 32u * u) : 0u;
+
+    const uint4 e4 = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    const uint32_t hinit = a.hder * a.kp;  // derived HOPH bins are written, not initialised (a multiple of 4)
+    for (int t = 0; t < SPW; t++) {
+        if ((uint32_t)t >= nmine) break;
+        uint4 *r = reinterpret_cast<uint4 *>(so + (size_t)(j0 + t) * kst);
+        for (uint32_t i = lane; i < kst / 4; i += 32u) r[i] = e4;
+        uint4 *h = reinterpret_cast<uint4 *>(sh + (size_t)(j0 + t) * hst);
+        for (uint32_t i = hinit / 4 + lane; i < hst / 4; i += 32u) h[i] = e4;
+    }
+    __syncwarp();
+
+    uint32_t kap[4], mu[4];
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        kap[r] = a.psi.kappa[r];
+        mu[r] = a.psi.mu[r];
+    }
+    const uint32_t mask = a.psi.mask, pshift = a.psi.shift, hmul = a.psi.hmul, hsh = a.psi.hsh;
+    const uint32_t fsh = a.flat.shift, fmask = (1u << a.flat.shift) - 1u;
+    const uint32_t vsh = 32u - a.log2V, Lm1 = a.L - 1u, lkp = a.log2kp, kpw = a.kp;
+    const uint32_t osh = 32u - a.log2V + a.log2kp, bsh = 32u - a.log2kp;
+    const uint32_t hthr = a.hder ? (0xFFFFFFFFu << (32u - a.hder)) : 0u;  // t >= hthr <=> group >= hder
+    const uint32_t so_w = smem_addr(so) + 4u * j0 * kst, sh_w = smem_addr(sh) + 4u * j0 * hst;
+
+    for (uint32_t base = 0; base < n; base += 32u * kU) {
+        uint32_t id[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) id[u] = idn[u];
+        const uint32_t nb = base + 32u * kU;
+        if (nb < n) {
+#pragma unroll
+            for (int u = 0; u < kU; u++) idn[u] = nb + lane + 32u * u < n ? __ldg(ids + nb + lane + 32u * u) : 0u;
+        }
+        // one element: both layouts' bin minima (hthr: only groups past the derived ones)
+        auto one = [&](uint32_t e, uint32_t x) {
+            uint32_t jl = 0;
+#pragma unroll
+            for (int t = 1; t < SPW; t++) jl += e >= bnd[t] ? 1u : 0u;
+            const uint32_t p = psi_pass<W32>(kap, mu, mask, pshift, hmul, hsh, x);
+            asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(so_w + 4u * (jl * kst + (p >> fsh))), "r"(p & fmask)
+                         : "memory");
+            // (branch-free: the HOPH update is predicated on t >= hthr, always true without derivation)
+            const uint32_t t = p << vsh;
+            const uint32_t g = min(clz_alu(~t), Lm1);
+            const uint32_t sc = g + (g < Lm1 ? 1u : 0u);
+            const uint32_t y = t << sc;
+            const uint32_t hb = y >> bsh;
+            const uint32_t ho = __funnelshift_rc(y << lkp, 0u, osh + sc);
+            asm volatile(
+                "{\n\t.reg .pred q;\n\tsetp.ge.u32 q, %2, %3;\n\t@q red.shared.min.u32 [%0], %1;\n}" ::"r"(
+                    sh_w + 4u * (jl * hst + g * kpw + hb)),
+                "r"(ho), "r"(t), "r"(hthr)
+                : "memory");
+        };
+        if (nb <= n) {  // a whole batch (warp-uniform): no per-element guard, so the 8 elements'
+                        // hashes interleave (the clz of the group lookup is a variable-latency op)
+#pragma unroll
+            for (int u = 0; u < kU; u++) one(base + lane + 32u * u, id[u]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < kU; u++) {
+                const uint32_t e = base + lane + 32u * u;
+                if (e < n) one(e, id[u]);
+            }
+        }
+    }
+    __syncwarp();
+
+    // derived HOPH groups: lane = 4 OPH bins b .. b+3 < k - k / 2^hder (one group: group
+    // boundaries are multiples of k / 2^hder >= k' >= 4); g = leading ones of b (log2 k
+    // bits), M_g = 2^lm OPH bins per HOPH bin, aligned
+    if (a.hder) {
+        const uint32_t log2k = a.log2V - fsh;
+        const uint32_t nq4 = (a.k - (a.k >> a.hder)) / 4u;
+        const uint32_t M0q = 1u << (log2k - lkp - 1u);  // M_0 (M_0 / 4 lanes per HOPH bin of group 0)
+        for (int t = 0; t < SPW; t++) {
+            if ((uint32_t)t >= nmine) break;
+            const uint4 *r4 = reinterpret_cast<const uint4 *>(so + (size_t)(j0 + t) * kst);
+            uint32_t *h = sh + (size_t)(j0 + t) * hst;
+            for (uint32_t q0 = 0; q0 < nq4; q0 += 32u) {
+                const uint32_t q = q0 + lane, b = 4u * q;
+                const bool in = q < nq4;
+                const uint4 v = in ? r4[q] : e4;
+                const uint32_t g = in ? (uint32_t)__clz(~(b << (32u - log2k))) : 0u;
+                const uint32_t lm = log2k - lkp - 1u - g;  // log2 M_g
+                const uint32_t M1 = (1u << lm) - 1u;
+                const uint32_t c0 = derive_cand(v.x, b & M1, fsh), c1 = derive_cand(v.y, (b + 1u) & M1, fsh);
+                const uint32_t c2 = derive_cand(v.z, (b + 2u) & M1, fsh), c3 = derive_cand(v.w, (b + 3u) & M1, fsh);
+                uint32_t c = min(min(c0, c1), min(c2, c3));
+                for (uint32_t d = 1; 4u * d < M0q; d <<= 1) {  // warp-uniform trip count
+                    const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, c, d);
+                    if (4u * d < (1u << lm)) c = min(c, o);
+                }
+                if (in) {
+                    const uint32_t hb = g * kpw + ((b - (a.k - (a.k >> g))) >> lm);
+                    if (lm >= 2) {
+                        if ((b & M1) == 0u) h[hb] = c;
+                    } else if (lm == 1) {
+                        *reinterpret_cast<uint2 *>(h + hb) = make_uint2(min(c0, c1), min(c2, c3));
+                    } else {
+                        *reinterpret_cast<uint4 *>(h + hb) = make_uint4(c0, c1, c2, c3);
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    write_sketch<SB>(so, kst, a.k, nloc, a.oph, a.oph_empty, a.ld, s0);
+    write_sketch<SB>(sh, hst, nbh, nloc, a.hoph, a.hoph_empty, a.ld, s0);
+}
+
 // ---------------------------------------------------------------------------
 // K2: MinWise build.  One CTA = 8 consecutive sets x all k permutations; a
 // thread owns permutation i (keys derived on the fly from the counter-based
@@ -1795,11 +1979,35 @@ cudaError_t launch_jaccard(const JaccardArgs &a, cudaStream_t st) {
 // launchers
 // ---------------------------------------------------------------------------
 template <int SB>
-static cudaError_t launch_build_sb(const BuildArgs &a, size_t smem, cudaStream_t st, uint32_t threads) {
-    const uint64_t grid = (a.n_sets + SB - 1) / SB;
-    const bool fast = a.do_flat && a.flat.pow2 && a.flat.start == 0 && a.psi.pow2 && !a.psi.identity && a.do_hier &&
-                      a.hier_pow2_halves && a.L <= 32 && a.log2kp >= 1;
-    const bool w32 = a.psi.mask == 0xFFFFFFFFu;
+static cudaError_t launch_build_sb(const BuildArgs &a0, size_t smem, cudaStream_t st, uint32_t threads) {
+    const uint64_t grid = (a0.n_sets + SB - 1) / SB;
+    const bool fast = a0.do_flat && a0.flat.pow2 && a0.flat.start == 0 && a0.psi.pow2 && !a0.psi.identity &&
+                      a0.do_hier && a0.hier_pow2_halves && a0.L <= 32 && a0.log2kp >= 1;
+    const bool w32 = a0.psi.mask == 0xFFFFFFFFu;
+    BuildArgs a = a0;
+    // the warp-per-set kernel (default; OPHGPU_BUILD_V1=1 keeps the element-strided one)
+    const char *v1 = getenv("OPHGPU_BUILD_V1");
+    const size_t smem_w = (size_t)SB * (build_warp_stride(a0.k) + build_warp_stride(a0.L * a0.kp)) * 4;
+    if constexpr (SB == 8 || SB == 16) if (fast && !(v1 && atoi(v1)) && smem_w <= 200 * 1024) {
+        const uint32_t log2k = a.log2V - a.flat.shift;
+        // derivable leading HOPH groups: g <= log2 k - log2 k' - 1 and g < L - 1; k' >= 4 (4-bin
+        // lanes); M_0 <= 128 (M_0 / 4 <= 32 lanes)
+        uint32_t hder = 0;
+        if (log2k > a.log2kp && a.log2kp >= 2 && log2k - a.log2kp - 1 <= 7) hder = std::min(log2k - a.log2kp, a.L - 1);
+        // (measured r02z3: the derivation halves the shared reductions but is not faster -- image-like
+        // 3.53 vs 3.49 ms, text-like 0.551 vs 0.538: the build is not bound by the shared-memory
+        // pipe (29 % of its wavefront peak) -- so it is an A/B option, OPHGPU_BUILD_DERIVE=1)
+        const char *dv = getenv("OPHGPU_BUILD_DERIVE");
+        if (!(dv && atoi(dv))) hder = 0;
+        a.hder = hder;
+        const uint32_t spw = threads == 256 ? 1u : 2u;  // 128 threads: 2 sets per warp at SB 8
+        auto kern = w32 ? (spw == 1 ? build_warp_kernel<true, SB, SB / 8> : build_warp_kernel<true, SB, SB / 4>)
+                        : (spw == 1 ? build_warp_kernel<false, SB, SB / 8> : build_warp_kernel<false, SB, SB / 4>);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w);
+        if (e != cudaSuccess) return e;
+        kern<<<(unsigned)grid, 32u * SB / (spw == 1 ? SB / 8 : SB / 4), smem_w, st>>>(a);
+        return cudaGetLastError();
+    }
     auto kern = fast ? (w32 ? build_kernel<true, SB, true> : build_kernel<false, SB, true>)
                      : (w32 ? build_kernel<true, SB, false> : build_kernel<false, SB, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

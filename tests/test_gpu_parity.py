@@ -1041,3 +1041,38 @@ def test_hoph_empty_aware_ragged(V, hkp, seed):
         kw = dict(t_num=7, t_den=10, eps=1e-4, joint=joint)
         assert_records_equal(gpu_dense("hoph_e", qh, sh, layout=hier, **kw),
                              oracle_records("hoph_e", QH, H, kprime=hkp, L=len(glay), **kw), f"hoph_e {V}")
+
+
+# ----------------------------------------------------------------------------- build kernel variants (r02)
+@pytest.mark.parametrize("V,k,hkp", [(1 << 16, 64, 16), (1 << 20, 512, 32), (1 << 32, 256, 32), (1 << 20, 512, 8),
+                                     (1 << 20, 1024, 8), (1 << 12, 64, 2), (1 << 24, 32, 32), (1 << 16, 256, 4),
+                                     (1 << 22, 2048, 8)])
+@pytest.mark.parametrize("variant", ["default", "derive", "v1", "sb16_256", "sb8_256_derive"])
+def test_build_variants_bit_exact(V, k, hkp, variant, monkeypatch):
+    """Every build kernel of the power-of-two layout (warp-per-set, the same with the
+    leading HOPH groups derived from the OPH minima (OPHGPU_BUILD_DERIVE), the r01
+    element-strided kernel; tiles of 8 / 16 sets, 128 / 256 threads) gives the
+    oracle's OPH and HOPH sketches.  Layouts span M_0 = k / 2k' OPH bins per derived
+    HOPH bin of 2 .. 128 (lanes of 4 OPH bins: 1 .. 32 lanes per HOPH bin), k' < 4 (derivation
+    off) and no derivable group at all."""
+    env = dict(derive={"OPHGPU_BUILD_DERIVE": "1"}, v1={"OPHGPU_BUILD_V1": "1"},
+               sb16_256={"OPHGPU_BUILD_SB": "16", "OPHGPU_BUILD_THREADS": "256"},
+               sb8_256_derive={"OPHGPU_BUILD_THREADS": "256", "OPHGPU_BUILD_DERIVE": "1"}).get(variant, {})
+    for kk, vv in env.items():
+        monkeypatch.setenv(kk, vv)
+    rng = np.random.default_rng(V % 1000 + k + hkp)
+    nset = 1037  # not a multiple of 8 / 16 sets per tile
+    sizes = rng.integers(0, 900, size=nset)
+    sizes[[0, 5, 6, 7, 8, 100]] = 0  # empty sets inside a warp's pair, a whole empty tile row
+    sizes[9] = 5000
+    sets = [np.sort(rng.choice(V, size=min(int(s), V), replace=False)) if s else [] for s in sizes]
+    offs, ids = make_csr(sets)
+    hier = og.oph_hier_layout_make(V, 1, 1, hkp)
+    _, so, sh = gpu_build(offs, ids, V, 11, k=k, kprime=8, hier=hier)
+    F = oracle.oph_sketch(offs, ids, V, k, 11)
+    glay = oracle.hoph_layout(V, 1, 1, hkp)
+    H = oracle.hoph_sketch(offs, ids, V, glay, hkp, 11)
+    assert (so.numpy() == F).all()
+    assert (so.empty_numpy() == masks_from_values(F)).all()
+    assert (sh.numpy() == H).all()
+    assert (sh.empty_numpy() == masks_from_values(H)).all()
