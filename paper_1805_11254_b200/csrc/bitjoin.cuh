@@ -178,11 +178,26 @@ __device__ __forceinline__ void bit_tile_load(const BitArgs &a, uint64_t tile, u
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
+// termination histogram in shared memory (one global add per level per CTA at the end; a
+// global add per warp and set serialises on the histogram words in L2)
+__device__ __forceinline__ void shist_add(unsigned long long *s_hist, const unsigned long long *g, uint32_t level,
+                                          uint32_t n) {
+    if (!g) return;
+    const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, n);
+    if ((threadIdx.x & 31u) == 0 && tot) atomicAdd(s_hist + level, (unsigned long long)tot);
+}
+__device__ __forceinline__ void shist_flush(const unsigned long long *s_hist, unsigned long long *g) {
+    if (!g) return;
+    __syncthreads();
+    if (threadIdx.x <= kMaxGroups && s_hist[threadIdx.x]) atomicAdd(g + threadIdx.x, s_hist[threadIdx.x]);
+}
+
 // Per-set software pipeline (full OPH, GOPH), blocks of 1,024 queries.
 template <int MINB>
 __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __grid_constant__ BitArgs a) {
     __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
     __shared__ uint64_t s_full[kBitMaxStages];
+    __shared__ unsigned long long s_hist[kMaxGroups + 1];
     __shared__ uint32_t s_done[kBitMaxStages];
     extern __shared__ __align__(128) uint32_t s_vals[];  // [2][npre][8]
     for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
@@ -203,6 +218,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
     // aligned and in bounds; sets past n_sets are never scored)
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
     const uint32_t vstride = a.npre * 8u;  // words per buffer
+    if (threadIdx.x <= kMaxGroups) s_hist[threadIdx.x] = 0ull;
     if (threadIdx.x == 0) {
         for (uint32_t i = 0; i < a.nstage; i++) {
             mbar_init(&s_full[i], 32);  // the 32 lanes of the filling warp
@@ -302,7 +318,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
                 dec = acc | (R >= 0 ? ~sliced_ge<kBitCS>(c, (uint32_t)R + 1u) : 0u);
                 acc &= alive;
                 dec &= alive;
-                hist_add(a.out.hist, l, __popc(dec));
+                shist_add(s_hist, a.out.hist, l, __popc(dec));
                 uint32_t want = a.out.dense ? dec : acc;
                 while (__any_sync(0xFFFFFFFFu, want != 0u)) {
                     const bool has = want != 0u;
@@ -325,7 +341,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
                 return false;
             }
             // ---- the final verdict of every pair still alive
-            hist_add(a.out.hist, a.level_final, __popc(alive));
+            shist_add(s_hist, a.out.hist, a.level_final, __popc(alive));
             {
                 // full-OPH verdict (Eq. 6): den = k - N_excl >= k - (max_q |Eq| + |Es|) (EitherEmpty)
                 // or k - min(max_q |Eq|, |Es|) (JointEmpty), so a pair can only be Similar if
@@ -365,6 +381,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_kernel(const __
         }
         release();
     }
+    shist_flush(s_hist, a.out.hist);
 }
 
 // Full OPH / GOPH with QW query words per lane (QW = 2: blocks of 2,048 queries, rows of
@@ -375,6 +392,7 @@ template <int QW, int MINB, bool ALLSTAGED>
 __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_q_kernel(const __grid_constant__ BitArgs a) {
     __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
     __shared__ uint64_t s_full[kBitMaxStages];
+    __shared__ unsigned long long s_hist[kMaxGroups + 1];
     __shared__ uint32_t s_done[kBitMaxStages];
     extern __shared__ __align__(128) uint32_t s_vals[];  // [nstage][npre][8]
     for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
@@ -397,6 +415,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_q_kernel(const 
     const uint32_t bins_per_level = a.method == kGoph ? a.kp : a.nscan;
     const uint64_t ntiles = (a.n_sets - a.s_begin + kBitWarps - 1) / kBitWarps;
     const uint32_t vstride = a.npre * 8u;  // words per buffer
+    if (threadIdx.x <= kMaxGroups) s_hist[threadIdx.x] = 0ull;
     if (threadIdx.x == 0) {
         for (uint32_t i = 0; i < a.nstage; i++) {
             mbar_init(&s_full[i], 32);  // the 32 lanes of the filling warp
@@ -503,7 +522,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_q_kernel(const 
                     uint32_t dec = acc | (R >= 0 ? ~sliced_ge<kBitCS>(c[w], (uint32_t)R + 1u) : 0u);
                     acc &= alive[w];
                     dec &= alive[w];
-                    hist_add(a.out.hist, l, __popc(dec));
+                    shist_add(s_hist, a.out.hist, l, __popc(dec));
                     uint32_t want = a.out.dense ? dec : acc;
                     while (__any_sync(0xFFFFFFFFu, want != 0u)) {
                         const bool has = want != 0u;
@@ -538,7 +557,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_q_kernel(const 
             const uint32_t k = a.nbins_total;
 #pragma unroll
             for (int w = 0; w < QW; w++) {
-                hist_add(a.out.hist, a.level_final, __popc(alive[w]));
+                shist_add(s_hist, a.out.hist, a.level_final, __popc(alive[w]));
                 const uint32_t den_min = a.joint ? k - min(max_eq[w], es) : k - min(k, max_eq[w] + es);
                 const uint32_t theta =
                     a.out.dense ? 0u : (uint32_t)(((uint64_t)a.t_num * den_min + a.t_den - 1) / a.t_den);
@@ -570,6 +589,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_q_kernel(const 
         }
         release();
     }
+    shist_flush(s_hist, a.out.hist);
 }
 
 // HOPH (1:1): group 1 by the bitmap join in blocks of 2,048 queries (two words per lane) with
@@ -719,6 +739,9 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_x_kernel(const 
     };
 
     // ---- stage C: count item (tiC, bjC); after group 1, decide and walk the undecided pairs
+    // (h1: this lane's pairs decided at level 1 -- a global atomic per warp and set on the one
+    // histogram word serialised in L2: 4·10^6 same-address adds per image-like call)
+    unsigned long long h1 = 0;
     uint64_t tiC = 0;
     uint32_t bjC = 0;
     uint32_t c[QW][kBitCS];
@@ -743,7 +766,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_x_kernel(const 
         for (int w = 0; w < QW; w++) {
             uint32_t acc = sliced_ge<6>(c[w], A) & qvalid[w];
             uint32_t dec = (acc | (R >= 0 ? ~sliced_ge<6>(c[w], (uint32_t)R + 1u) : 0u)) & qvalid[w];
-            hist_add(a.out.hist, 1, __popc(dec));
+            h1 += __popc(dec);  // (per lane; one global add per warp at the end, not per set)
             uint32_t want = a.out.dense ? dec : acc;
             while (__any_sync(0xFFFFFFFFu, want != 0u)) {
                 const bool has = want != 0u;
@@ -788,6 +811,10 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_x_kernel(const 
             step(g, x, xb);
             if (g + 1 < nitems) step(g + 1, xb, x);
         }
+    }
+    if (a.out.hist) {
+        const unsigned long long tot = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)h1);  // < 2^32 per warp
+        if (lane == 0 && tot) atomicAdd(a.out.hist + 1, tot);
     }
 }
 
