@@ -148,6 +148,7 @@ struct ProbeArgs {
     const uint32_t *bloom;
     uint32_t log2S, nscan, log2W;
     uint32_t R;             // sets per CTA (multiple of 32; set by launch_probe)
+    uint32_t nlist;         // matched-query list entries per set, 2 or kJoinList (set by launch_probe)
     const uint32_t *QEM;    // query masks, query-major [n_q][nw]
     const uint8_t *qflags;  // MinWise query flags, indexed by global query
     uint32_t nw, nbins_total;

@@ -1134,12 +1134,12 @@ struct JoinLayout {
     uint32_t bars, tab, lists, ovf, queue, qcount, total;
 };
 __host__ __device__ inline uint32_t join_align(uint32_t x) { return (x + 127u) & ~127u; }
-__host__ __device__ inline JoinLayout join_layout(uint32_t W, uint32_t R) {
+__host__ __device__ inline JoinLayout join_layout(uint32_t W, uint32_t R, uint32_t nlist) {
     JoinLayout L;
     L.bars = 0;
     L.tab = 128;
     L.lists = L.tab + 2 * kJoinSlabWords * 4;
-    L.ovf = join_align(L.lists + kJoinList * R * 4);
+    L.ovf = join_align(L.lists + nlist * R * 4);
     L.queue = join_align(L.ovf + R / 8);
     L.qcount = L.queue + kJoinWarps * kJoinQCap * 4;  // per slab: tile counter, done counter
     L.total = join_align(L.qcount + 2 * kJoinMaxSlabs * 4);
@@ -1148,10 +1148,12 @@ __host__ __device__ inline JoinLayout join_layout(uint32_t W, uint32_t R) {
 
 // count one more matched bin of query q for the set at local index sl:
 // list entry = (q + 1) << 16 | count, 0 = free; a full list flags the set
-__device__ __forceinline__ void list_add(uint32_t *lists, uint32_t R, uint32_t *ovf, uint32_t sl, uint32_t q) {
+__device__ __forceinline__ void list_add(uint32_t *lists, uint32_t R, uint32_t nlist, uint32_t *ovf, uint32_t sl,
+                                         uint32_t q) {
     const uint32_t key = (q + 1u) << 16;
 #pragma unroll
     for (int e = 0; e < kJoinList; e++) {
+        if ((uint32_t)e == nlist) break;
         uint32_t *p = lists + e * R + sl;
         uint32_t x = *(volatile uint32_t *)p;
         for (;;) {
@@ -1200,7 +1202,7 @@ __device__ __noinline__ void join_flush(const ProbeArgs &a, uint64_t s_lo, uint3
         unsigned long long sl8 = slot[r];
         uint32_t h = probe_hash(v[r], a.log2S);
         while (sl8 != 0ull) {
-            if ((uint32_t)(sl8 >> 32) == v[r]) list_add(lists, a.R, ovf, c[r] & 0xFFFFu, (uint32_t)sl8 - 1u);
+            if ((uint32_t)(sl8 >> 32) == v[r]) list_add(lists, a.R, a.nlist, ovf, c[r] & 0xFFFFu, (uint32_t)sl8 - 1u);
             h = (h + 1) & smask;
             sl8 = __ldg(T + h);
         }
@@ -1282,10 +1284,10 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
     constexpr uint32_t SBN = kJoinSlabWords / W;   // bins per slab: 32 / 16 / 8
     static_assert(SBN % kJoinRPT == 0, "a slab holds whole tile row blocks");
     const uint32_t R = a.R;
-    const JoinLayout Ly = join_layout(W, R);
+    const JoinLayout Ly = join_layout(W, R, a.nlist);
     uint64_t *tfull = reinterpret_cast<uint64_t *>(jsm + Ly.bars);
     uint32_t *tab = reinterpret_cast<uint32_t *>(jsm + Ly.tab);      // [2][32][W]
-    uint32_t *lists = reinterpret_cast<uint32_t *>(jsm + Ly.lists);  // [kJoinList][R]
+    uint32_t *lists = reinterpret_cast<uint32_t *>(jsm + Ly.lists);  // [nlist][R]
     uint32_t *ovf = reinterpret_cast<uint32_t *>(jsm + Ly.ovf);      // [R / 32]
     uint32_t *queue = reinterpret_cast<uint32_t *>(jsm + Ly.queue);  // [kJoinWarps][kJoinQCap]
     uint32_t *tctl = reinterpret_cast<uint32_t *>(jsm + Ly.qcount);  // per slab: next tile, warps done
@@ -1296,7 +1298,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
     const uint32_t nslab = (a.nscan + SBN - 1) / SBN;
     const uint32_t slab_bytes = kJoinSlabWords * 4u;
 
-    for (uint32_t x = threadIdx.x; x < kJoinList * R; x += blockDim.x) lists[x] = 0u;
+    for (uint32_t x = threadIdx.x; x < a.nlist * R; x += blockDim.x) lists[x] = 0u;
     for (uint32_t x = threadIdx.x; x < R / 32; x += blockDim.x) ovf[x] = 0u;
     for (uint32_t x = threadIdx.x; x < 2 * nslab; x += blockDim.x) tctl[x] = 0u;
     if (threadIdx.x == 0) {
@@ -1420,7 +1422,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) join_kernel(const __grid_cons
         }
         uint32_t n_surv = 0;  // this set's pairs that go on to the next level
 #pragma unroll 1
-        for (int e = 0; e < kJoinList; e++) {
+        for (int e = 0; e < (int)a.nlist; e++) {
             const uint32_t x = (act && !of) ? lists[e * R + sl] : 0u;
             const bool has = x != 0u;
             if (!__any_sync(0xFFFFFFFFu, has)) break;
@@ -2131,13 +2133,37 @@ cudaError_t launch_probe(const ProbeArgs &a0, cudaStream_t st) {
     const uint32_t W = 0;  // the layout does not depend on the filter width (64-KB buffers)
     constexpr uint32_t kSmemMax = 227 * 1024;
     // one CTA per SM; sets per CTA: the fewest waves whose per-CTA lists fit next to
-    // the filter double buffer, split evenly (multiple of the tile's kJoinTile sets)
-    uint32_t Rmax = kJoinTile;
-    while (join_layout(W, Rmax + kJoinTile).total <= kSmemMax && Rmax + kJoinTile <= 65504) Rmax += kJoinTile;
-    const uint64_t waves = (n + 148ull * Rmax - 1) / (148ull * Rmax);
+    // the filter double buffer, split evenly (multiple of the tile's kJoinTile sets).  Lists
+    // of 2 matched queries per set instead of kJoinList when that saves a wave and at most 128
+    // bins are scanned (scale shard, GOPH / HOPH: 1.25M sets in one wave instead of two, 0.72 ->
+    // 0.70 / 0.68 -> 0.64 ms per call; full OPH's 256 bins give enough sets 3+ spurious
+    // single-bin matches that the BRUTE list scan of the overflow, 8 -> 366 us, eats the gain).
+    // A set matching more queries goes to that scan either way: the records do not change.
+    // OPHGPU_JOIN_LISTS=2|4 forces the choice (A/B).
+    auto rmax_for = [&](uint32_t nl) {
+        uint32_t r = kJoinTile;
+        while (join_layout(W, r + kJoinTile, nl).total <= kSmemMax && r + kJoinTile <= 65504) r += kJoinTile;
+        return r;
+    };
+    auto waves_for = [&](uint32_t rm) { return (n + 148ull * rm - 1) / (148ull * rm); };
+    uint32_t nlist = kJoinList;
+    uint32_t Rmax = rmax_for(nlist);
+    if (a.nscan <= 128 && waves_for(Rmax) > 1 && waves_for(rmax_for(2)) < waves_for(Rmax)) {
+        nlist = 2;
+        Rmax = rmax_for(2);
+    }
+    if (const char *e = getenv("OPHGPU_JOIN_LISTS")) {
+        const int v = atoi(e);
+        if (v == 2 || v == kJoinList) {
+            nlist = (uint32_t)v;
+            Rmax = rmax_for(nlist);
+        }
+    }
+    const uint64_t waves = waves_for(Rmax);
     const uint32_t R = (uint32_t)((((n + 148 * waves - 1) / (148 * waves)) + kJoinTile - 1) / kJoinTile * kJoinTile);
     a.R = R;
-    const size_t smem = join_layout(W, R).total;
+    a.nlist = nlist;
+    const size_t smem = join_layout(W, R, nlist).total;
     if (smem > kSmemMax) return cudaErrorInvalidConfiguration;
     const bool mw = a.method == kMinwise;
     auto kern = mw ? join_kernel<true, 9> : join_kernel<false, 9>;

@@ -19,6 +19,8 @@ ap.add_argument("--variant", type=int, default=0, help="1: the empty-aware GOPH 
 args = ap.parse_args()
 if args.config == "text":
     w = text_like()
+elif args.config == "scale":
+    w = gen_gpu.scale_shard()
 elif args.config.startswith("sweep"):
     w = gen_gpu.sweep(float(args.config[5:]))
 else:
