@@ -473,8 +473,12 @@ oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketche
     // bins staged per CTA tile: all (GOPH staging only up to level l0 + 1 measured 13.5 vs
     // 12.9 ms on image-like: the branch-free all-staged lookup wins)
     ba.npre = ba.nscan;
-    // short staged tiles (HOPH: one group) need more of them in flight: ~32 KB of staged values
-    ba.nstage = std::max<uint32_t>(2, std::min<uint32_t>(8, 32768 / (ba.npre * 32)));
+    // short staged tiles (HOPH: one group) need more of them in flight: ~48 KB of staged values
+    // per CTA (r02z17 A/B, image-like full OPH: 32 KB 16.02 ms, 48 KB 15.91, 64 KB 15.88, 96 KB
+    // 18.10 -- one CTA per SM; GOPH / HOPH flat); OPHGPU_BIT_STAGE_KB overrides the budget
+    static const uint32_t stage_bytes =
+        getenv("OPHGPU_BIT_STAGE_KB") ? 1024u * (uint32_t)atoi(getenv("OPHGPU_BIT_STAGE_KB")) : 49152u;
+    ba.nstage = std::max<uint32_t>(2, std::min<uint32_t>(8, stage_bytes / (ba.npre * 32)));
     ba.kp = kp;
     ba.nbins_total = nb;
     ba.method = method;
@@ -542,7 +546,7 @@ oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketche
                 ba.pipe = 1;
                 ba.level_b = Lb;
                 ba.nscan = ba.npre = Lb * kp;
-                ba.nstage = std::max<uint32_t>(2, std::min<uint32_t>(8, 32768 / (ba.npre * 32)));
+                ba.nstage = std::max<uint32_t>(2, std::min<uint32_t>(8, stage_bytes / (ba.npre * 32)));
             }
         }
     }
