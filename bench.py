@@ -343,11 +343,15 @@ def run_ours(args):
     counts = torch.zeros((4,), dtype=torch.int64, device="cuda")
     # termination-level histograms of the four scorings (include/ophgpu.h d_stop_hist), per step
     hists = torch.zeros((4, og.OPH_STOP_HIST_LEN), dtype=torch.int64, device="cuda")
+    # (set, bin) rows gathered by the BITMAP pipeline scans per step (include/ophgpu.h d_bins_scanned):
+    # the measured algorithmic work of full OPH's scan, which stops a set once no pair can reach T
+    scanned = torch.zeros((4,), dtype=torch.int64, device="cuda")
     res = []
     for i in range(4):
         r = og.Results(cap)
         r.count = counts[i:i + 1]
         r.stop_hist = hists[i]
+        r.bins_scanned = scanned[i:i + 1]
         res.append(r)
     surv_cap = min(((Q + 31) // 32) * 32 * N, surv_limit)
     ws = [og.Workspace() for _ in range(5)]
@@ -382,6 +386,7 @@ def run_ours(args):
         mark(ev, 0)
         counts[:3].zero_()
         hists[:3].zero_()
+        scanned[:3].zero_()
         nvtx.range_push("build_oph_hoph")
         og.oph_build_sketches(sets, V, seed, flat=flat, hier=hier, out_oph=so, out_hoph=sh)
         nvtx.range_pop()
@@ -498,6 +503,7 @@ def run_ours(args):
     def step_dev():
         counts[:3].zero_()
         hists[:3].zero_()
+        scanned[:3].zero_()
         og.oph_build_sketches(sets, V, seed, flat=flat, hier=hier, out_oph=so, out_hoph=sh)
         og.oph_build_sketches(qsets, V, seed, flat=flat, hier=hier, out_oph=qo, out_hoph=qh)
         og.compare_full(qo, so, flat, prm, res[0], set_id_base=base, ws=ws[0])
@@ -536,6 +542,7 @@ def run_ours(args):
     ms, evs, hits_last, clk = timed(step, K, 7, ClockSampler(dev))
     phase_ms = {n: statistics.mean(evs[i][a].elapsed_time(evs[i][b]) for i in range(K)) for n, a, b in phase_ev}
     hh = hists.cpu().numpy().copy()
+    scanned_step = [int(x) for x in scanned.cpu()]  # (last eager step)
     ms_eager = ms
     if graph is not None:
         for _ in range(2):
@@ -688,6 +695,11 @@ def run_ours(args):
             m = phase.split("_")[1]
             bins = (bins_compared.get(m, Q * N * k) / Q) if m != "full" else N * k  # (set, bin) pairs scanned
             gathered = bins * -(-Q // (1024 * qwords)) * (row + 4)
+            # the pipelined scans count the rows they gathered (d_bins_scanned, over all blocks):
+            # measured work instead of the model (full OPH's exit, R32; GOPH's levels 1 .. l0 + 1)
+            ph_i = {"full": 0, "goph": 1}.get(m)
+            if kernel.startswith("bit_pipe") and ph_i is not None and scanned_step[ph_i] > 0:
+                gathered = scanned_step[ph_i] * (row + 4)
             peak = l2_peak_for(row)
             nonlocal l2_src
             l2_src = (f"measured: scripts/ubench.cu random {row}-B row gathers, 16-MB table "

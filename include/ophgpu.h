@@ -244,6 +244,12 @@ typedef struct {
     uint32_t mode;
     uint32_t pad;
     unsigned long long *d_stop_hist;
+    /* d_bins_scanned (optional, may be NULL; r02): the call ADDS the number of (set, bin)
+     * value rows its pipelined BITMAP scan (full OPH; GOPH's levels 1 .. l0+1) gathered,
+     * summed over its query blocks of 2,048 -- that scan's algorithmic work (full OPH in
+     * threshold mode stops gathering a set's rows once no pair of the block can reach T even
+     * if every remaining non-empty bin matched; R32).  Other scans leave it unchanged. */
+    unsigned long long *d_bins_scanned;
 } oph_results;
 
 /* ---------------------------------------------------------------- host helpers */

@@ -73,7 +73,7 @@ class oph_params(ctypes.Structure):
 
 class oph_results(ctypes.Structure):
     _fields_ = [("d_hits", c_vp), ("capacity", c_u64), ("d_count", c_vp), ("mode", c_u32), ("pad", c_u32),
-                ("d_stop_hist", c_vp)]
+                ("d_stop_hist", c_vp), ("d_bins_scanned", c_vp)]
 
 
 OPH_STOP_HIST_LEN = 65  # include/ophgpu.h: OPH_MAX_GROUPS + 1
@@ -292,7 +292,7 @@ def _minwise_build_sketches_impl(sets: SetCollection, vocab_size: int, seed: int
 class Results:
     """A result sink: `capacity` oph_hit records + a device counter."""
 
-    def __init__(self, capacity: int, dense: bool = False, stop_hist: bool = False):
+    def __init__(self, capacity: int, dense: bool = False, stop_hist: bool = False, bins_scanned: bool = False):
         torch = _torch()
         self.capacity = int(capacity)
         self.mode = OPH_RES_DENSE if dense else OPH_RES_THRESHOLD
@@ -300,15 +300,20 @@ class Results:
         self.count = torch.zeros((1,), dtype=torch.int64, device="cuda")
         # termination-level histogram (include/ophgpu.h d_stop_hist), accumulated over calls
         self.stop_hist = torch.zeros((OPH_STOP_HIST_LEN,), dtype=torch.int64, device="cuda") if stop_hist else None
+        # (set, bin) rows gathered by BITMAP scans (include/ophgpu.h d_bins_scanned), accumulated
+        self.bins_scanned = torch.zeros((1,), dtype=torch.int64, device="cuda") if bins_scanned else None
 
     def reset(self):
         self.count.zero_()
         if self.stop_hist is not None:
             self.stop_hist.zero_()
+        if self.bins_scanned is not None:
+            self.bins_scanned.zero_()
 
     def c(self) -> oph_results:
         return oph_results(_ptr(self.hits), self.capacity, _ptr(self.count), self.mode, 0,
-                           _ptr(self.stop_hist) if self.stop_hist is not None else None)
+                           _ptr(self.stop_hist) if self.stop_hist is not None else None,
+                           _ptr(self.bins_scanned) if getattr(self, "bins_scanned", None) is not None else None)
 
     def hist(self) -> np.ndarray:
         """The termination-level histogram (synchronises)."""

@@ -959,6 +959,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_pipe_kernel(const __
 #pragma unroll
         for (int i = 0; i < (int)kBitCS; i++) c[w][i] = 0u;
     uint32_t pend = 0u, n_final = 0u;
+    uint32_t n_gathered = 0;  // row batches this warp gathered (oph_results.d_bins_scanned)
     uint32_t alive[2] = {qvalid[0], qvalid[1]};
     uint32_t lev = 1, lend = a.kp / 16u;  // GOPH: the level being counted, the batch it ends at
     uint32_t gb = 0;                      // batches of the warp's earlier sets (ring slots)
@@ -1028,10 +1029,80 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_pipe_kernel(const __
         uint32_t es_w = 0;
         if (s < a.n_sets) es_w = lane < a.nw ? __ldg(a.E + (uint64_t)lane * a.ld + s) : 0u;
         uint32_t j = 0;
+        bool early = false;
+        uint32_t theta = 0u;  // full OPH exit: a lower bound on the thresholds of the block's queries
         for (; j + 4 < nbs; j += 2) {
             step(j, x, xb, look(slot, j + 3));
             step(j + 1, xb, x, look(slot, j + 4));
+            if constexpr (!GOPH) {
+                // R32: after B = 16 (j + 2) bins a pair can still reach T only if its count plus the
+                // set's non-empty bins in [B, k) reaches its threshold; theta = ceil(T den_min)
+                // with den_min from the largest query-empty count of the lane's two words is a
+                // lower bound on it (as in the final filter below; one register: per-word bounds
+                // cost spills, 14.55 vs 13.86 ms).  No such pair in the block: the set is done --
+                // every pair is NotSimilar, and threshold results emit nothing for them.
+                const uint32_t B = 16u * (j + 2);
+                if (a.exit_from && B >= a.exit_from && (B & 63u) == 0u && B < a.nbins_total) {
+                    const uint32_t k = a.nbins_total;
+                    if (theta == 0u) {  // (the lane's two words share one bound: one register)
+                        const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, k));
+                        const uint32_t me = max(max_eq[0], max_eq[1]);
+                        const uint32_t den_min = a.joint ? k - min(me, es) : k - min(k, me + es);
+                        theta = max(1u, (uint32_t)(((uint64_t)a.t_num * den_min + a.t_den - 1) / a.t_den));
+                    }
+                    const uint32_t emp = __reduce_add_sync(
+                        0xFFFFFFFFu, (lane < a.nw && 32u * lane >= B) ? popc_masked(0u, es_w, 0, lane, k) : 0u);
+                    const uint32_t rem = (k - B) - emp;  // the set's non-empty bins not counted yet
+                    bool cand = false;
+#pragma unroll
+                    for (int w = 0; w < 2; w++)
+                        cand |= (theta <= rem ? qvalid[w] : (sliced_ge<kBitCS>(c[w], theta - rem) & qvalid[w])) != 0u;
+                    if (!__any_sync(0xFFFFFFFFu, cand)) {
+                        early = true;
+                        break;
+                    }
+                }
+            }
         }
+        if (!GOPH && early) {
+            // release the tile (every lookup this set issued has read its staged value), start
+            // the next set's pipeline afresh (its lookups 0-2, rows of batch 0), count the pairs
+            // as decided at the last level (the histogram of full OPH, as the paper's method)
+            __syncwarp();
+            uint32_t last = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                last = atomicAdd(&s_done[slot], 1u) == kBitWarps - 1;
+                if (last) s_done[slot] = 0u;
+            }
+            last = __shfl_sync(0xFFFFFFFFu, last, 0);
+            const uint64_t tn = tile + (uint64_t)a.nstage * gridDim.x;
+            if (last && tn < ntiles) bit_tile_load(a, tn, s_vals + slot * vstride, &s_full[slot], lane);
+            const bool more = it + 1 < n_it;
+            if (++slot == a.nstage) {
+                slot = 0;
+                phase ^= 1u;
+            }
+            if (more) {
+                mbar_wait(&s_full[slot], phase);
+                const uint32_t r0 = look(slot, 0), r1 = look(slot, 1);
+                pend = look(slot, 2);
+                if (lane < 16u) {
+                    ring[lane] = r0;
+                    ring[16u + lane] = r1;
+                }
+                __syncwarp();
+                rows(0, x);
+            }
+            if (s < a.n_sets) n_final += __popc(qvalid[0]) + __popc(qvalid[1]);
+            if (s < a.n_sets) n_gathered += j + 3;  // row batches issued for this set: 0 .. j + 2
+#pragma unroll
+            for (int w = 0; w < 2; w++)
+#pragma unroll
+                for (int i = 0; i < (int)kBitCS; i++) c[w][i] = 0u;
+            continue;
+        }
+        if (s < a.n_sets) n_gathered += nbs;
         // j = nbs - 4: the set's last lookup, then its tile is released and the next one awaited
         step(j, x, xb, look(slot, j + 3));
         {
@@ -1112,6 +1183,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_pipe_kernel(const __
             gb += nbs;
         }
     }
+    if (a.scanned && lane == 0 && n_gathered) atomicAdd(a.scanned, 16ull * n_gathered);
     if (a.out.hist) {
         const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, n_final);
         if (lane == 0 && tot) atomicAdd(&s_hist[a.level_final], (unsigned long long)tot);

@@ -1076,3 +1076,32 @@ def test_build_variants_bit_exact(V, k, hkp, variant, monkeypatch):
     assert (so.empty_numpy() == masks_from_values(F)).all()
     assert (sh.numpy() == H).all()
     assert (sh.empty_numpy() == masks_from_values(H)).all()
+
+
+@pytest.mark.parametrize("joint", [False, True])
+def test_full_oph_exit_exact(image_small, monkeypatch, joint):
+    """R32: full OPH's BITMAP scan stops a set once no pair of the query block can reach T
+    (count + the set's non-empty bins left < a lower bound of every threshold).  The threshold
+    list and the histogram are byte-identical to the scan of every bin (OPHGPU_FULL_EXIT=0)
+    and to the oracle; d_bins_scanned counts the rows gathered: every (set, bin) of both
+    query blocks without the exit, fewer with it."""
+    r, o, p = image_small, image_small["orc"], image_small["p"]
+    q, s = r["qo"], r["so"]
+    lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
+    prm = og.params(p["t_num"], p["t_den"], p["eps"], joint, og.OPH_STRATEGY_BITMAP)
+    runs = {}
+    for env in ("1", "0"):
+        monkeypatch.setenv("OPHGPU_FULL_EXIT", env)
+        res = og.Results(1 << 22, stop_hist=True, bins_scanned=True)
+        og.compare_full(q, s, lay, prm, res)
+        n = res.n()
+        out = og.Results(max(n, 1))
+        og.topk_or_threshold_results(res, n, og.OPH_SELECT_THRESHOLD, out)
+        runs[env] = (out.numpy(n).tobytes(), res.hist().tobytes(), int(res.bins_scanned.item()), n)
+    want = oracle_records("full", o["QF"], o["F"], k=p["k"], kprime=p["kprime"], t_num=p["t_num"],
+                          t_den=p["t_den"], eps=p["eps"], joint=joint)
+    assert runs["1"][0] == runs["0"][0] and runs["1"][1] == runs["0"][1]
+    assert runs["1"][3] == len(oracle.threshold_list(want)) > 0
+    blocks = -(-q.n_sets // 2048)
+    assert runs["0"][2] == s.n_sets * p["k"] * blocks
+    assert 0 < runs["1"][2] < runs["0"][2]
