@@ -1042,7 +1042,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_pipe_kernel(const __
                 // cost spills, 14.55 vs 13.86 ms).  No such pair in the block: the set is done --
                 // every pair is NotSimilar, and threshold results emit nothing for them.
                 const uint32_t B = 16u * (j + 2);
-                if (a.exit_from && B >= a.exit_from && (B & 63u) == 0u && B < a.nbins_total) {
+                if (a.exit_from && B >= a.exit_from && (B & 31u) == 0u && B < a.nbins_total) {
                     const uint32_t k = a.nbins_total;
                     if (theta == 0u) {  // (the lane's two words share one bound: one register)
                         const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, k));
