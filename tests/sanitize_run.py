@@ -70,6 +70,28 @@ def main():
     offs = torch.tensor(np.cumsum([0] + [len(d) for d in docs]), dtype=torch.int64, device="cuda")
     sh_sets = og.shingle_text(text, offs, 3, 1 << 20, 7)
     total += int(sh_sets.n_sets)
+    # BITMAP at image-like widths (k = 512, two 2,048-query blocks, the second ragged): the
+    # pipelined full-OPH scan with its exact exit (R32) and GOPH / HOPH, plus the r02 build
+    # kernel (warp per set) with and without the derived HOPH groups
+    from workloads import gen
+    wi = gen.image_like(n_sets=3000, n_queries=2100, planted_per_query=0)
+    pi = wi.params
+    Vi, si_ = wi.vocab_size, pi["perm_seed"]
+    hier_i = og.oph_hier_layout_make(Vi, 1, 1, pi["hoph_kprime"])
+    flat_i = og.flat_layout(Vi, pi["k"], pi["kprime"])
+    sets_i = og.SetCollection.from_numpy(wi.offsets, wi.ids)
+    qs_i = og.SetCollection.from_numpy(wi.q_offsets, wi.q_ids)
+    for derive in ("0", "1"):
+        os.environ["OPHGPU_BUILD_DERIVE"] = derive
+        so_i, sh_i = og.oph_build_sketches(sets_i, Vi, si_, flat=flat_i, hier=hier_i)
+    os.environ.pop("OPHGPU_BUILD_DERIVE", None)
+    qo_i, qh_i = og.oph_build_sketches(qs_i, Vi, si_, flat=flat_i, hier=hier_i)
+    prm_b = og.params(pi["t_num"], pi["t_den"], pi["eps"], strategy=og.OPH_STRATEGY_BITMAP)
+    for fn, q_, s_, lay in ((og.compare_full, qo_i, so_i, flat_i), (og.compare_goph, qo_i, so_i, flat_i),
+                            (og.compare_hoph, qh_i, sh_i, hier_i)):
+        r = og.Results(1 << 20, stop_hist=True, bins_scanned=True)
+        fn(q_, s_, lay, prm_b, r)
+        total += r.n() + int(r.bins_scanned.item())
     torch.cuda.synchronize()
     print("sanitize_run ok", total)
 
