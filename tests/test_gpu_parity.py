@@ -1105,3 +1105,33 @@ def test_full_oph_exit_exact(image_small, monkeypatch, joint):
     blocks = -(-q.n_sets // 2048)
     assert runs["0"][2] == s.n_sets * p["k"] * blocks
     assert 0 < runs["1"][2] < runs["0"][2]
+
+
+@pytest.mark.parametrize("tn,td", [(7, 10), (1, 20), (9, 10), (1, 1)])
+@pytest.mark.parametrize("joint", [False, True])
+def test_full_oph_exit_ragged(tn, td, joint):
+    """R32 on a ragged collection (517 sets: not a whole number of 8-set tiles; empty sets, a
+    whole-universe-sized set, 45 queries incl. exact copies and an empty query) at k = 512,
+    thresholds from 1/20 (almost no set exits) to 1 (almost every set exits at bin 256): the
+    BITMAP threshold list == BRUTE's == the oracle's."""
+    rng = np.random.default_rng(tn * 100 + td + joint)
+    V, k, kp = 1 << 20, 512, 32
+    sizes = rng.integers(0, 700, size=517)
+    sizes[:3] = 0
+    sizes[7] = 20000
+    sets = [rng.choice(V, size=int(s), replace=False) if s else [] for s in sizes]
+    qsets = [sets[i] if i % 3 == 0 else rng.choice(V, size=int(rng.integers(0, 700)), replace=False)
+             for i in range(45)]
+    qsets[1] = []
+    offs, ids = make_csr(sets)
+    qoffs, qids = make_csr(qsets)
+    _, so, _ = gpu_build(offs, ids, V, 5, k=k, kprime=kp)
+    _, qo, _ = gpu_build(qoffs, qids, V, 5, k=k, kprime=kp)
+    lay = og.flat_layout(V, k, kp)
+    kw = dict(t_num=tn, t_den=td, joint=joint)
+    bit = gpu_threshold_hits("full", qo, so, layout=lay, strategy=og.OPH_STRATEGY_BITMAP, **kw)
+    brute = gpu_threshold_hits("full", qo, so, layout=lay, strategy=og.OPH_STRATEGY_BRUTE, **kw)
+    assert bit.tobytes() == brute.tobytes()
+    want = oracle_records("full", oracle.oph_sketch(qoffs, qids, V, k, 5), oracle.oph_sketch(offs, ids, V, k, 5),
+                          k=k, kprime=kp, **kw)
+    assert [(int(h["query"]), int(h["set_id"])) for h in bit] == oracle.threshold_list(want)
