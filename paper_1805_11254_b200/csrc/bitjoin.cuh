@@ -27,6 +27,10 @@ constexpr uint32_t kBitMaxBins = 1023;  // bins scanned: counts fit 10 bit slice
 constexpr uint32_t kBitCS = 10;       // count slices: ones, twos, fours, eights, hi[6]
 constexpr int kBitWarps = 8;          // warps per CTA = consecutive sets per CTA tile
 constexpr uint32_t kBitMaxStages = 8; // staged CTA tiles in flight (ring of value buffers)
+#ifndef OPHGPU_BIT_XRING
+#define OPHGPU_BIT_XRING 1
+#endif
+constexpr bool kBitXRing = OPHGPU_BIT_XRING;  // HOPH scan: row indices via a shared ring (-D...=0: shuffles)
 
 // bin b -> (first position, width) of its value range
 __device__ __forceinline__ void bit_bin_range(const BitArgs &a, uint32_t b, uint32_t &start, uint32_t &width) {
@@ -658,6 +662,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_x_kernel(const 
     __shared__ uint32_t s_start[kBitMaxBins + 1], s_width[kBitMaxBins + 1];
     __shared__ uint64_t s_full[kBitMaxStages];
     __shared__ uint32_t s_done[kBitMaxStages];
+    __shared__ __align__(16) uint32_t s_xring[kBitWarps][2][16];  // row indices parked for broadcast
     extern __shared__ __align__(128) uint32_t s_vals[];  // [nstage][npre][8]
     for (uint32_t b = threadIdx.x; b < a.npre; b += blockDim.x) {
         uint32_t st, wd;
@@ -724,10 +729,23 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_scan_x_kernel(const 
         }
         return r;
     };
+    // the 16 row indices of an item (lanes 0-15) reach every lane through the warp's shared
+    // ring (one store, 4 broadcast 16-B loads) instead of 16 shuffles (bit_pipe_kernel's way)
+    uint32_t xq = 0;
     auto rload = [&](uint32_t r, uint32_t (&x)[QW][16]) {
+        uint32_t *rq = &s_xring[threadIdx.x >> 5][xq][0];
+        xq ^= 1u;
+        if (kBitXRing) {
+            if ((threadIdx.x & 31u) < 16u) rq[threadIdx.x & 31u] = r;
+            __syncwarp();
+        }
+        uint4 o = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
         for (int u = 0; u < 16; u++) {
-            const uint32_t ru = __shfl_sync(0xFFFFFFFFu, r, u);
+            if (kBitXRing && (u & 3) == 0) o = reinterpret_cast<const uint4 *>(rq)[u >> 2];
+            const uint32_t ru =
+                kBitXRing ? ((u & 3) == 0 ? o.x : (u & 3) == 1 ? o.y : (u & 3) == 2 ? o.z : o.w)
+                          : __shfl_sync(0xFFFFFFFFu, r, u);
             if (QW == 2) {
                 const uint2 y = __ldg(reinterpret_cast<const uint2 *>(rows_lane + (uint64_t)ru * 64));
                 x[0][u] = y.x;
