@@ -77,14 +77,18 @@ __global__ void bit_fill_kernel(const __grid_constant__ BitArgs a) {
 }
 
 // max over each word's 32 queries of the query's empty bins (the filter bound of the
-// final verdict, see bit_final)
+// final verdict, see bit_final), and of its empty bins in every prefix [0, 32 c) (the
+// full-OPH exit's bound, R32)
 __global__ void bit_maxeq_kernel(const __grid_constant__ BitArgs a) {
     const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;  // qw CTAs of 1024 threads
+    const bool in = q < a.nqb;
+    const uint32_t qg = a.qb0 + q;
     uint32_t e = 0;
-    if (q < a.nqb) {
-        const uint32_t qg = a.qb0 + q;
-        for (uint32_t w = 0; w < a.nw; w++)
-            e += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + w), 0u, 0, w, a.nbins_total);
+    if ((q & 31u) == 0) a.max_eq_pref[q >> 5] = 0u;
+    for (uint32_t w = 0; w < a.nw; w++) {  // (warp-uniform trip count)
+        if (in) e += popc_masked(__ldg(a.QEM + (uint64_t)qg * a.nw + w), 0u, 0, w, a.nbins_total);
+        const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, e);
+        if ((q & 31u) == 0) a.max_eq_pref[(w + 1) * 64u + (q >> 5)] = m;
     }
     const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, e);
     if ((q & 31u) == 0) a.max_eq[q >> 5] = m;
@@ -909,12 +913,16 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_pipe_kernel(const __
     __shared__ uint32_t s_done[kBitMaxStages];
     __shared__ __align__(16) uint32_t s_ring[kBitWarps][4][16];
     __shared__ unsigned long long s_hist[kMaxGroups + 1];
+    __shared__ uint32_t s_ceilT[GOPH ? 1 : kBitMaxBins + 2];  // full OPH exit: ceil(T x), x = 0 .. k
     extern __shared__ __align__(128) uint32_t s_vals[];  // [nstage][npre][8]
     for (uint32_t b = threadIdx.x; b < a.nscan; b += blockDim.x) {
         uint32_t st, wd;
         bit_bin_range(a, b, st, wd);
         s_sw[b] = make_uint2(st, wd);
     }
+    if (!GOPH && a.exit_from)
+        for (uint32_t x = threadIdx.x; x <= a.nbins_total; x += blockDim.x)
+            s_ceilT[x] = (uint32_t)(((uint64_t)a.t_num * x + a.t_den - 1) / a.t_den);
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     uint32_t qw0[2], qvalid[2], max_eq[2];
 #pragma unroll
@@ -1057,24 +1065,35 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_pipe_kernel(const __
                 // set's non-empty bins in [B, k) reaches its threshold; theta = ceil(T den_min)
                 // with den_min from the largest query-empty count of the lane's two words is a
                 // lower bound on it (as in the final filter below; one register: per-word bounds
-                // cost spills, 14.55 vs 13.86 ms).  No such pair in the block: the set is done --
-                // every pair is NotSimilar, and threshold results emit nothing for them.
+                // cost spills, 14.55 vs 13.86 ms).  R32b, tighter: the bins in [B, k) add at most
+                // R (the set's non-empty bins there) to the count and at least as much to the
+                // denominator, so a pair needs M_B >= ceil(T (den_B + R)) - R, den_B >= B - eq_B -
+                // es_B (JointEmpty: B - min(eq_B, es_B)) with eq_B the largest query-empty count
+                // in [0, B) of the lane's queries (bit_maxeq_kernel's prefix maxima) -- the query's
+                // empty bins past B then no longer loosen the bound.  Both bounds are necessary; the
+                // larger is used.  No such pair in the block: the set is done -- every pair is
+                // NotSimilar, and threshold results emit nothing for them.
                 const uint32_t B = 16u * (j + 2);
                 if (a.exit_from && B >= a.exit_from && (B & 31u) == 0u && B < a.nbins_total) {
                     const uint32_t k = a.nbins_total;
+                    const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, k));
                     if (theta == 0u) {  // (the lane's two words share one bound: one register)
-                        const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, k));
                         const uint32_t me = max(max_eq[0], max_eq[1]);
                         const uint32_t den_min = a.joint ? k - min(me, es) : k - min(k, me + es);
-                        theta = max(1u, (uint32_t)(((uint64_t)a.t_num * den_min + a.t_den - 1) / a.t_den));
+                        theta = max(1u, s_ceilT[den_min]);
                     }
                     const uint32_t emp = __reduce_add_sync(
                         0xFFFFFFFFu, (lane < a.nw && 32u * lane >= B) ? popc_masked(0u, es_w, 0, lane, k) : 0u);
                     const uint32_t rem = (k - B) - emp;  // the set's non-empty bins not counted yet
+                    const uint32_t *pref = a.max_eq_pref + (B >> 5) * 64u + 2u * lane;
+                    const uint32_t eqB = max(__ldg(pref), __ldg(pref + 1));
+                    const uint32_t esB = es - emp;
+                    const uint32_t denB = a.joint ? B - min(eqB, esB) : B - min(B, eqB + esB);
+                    const uint32_t th = max(theta, s_ceilT[denB + rem]);
                     bool cand = false;
 #pragma unroll
                     for (int w = 0; w < 2; w++)
-                        cand |= (theta <= rem ? qvalid[w] : (sliced_ge<kBitCS>(c[w], theta - rem) & qvalid[w])) != 0u;
+                        cand |= (th <= rem ? qvalid[w] : (sliced_ge<kBitCS>(c[w], th - rem) & qvalid[w])) != 0u;
                     if (!__any_sync(0xFFFFFFFFu, cand)) {
                         early = true;
                         break;

@@ -409,7 +409,8 @@ constexpr uint32_t kBitMaxNb = 1023;
 bool bitmap_sizes_ok(uint64_t V, uint32_t nb) { return V <= kBitMaxV && nb <= kBitMaxNb; }
 // (rows of up to 2,048 query bits: blocks of 2,048 queries for full OPH / GOPH)
 size_t bitmap_region_bytes(uint64_t V, uint32_t nb) {
-    return align256(V * 4) + align256((1 + (uint64_t)nb * 2048) * 256) + align256(4) + align256(64 * 4);
+    return align256(V * 4) + align256((1 + (uint64_t)nb * 2048) * 256) + align256(4) + align256(64 * 4) +
+           align256(33 * 64 * 4);
 }
 
 // largest survivor capacity that fits in ws_bytes
@@ -437,7 +438,8 @@ oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketche
     ba.idx = (uint32_t *)bp; bp += align256(V * 4);
     ba.rows = (uint32_t *)bp; bp += align256((1 + (uint64_t)nb * 2048) * 256);
     ba.nrows = (uint32_t *)bp; bp += align256(4);
-    ba.max_eq = (uint32_t *)bp;
+    ba.max_eq = (uint32_t *)bp; bp += align256(64 * 4);
+    ba.max_eq_pref = (uint32_t *)bp;  // [nw + 1][64], nw <= 32
     ba.vpos = V;
 
     PrepArgs pa{};
@@ -500,7 +502,11 @@ oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketche
     // (R32; checked every 32 bins from bin 256 on: 13.49 ms vs 13.88 every 64 from 192, same box);
     // OPHGPU_FULL_EXIT=0 scans every bin (A/B)
     const bool no_exit = getenv("OPHGPU_FULL_EXIT") && atoi(getenv("OPHGPU_FULL_EXIT")) == 0;  // (per call: tests)
-    ba.exit_from = (method == OPH_METHOD_FULL && res->mode != OPH_RES_DENSE && !no_exit) ? 256u : 0u;
+    // (OPHGPU_FULL_EXIT_FROM: the first bin count checked, a multiple of 32, A/B; per call: tests)
+    const uint32_t exit_from = getenv("OPHGPU_FULL_EXIT_FROM")
+                                          ? std::max<uint32_t>(32u, (uint32_t)atoi(getenv("OPHGPU_FULL_EXIT_FROM")) / 32u * 32u)
+                                          : 256u;
+    ba.exit_from = (method == OPH_METHOD_FULL && res->mode != OPH_RES_DENSE && !no_exit) ? exit_from : 0u;
     // the bins' value ranges: flat = one range of nb bins; HOPH = nlev group ranges of kp bins
     if (method == OPH_METHOD_HOPH) {
         oph_hier_layout lay;

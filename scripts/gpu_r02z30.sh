@@ -1,0 +1,14 @@
+# r02z30: full-OPH exit with the prefix bound R32b (a; exit checked from bin 256, 224, 192) vs HEAD's R32 (b), same box, two rounds; exit / bitmap parity subset
+mkdir -p gpurun_out
+cp paper_1805_11254_b200/lib/libophgpu.so /tmp/lib_a.so
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -q -x --timeout 900 -k "bitmap or exit or ragged or tiny" > gpurun_out/pytest_z30.log 2>&1; echo pytest=$?
+for round in 1 2; do
+  cp /tmp/lib_a.so paper_1805_11254_b200/lib/libophgpu.so
+  for ef in 256 224 192; do
+    OPHGPU_FULL_EXIT_FROM=$ef timeout 600 python scripts/call_probe.py --config image --methods full --strategy 3 --reps 9 > gpurun_out/probe_a${ef}_${round}_z30.log 2>&1; echo a$ef$round=$?
+  done
+  cp paper_1805_11254_b200/lib/libophgpu_b.so paper_1805_11254_b200/lib/libophgpu.so
+  timeout 600 python scripts/call_probe.py --config image --methods full --strategy 3 --reps 9 > gpurun_out/probe_b_${round}_z30.log 2>&1; echo b$round=$?
+done
+cp /tmp/lib_a.so paper_1805_11254_b200/lib/libophgpu.so
+timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-minwise > gpurun_out/bench_z30.log 2>&1; echo bench=$?

@@ -1090,8 +1090,10 @@ def test_full_oph_exit_exact(image_small, monkeypatch, joint):
     lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
     prm = og.params(p["t_num"], p["t_den"], p["eps"], joint, og.OPH_STRATEGY_BITMAP)
     runs = {}
-    for env in ("1", "0"):
-        monkeypatch.setenv("OPHGPU_FULL_EXIT", env)
+    for env in ("1", "0", "from32"):
+        monkeypatch.setenv("OPHGPU_FULL_EXIT", "0" if env == "0" else "1")
+        if env == "from32":  # R32b's prefix bounds checked at every 32 bins
+            monkeypatch.setenv("OPHGPU_FULL_EXIT_FROM", "32")
         res = og.Results(1 << 22, stop_hist=True, bins_scanned=True)
         og.compare_full(q, s, lay, prm, res)
         n = res.n()
@@ -1101,19 +1103,26 @@ def test_full_oph_exit_exact(image_small, monkeypatch, joint):
     want = oracle_records("full", o["QF"], o["F"], k=p["k"], kprime=p["kprime"], t_num=p["t_num"],
                           t_den=p["t_den"], eps=p["eps"], joint=joint)
     assert runs["1"][0] == runs["0"][0] and runs["1"][1] == runs["0"][1]
+    assert runs["from32"][0] == runs["0"][0] and runs["from32"][1] == runs["0"][1]
+    assert runs["from32"][2] <= runs["1"][2]
     assert runs["1"][3] == len(oracle.threshold_list(want)) > 0
     blocks = -(-q.n_sets // 2048)
     assert runs["0"][2] == s.n_sets * p["k"] * blocks
     assert 0 < runs["1"][2] < runs["0"][2]
 
 
+@pytest.mark.parametrize("exit_from", [None, "32"])
 @pytest.mark.parametrize("tn,td", [(7, 10), (1, 20), (9, 10), (1, 1)])
 @pytest.mark.parametrize("joint", [False, True])
-def test_full_oph_exit_ragged(tn, td, joint):
-    """R32 on a ragged collection (517 sets: not a whole number of 8-set tiles; empty sets, a
-    whole-universe-sized set, 45 queries incl. exact copies and an empty query) at k = 512,
-    thresholds from 1/20 (almost no set exits) to 1 (almost every set exits at bin 256): the
-    BITMAP threshold list == BRUTE's == the oracle's."""
+def test_full_oph_exit_ragged(tn, td, joint, exit_from, monkeypatch):
+    """R32 / R32b on a ragged collection (517 sets: not a whole number of 8-set tiles; empty
+    sets, a whole-universe-sized set, 45 queries incl. exact copies and an empty query) at
+    k = 512, thresholds from 1/20 (almost no set exits) to 1 (almost every set exits at the
+    first check), the exit checked from bin 256 (default) or at every 32 bins from bin 32
+    (the prefix bounds R32b at every checkpoint): the BITMAP threshold list == BRUTE's ==
+    the oracle's."""
+    if exit_from:
+        monkeypatch.setenv("OPHGPU_FULL_EXIT_FROM", exit_from)
     rng = np.random.default_rng(tn * 100 + td + joint)
     V, k, kp = 1 << 20, 512, 32
     sizes = rng.integers(0, 700, size=517)
