@@ -1074,7 +1074,7 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_pipe_kernel(const __
                 // larger is used.  No such pair in the block: the set is done -- every pair is
                 // NotSimilar, and threshold results emit nothing for them.
                 const uint32_t B = 16u * (j + 2);
-                if (a.exit_from && B >= a.exit_from && (B & 31u) == 0u && B < a.nbins_total) {
+                if (a.exit_from && B >= a.exit_from && ((B - a.exit_from) & (a.exit_every - 1u)) == 0u && B < a.nbins_total) {
                     const uint32_t k = a.nbins_total;
                     const uint32_t es = __reduce_add_sync(0xFFFFFFFFu, popc_masked(0u, es_w, 0, lane, k));
                     if (theta == 0u) {  // (the lane's two words share one bound: one register)
@@ -1085,15 +1085,17 @@ __global__ void __launch_bounds__(32 * kBitWarps, MINB) bit_pipe_kernel(const __
                     const uint32_t emp = __reduce_add_sync(
                         0xFFFFFFFFu, (lane < a.nw && 32u * lane >= B) ? popc_masked(0u, es_w, 0, lane, k) : 0u);
                     const uint32_t rem = (k - B) - emp;  // the set's non-empty bins not counted yet
+                    // (per word: the prefix bounds are loaded per check, no register kept)
                     const uint32_t *pref = a.max_eq_pref + (B >> 5) * 64u + 2u * lane;
-                    const uint32_t eqB = max(__ldg(pref), __ldg(pref + 1));
                     const uint32_t esB = es - emp;
-                    const uint32_t denB = a.joint ? B - min(eqB, esB) : B - min(B, eqB + esB);
-                    const uint32_t th = max(theta, s_ceilT[denB + rem]);
                     bool cand = false;
 #pragma unroll
-                    for (int w = 0; w < 2; w++)
+                    for (int w = 0; w < 2; w++) {
+                        const uint32_t eqB = __ldg(pref + w);
+                        const uint32_t denB = a.joint ? B - min(eqB, esB) : B - min(B, eqB + esB);
+                        const uint32_t th = max(theta, s_ceilT[denB + rem]);
                         cand |= (th <= rem ? qvalid[w] : (sliced_ge<kBitCS>(c[w], th - rem) & qvalid[w])) != 0u;
+                    }
                     if (!__any_sync(0xFFFFFFFFu, cand)) {
                         early = true;
                         break;

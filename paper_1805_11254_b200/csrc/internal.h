@@ -241,6 +241,7 @@ struct BitArgs {
     uint32_t *max_eq;               // [32 qw] per query word: max empty bins of its queries
     uint32_t *max_eq_pref;          // [nw + 1][64]: per query word, max over its queries of the empty bins in [0, 32 c)
     uint32_t exit_from;             // full OPH, threshold mode: first bin count checked for a set's exit (0: off)
+    uint32_t exit_every;            // then every exit_every bins (32 or 64; exit_from a multiple of 32)
     unsigned long long *scanned;    // optional: adds the (set, bin) rows gathered (oph_results.d_bins_scanned)
     OutArgs out;
 };

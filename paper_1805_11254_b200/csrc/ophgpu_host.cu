@@ -499,14 +499,18 @@ oph_status run_bitmap(uint32_t method, const oph_sketches *Qv, const oph_sketche
     ba.out.hist = res->d_stop_hist;
     ba.scanned = res->d_bins_scanned;
     // full OPH in threshold mode: a set's scan stops once no pair of the block can reach T
-    // (R32; checked every 32 bins from bin 256 on: 13.49 ms vs 13.88 every 64 from 192, same box);
+    // (R32 / R32b), checked every 32 bins from bin ceil32(9 k / 16) on (288 at k = 512: image-like
+    // sweep of the first checkpoint, same box: 256 11.54 ms, 288 11.16, 320 11.96, 352 12.79;
+    // every 64 from 288 11.11 -- profiles/r02/full_exit_schedule_r02z32.log);
     // OPHGPU_FULL_EXIT=0 scans every bin (A/B)
     const bool no_exit = getenv("OPHGPU_FULL_EXIT") && atoi(getenv("OPHGPU_FULL_EXIT")) == 0;  // (per call: tests)
     // (OPHGPU_FULL_EXIT_FROM: the first bin count checked, a multiple of 32, A/B; per call: tests)
     const uint32_t exit_from = getenv("OPHGPU_FULL_EXIT_FROM")
-                                          ? std::max<uint32_t>(32u, (uint32_t)atoi(getenv("OPHGPU_FULL_EXIT_FROM")) / 32u * 32u)
-                                          : 256u;
+                                   ? std::max<uint32_t>(32u, (uint32_t)atoi(getenv("OPHGPU_FULL_EXIT_FROM")) / 32u * 32u)
+                                   : std::max<uint32_t>(32u, (9u * nb / 16u + 31u) / 32u * 32u);
     ba.exit_from = (method == OPH_METHOD_FULL && res->mode != OPH_RES_DENSE && !no_exit) ? exit_from : 0u;
+    // (OPHGPU_FULL_EXIT_EVERY=64: every other checkpoint, A/B)
+    ba.exit_every = getenv("OPHGPU_FULL_EXIT_EVERY") && atoi(getenv("OPHGPU_FULL_EXIT_EVERY")) == 64 ? 64u : 32u;
     // the bins' value ranges: flat = one range of nb bins; HOPH = nlev group ranges of kp bins
     if (method == OPH_METHOD_HOPH) {
         oph_hier_layout lay;

@@ -1118,7 +1118,7 @@ def test_full_oph_exit_ragged(tn, td, joint, exit_from, monkeypatch):
     """R32 / R32b on a ragged collection (517 sets: not a whole number of 8-set tiles; empty
     sets, a whole-universe-sized set, 45 queries incl. exact copies and an empty query) at
     k = 512, thresholds from 1/20 (almost no set exits) to 1 (almost every set exits at the
-    first check), the exit checked from bin 256 (default) or at every 32 bins from bin 32
+    first check), the exit checked from bin 288 (default: ceil32(9 k / 16)) or at every 32 bins from bin 32
     (the prefix bounds R32b at every checkpoint): the BITMAP threshold list == BRUTE's ==
     the oracle's."""
     if exit_from:
