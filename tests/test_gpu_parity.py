@@ -1090,10 +1090,11 @@ def test_full_oph_exit_exact(image_small, monkeypatch, joint):
     lay = og.flat_layout(r["w"].vocab_size, p["k"], p["kprime"])
     prm = og.params(p["t_num"], p["t_den"], p["eps"], joint, og.OPH_STRATEGY_BITMAP)
     runs = {}
-    for env in ("1", "0", "from32"):
+    for env in ("1", "0", "from64", "from32"):
         monkeypatch.setenv("OPHGPU_FULL_EXIT", "0" if env == "0" else "1")
-        if env == "from32":  # R32b's prefix bounds checked at every 32 bins
-            monkeypatch.setenv("OPHGPU_FULL_EXIT_FROM", "32")
+        if env.startswith("from"):  # R32b's prefix bounds checked at every 32 bins (from 64: the
+            # next set's lookups are fetched ahead at bin 32; from 32: no room for that, none fetched)
+            monkeypatch.setenv("OPHGPU_FULL_EXIT_FROM", env[4:])
         res = og.Results(1 << 22, stop_hist=True, bins_scanned=True)
         og.compare_full(q, s, lay, prm, res)
         n = res.n()
@@ -1104,6 +1105,7 @@ def test_full_oph_exit_exact(image_small, monkeypatch, joint):
                           t_den=p["t_den"], eps=p["eps"], joint=joint)
     assert runs["1"][0] == runs["0"][0] and runs["1"][1] == runs["0"][1]
     assert runs["from32"][0] == runs["0"][0] and runs["from32"][1] == runs["0"][1]
+    assert runs["from64"][0] == runs["0"][0] and runs["from64"][1] == runs["0"][1]
     assert runs["from32"][2] <= runs["1"][2]
     assert runs["1"][3] == len(oracle.threshold_list(want)) > 0
     blocks = -(-q.n_sets // 2048)
@@ -1111,7 +1113,7 @@ def test_full_oph_exit_exact(image_small, monkeypatch, joint):
     assert 0 < runs["1"][2] < runs["0"][2]
 
 
-@pytest.mark.parametrize("exit_from", [None, "32"])
+@pytest.mark.parametrize("exit_from", [None, "32", "64"])
 @pytest.mark.parametrize("tn,td", [(7, 10), (1, 20), (9, 10), (1, 1)])
 @pytest.mark.parametrize("joint", [False, True])
 def test_full_oph_exit_ragged(tn, td, joint, exit_from, monkeypatch):
