@@ -669,9 +669,11 @@ def run_ours(args):
     # profiles/ubench_r02.json (scripts/ubench.cu)
     issue_peak = 148 * 4 * 16 * f_sm
     issue_src = "derived: 148 SM x 4 SMSP x 16 bin-compares/clk (2 warp-instr per 32 compares) x sm_max_mhz"
+    # (scripts/ubench.cu's stand-alone ISETP+IMAD loop reaches 1.04e13/s, LESS than scan_kernel itself
+    # on the sweep configs (1.12e13/s): it is not a ceiling, so the derived one is the peak; the
+    # microbenchmark's LOP3 / IMAD lane rates (1.86e13/s = one warp-instr per SMSP per clock) confirm it)
     if ub and ub.get("brute_compares_per_s"):
-        issue_peak = ub["brute_compares_per_s"]
-        issue_src = "measured: scripts/ubench.cu ISETP+IMAD compare loop (profiles/ubench_r02.json)"
+        issue_src += f"; scripts/ubench.cu compare loop: {ub['brute_compares_per_s']:.3e}/s (below the kernel: not used)"
     # algorithmic bytes / work per launch
     build_bytes = 4 * nnz + 8 * (N + 1) + 4 * N * (k + L * hkp) + 4 * N * (nw_k + nw_h)
     scan_bytes = {"compare_full": N * (4 * k + 4 * nw_k),
