@@ -632,7 +632,12 @@ oph_status run_compare(uint32_t method, const oph_sketches *Qv, const oph_sketch
             use = true;
         } else if (p->strategy == OPH_STRATEGY_AUTO && dom && fits && n_q >= 1024) {
             // (a block's scan costs the same for 1 or 2,048 queries: below ~1,024 queries the
-            // register scan's Q N k compares are cheaper -- sweep, 256 queries: 122 vs 55 ms)
+            // register scan's Q N k compares are cheaper -- sweep-0.5, full OPH, r02z36: 256 queries
+            // 41.6 vs 23.3 ms, 512 queries 42.6 vs 45.8 ms.  GOPH / HOPH on a collection whose
+            // pairs mostly survive the bitmap's levels (the sweep: every set a near-duplicate of
+            // the hub) walk those pairs one by one and lose to the register scan at any query
+            // count -- 512 queries: 225 vs 24.9 ms, 78 vs 6.4 ms; AUTO does not detect that
+            // regime)
             // AUTO: where PROBE would not apply, or this collection was found to be a BRUTE one
             const bool probe_ok =
                 res->mode != OPH_RES_DENSE &&

@@ -16,13 +16,14 @@ ap.add_argument("--methods", default="goph,hoph")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--strategy", type=int, default=og.OPH_STRATEGY_AUTO)
 ap.add_argument("--variant", type=int, default=0, help="1: the empty-aware GOPH rule")
+ap.add_argument("--queries", type=int, default=0, help="sweep configs: the number of queries (default 1,024)")
 args = ap.parse_args()
 if args.config == "text":
     w = text_like()
 elif args.config == "scale":
     w = gen_gpu.scale_shard()
 elif args.config.startswith("sweep"):
-    w = gen_gpu.sweep(float(args.config[5:]))
+    w = gen_gpu.sweep(float(args.config[5:]), **({"n_queries": args.queries} if args.queries else {}))
 else:
     w = gen_gpu.image_like()
 p = w.params
